@@ -1,0 +1,245 @@
+/*
+ * gb_bal.h — C ABI of the B200-native Levenberg–Marquardt bundle-adjustment
+ * solver (the LM inner loop of arXiv 2509.26581, reference `gopt`).
+ *
+ * This is the drop-in boundary for the reference's hot path. Each entry point
+ * names the reference interface it replaces (paths relative to
+ * /root/reference/proj). Plain pointers and sizes only: no C++ or torch types.
+ *
+ * Element types follow the reference's precision pairs
+ * (src/experiment.cpp:153-157):
+ *   GB_FP64       graph FP = double, system SP = double
+ *   GB_FP32       graph FP = float,  system SP = float
+ *   GB_FP32_BF16  graph FP = float,  system SP = bfloat16 (uint16 storage,
+ *                 include/gopt/bfloat16.hpp:12-37), arithmetic in float
+ * Buffers documented as "FP" hold double for GB_FP64 and float otherwise;
+ * "SP" buffers hold double / float / uint16 bf16 bits; "Arith" buffers hold
+ * double for GB_FP64 and float otherwise.
+ *
+ * Error model: every int-returning call returns GB_OK or one of the GB_ERR_*
+ * codes, which map one-to-one onto the exception the reference throws in the
+ * same situation; gb_last_error() returns the message.
+ */
+#ifndef GB_BAL_H_
+#define GB_BAL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+#define GB_OK 0
+#define GB_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument (vertex_descriptor.hpp:71-74,
+                                     factor_descriptor.hpp:553-555, precision.hpp:44-49) */
+#define GB_ERR_OUT_OF_RANGE 2     /* std::out_of_range (factor_descriptor.hpp:543-547) */
+#define GB_ERR_LOGIC 3            /* std::logic_error (graph.hpp:64-65, 92) */
+#define GB_ERR_RUNTIME 4          /* std::runtime_error (levenberg_marquardt.hpp:133-134) */
+#define GB_ERR_CUDA 5             /* device failure (no reference counterpart) */
+#define GB_ERR_NO_DEVICE 6        /* no CUDA device: the device path never falls back to CPU */
+
+/* ---- enums (values match the reference enum order) ---------------------- */
+/* bench/experiment.hpp:16 PrecisionMode */
+#define GB_FP64 0
+#define GB_FP32 1
+#define GB_FP32_BF16 2
+/* factor_descriptor.hpp:23 DifferentiationMode */
+#define GB_ANALYTIC 0
+#define GB_AUTO 1
+#define GB_DYNAMIC 2
+/* loss.hpp:10 LossKind */
+#define GB_LOSS_DEFAULT 0
+#define GB_LOSS_HUBER 1
+/* factor_descriptor.hpp:37 DampingPlacement */
+#define GB_DAMPING_AFTER_SCALING 0
+#define GB_DAMPING_BEFORE_SCALING 1
+/* levenberg_marquardt.hpp:28-35 Termination */
+#define GB_TERM_MAX_ITERATIONS 0
+#define GB_TERM_TOLERANCE_REACHED 1
+#define GB_TERM_GRADIENT_SMALL 2
+#define GB_TERM_DAMPING_OVERFLOW 3
+#define GB_TERM_NON_FINITE_LINEARIZATION 4
+#define GB_TERM_NO_FREE_PARAMETERS 5
+
+/* ---- configuration (same fields and defaults as the reference) ---------- */
+/* pcg.hpp:12-17 PCGConfig */
+typedef struct gb_pcg_config {
+  int32_t max_iterations;  /* 50 */
+  double tolerance;        /* 1e-6 */
+  double rejection_ratio;  /* 10 */
+  int32_t normalize_rhs;   /* 1 */
+} gb_pcg_config;
+
+/* pcg.hpp:19-23 PCGStats */
+typedef struct gb_pcg_stats {
+  int32_t iterations;
+  double final_relative_residual;
+  int32_t converged;
+} gb_pcg_stats;
+
+/* levenberg_marquardt.hpp:15-26 LMConfig + linear_system.hpp:15-19 LinearSystemOptions */
+typedef struct gb_lm_config {
+  int32_t max_iterations;      /* 10 */
+  double tolerance;            /* 1e-6 */
+  int32_t level;               /* 0 */
+  double tau;                  /* 1e-4 */
+  gb_pcg_config pcg;
+  double clamp_min;            /* 1e-6 */
+  double clamp_max;            /* 1e32 */
+  int32_t damping;             /* GB_DAMPING_AFTER_SCALING */
+  int32_t use_rejection_guard; /* 1 */
+  int32_t refresh_on_reject;   /* 0 */
+  double lambda_max;           /* 1e32 */
+  double gradient_tolerance;   /* 1e-12 */
+} gb_lm_config;
+
+/* levenberg_marquardt.hpp:49-61 IterationRecord */
+typedef struct gb_iteration_record {
+  int32_t iteration;
+  double chi2_before;
+  double chi2_after;
+  double lambda;
+  int32_t pcg_iterations;
+  int32_t pcg_converged;
+  double pcg_relative_residual;
+  int32_t low_quality_step;
+  int32_t precond_fallback_blocks;
+  int32_t accepted;
+  double wall_seconds;
+} gb_iteration_record;
+
+/* levenberg_marquardt.hpp:63-68 MemoryAccount (analytic, SPEC "Memory accounting") */
+typedef struct gb_memory_account {
+  uint64_t jacobian_bytes;
+  uint64_t preconditioner_bytes;
+  uint64_t workspace_bytes;
+  uint64_t graph_bytes;
+} gb_memory_account;
+
+/* levenberg_marquardt.hpp:72-83 SolveReport (iterations returned separately) */
+typedef struct gb_solve_report {
+  double initial_chi2;
+  double final_chi2;
+  int32_t accepted_steps;
+  int32_t termination;
+  double total_seconds;
+  int64_t free_dims;
+  int64_t residual_dims;
+  uint64_t active_factors;
+  gb_memory_account memory;
+  int32_t iterations_run;
+  /* device-side extras (no reference field): */
+  double setup_seconds;    /* host->device upload + activation + initial linearize */
+  double h2d_bytes;
+  double d2h_bytes;
+} gb_solve_report;
+
+typedef struct gb_graph gb_graph;
+
+/* Fills the reference defaults (levenberg_marquardt.hpp:15-26, pcg.hpp:12-17,
+ * linear_system.hpp:15-19). */
+void gb_default_config(gb_lm_config* cfg);
+
+/* Last error message of the calling thread ("" if none). */
+const char* gb_last_error(void);
+
+/* Number of visible CUDA devices (0 on a host without a GPU). */
+int gb_device_count(void);
+
+/* ---- graph construction -------------------------------------------------
+ * Replaces bal::build_graph<FP,SP> (include/gopt/bal/adapter.hpp:106-143),
+ * which builds CameraDescriptor / Point3Descriptor / ReprojectionFactor and a
+ * Graph<FP,SP> (graph.hpp:26-45). precision is a GB_FP* code, diff_mode a
+ * GB_* differentiation mode (factor_descriptor.hpp:230-235). device is the
+ * CUDA ordinal this handle runs on. Returns NULL on error (gb_last_error). */
+gb_graph* gb_create(int precision, int diff_mode, int device);
+void gb_destroy(gb_graph* g);
+
+/* Cameras: AoS FP[9*n] in the Snavely layout [w1 w2 w3 t1 t2 t3 f k1 k2]
+ * (bal/snavely.hpp:47). The buffer is the user's vertex storage and is
+ * refined IN PLACE by gb_optimize (CameraTraits::update, adapter.hpp:16-28);
+ * it must stay valid for the handle's lifetime. fixed: NULL or uint8[n]
+ * (VertexDescriptor::set_fixed, vertex_descriptor.hpp:80-83). Vertex ids are
+ * the positions 0..n-1 (build_graph adds vertex c with id c, adapter.hpp:117). */
+int gb_set_cameras(gb_graph* g, void* params_fp, uint64_t n, const uint8_t* fixed);
+/* Points: AoS FP[3*n], refined in place (Point3Traits, adapter.hpp:30-42). */
+int gb_set_points(gb_graph* g, void* params_fp, uint64_t n, const uint8_t* fixed);
+/* Observations, one reprojection factor each (FactorDescriptor::add_factor,
+ * factor_descriptor.hpp:192-210, via build_graph adapter.hpp:136-141):
+ * camera/point ids, observed pixel FP[2*n], identity information, level
+ * (NULL = all 0; FactorDescriptor::set_level :222-226), loss kind and Huber
+ * delta (loss.hpp:15-23). Data is copied. Unknown ids -> GB_ERR_INVALID_ARGUMENT
+ * (resolve_slots :549-558). */
+int gb_set_observations(gb_graph* g, uint64_t n, const uint32_t* camera_index,
+                        const uint32_t* point_index, const void* observed_fp,
+                        const uint8_t* level, int loss_kind, double huber_delta);
+/* FactorDescriptor::set_differentiation_mode (factor_descriptor.hpp:230-235). */
+int gb_set_differentiation_mode(gb_graph* g, int diff_mode);
+
+/* ---- the solve ------------------------------------------------------------
+ * Replaces levenberg_marquardt<FP,SP>(Graph&, const LMConfig&)
+ * (levenberg_marquardt.hpp:115-224). Uploads once, runs every LM iteration on
+ * the device (no host round-trip per iteration), writes the refined cameras
+ * and points back into the registered user buffers. records: NULL or an array
+ * of max_records IterationRecords (report->iterations_run are valid).
+ * Non-finite initial chi^2 -> GB_ERR_RUNTIME with the reference message. */
+int gb_optimize(gb_graph* g, const gb_lm_config* cfg, gb_solve_report* report,
+                gb_iteration_record* records, int32_t max_records);
+
+/* BalGraph::mse (adapter.hpp:95-99) at the current user parameters. */
+int gb_mse(gb_graph* g, double* out);
+/* Graph::total_error(level) (graph.hpp:99-104). */
+int gb_total_error(gb_graph* g, int level, double* out);
+
+/* ---- LinearSystem surface (linear_system.hpp:44-216) ----------------------
+ * These expose the same intermediate quantities as the reference's public
+ * LinearSystem accessors so parity can be checked step by step. Vectors are
+ * in the REFERENCE column layout (free cameras 9 each in insertion order,
+ * then free points 3 each; VertexDescriptor::assign_columns :115-126). */
+
+/* Graph::activate + LinearSystem::prepare + linearize (linear_system.hpp:44-82).
+ * Any output pointer may be NULL. free_dims receives N. */
+int gb_ls_linearize(gb_graph* g, int level, double clamp_min, double clamp_max, int damping,
+                    double* chi2, int64_t* free_dims, void* b_fp, void* diag_fp,
+                    void* clamped_fp, void* scaling_fp, int32_t* finite);
+/* out = (D H D + damp) v   (LinearSystem::hvp, linear_system.hpp:104-115).
+ * v: SP[N], out: Arith[N]. */
+int gb_ls_hvp(gb_graph* g, const void* v_sp, void* out_arith, double lambda);
+/* LinearSystem::build_preconditioner (linear_system.hpp:120-160): inverse
+ * blocks in the reference's PrecondLayout order (camera 9x9 blocks, then point
+ * 3x3 blocks, one per free vertex), FP. fallbacks may be NULL. */
+int gb_ls_preconditioner(gb_graph* g, double lambda, void* blocks_fp, int32_t* fallbacks);
+/* LinearSystem::solve_step (linear_system.hpp:185-207): dx FP[N]. */
+int gb_ls_solve_step(gb_graph* g, double lambda, const gb_pcg_config* pcg, void* dx_fp,
+                     gb_pcg_stats* stats, double* predicted_decrease, int32_t* finite);
+/* Stored Jacobian blocks, per active factor [Jc 2x9 | Jp 2x3] row-major, SP
+ * (factor_descriptor.hpp:662-670 layout), active-factor order. */
+int gb_ls_jacobians(gb_graph* g, void* out_sp);
+/* The edge->vertex incidence CSR of FactorDescriptor::build_incidence
+ * (factor_descriptor.hpp:710-753) for descriptor 0 (cameras) or 1 (points):
+ * call once with NULL arrays to get the sizes, then again with buffers.
+ * vertex_of_segment: uint64[nseg], offsets: uint64[nseg+1], items_factor:
+ * uint32[nitems] (active factor index a), items_slot: uint16[nitems]. */
+int gb_incidence(gb_graph* g, int descriptor, uint64_t* nseg, uint64_t* nitems,
+                 uint64_t* vertex_of_segment, uint64_t* offsets, uint32_t* items_factor,
+                 uint16_t* items_slot);
+
+/* ---- synthetic BAL-shaped problems (bench / test input) -------------------
+ * Deterministic generator with the semantics of tests/synthetic_bal.hpp:16-113
+ * (camera ring, point cloud, pixel noise, perturbed initial estimate), sized
+ * to an exact (cameras, points, observations) shape; see DESIGN.md. Outputs
+ * are binary64 (BALProblem layout, bal/problem.hpp:25-40). camera_stride 0
+ * picks the default; zipf_s > 0 draws each point's first camera from a
+ * Zipf(s) law (skewed camera degrees). Host-only, no GPU needed. */
+int gb_synthetic_bal(uint64_t num_cameras, uint64_t num_points, uint64_t num_observations,
+                     uint64_t seed, uint64_t camera_stride, double zipf_s,
+                     uint32_t* camera_index, uint32_t* point_index, double* observed,
+                     double* cameras, double* points);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GB_BAL_H_ */

@@ -1,0 +1,419 @@
+"""Host-side mirror of the reference's BAL API over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API so
+that parity tests read like the reference's own tests:
+
+  reference (C++, /root/reference/proj)                 here
+  ----------------------------------------------------  -------------------------------
+  bal::BALProblem           bal/problem.hpp:25-40       BALProblem
+  bal::parse_bal_text / serialize_bal_text              parse_bal_text / serialize_bal_text
+  bal::build_graph<FP,SP>   bal/adapter.hpp:106-143     build_graph(problem, precision, mode)
+  BalGraph::mse             bal/adapter.hpp:95-99       BalGraph.mse()
+  Graph::total_error        graph.hpp:99-104            BalGraph.total_error(level)
+  VertexDescriptor::set_fixed vertex_descriptor.hpp:80  BalGraph.set_fixed(...)
+  FactorDescriptor::set_level factor_descriptor.hpp:222 BalGraph.set_levels(...)
+  LMConfig / PCGConfig      levenberg_marquardt.hpp:15  LMConfig / PCGConfig
+  levenberg_marquardt       levenberg_marquardt.hpp:115 levenberg_marquardt(graph, config)
+  SolveReport / IterationRecord :49-83                  SolveReport / IterationRecord
+  LinearSystem accessors    linear_system.hpp:44-216    BalGraph.ls_* (parity surface)
+
+Errors raise the Python counterpart of the reference exception
+(ValueError <- std::invalid_argument, IndexError <- std::out_of_range,
+LogicError <- std::logic_error, RuntimeError <- std::runtime_error).
+The device path never falls back to the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _abi
+
+PRECISIONS = {"fp64": _abi.GB_FP64, "fp32": _abi.GB_FP32, "fp32-bf16": _abi.GB_FP32_BF16}
+MODES = {"analytic": _abi.GB_ANALYTIC, "auto": _abi.GB_AUTO, "dynamic": _abi.GB_DYNAMIC}
+
+
+class LogicError(RuntimeError):
+    """std::logic_error counterpart."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or no device (no reference counterpart)."""
+
+
+def dtypes(precision: str):
+    """(FP, SP, Arith) numpy dtypes of a precision pair (precision.hpp:72-81)."""
+    if precision == "fp64":
+        return np.float64, np.float64, np.float64
+    if precision == "fp32":
+        return np.float32, np.float32, np.float32
+    if precision == "fp32-bf16":
+        return np.float32, np.uint16, np.float32
+    raise ValueError(f"invalid precision pair: {precision}")
+
+
+# --------------------------------------------------------------------- configs
+@dataclass
+class PCGConfig:
+    """pcg.hpp:12-17."""
+    max_iterations: int = 50
+    tolerance: float = 1e-6
+    rejection_ratio: float = 10.0
+    normalize_rhs: bool = True
+
+    def to_c(self) -> _abi.gb_pcg_config:
+        return _abi.gb_pcg_config(self.max_iterations, self.tolerance, self.rejection_ratio, int(self.normalize_rhs))
+
+
+@dataclass
+class LMConfig:
+    """levenberg_marquardt.hpp:15-26 (+ LinearSystemOptions, linear_system.hpp:15-19)."""
+    max_iterations: int = 10
+    tolerance: float = 1e-6
+    level: int = 0
+    tau: float = 1e-4
+    pcg: PCGConfig = field(default_factory=PCGConfig)
+    clamp_min: float = 1e-6
+    clamp_max: float = 1e32
+    damping: str = "after_scaling"
+    use_rejection_guard: bool = True
+    refresh_on_reject: bool = False
+    lambda_max: float = 1e32
+    gradient_tolerance: float = 1e-12
+
+    def to_c(self) -> _abi.gb_lm_config:
+        c = _abi.gb_lm_config()
+        c.max_iterations = self.max_iterations
+        c.tolerance = self.tolerance
+        c.level = self.level
+        c.tau = self.tau
+        c.pcg = self.pcg.to_c()
+        c.clamp_min = self.clamp_min
+        c.clamp_max = self.clamp_max
+        c.damping = _abi.GB_DAMPING_BEFORE_SCALING if self.damping == "before_scaling" else _abi.GB_DAMPING_AFTER_SCALING
+        c.use_rejection_guard = int(self.use_rejection_guard)
+        c.refresh_on_reject = int(self.refresh_on_reject)
+        c.lambda_max = self.lambda_max
+        c.gradient_tolerance = self.gradient_tolerance
+        return c
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    chi2_before: float
+    chi2_after: float
+    lambda_: float
+    pcg_iterations: int
+    pcg_converged: bool
+    pcg_relative_residual: float
+    low_quality_step: bool
+    precond_fallback_blocks: int
+    accepted: bool
+    wall_seconds: float
+
+
+@dataclass
+class SolveReport:
+    iterations: List[IterationRecord]
+    initial_chi2: float
+    final_chi2: float
+    accepted_steps: int
+    termination: str
+    total_seconds: float
+    free_dims: int
+    residual_dims: int
+    active_factors: int
+    memory: dict
+    setup_seconds: float = 0.0
+    h2d_bytes: float = 0.0
+    d2h_bytes: float = 0.0
+
+    def to_dict(self) -> dict:
+        d = dataclasses.asdict(self)
+        for it in d["iterations"]:
+            it["lambda"] = it.pop("lambda_")
+        return d
+
+
+# ---------------------------------------------------------------- BAL problem
+@dataclass
+class BALProblem:
+    """bal/problem.hpp:25-40 (binary64 values)."""
+    cameras: np.ndarray  # (nc, 9) float64
+    points: np.ndarray  # (np, 3) float64
+    camera_index: np.ndarray  # (ne,) uint32
+    point_index: np.ndarray  # (ne,) uint32
+    observations: np.ndarray  # (ne, 2) float64
+
+    @property
+    def num_cameras(self) -> int:
+        return int(self.cameras.shape[0])
+
+    @property
+    def num_points(self) -> int:
+        return int(self.points.shape[0])
+
+    @property
+    def num_observations(self) -> int:
+        return int(self.camera_index.shape[0])
+
+    def copy(self) -> "BALProblem":
+        return BALProblem(self.cameras.copy(), self.points.copy(), self.camera_index.copy(), self.point_index.copy(),
+                          self.observations.copy())
+
+
+def synthetic_bal(num_cameras: int, num_points: int, num_observations: int, seed: int = 42,
+                  camera_stride: int = 0, zipf: float = 0.0) -> BALProblem:
+    """Deterministic BAL-shaped problem (gb_synthetic_bal)."""
+    nc, np_, ne = int(num_cameras), int(num_points), int(num_observations)
+    cam = np.empty(ne, np.uint32)
+    pt = np.empty(ne, np.uint32)
+    obs = np.empty((ne, 2), np.float64)
+    cams = np.empty((nc, 9), np.float64)
+    pts = np.empty((np_, 3), np.float64)
+    rc = _abi.lib().gb_synthetic_bal(nc, np_, ne, seed, camera_stride, zipf, cam.ctypes.data, pt.ctypes.data,
+                                     obs.ctypes.data, cams.ctypes.data, pts.ctypes.data)
+    if rc != _abi.GB_OK:
+        raise ValueError("synthetic_bal: invalid shape (need observations >= points and degree <= cameras)")
+    return BALProblem(cams, pts, cam, pt, obs)
+
+
+def parse_bal_text(text: str) -> BALProblem:
+    """bal/problem.hpp:46-55, src/bal_problem.cpp:81-115 (header, observations, cameras, points)."""
+    tok = text.split()
+    pos = 0
+
+    def take(n):
+        nonlocal pos
+        if pos + n > len(tok):
+            raise ValueError("truncated file")
+        out = tok[pos:pos + n]
+        pos += n
+        return out
+
+    nc, np_, ne = (int(v) for v in take(3))
+    raw = np.array(take(4 * ne), dtype=object).reshape(ne, 4) if ne else np.zeros((0, 4), dtype=object)
+    cam = raw[:, 0].astype(np.uint64)
+    pt = raw[:, 1].astype(np.uint64)
+    if ne and (cam.max() >= nc or pt.max() >= np_):
+        raise ValueError("observation index out of range")
+    obs = raw[:, 2:4].astype(np.float64)
+    cams = np.array(take(9 * nc), dtype=np.float64).reshape(nc, 9)
+    pts = np.array(take(3 * np_), dtype=np.float64).reshape(np_, 3)
+    return BALProblem(cams, pts, cam.astype(np.uint32), pt.astype(np.uint32), obs.reshape(ne, 2))
+
+
+def serialize_bal_text(p: BALProblem) -> str:
+    """src/bal_problem.cpp:121-136 (%.17g round trip)."""
+    lines = [f"{p.num_cameras} {p.num_points} {p.num_observations}"]
+    for c, q, (x, y) in zip(p.camera_index, p.point_index, p.observations):
+        lines.append(f"{int(c)} {int(q)} {x:.17g} {y:.17g}")
+    lines.extend(f"{v:.17g}" for v in p.cameras.reshape(-1))
+    lines.extend(f"{v:.17g}" for v in p.points.reshape(-1))
+    return "\n".join(lines) + "\n"
+
+
+# ---------------------------------------------------------------- the graph
+class Backend:
+    """A C ABI implementing include/gb_bal.h (the device library, or the
+    reference compiled as the oracle with prefix 'ref_')."""
+
+    def __init__(self, lib: ctypes.CDLL, prefix: str):
+        self.lib = lib
+        self.prefix = prefix
+
+    def fn(self, name):
+        return getattr(self.lib, self.prefix + name)
+
+    def create(self, precision: int, mode: int, arg: int):
+        return self.fn("create")(precision, mode, arg)
+
+    def check(self, rc: int):
+        if rc == _abi.GB_OK:
+            return
+        msg = self.fn("last_error")().decode()
+        if rc == _abi.GB_ERR_INVALID_ARGUMENT:
+            raise ValueError(msg)
+        if rc == _abi.GB_ERR_OUT_OF_RANGE:
+            raise IndexError(msg)
+        if rc == _abi.GB_ERR_LOGIC:
+            raise LogicError(msg)
+        if rc == _abi.GB_ERR_RUNTIME:
+            raise RuntimeError(msg)
+        raise DeviceError(msg)
+
+
+def device_backend() -> Backend:
+    return Backend(_abi.lib(), "gb_")
+
+
+class BalGraph:
+    """bal::BalGraph (adapter.hpp:82-100): owns the camera and point arrays
+    (AoS, graph precision) that the solver refines IN PLACE."""
+
+    def __init__(self, problem: BALProblem, precision: str = "fp64", diff_mode: str = "analytic",
+                 huber_delta: Optional[float] = None, device: int = 0, backend: Optional[Backend] = None,
+                 create_arg: Optional[int] = None):
+        if precision not in PRECISIONS:
+            raise ValueError(f"invalid precision pair: {precision}")
+        if diff_mode not in MODES:
+            raise ValueError(f"unknown differentiation mode: {diff_mode}")
+        self.precision = precision
+        self.diff_mode = diff_mode
+        self.backend = backend or device_backend()
+        self.FP, self.SP, self.A = dtypes(precision)
+        self.num_observations = problem.num_observations
+        self.cameras = np.ascontiguousarray(problem.cameras, dtype=self.FP).copy()
+        self.points = np.ascontiguousarray(problem.points, dtype=self.FP).copy()
+        self._cam_idx = np.ascontiguousarray(problem.camera_index, dtype=np.uint32)
+        self._pt_idx = np.ascontiguousarray(problem.point_index, dtype=np.uint32)
+        self._obs = np.ascontiguousarray(problem.observations, dtype=self.FP)
+        h = self.backend.create(PRECISIONS[precision], MODES[diff_mode], device if create_arg is None else create_arg)
+        if not h:
+            self.backend.check(_abi.GB_ERR_NO_DEVICE if self.backend.prefix == "gb_" else _abi.GB_ERR_INVALID_ARGUMENT)
+        self._h = h
+        self._cam_fixed = None
+        self._pt_fixed = None
+        self._levels = None
+        self._loss = (_abi.GB_LOSS_HUBER, float(huber_delta)) if huber_delta is not None else (_abi.GB_LOSS_DEFAULT, 1.0)
+        self._bind()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self.backend.fn("destroy")(h)
+            self._h = None
+
+    def _bind(self):
+        fn = self.backend.fn
+        ptr = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+        self.backend.check(fn("set_cameras")(self._h, self.cameras.ctypes.data, self.cameras.shape[0],
+                                             ptr(self._cam_fixed)))
+        self.backend.check(fn("set_points")(self._h, self.points.ctypes.data, self.points.shape[0],
+                                            ptr(self._pt_fixed)))
+        self.backend.check(fn("set_observations")(self._h, self._cam_idx.shape[0], self._cam_idx.ctypes.data,
+                                                  self._pt_idx.ctypes.data, self._obs.ctypes.data, ptr(self._levels),
+                                                  self._loss[0], self._loss[1]))
+
+    # -- structure edits
+    def set_fixed(self, cameras=None, points=None):
+        """VertexDescriptor::set_fixed for many vertices at once (boolean masks)."""
+        if cameras is not None:
+            self._cam_fixed = np.ascontiguousarray(cameras, dtype=np.uint8)
+        if points is not None:
+            self._pt_fixed = np.ascontiguousarray(points, dtype=np.uint8)
+        self._bind()
+
+    def set_levels(self, levels):
+        """FactorDescriptor::set_level for every factor (uint8 per observation)."""
+        self._levels = np.ascontiguousarray(levels, dtype=np.uint8)
+        self._bind()
+
+    # -- objective
+    def mse(self) -> float:
+        out = ctypes.c_double()
+        self.backend.check(self.backend.fn("mse")(self._h, ctypes.byref(out)))
+        return out.value
+
+    def total_error(self, level: int = 0) -> float:
+        out = ctypes.c_double()
+        self.backend.check(self.backend.fn("total_error")(self._h, level, ctypes.byref(out)))
+        return out.value
+
+    # -- LinearSystem surface (linear_system.hpp:44-216)
+    def ls_linearize(self, level=0, clamp_min=1e-6, clamp_max=1e32, damping="after_scaling"):
+        n = ctypes.c_int64()
+        chi = ctypes.c_double()
+        fin = ctypes.c_int32()
+        # first call sizes N
+        self.backend.check(self.backend.fn("ls_linearize")(self._h, level, clamp_min, clamp_max,
+                                                           1 if damping == "before_scaling" else 0, ctypes.byref(chi),
+                                                           ctypes.byref(n), None, None, None, None, ctypes.byref(fin)))
+        N = n.value
+        b, diag, cl, D = (np.zeros(N, self.FP) for _ in range(4))
+        self.backend.check(self.backend.fn("ls_linearize")(self._h, level, clamp_min, clamp_max,
+                                                           1 if damping == "before_scaling" else 0, ctypes.byref(chi),
+                                                           ctypes.byref(n), b.ctypes.data, diag.ctypes.data,
+                                                           cl.ctypes.data, D.ctypes.data, ctypes.byref(fin)))
+        self._N = N
+        return dict(chi2=chi.value, b=b, diag=diag, clamped=cl, scaling=D, finite=bool(fin.value), n=N)
+
+    def ls_hvp(self, v, lam):
+        v = np.ascontiguousarray(v, dtype=self.SP)
+        out = np.zeros(v.shape[0], self.A)
+        self.backend.check(self.backend.fn("ls_hvp")(self._h, v.ctypes.data, out.ctypes.data, float(lam)))
+        return out
+
+    def ls_preconditioner(self, lam, nfree_cams, nfree_pts):
+        blocks = np.zeros(81 * nfree_cams + 9 * nfree_pts, self.FP)
+        fb = ctypes.c_int32()
+        self.backend.check(self.backend.fn("ls_preconditioner")(self._h, float(lam), blocks.ctypes.data,
+                                                                ctypes.byref(fb)))
+        return blocks, fb.value
+
+    def ls_solve_step(self, lam, pcg: PCGConfig):
+        dx = np.zeros(self._N, self.FP)
+        st = _abi.gb_pcg_stats()
+        pred = ctypes.c_double()
+        fin = ctypes.c_int32()
+        c = pcg.to_c()
+        self.backend.check(self.backend.fn("ls_solve_step")(self._h, float(lam), ctypes.byref(c), dx.ctypes.data,
+                                                            ctypes.byref(st), ctypes.byref(pred), ctypes.byref(fin)))
+        return dx, dict(iterations=st.iterations, final_relative_residual=st.final_relative_residual,
+                        converged=bool(st.converged)), pred.value, bool(fin.value)
+
+    def ls_jacobians(self, n_active):
+        out = np.zeros((n_active, 24), self.SP)
+        self.backend.check(self.backend.fn("ls_jacobians")(self._h, out.ctypes.data))
+        return out
+
+    def incidence(self, which: int):
+        nseg, nit = ctypes.c_uint64(), ctypes.c_uint64()
+        self.backend.check(self.backend.fn("incidence")(self._h, which, ctypes.byref(nseg), ctypes.byref(nit), None,
+                                                        None, None, None))
+        vos = np.zeros(nseg.value, np.uint64)
+        off = np.zeros(nseg.value + 1, np.uint64)
+        itf = np.zeros(nit.value, np.uint32)
+        its = np.zeros(nit.value, np.uint16)
+        self.backend.check(self.backend.fn("incidence")(self._h, which, ctypes.byref(nseg), ctypes.byref(nit),
+                                                        vos.ctypes.data, off.ctypes.data, itf.ctypes.data,
+                                                        its.ctypes.data))
+        return vos, off, itf, its
+
+
+def build_graph(problem: BALProblem, precision: str = "fp64", diff_mode: str = "analytic",
+                huber_delta: Optional[float] = None, device: int = 0) -> BalGraph:
+    """bal::build_graph<FP,SP> (adapter.hpp:106-143) on the B200 device path."""
+    return BalGraph(problem, precision, diff_mode, huber_delta, device)
+
+
+def _report(rep: _abi.gb_solve_report, recs) -> SolveReport:
+    its = []
+    for r in recs[: rep.iterations_run]:
+        its.append(IterationRecord(r.iteration, r.chi2_before, r.chi2_after, r.lambda_, r.pcg_iterations,
+                                   bool(r.pcg_converged), r.pcg_relative_residual, bool(r.low_quality_step),
+                                   r.precond_fallback_blocks, bool(r.accepted), r.wall_seconds))
+    m = rep.memory
+    return SolveReport(its, rep.initial_chi2, rep.final_chi2, rep.accepted_steps,
+                       _abi.TERMINATION_NAMES[rep.termination], rep.total_seconds, rep.free_dims, rep.residual_dims,
+                       rep.active_factors,
+                       dict(jacobian_bytes=m.jacobian_bytes, preconditioner_bytes=m.preconditioner_bytes,
+                            workspace_bytes=m.workspace_bytes, graph_bytes=m.graph_bytes),
+                       rep.setup_seconds, rep.h2d_bytes, rep.d2h_bytes)
+
+
+def levenberg_marquardt(graph: BalGraph, config: Optional[LMConfig] = None) -> SolveReport:
+    """levenberg_marquardt<FP,SP>(Graph&, const LMConfig&) (levenberg_marquardt.hpp:115-224).
+    graph.cameras / graph.points are refined in place."""
+    config = config or LMConfig()
+    c = config.to_c()
+    rep = _abi.gb_solve_report()
+    n = max(1, config.max_iterations)
+    recs = (_abi.gb_iteration_record * n)()
+    graph.backend.check(graph.backend.fn("optimize")(graph._h, ctypes.byref(c), ctypes.byref(rep), recs, n))
+    return _report(rep, recs)

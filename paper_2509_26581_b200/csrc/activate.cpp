@@ -1,0 +1,221 @@
+#include "activate.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+
+namespace gb {
+
+namespace {
+
+// Counting sort of `items` (already in ascending order of the secondary key)
+// by a dense primary key: a stable CSR build.
+void stable_bucket(const std::vector<uint32_t>& key, uint64_t nkeys, const std::vector<uint32_t>& items,
+                   std::vector<uint64_t>& off, std::vector<uint32_t>& sorted) {
+  off.assign(nkeys + 1, 0);
+  for (uint32_t it : items) ++off[key[it] + 1];
+  for (uint64_t k = 0; k < nkeys; ++k) off[k + 1] += off[k];
+  std::vector<uint64_t> cur(off.begin(), off.end() - 1);
+  sorted.resize(items.size());
+  for (uint32_t it : items) sorted[cur[key[it]]++] = it;
+}
+
+// FactorDescriptor::build_incidence (factor_descriptor.hpp:710-753) for one
+// slot: segments over free vertices with >= 1 active factor, ascending vertex;
+// items in ascending active-factor order.
+void build_incidence(uint64_t nvert, const std::vector<uint32_t>& vert_of_a, const uint8_t* fixed,
+                     Incidence& inc) {
+  const uint64_t na = vert_of_a.size();
+  std::vector<uint64_t> counts(nvert, 0);
+  for (uint64_t a = 0; a < na; ++a) {
+    const uint32_t v = vert_of_a[a];
+    if (!(fixed && fixed[v])) ++counts[v];
+  }
+  inc.vertex_of_segment.clear();
+  std::vector<uint64_t> seg_of(nvert, UINT64_MAX);
+  for (uint64_t v = 0; v < nvert; ++v)
+    if (counts[v]) {
+      seg_of[v] = inc.vertex_of_segment.size();
+      inc.vertex_of_segment.push_back(v);
+    }
+  inc.offsets.assign(inc.vertex_of_segment.size() + 1, 0);
+  for (uint64_t s = 0; s < inc.vertex_of_segment.size(); ++s)
+    inc.offsets[s + 1] = inc.offsets[s] + counts[inc.vertex_of_segment[s]];
+  inc.items.resize(inc.offsets.back());
+  std::vector<uint64_t> cur(inc.offsets.begin(), inc.offsets.end() - 1);
+  for (uint64_t a = 0; a < na; ++a) {
+    const uint32_t v = vert_of_a[a];
+    if (fixed && fixed[v]) continue;
+    inc.items[cur[seg_of[v]]++] = static_cast<uint32_t>(a);
+  }
+}
+
+}  // namespace
+
+void activate(const ActivationInput& in, Activation& out) {
+  out = Activation();
+  out.nc = in.nc;
+  out.np = in.np;
+  out.level = in.active_level;
+  for (uint64_t i = 0; i < in.ne; ++i) {
+    if (in.cam[i] >= in.nc)
+      throw std::invalid_argument("add_factor: slot 0 references unknown vertex id " + std::to_string(in.cam[i]));
+    if (in.pt[i] >= in.np)
+      throw std::invalid_argument("add_factor: slot 1 references unknown vertex id " + std::to_string(in.pt[i]));
+  }
+
+  // active list (factor_descriptor.hpp:255-257)
+  out.active.reserve(in.ne);
+  for (uint64_t i = 0; i < in.ne; ++i)
+    if (!in.level || static_cast<int>(in.level[i]) <= in.active_level) out.active.push_back(static_cast<uint32_t>(i));
+  const uint64_t na = out.n_active = out.active.size();
+
+  // columns (vertex_descriptor.hpp:115-126, graph.hpp:70-71): cameras then points
+  int64_t next = 0;
+  out.cam_col.assign(in.nc, -1);
+  for (uint64_t c = 0; c < in.nc; ++c)
+    if (!(in.cam_fixed && in.cam_fixed[c])) {
+      out.cam_col[c] = next;
+      next += 9;
+      ++out.free_cams;
+    }
+  out.pt_col.assign(in.np, -1);
+  for (uint64_t p = 0; p < in.np; ++p)
+    if (!(in.pt_fixed && in.pt_fixed[p])) {
+      out.pt_col[p] = next;
+      next += 3;
+      ++out.free_pts;
+    }
+  out.free_dims = next;
+
+  std::vector<uint32_t> cam_of_a(na), pt_of_a(na);
+  for (uint64_t a = 0; a < na; ++a) {
+    cam_of_a[a] = in.cam[out.active[a]];
+    pt_of_a[a] = in.pt[out.active[a]];
+  }
+  build_incidence(in.nc, cam_of_a, in.cam_fixed, out.cam_inc);
+  build_incidence(in.np, pt_of_a, in.pt_fixed, out.pt_inc);
+
+  // internal point order: stable bucket of points by their smallest active
+  // camera (points sharing camera sets become neighbours -> tiles touch few
+  // cameras); points without active edges go last.
+  std::vector<uint32_t> key(in.np, kNoKey);
+  std::vector<uint32_t> deg(in.np, 0);
+  for (uint64_t a = 0; a < na; ++a) {
+    const uint32_t p = pt_of_a[a];
+    key[p] = std::min(key[p], cam_of_a[a]);
+    ++deg[p];
+  }
+  {
+    std::vector<uint32_t> k2(in.np), ids(in.np);
+    for (uint64_t p = 0; p < in.np; ++p) {
+      k2[p] = key[p] == kNoKey ? static_cast<uint32_t>(in.nc) : key[p];
+      ids[p] = static_cast<uint32_t>(p);
+    }
+    std::vector<uint64_t> off;
+    stable_bucket(k2, in.nc + 1, ids, off, out.pt_order);
+  }
+  out.pt_rank.assign(in.np, 0);
+  for (uint64_t i = 0; i < in.np; ++i) out.pt_rank[out.pt_order[i]] = static_cast<uint32_t>(i);
+
+  // tiles: greedy over internal points, <= kTileEdges edges and <= kTilePoints
+  // points; a point with more than kTileEdges edges is a tile of its own
+  // ("heavy" tile, processed chunk by chunk).
+  std::vector<uint32_t> tile_of_pt(in.np);
+  out.tile_pbeg.push_back(0);
+  out.tile_ebeg.push_back(0);
+  {
+    uint64_t te = 0, tp = 0, ecount = 0;
+    for (uint64_t i = 0; i < in.np; ++i) {
+      const uint64_t d = deg[out.pt_order[i]];
+      const bool heavy = d > static_cast<uint64_t>(kTileEdges);
+      if (tp > 0 && (heavy || te + d > static_cast<uint64_t>(kTileEdges) || tp >= static_cast<uint64_t>(kTilePoints))) {
+        out.tile_pbeg.push_back(static_cast<uint32_t>(i));
+        out.tile_ebeg.push_back(static_cast<uint32_t>(ecount));
+        te = tp = 0;
+      }
+      tile_of_pt[i] = static_cast<uint32_t>(out.tile_pbeg.size() - 1);
+      te += d;
+      tp += 1;
+      ecount += d;
+      if (heavy) {  // close the heavy tile immediately
+        out.tile_pbeg.push_back(static_cast<uint32_t>(i + 1));
+        out.tile_ebeg.push_back(static_cast<uint32_t>(ecount));
+        te = tp = 0;
+      }
+    }
+    if (tp > 0 || out.tile_pbeg.size() == 1) {
+      out.tile_pbeg.push_back(static_cast<uint32_t>(in.np));
+      out.tile_ebeg.push_back(static_cast<uint32_t>(ecount));
+    }
+  }
+  out.ntiles = static_cast<uint32_t>(out.tile_pbeg.size() - 1);
+
+  // device edge order: active edges sorted by camera (stable in a), then
+  // stably bucketed by tile -> inside a tile: (camera, a).
+  {
+    std::vector<uint32_t> all(na);
+    for (uint64_t a = 0; a < na; ++a) all[a] = static_cast<uint32_t>(a);
+    std::vector<uint64_t> off;
+    std::vector<uint32_t> by_cam;
+    stable_bucket(cam_of_a, in.nc, all, off, by_cam);
+    std::vector<uint32_t> tile_of_a(na);
+    for (uint64_t a = 0; a < na; ++a) tile_of_a[a] = tile_of_pt[out.pt_rank[pt_of_a[a]]];
+    stable_bucket(tile_of_a, out.ntiles, by_cam, off, out.d_a);
+  }
+  out.d_cam.resize(na);
+  out.d_lpt.resize(na);
+  for (uint64_t d = 0; d < na; ++d) {
+    const uint32_t a = out.d_a[d];
+    const uint32_t r = out.pt_rank[pt_of_a[a]];
+    out.d_cam[d] = cam_of_a[a];
+    out.d_lpt[d] = static_cast<uint16_t>(r - out.tile_pbeg[tile_of_pt[r]]);
+  }
+
+  // per-point slot lists (tile-local, ascending)
+  out.pt_slot_off.assign(in.np + 1, 0);
+  for (uint64_t i = 0; i < in.np; ++i) out.pt_slot_off[i + 1] = out.pt_slot_off[i] + deg[out.pt_order[i]];
+  out.pt_slots.resize(na);
+  {
+    std::vector<uint32_t> cur(out.pt_slot_off.begin(), out.pt_slot_off.end() - 1);
+    for (uint32_t t = 0; t < out.ntiles; ++t)
+      for (uint32_t d = out.tile_ebeg[t]; d < out.tile_ebeg[t + 1]; ++d) {
+        const uint32_t r = out.tile_pbeg[t] + out.d_lpt[d];
+        out.pt_slots[cur[r]++] = static_cast<uint16_t>((d - out.tile_ebeg[t]) & 0xffffu);
+      }
+  }
+
+  // warp chunks and camera runs
+  out.tile_chunk_base.assign(out.ntiles + 1, 0);
+  for (uint32_t t = 0; t < out.ntiles; ++t) {
+    const uint32_t ne_t = out.tile_ebeg[t + 1] - out.tile_ebeg[t];
+    out.tile_chunk_base[t + 1] = out.tile_chunk_base[t] + (ne_t + 31) / 32;
+  }
+  out.nchunks = out.tile_chunk_base[out.ntiles];
+  out.chunk_part_base.assign(out.nchunks + 1, 0);
+  std::vector<uint32_t> run_cam;
+  for (uint32_t t = 0; t < out.ntiles; ++t) {
+    const uint32_t eb = out.tile_ebeg[t], ee = out.tile_ebeg[t + 1];
+    for (uint32_t k = 0; k < (ee - eb + 31) / 32; ++k) {
+      const uint32_t ch = out.tile_chunk_base[t] + k;
+      uint32_t runs = 0;
+      for (uint32_t d = eb + 32 * k; d < std::min(ee, eb + 32 * k + 32); ++d)
+        if (d == eb + 32 * k || out.d_cam[d] != out.d_cam[d - 1]) {
+          ++runs;
+          run_cam.push_back(out.d_cam[d]);
+        }
+      out.chunk_part_base[ch + 1] = out.chunk_part_base[ch] + runs;
+    }
+  }
+  out.nparts = out.chunk_part_base[out.nchunks];
+  {
+    std::vector<uint32_t> slots(out.nparts);
+    for (uint32_t s = 0; s < out.nparts; ++s) slots[s] = s;
+    std::vector<uint64_t> off;
+    stable_bucket(run_cam, in.nc, slots, off, out.cam_part_idx);
+    out.cam_part_off.assign(in.nc + 1, 0);
+    for (uint64_t c = 0; c <= in.nc; ++c) out.cam_part_off[c] = static_cast<uint32_t>(off[c]);
+  }
+}
+
+}  // namespace gb

@@ -1,0 +1,68 @@
+// Graph activation: everything the device needs that depends only on the
+// graph structure (not on parameter values). Reference counterparts:
+//   Graph::activate                  graph.hpp:59-83
+//   VertexDescriptor::assign_columns vertex_descriptor.hpp:115-126
+//   FactorDescriptor::activate       factor_descriptor.hpp:254-270
+//   FactorDescriptor::build_incidence factor_descriptor.hpp:710-753
+// The reference incidence CSRs are reproduced exactly (they are the
+// bit-exact parity target) and then turned into the device layout described
+// in DESIGN.md §Data layout: point tiles, camera-sorted edges inside each
+// tile, warp-chunk camera runs and the camera -> partial-slot CSR.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace gb {
+
+constexpr int kTileThreads = 256;  // CTA size of every tile kernel
+constexpr int kTileEdges = 512;    // max edges of a normal tile (SMEM staging)
+constexpr int kTilePoints = 256;   // max points of a tile
+constexpr uint32_t kNoKey = 0xffffffffu;
+
+struct Incidence {
+  std::vector<uint64_t> vertex_of_segment;
+  std::vector<uint64_t> offsets;
+  std::vector<uint32_t> items;  // active factor index a; slot is implied (0 cams, 1 points)
+};
+
+struct ActivationInput {
+  uint64_t nc = 0, np = 0, ne = 0;
+  const uint32_t* cam = nullptr;
+  const uint32_t* pt = nullptr;
+  const uint8_t* level = nullptr;      // may be null (all 0)
+  const uint8_t* cam_fixed = nullptr;  // may be null
+  const uint8_t* pt_fixed = nullptr;   // may be null
+  int active_level = 0;
+};
+
+struct Activation {
+  uint64_t nc = 0, np = 0, n_active = 0;
+  int level = 0;
+  std::vector<uint32_t> active;  // active factor a -> entry index (factor_descriptor.hpp:255-257)
+  // reference column layout (free cameras first, then free points, insertion order)
+  int64_t free_cams = 0, free_pts = 0, free_dims = 0;
+  std::vector<int64_t> cam_col, pt_col;  // -1 when fixed (kFixedColumn)
+  Incidence cam_inc, pt_inc;
+  // internal point order: points sorted by (min active camera, id)
+  std::vector<uint32_t> pt_order;  // internal i -> point id
+  std::vector<uint32_t> pt_rank;   // point id -> internal i
+  // tiles over internal points
+  uint32_t ntiles = 0, nchunks = 0, nparts = 0;
+  std::vector<uint32_t> tile_ebeg, tile_pbeg, tile_chunk_base;  // size ntiles+1
+  // device edge order d (tile-major, camera then factor index inside a tile)
+  std::vector<uint32_t> d_a;    // d -> active factor a
+  std::vector<uint32_t> d_cam;  // d -> camera
+  std::vector<uint16_t> d_lpt;  // d -> point index local to its tile
+  std::vector<uint32_t> pt_slot_off;  // internal point -> offsets into pt_slots (size np+1)
+  std::vector<uint16_t> pt_slots;     // tile-local edge slots of each point, ascending
+  // warp-chunk camera runs -> partial slots
+  std::vector<uint32_t> chunk_part_base;  // size nchunks+1
+  std::vector<uint32_t> cam_part_off;     // size nc+1
+  std::vector<uint32_t> cam_part_idx;     // partial slots of each camera, ascending
+};
+
+// Throws std::invalid_argument on out-of-range indices.
+void activate(const ActivationInput& in, Activation& out);
+
+}  // namespace gb

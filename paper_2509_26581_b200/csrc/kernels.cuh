@@ -1,0 +1,1076 @@
+// Device kernels of the LM inner loop. See DESIGN.md for the data layout and
+// the roofline of each kernel. Reference semantics are cited per kernel.
+//
+// Layout recap (all device-resident for the whole solve):
+//   columns   internal layout: camera c at [9c, 9c+9) (insertion order),
+//             point i (internal order) at [9nc + 3i, 9nc + 3i + 3). Fixed
+//             vertices keep their columns but every vector is 0 there, so
+//             dot products and norms equal the reference's free-only ones.
+//   edges     "device order" d: point tiles (<= kTileEdges edges, <=
+//             kTilePoints points), inside a tile sorted by (camera, factor).
+//             SoA: cam[d], lpt[d], obs[2][d], J[24][d] (SP, row-major Jc|Jp).
+//   cameras   per-warp-chunk camera runs are reduced with shuffles and
+//             written to partial slots; a camera kernel sums its slots in
+//             slot order (deterministic, no float atomics).
+//   points    per-edge point contributions are staged in shared memory and
+//             summed per point in slot order inside the tile.
+#pragma once
+
+#include "activate.hpp"
+#include "common.cuh"
+#include "gb_bal.h"
+#include "snavely.cuh"
+
+namespace gb {
+
+// packed upper-triangular (row-major, i <= j) index helpers; always called
+// with compile-time arguments inside unrolled loops so register arrays stay
+// in registers.
+__host__ __device__ constexpr int p9row(int q) {
+  int i = 0;
+  while (q >= 9 - i) {
+    q -= 9 - i;
+    ++i;
+  }
+  return i;
+}
+__host__ __device__ constexpr int p9col(int q) {
+  int i = 0;
+  while (q >= 9 - i) {
+    q -= 9 - i;
+    ++i;
+  }
+  return i + q;
+}
+// std::clamp semantics (NaN passes through), linear_system.hpp:75
+template <typename T>
+__host__ __device__ inline T clampv(T v, T lo, T hi) {
+  return v < lo ? lo : (hi < v ? hi : v);
+}
+__host__ __device__ constexpr int p9(int i, int j) { return i <= j ? i * 9 - i * (i - 1) / 2 + (j - i) : j * 9 - j * (j - 1) / 2 + (i - j); }
+__host__ __device__ constexpr int p3(int i, int j) { return i <= j ? i * 3 - i * (i - 1) / 2 + (j - i) : j * 3 - j * (j - 1) / 2 + (i - j); }
+
+constexpr int kLinVals = 54;  // per camera run at linearize: b (9) + upper H (45)
+constexpr int kCamWarps = 8;  // warps per block in camera kernels
+
+// Device-resident solver state (one per handle). Scalars are FP like the
+// reference's locals (levenberg_marquardt.hpp:145-147, pcg.hpp:303-330).
+template <typename FP>
+struct State {
+  // configuration
+  double tol, grad_tol, lambda_max, tau, pcg_tol, pcg_ratio;
+  double clamp_min, clamp_max;
+  int max_iterations, pcg_max_it, normalize_rhs, before_scaling, use_guard, refresh_on_reject;
+  // PCG
+  FP rho, pap, alpha, beta, rhs_norm, scale, unscale, ref_norm;
+  double pcg_relres;
+  int pcg_it, pcg_done, pcg_conv, pcg_zero;
+  // step / candidate
+  FP pred, chi2_new;
+  int step_finite;
+  // LM
+  FP chi2, lambda, nu, lambda_solve, rel_decrease;
+  int lm_it, terminated, termination, iter_active, accepted, do_linearize, accepted_steps, fallbacks;
+  // linearization
+  FP lin_chi2, grad_max;
+  int lin_finite;
+  // last-block counters, one per kernel that uses them
+  unsigned cnt[16];
+};
+
+template <typename FP, typename SP>
+struct Dev {
+  using A = arith_t<SP>;
+  uint32_t nc, np, na, ntiles, nparts;
+  uint64_t ncols;  // 9nc + 3np
+  FP* x;
+  FP* x_new;
+  const uint8_t* col_free;  // ncols
+  const uint32_t* d_cam;
+  const uint16_t* d_lpt;
+  const FP* d_obs;  // [2][na]
+  SP* J;            // [24][na] or null (dynamic)
+  FP* w;            // [na] or null (default loss: w == 1)
+  const uint32_t* tile_ebeg;
+  const uint32_t* tile_pbeg;
+  const uint32_t* tile_chunk_base;
+  const uint32_t* chunk_part_base;
+  const uint32_t* pt_slot_off;
+  const uint16_t* pt_slots;
+  const uint32_t* cam_part_off;
+  const uint32_t* cam_part_idx;
+  FP* part;  // [nparts][54]
+  FP* b;
+  FP* clamped;
+  FP* D;
+  FP* Hc;  // [nc][45]
+  FP* Hp;  // [np][6]
+  FP* Mc;  // [nc][45]
+  FP* Mp;  // [np][6]
+  SP* xs;
+  SP* r;
+  SP* z;
+  SP* p;
+  SP* ap;
+  A* dbg_out;  // optional wide HVP output (LinearSystem::hvp surface)
+  FP* dx;
+  FP* tile_red;   // [ntiles]
+  FP* tile_red2;  // [ntiles]
+  int* tile_flag; // [ntiles]
+  FP* cam_red;    // [nc]
+  FP* cam_red2;   // [nc]
+  int* cam_flag;  // [nc]
+  FP* blk_red;    // [nblk]
+  FP* blk_red2;   // [nblk]
+  int* blk_flag;  // [nblk]
+  State<FP>* st;
+  gb_iteration_record* recs;
+  int loss_kind;
+  FP huber;
+};
+
+// ------------------------------------------------------------------ helpers
+
+// Warp-segmented suffix reduction over runs of equal camera inside a warp
+// chunk: afterwards the head lane of each run holds the run total. Fixed
+// association order (deterministic). run_end: last lane of this lane's run.
+template <typename T, int K>
+__device__ inline void seg_reduce(T (&v)[K], int lane, int run_end) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const T t = __shfl_down_sync(0xffffffffu, v[k], o);
+      if (lane + o <= run_end) v[k] += t;
+    }
+  }
+}
+
+struct RunInfo {
+  bool head;
+  int run_end;
+  uint32_t slot;
+};
+
+__device__ inline RunInfo run_info(uint32_t cam, bool valid, uint32_t chunk_slot_base) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, cam, 1);
+  const bool head = valid && (lane == 0 || cam != prev);
+  const unsigned hm = __ballot_sync(0xffffffffu, head);
+  const unsigned vm = __ballot_sync(0xffffffffu, valid);
+  const unsigned later = lane == 31 ? 0u : (hm & (0xffffffffu << (lane + 1)));
+  RunInfo ri;
+  ri.head = head;
+  ri.run_end = later ? (__ffs(later) - 2) : (vm ? 31 - __clz(vm) : -1);
+  ri.slot = chunk_slot_base + __popc(hm & ((1u << lane) - 1u));
+  return ri;
+}
+
+template <typename FP, typename SP>
+__device__ inline void load_J(const Dev<FP, SP>& d, uint32_t e, arith_t<SP>* jc, arith_t<SP>* jp) {
+  using A = arith_t<SP>;
+  const SP* J = d.J;
+  const uint64_t na = d.na;
+#pragma unroll
+  for (int k = 0; k < 18; ++k) jc[k] = widen<A>(J[k * na + e]);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) jp[k] = widen<A>(J[(18 + k) * na + e]);
+}
+
+// =====================================================================
+// Linearize (FactorDescriptor::linearize factor_descriptor.hpp:272-292,
+// accumulate_gradient_and_diagonal :322-370 and the unscaled half of
+// accumulate_precond_blocks :435-482; LinearSystem::linearize
+// linear_system.hpp:67-82). One CTA per tile: Snavely residual + both
+// Jacobian blocks from one chain per edge, J narrowed to SP and stored SoA,
+// camera b/H via warp-segmented runs -> partial slots, point b/H summed in
+// shared memory. Point epilogue: clamp, D = 1/sqrt(clamped), finiteness,
+// max |b|.
+// =====================================================================
+template <typename FP, typename SP, bool STORE>
+__global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, int force) {
+  if (!force && !d.st->do_linearize) return;
+  const uint32_t t = blockIdx.x;
+  const uint32_t eb = d.tile_ebeg[t], ee = d.tile_ebeg[t + 1];
+  const uint32_t pb = d.tile_pbeg[t], pe = d.tile_pbeg[t + 1];
+  const uint32_t ne_t = ee - eb, npt = pe - pb;
+  const bool heavy = ne_t > static_cast<uint32_t>(kTileEdges);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint64_t pcol0 = 9ull * d.nc;
+
+  __shared__ FP sX[kTilePoints * 3];
+  __shared__ FP stage[kTileEdges * 9];
+  __shared__ FP hacc[9];
+  __shared__ FP scratch[32];
+
+  for (uint32_t i = tid; i < npt * 3; i += blockDim.x) sX[i] = d.x[pcol0 + 3ull * pb + i];
+  if (tid < 9) hacc[tid] = FP(0);
+  __syncthreads();
+
+  const int loss = d.loss_kind;
+  const FP delta = d.huber;
+  FP chi = FP(0);
+  for (uint32_t c0 = 0; c0 < ne_t; c0 += kTileThreads) {
+    const uint32_t j = c0 + tid;
+    const bool valid = j < ne_t;
+    const uint32_t e = eb + (valid ? j : 0);
+    const uint32_t cam = d.d_cam[e];
+    const uint32_t lp = d.d_lpt[e];
+    FP cp[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) cp[k] = d.x[9ull * cam + k];
+    const FP* X = &sX[3 * lp];
+    FP res[2];
+    snavely_residual<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res);
+    const FP s = res[0] * res[0] + res[1] * res[1];
+    const FP w = valid ? loss_weight<FP>(loss, delta, s) : FP(0);
+    if (valid) chi += loss_value<FP>(loss, delta, s);
+    FP jc[18], jp[6];
+    snavely_jacobians<FP>(cp, X, jc, jp);
+    if (STORE) {
+#pragma unroll
+      for (int k = 0; k < 18; ++k) {
+        const SP v = narrow<SP>(jc[k]);
+        if (valid) d.J[k * static_cast<uint64_t>(d.na) + e] = v;
+        jc[k] = widen<FP>(v);
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const SP v = narrow<SP>(jp[k]);
+        if (valid) d.J[(18 + k) * static_cast<uint64_t>(d.na) + e] = v;
+        jp[k] = widen<FP>(v);
+      }
+    }
+    if (d.w && valid) d.w[e] = w;
+    const FP wr0 = w * res[0], wr1 = w * res[1];
+    if (!valid) {
+#pragma unroll
+      for (int k = 0; k < 18; ++k) jc[k] = FP(0);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) jp[k] = FP(0);
+    }
+    // camera side: 6 groups of 9 values (b, then packed upper H)
+    const uint32_t chunk = d.tile_chunk_base[t] + (c0 + (tid & ~31)) / 32;
+    const RunInfo ri = run_info(cam, valid, d.chunk_part_base[chunk]);
+#pragma unroll
+    for (int g = 0; g < 6; ++g) {
+      FP v[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const int idx = 9 * g + k;
+        if (idx < 9) {
+          v[k] = jc[k] * (valid ? wr0 : FP(0)) + jc[9 + k] * (valid ? wr1 : FP(0));
+        } else {
+          const int q = idx - 9;
+          const int a = p9row(q), bb = p9col(q);
+          v[k] = w * (jc[a] * jc[bb] + jc[9 + a] * jc[9 + bb]);
+        }
+      }
+      seg_reduce<FP, 9>(v, lane, ri.run_end);
+      if (ri.head) {
+        FP* dst = d.part + static_cast<uint64_t>(ri.slot) * kLinVals + 9 * g;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) dst[k] = v[k];
+      }
+    }
+    // point side: b (3) + packed H (6)
+    FP pv[9];
+    pv[0] = jp[0] * wr0 + jp[3] * wr1;
+    pv[1] = jp[1] * wr0 + jp[4] * wr1;
+    pv[2] = jp[2] * wr0 + jp[5] * wr1;
+    pv[3] = w * (jp[0] * jp[0] + jp[3] * jp[3]);
+    pv[4] = w * (jp[0] * jp[1] + jp[3] * jp[4]);
+    pv[5] = w * (jp[0] * jp[2] + jp[3] * jp[5]);
+    pv[6] = w * (jp[1] * jp[1] + jp[4] * jp[4]);
+    pv[7] = w * (jp[1] * jp[2] + jp[4] * jp[5]);
+    pv[8] = w * (jp[2] * jp[2] + jp[5] * jp[5]);
+    if (!heavy) {
+      if (valid)
+#pragma unroll
+        for (int k = 0; k < 9; ++k) stage[j * 9 + k] = pv[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) stage[tid * 9 + k] = valid ? pv[k] : FP(0);
+      __syncthreads();
+      if (tid < 9) {
+        FP acc = hacc[tid];
+        const uint32_t nvalid = min(static_cast<uint32_t>(kTileThreads), ne_t - c0);
+        for (uint32_t q = 0; q < nvalid; ++q) acc += stage[q * 9 + tid];
+        hacc[tid] = acc;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+
+  // point epilogue
+  FP gmax = FP(0);
+  int fin = 1;
+  for (uint32_t i = tid; i < npt; i += blockDim.x) {
+    FP acc[9];
+    if (heavy) {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] = hacc[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] = FP(0);
+      for (uint32_t q = d.pt_slot_off[pb + i]; q < d.pt_slot_off[pb + i + 1]; ++q) {
+        const uint32_t sl = d.pt_slots[q];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc[k] += stage[sl * 9 + k];
+      }
+    }
+    const uint64_t col = pcol0 + 3ull * (pb + i);
+    const bool freev = d.col_free[col];
+    const uint64_t pidx = static_cast<uint64_t>(pb + i);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const FP bk = freev ? acc[k] : FP(0);
+      d.b[col + k] = bk;
+      const FP diag = freev ? acc[3 + p3(k, k)] : FP(0);
+      const FP cl = clampv(diag, FP(d.st->clamp_min), FP(d.st->clamp_max));
+      d.clamped[col + k] = freev ? cl : FP(0);
+      d.D[col + k] = freev ? FP(1) / sqrt(cl) : FP(0);
+      if (freev) {
+        fin &= (is_finite(bk) && is_finite(diag)) ? 1 : 0;
+        gmax = fmax(gmax, fabs(bk));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) d.Hp[6 * pidx + k] = freev ? acc[3 + k] : FP(0);
+  }
+  const FP tchi = block_sum(chi, scratch);
+  const FP tmax = block_max(gmax, scratch);
+  const int tfin = __syncthreads_and(fin);
+  if (tid == 0) {
+    d.tile_red[t] = tchi;
+    d.tile_red2[t] = tmax;
+    d.tile_flag[t] = tfin;
+  }
+}
+
+// Camera side of the linearization: sum each camera's partial slots (slot
+// order), write b_c, packed H_c, clamped diagonal and D; the last block
+// finalizes chi^2, finiteness and max |b| (linear_system.hpp:67-90).
+template <typename FP, typename SP>
+__global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int force) {
+  if (!force && !d.st->do_linearize) return;
+  __shared__ FP scratch[32];
+  const int lane = threadIdx.x & 31;
+  const uint32_t c = blockIdx.x * kCamWarps + (threadIdx.x >> 5);
+  if (c < d.nc) {
+    FP a0 = FP(0), a1 = FP(0);
+    for (uint32_t q = d.cam_part_off[c]; q < d.cam_part_off[c + 1]; ++q) {
+      const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * kLinVals;
+      a0 += src[lane];
+      if (lane < kLinVals - 32) a1 += src[32 + lane];
+    }
+    const bool freev = d.col_free[9ull * c];
+    // value v lives in lane v (a0) or lane v-32 (a1)
+    if (lane < 9) d.b[9ull * c + lane] = freev ? a0 : FP(0);
+    if (lane >= 9) d.Hc[45ull * c + (lane - 9)] = freev ? a0 : FP(0);
+    if (lane < kLinVals - 32) d.Hc[45ull * c + (lane + 32 - 9)] = freev ? a1 : FP(0);
+    // diagonal H(k,k) sits at value 9 + p9(k,k)
+    const int k = lane < 9 ? lane : 0;
+    const int v = 9 + p9(k, k);
+    const FP from0 = __shfl_sync(0xffffffffu, a0, v & 31);
+    const FP from1 = __shfl_sync(0xffffffffu, a1, v & 31);
+    const FP diag = v < 32 ? from0 : from1;
+    FP gm = FP(0);
+    int fin = 1;
+    if (lane < 9) {
+      const FP cl = clampv(diag, FP(d.st->clamp_min), FP(d.st->clamp_max));
+      d.clamped[9ull * c + lane] = freev ? cl : FP(0);
+      d.D[9ull * c + lane] = freev ? FP(1) / sqrt(cl) : FP(0);
+      if (freev) {
+        fin = (is_finite(a0) && is_finite(diag)) ? 1 : 0;
+        gm = fabs(a0);
+      }
+    }
+    gm = warp_max(gm);
+    fin = __all_sync(0xffffffffu, fin);
+    if (lane == 0) {
+      d.cam_red2[c] = gm;
+      d.cam_flag[c] = fin;
+    }
+  }
+  if (last_block(&d.st->cnt[0])) {
+    const FP chi = reduce_partials(d.tile_red, d.ntiles, scratch);
+    const FP m1 = reduce_partials_max(d.tile_red2, d.ntiles, scratch);
+    const FP m2 = reduce_partials_max(d.cam_red2, d.nc, scratch);
+    int f = 1;
+    for (uint32_t i = threadIdx.x; i < d.ntiles; i += blockDim.x) f &= static_cast<const volatile int*>(d.tile_flag)[i];
+    for (uint32_t i = threadIdx.x; i < d.nc; i += blockDim.x) f &= static_cast<const volatile int*>(d.cam_flag)[i];
+    f = __syncthreads_and(f);
+    if (threadIdx.x == 0) {
+      d.st->lin_chi2 = chi;
+      d.st->grad_max = fmax(fmax(m1, m2), FP(0));
+      d.st->lin_finite = (f && is_finite(chi)) ? 1 : 0;
+    }
+  }
+}
+
+// lambda0 = tau * max over free columns of D^2 * clamped (linear_system.hpp:94-99)
+template <typename FP, typename SP>
+__global__ void k_init_damping(Dev<FP, SP> d) {
+  __shared__ FP scratch[32];
+  FP m = FP(0);
+  bool any = false;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    if (d.col_free[i]) {
+      any = true;
+      m = fmax(m, d.D[i] * d.D[i] * d.clamped[i]);
+    }
+  m = block_max(m, scratch);
+  const int anyb = __syncthreads_or(any);
+  if (threadIdx.x == 0) {
+    d.blk_red[blockIdx.x] = m;
+    d.blk_flag[blockIdx.x] = anyb;
+  }
+  if (last_block(&d.st->cnt[1])) {
+    const FP mm = reduce_partials_max(d.blk_red, gridDim.x, scratch);
+    int a = 0;
+    for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) a |= static_cast<const volatile int*>(d.blk_flag)[i];
+    a = __syncthreads_or(a);
+    if (threadIdx.x == 0) {
+      const FP tau = static_cast<FP>(d.st->tau);
+      d.st->lambda = a ? tau * fmax(mm, FP(0)) : tau;
+      d.st->nu = FP(2);
+    }
+  }
+}
+
+// =====================================================================
+// LM iteration prologue (levenberg_marquardt.hpp:149-169): one thread.
+// =====================================================================
+template <typename FP>
+__global__ void k_iter_begin(State<FP>* st, gb_iteration_record* recs) {
+  if (st->terminated) {
+    st->iter_active = 0;
+    return;
+  }
+  const int it = ++st->lm_it;
+  gb_iteration_record& rec = recs[it - 1];
+  rec = gb_iteration_record{};
+  rec.iteration = it;
+  rec.chi2_before = static_cast<double>(st->chi2);
+  rec.lambda = static_cast<double>(st->lambda);
+  st->iter_active = 0;
+  st->accepted = 0;
+  st->do_linearize = 0;
+  if (!st->lin_finite) {
+    rec.chi2_after = rec.chi2_before;
+    st->termination = GB_TERM_NON_FINITE_LINEARIZATION;
+    st->terminated = 1;
+    return;
+  }
+  if (st->grad_max < static_cast<FP>(st->grad_tol)) {
+    rec.chi2_after = rec.chi2_before;
+    st->termination = GB_TERM_GRADIENT_SMALL;
+    st->terminated = 1;
+    return;
+  }
+  st->iter_active = 1;
+  st->lambda_solve = st->lambda;
+  st->pcg_done = 0;
+  st->pcg_it = 0;
+  st->pcg_conv = 0;
+  st->pcg_zero = 0;
+  st->pcg_relres = 0.0;
+  st->fallbacks = 0;
+}
+
+// =====================================================================
+// Block-Jacobi preconditioner (LinearSystem::build_preconditioner,
+// linear_system.hpp:120-160): B = D H D + damp, lower Cholesky (LLT), inverse
+// L^-T L^-1 stored packed; non-SPD or non-finite inverse -> clamped diagonal
+// inverse fallback (counted). One thread per vertex (cameras, then points).
+// =====================================================================
+template <typename FP, int N>
+__device__ inline bool chol_inverse(FP (&B)[N * (N + 1) / 2], FP* out_packed) {
+  // B: packed upper row-major == packed lower column-major; L stored in place
+  // as lower row-major packed: L(i,j) (j<=i) at i*(i+1)/2 + j.
+  FP L[N * (N + 1) / 2];
+  auto up = [](int i, int j) { return i * N - i * (i - 1) / 2 + (j - i); };  // i <= j
+  auto lo = [](int i, int j) { return i * (i + 1) / 2 + j; };                // j <= i
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    FP x = B[up(k, k)];
+#pragma unroll
+    for (int j = 0; j < k; ++j) x -= L[lo(k, j)] * L[lo(k, j)];
+    if (!(x > FP(0)) && !(x != x)) return false;  // Eigen fails on x <= 0; NaN propagates
+    x = sqrt(x);
+    L[lo(k, k)] = x;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      FP v = B[up(k, i)];
+#pragma unroll
+      for (int j = 0; j < k; ++j) v -= L[lo(i, j)] * L[lo(k, j)];
+      L[lo(i, k)] = v / x;
+    }
+  }
+  // Linv (lower) in place: forward substitution on the identity
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const FP dii = FP(1) / L[lo(i, i)];
+#pragma unroll
+    for (int j = 0; j < i; ++j) {
+      FP v = FP(0);
+#pragma unroll
+      for (int k = j; k < i; ++k) v -= L[lo(i, k)] * L[lo(k, j)];
+      L[lo(i, j)] = v * dii;
+    }
+    L[lo(i, i)] = dii;
+  }
+  // inv = Linv^T Linv, upper packed
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = i; j < N; ++j) {
+      FP v = FP(0);
+#pragma unroll
+      for (int k = j; k < N; ++k) v += L[lo(k, i)] * L[lo(k, j)];
+      out_packed[up(i, j)] = v;
+      ok = ok && is_finite(v);
+    }
+  return ok;
+}
+
+template <typename FP, typename SP, int N>
+__device__ inline void precond_vertex(const Dev<FP, SP>& d, const FP* H, FP* M, uint64_t col, bool freev) {
+  constexpr int NP = N * (N + 1) / 2;
+  if (!freev) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) M[k] = FP(0);
+    return;
+  }
+  const FP lam = d.st->lambda_solve;
+  FP Dv[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) Dv[k] = d.D[col + k];
+  FP B[NP];
+  int q = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = i; j < N; ++j, ++q) {
+      B[q] = Dv[i] * H[q] * Dv[j];
+      if (i == j) B[q] += d.st->before_scaling ? lam * Dv[i] * Dv[i] : lam;
+    }
+  FP out[NP];
+  if (!chol_inverse<FP, N>(B, out)) {
+    FP diag[N];
+    q = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = i; j < N; ++j, ++q)
+        if (i == j) diag[i] = clampv(B[q], FP(d.st->clamp_min), FP(d.st->clamp_max));
+    q = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = i; j < N; ++j, ++q) out[q] = (i == j) ? FP(1) / diag[i] : FP(0);
+    atomicAdd(&d.st->fallbacks, 1);
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) M[k] = out[k];
+}
+
+template <typename FP, typename SP>
+__global__ void k_precond(Dev<FP, SP> d) {
+  if (!d.st->iter_active) return;
+  const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (v < d.nc) {
+    const uint64_t col = 9 * v;
+    precond_vertex<FP, SP, 9>(d, d.Hc + 45 * v, d.Mc + 45 * v, col, d.col_free[col]);
+  } else if (v < static_cast<uint64_t>(d.nc) + d.np) {
+    const uint64_t i = v - d.nc;
+    const uint64_t col = 9ull * d.nc + 3 * i;
+    precond_vertex<FP, SP, 3>(d, d.Hp + 6 * i, d.Mp + 6 * i, col, d.col_free[col]);
+  }
+}
+
+// z = M r for one vertex (LinearSystem::apply_preconditioner,
+// linear_system.hpp:164-180): FP accumulation, narrowed to SP.
+template <typename FP, typename SP, int N>
+__device__ inline void apply_block(const FP* M, const SP* r, SP* z, FP* rz, FP* rr) {
+  FP rv[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) rv[k] = widen<FP>(r[k]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    FP acc = FP(0);
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc += M[i <= j ? i * N - i * (i - 1) / 2 + (j - i) : j * N - j * (j - 1) / 2 + (i - j)] * rv[j];
+    const SP zi = narrow<SP>(acc);
+    z[i] = zi;
+    *rz += rv[i] * widen<FP>(zi);
+    *rr += rv[i] * rv[i];
+  }
+}
+
+// =====================================================================
+// PCG (pcg_solve, pcg.hpp:34-105) on (D H D + damp) with block Jacobi.
+// =====================================================================
+
+// rhs = -D b; ||rhs|| (pcg.hpp:303-310, linear_system.hpp:188-189)
+template <typename FP, typename SP>
+__global__ void k_rhs_norm(Dev<FP, SP> d) {
+  if (!d.st->iter_active) return;
+  __shared__ FP scratch[32];
+  FP acc = FP(0);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const FP rhs = -d.D[i] * d.b[i];
+    acc += rhs * rhs;
+  }
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) d.blk_red[blockIdx.x] = acc;
+  if (last_block(&d.st->cnt[2])) {
+    const FP s = reduce_partials(d.blk_red, gridDim.x, scratch);
+    if (threadIdx.x == 0) {
+      State<FP>* st = d.st;
+      const FP nrm = sqrt(s);
+      st->rhs_norm = nrm;
+      if (!(nrm > FP(0))) {
+        st->pcg_done = 1;
+        st->pcg_zero = 1;
+        st->pcg_conv = is_finite(nrm) ? 1 : 0;
+        st->pcg_relres = 0.0;
+      }
+      st->scale = st->normalize_rhs ? FP(1) / nrm : FP(1);
+      st->ref_norm = st->normalize_rhs ? FP(1) : nrm;
+      st->unscale = st->normalize_rhs ? nrm : FP(1);
+    }
+  }
+}
+
+// r = narrow(rhs * scale), x = 0, z = M r, p = z, rho = r.z, res = |r|
+template <typename FP, typename SP>
+__global__ void k_pcg_init(Dev<FP, SP> d) {
+  if (!d.st->iter_active) return;
+  __shared__ FP scratch[32];
+  const FP scale = d.st->scale;
+  FP rz = FP(0), rr = FP(0);
+  const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t nv = static_cast<uint64_t>(d.nc) + d.np;
+  if (v < nv) {
+    const bool cam = v < d.nc;
+    const int n = cam ? 9 : 3;
+    const uint64_t col = cam ? 9 * v : 9ull * d.nc + 3 * (v - d.nc);
+    for (int k = 0; k < n; ++k) {
+      const FP rhs = -d.D[col + k] * d.b[col + k];
+      d.r[col + k] = narrow<SP>(rhs * scale);
+      d.xs[col + k] = narrow<SP>(FP(0));
+    }
+    if (cam)
+      apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &rz, &rr);
+    else
+      apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &rz, &rr);
+    for (int k = 0; k < n; ++k) d.p[col + k] = d.z[col + k];
+  }
+  rz = block_sum(rz, scratch);
+  rr = block_sum(rr, scratch);
+  if (threadIdx.x == 0) {
+    d.blk_red[blockIdx.x] = rz;
+    d.blk_red2[blockIdx.x] = rr;
+  }
+  if (last_block(&d.st->cnt[3])) {
+    const FP srz = reduce_partials(d.blk_red, gridDim.x, scratch);
+    const FP srr = reduce_partials(d.blk_red2, gridDim.x, scratch);
+    if (threadIdx.x == 0 && !d.st->pcg_done) {
+      d.st->rho = srz;
+      d.st->pcg_relres = static_cast<double>(sqrt(srr) / d.st->ref_norm);
+    }
+  }
+}
+
+// HVP, point side + camera runs (LinearSystem::hvp linear_system.hpp:104-115,
+// hvp_forward factor_descriptor.hpp:372-407, hvp_scatter :409-433).
+template <typename FP, typename SP, bool DYN>
+__global__ void __launch_bounds__(kTileThreads) k_hvp_tiles(Dev<FP, SP> d) {
+  using A = arith_t<SP>;
+  if (!d.st->iter_active || d.st->pcg_done) return;
+  const uint32_t t = blockIdx.x;
+  const uint32_t eb = d.tile_ebeg[t], ee = d.tile_ebeg[t + 1];
+  const uint32_t pb = d.tile_pbeg[t], pe = d.tile_pbeg[t + 1];
+  const uint32_t ne_t = ee - eb, npt = pe - pb;
+  const bool heavy = ne_t > static_cast<uint32_t>(kTileEdges);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint64_t pcol0 = 9ull * d.nc;
+
+  __shared__ A vt[kTilePoints * 3];
+  __shared__ A stage[kTileEdges * 3];
+  __shared__ A hacc[3];
+  __shared__ FP sX[DYN ? kTilePoints * 3 : 1];
+  __shared__ FP scratch[32];
+
+  for (uint32_t i = tid; i < npt * 3; i += blockDim.x) {
+    const uint64_t col = pcol0 + 3ull * pb + i;
+    vt[i] = static_cast<A>(d.D[col]) * widen<A>(d.p[col]);
+    if (DYN) sX[i] = d.x[col];
+  }
+  if (tid < 3) hacc[tid] = A(0);
+  __syncthreads();
+
+  for (uint32_t c0 = 0; c0 < ne_t; c0 += kTileThreads) {
+    const uint32_t j = c0 + tid;
+    const bool valid = j < ne_t;
+    const uint32_t e = eb + (valid ? j : 0);
+    const uint32_t cam = d.d_cam[e];
+    const uint32_t lp = d.d_lpt[e];
+    A jc[18], jp[6];
+    if (DYN) {
+      FP cp[9], fjc[18], fjp[6];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) cp[k] = d.x[9ull * cam + k];
+      snavely_jacobians<FP>(cp, &sX[3 * lp], fjc, fjp);
+#pragma unroll
+      for (int k = 0; k < 18; ++k) jc[k] = static_cast<A>(fjc[k]);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) jp[k] = static_cast<A>(fjp[k]);
+    } else {
+      load_J(d, e, jc, jp);
+    }
+    A vc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) vc[k] = static_cast<A>(d.D[9ull * cam + k]) * widen<A>(d.p[9ull * cam + k]);
+    A u0 = A(0), u1 = A(0), s0 = A(0), s1 = A(0);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      u0 += jc[k] * vc[k];
+      u1 += jc[9 + k] * vc[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      s0 += jp[k] * vt[3 * lp + k];
+      s1 += jp[3 + k] * vt[3 * lp + k];
+    }
+    u0 += s0;
+    u1 += s1;
+    const A wgt = d.w ? static_cast<A>(d.w[e]) : A(1);
+    const A q0 = valid ? wgt * u0 : A(0), q1 = valid ? wgt * u1 : A(0);
+    A g[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) g[k] = jc[k] * q0 + jc[9 + k] * q1;
+    const uint32_t chunk = d.tile_chunk_base[t] + (c0 + (tid & ~31)) / 32;
+    const RunInfo ri = run_info(cam, valid, d.chunk_part_base[chunk]);
+    seg_reduce<A, 9>(g, lane, ri.run_end);
+    if (ri.head) {
+      FP* dst = d.part + static_cast<uint64_t>(ri.slot) * 9;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) dst[k] = static_cast<FP>(g[k]);
+    }
+    A h[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) h[k] = jp[k] * q0 + jp[3 + k] * q1;
+    if (!heavy) {
+      if (valid)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) stage[j * 3 + k] = h[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) stage[tid * 3 + k] = h[k];
+      __syncthreads();
+      if (tid < 3) {
+        A acc = hacc[tid];
+        const uint32_t nvalid = min(static_cast<uint32_t>(kTileThreads), ne_t - c0);
+        for (uint32_t q = 0; q < nvalid; ++q) acc += stage[q * 3 + tid];
+        hacc[tid] = acc;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+
+  const A lam = static_cast<A>(d.st->lambda_solve);
+  const int before = d.st->before_scaling;
+  FP dot = FP(0);
+  for (uint32_t i = tid; i < npt; i += blockDim.x) {
+    A acc[3];
+    if (heavy) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) acc[k] = hacc[k];
+    } else {
+      acc[0] = acc[1] = acc[2] = A(0);
+      for (uint32_t q = d.pt_slot_off[pb + i]; q < d.pt_slot_off[pb + i + 1]; ++q) {
+        const uint32_t sl = d.pt_slots[q];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += stage[sl * 3 + k];
+      }
+    }
+    const uint64_t col = pcol0 + 3ull * (pb + i);
+    const bool freev = d.col_free[col];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const FP Dk = d.D[col + k];
+      const A damp = before ? static_cast<A>(static_cast<FP>(d.st->lambda_solve) * Dk * Dk) : lam;
+      const SP pk = d.p[col + k];
+      const A out = freev ? damp * widen<A>(pk) + static_cast<A>(Dk) * acc[k] : A(0);
+      const SP o = narrow<SP>(out);
+      d.ap[col + k] = o;
+      if (d.dbg_out) d.dbg_out[col + k] = out;
+      dot += widen<FP>(pk) * widen<FP>(o);
+    }
+  }
+  const FP tdot = block_sum(dot, scratch);
+  if (tid == 0) d.tile_red[t] = tdot;
+}
+
+// Camera side of the HVP + p.Ap finalization (pcg.hpp:332-340).
+template <typename FP, typename SP>
+__global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams(Dev<FP, SP> d) {
+  using A = arith_t<SP>;
+  if (!d.st->iter_active || d.st->pcg_done) return;
+  __shared__ FP scratch[32];
+  const int lane = threadIdx.x & 31;
+  const uint32_t c = blockIdx.x * kCamWarps + (threadIdx.x >> 5);
+  if (c < d.nc) {
+    FP acc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] = FP(0);
+    for (uint32_t q = d.cam_part_off[c] + lane; q < d.cam_part_off[c + 1]; q += 32) {
+      const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * 9;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] += src[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] = warp_sum(acc[k]);
+    FP dot = FP(0);
+    const bool freev = d.col_free[9ull * c];
+    if (lane < 9) {
+      const uint64_t col = 9ull * c + lane;
+      FP a = acc[0];
+#pragma unroll
+      for (int k = 1; k < 9; ++k)
+        if (lane == k) a = acc[k];
+      const FP Dk = d.D[col];
+      const A damp = d.st->before_scaling ? static_cast<A>(d.st->lambda_solve * Dk * Dk)
+                                          : static_cast<A>(d.st->lambda_solve);
+      const SP pk = d.p[col];
+      const A out = freev ? damp * widen<A>(pk) + static_cast<A>(Dk) * static_cast<A>(a) : A(0);
+      const SP o = narrow<SP>(out);
+      d.ap[col] = o;
+      if (d.dbg_out) d.dbg_out[col] = out;
+      dot = widen<FP>(pk) * widen<FP>(o);
+    }
+    dot = warp_sum(dot);
+    if (lane == 0) d.cam_red[c] = dot;
+  }
+  if (last_block(&d.st->cnt[4])) {
+    const FP s1 = reduce_partials(d.tile_red, d.ntiles, scratch);
+    const FP s2 = reduce_partials(d.cam_red, d.nc, scratch);
+    if (threadIdx.x == 0) {
+      const FP pap = s1 + s2;
+      d.st->pap = pap;
+      if (!(pap > FP(0)) || !is_finite(pap)) {
+        d.st->pcg_done = 1;
+        d.st->pcg_conv = 0;
+      } else {
+        d.st->alpha = d.st->rho / pap;
+      }
+    }
+  }
+}
+
+// x += alpha p; r -= alpha Ap; z = M r; rr, rz (pcg.hpp:340-357)
+template <typename FP, typename SP>
+__global__ void k_pcg_update(Dev<FP, SP> d) {
+  if (!d.st->iter_active || d.st->pcg_done) return;
+  __shared__ FP scratch[32];
+  const FP alpha = d.st->alpha;
+  FP rz = FP(0), rr = FP(0);
+  const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t nv = static_cast<uint64_t>(d.nc) + d.np;
+  if (v < nv) {
+    const bool cam = v < d.nc;
+    const int n = cam ? 9 : 3;
+    const uint64_t col = cam ? 9 * v : 9ull * d.nc + 3 * (v - d.nc);
+    for (int k = 0; k < n; ++k) {
+      d.xs[col + k] = narrow<SP>(widen<FP>(d.xs[col + k]) + alpha * widen<FP>(d.p[col + k]));
+      d.r[col + k] = narrow<SP>(widen<FP>(d.r[col + k]) - alpha * widen<FP>(d.ap[col + k]));
+    }
+    if (cam)
+      apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &rz, &rr);
+    else
+      apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &rz, &rr);
+  }
+  rz = block_sum(rz, scratch);
+  rr = block_sum(rr, scratch);
+  if (threadIdx.x == 0) {
+    d.blk_red[blockIdx.x] = rz;
+    d.blk_red2[blockIdx.x] = rr;
+  }
+  if (last_block(&d.st->cnt[5])) {
+    const FP srz = reduce_partials(d.blk_red, gridDim.x, scratch);
+    const FP srr = reduce_partials(d.blk_red2, gridDim.x, scratch);
+    if (threadIdx.x == 0) {
+      State<FP>* st = d.st;
+      st->pcg_it += 1;
+      const FP res = sqrt(srr);
+      const double rel = static_cast<double>(res / st->ref_norm);
+      st->pcg_relres = rel;
+      if (!isfinite(rel)) {
+        st->pcg_done = 1;
+        st->pcg_conv = 0;
+      } else if (res <= static_cast<FP>(st->pcg_tol) * st->ref_norm) {
+        st->pcg_done = 1;
+        st->pcg_conv = 1;
+      } else {
+        st->beta = srz / st->rho;
+        st->rho = srz;
+      }
+    }
+  }
+}
+
+// p = narrow(z + beta p) (pcg.hpp:358-361)
+template <typename FP, typename SP>
+__global__ void k_pcg_dir(Dev<FP, SP> d) {
+  if (!d.st->iter_active || d.st->pcg_done) return;
+  const FP beta = d.st->beta;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    d.p[i] = narrow<SP>(widen<FP>(d.z[i]) + beta * widen<FP>(d.p[i]));
+}
+
+// Unscale, predicted decrease, dx = D x, candidate x_new = x + dx
+// (pcg.hpp:364-365, linear_system.hpp:195-206, graph.hpp:126-128).
+template <typename FP, typename SP>
+__global__ void k_step(Dev<FP, SP> d) {
+  if (!d.st->iter_active) return;
+  __shared__ FP scratch[32];
+  const FP unscale = d.st->unscale;
+  const FP lam = d.st->lambda_solve;
+  const int before = d.st->before_scaling;
+  const bool zero = d.st->pcg_zero;
+  FP pred = FP(0);
+  int fin = 1;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const FP Di = d.D[i];
+    const FP xsi = zero ? FP(0) : widen<FP>(d.xs[i]) * unscale;
+    const FP rhs = -Di * d.b[i];
+    const FP damp = before ? lam * Di * Di : lam;
+    pred += xsi * (damp * xsi + rhs);
+    const FP dxi = Di * xsi;
+    d.dx[i] = dxi;
+    if (!is_finite(dxi)) fin = 0;
+    const FP xi = d.x[i];
+    d.x_new[i] = d.col_free[i] ? xi + dxi : xi;
+  }
+  pred = block_sum(pred, scratch);
+  fin = __syncthreads_and(fin);
+  if (threadIdx.x == 0) {
+    d.blk_red[blockIdx.x] = pred;
+    d.blk_flag[blockIdx.x] = fin;
+  }
+  if (last_block(&d.st->cnt[6])) {
+    const FP s = reduce_partials(d.blk_red, gridDim.x, scratch);
+    int f = 1;
+    for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) f &= static_cast<const volatile int*>(d.blk_flag)[i];
+    f = __syncthreads_and(f);
+    if (threadIdx.x == 0) {
+      d.st->pred = s;
+      d.st->step_finite = f;
+    }
+  }
+}
+
+// Candidate chi^2 at x_new (Graph::total_error_active graph.hpp:107-111,
+// FactorDescriptor::evaluate_chi2 factor_descriptor.hpp:294-305); RAW=true
+// gives raw_residual_sqnorm (:307-320) for BalGraph::mse. params: x or x_new.
+template <typename FP, typename SP, bool RAW>
+__global__ void __launch_bounds__(kTileThreads) k_chi2_tiles(Dev<FP, SP> d, const FP* params, int force) {
+  if (!force && (!d.st->iter_active || !d.st->step_finite)) return;
+  __shared__ FP scratch[32];
+  const uint32_t t = blockIdx.x;
+  const uint32_t eb = d.tile_ebeg[t], ee = d.tile_ebeg[t + 1], pb = d.tile_pbeg[t];
+  const uint64_t pcol0 = 9ull * d.nc;
+  FP chi = FP(0);
+  for (uint32_t e = eb + threadIdx.x; e < ee; e += blockDim.x) {
+    const uint32_t cam = d.d_cam[e];
+    FP cp[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) cp[k] = params[9ull * cam + k];
+    const FP* X = params + pcol0 + 3ull * (pb + d.d_lpt[e]);
+    FP res[2];
+    snavely_residual<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res);
+    const FP s = res[0] * res[0] + res[1] * res[1];
+    chi += RAW ? s : loss_value<FP>(d.loss_kind, d.huber, s);
+  }
+  chi = block_sum(chi, scratch);
+  if (threadIdx.x == 0) d.tile_red[t] = chi;
+  if (last_block(&d.st->cnt[7])) {
+    const FP s = reduce_partials(d.tile_red, d.ntiles, scratch);
+    if (threadIdx.x == 0) d.st->chi2_new = s;
+  }
+}
+
+// Accept / reject, Nielsen damping, termination, per-iteration record
+// (levenberg_marquardt.hpp:171-220, update_damping :88-98). One thread.
+template <typename FP>
+__global__ void k_decide(State<FP>* st, gb_iteration_record* recs) {
+  if (!st->iter_active) return;
+  gb_iteration_record& rec = recs[st->lm_it - 1];
+  rec.pcg_iterations = st->pcg_it;
+  rec.pcg_converged = st->pcg_conv;
+  rec.pcg_relative_residual = st->pcg_relres;
+  rec.precond_fallback_blocks = st->fallbacks;
+  FP lambda = st->lambda, nu = st->nu;
+  if (st->use_guard && !st->pcg_conv && st->pcg_relres > st->pcg_ratio * st->pcg_tol) {
+    rec.low_quality_step = 1;
+    lambda *= nu;
+  }
+  const FP chi2 = st->chi2;
+  const FP chi2_new = st->step_finite ? st->chi2_new : FP(NAN);
+  rec.chi2_after = static_cast<double>(chi2_new);
+  const bool accepted = is_finite(chi2_new) && chi2_new < chi2;
+  rec.accepted = accepted ? 1 : 0;
+  st->accepted = accepted ? 1 : 0;
+  FP rel = FP(0);
+  if (accepted) {
+    st->accepted_steps += 1;
+    const FP gain = st->pred > FP(0) ? (chi2 - chi2_new) / st->pred : FP(INFINITY);
+    const FP g = FP(2) * gain - FP(1);
+    lambda *= fmax(FP(1) / FP(3), FP(1) - g * g * g);
+    nu = FP(2);
+    rel = (chi2 - chi2_new) / chi2;
+    st->chi2 = chi2_new;  // == LinearSystem::linearize() at the accepted point
+    st->do_linearize = 1;
+  } else {
+    lambda *= nu;
+    nu *= FP(2);
+    st->do_linearize = st->refresh_on_reject;
+  }
+  st->lambda = lambda;
+  st->nu = nu;
+  st->rel_decrease = rel;
+  if (accepted && static_cast<double>(rel) < st->tol) {
+    st->termination = GB_TERM_TOLERANCE_REACHED;
+    st->terminated = 1;
+  } else if (static_cast<double>(lambda) > st->lambda_max) {
+    st->termination = GB_TERM_DAMPING_OVERFLOW;
+    st->terminated = 1;
+  } else if (st->lm_it >= st->max_iterations) {
+    st->termination = GB_TERM_MAX_ITERATIONS;
+    st->terminated = 1;
+  }
+  if (st->terminated) st->do_linearize = 0;  // the refreshed linearization is never observed
+}
+
+// Accepted step becomes the current point (the reference mutates in place and
+// restores the snapshot on reject, graph.hpp:114-128; here the candidate
+// lives in x_new and is copied on accept, so restore is a no-op).
+template <typename FP, typename SP>
+__global__ void k_commit(Dev<FP, SP> d) {
+  if (!d.st->iter_active || !d.st->accepted) return;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    d.x[i] = d.x_new[i];
+}
+
+}  // namespace gb

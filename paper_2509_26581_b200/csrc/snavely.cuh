@@ -1,0 +1,168 @@
+// Snavely camera model on the device (reference include/gopt/bal/snavely.hpp).
+//
+// One edge = one observation of point X by camera [w1 w2 w3 t1 t2 t3 f k1 k2].
+// The residual follows snavely_project (snavely.hpp:48-61) through the direct
+// Rodrigues formula rotate_angle_axis (:18-43); the Jacobians follow the
+// analytic chain SnavelyChain (:67-129) built ONCE per edge and shared by the
+// 2x9 camera block and the 2x3 point block (the reference builds the chain
+// twice, once per slot, adapter.hpp:67-74). Both share the Taylor switch
+// kRodriguesTaylorThreshold (:13-14).
+#pragma once
+
+#include "common.cuh"
+
+namespace gb {
+
+template <typename FP>
+struct taylor_threshold;
+template <>
+struct taylor_threshold<double> {
+  static constexpr double value = 1e-6;
+};
+template <>
+struct taylor_threshold<float> {
+  static constexpr float value = 1e-2f;
+};
+
+__device__ inline void sin_cos(double x, double* s, double* c) { sincos(x, s, c); }
+__device__ inline void sin_cos(float x, float* s, float* c) { sincosf(x, s, c); }
+
+// Residual r = predicted - observed (adapter.hpp:58-65).
+template <typename FP>
+__device__ inline void snavely_residual(const FP* cam, const FP* X, FP o0, FP o1, FP* r) {
+  const FP w0 = cam[0], w1 = cam[1], w2 = cam[2];
+  const FP theta2 = w0 * w0 + w1 * w1 + w2 * w2;
+  FP a, s, c;
+  if (theta2 < taylor_threshold<FP>::value) {
+    const FP u = theta2;
+    a = FP(1) - u * FP(0.5) + u * u * (FP(1) / FP(24));
+    s = FP(1) - u * (FP(1) / FP(6)) + u * u * (FP(1) / FP(120));
+    c = FP(0.5) - u * (FP(1) / FP(24)) + u * u * (FP(1) / FP(720));
+  } else {
+    const FP theta = sqrt(theta2);
+    FP sn, cs;
+    sin_cos(theta, &sn, &cs);
+    a = cs;
+    s = sn / theta;
+    c = (FP(1) - a) / theta2;
+  }
+  const FP wx = w1 * X[2] - w2 * X[1];
+  const FP wy = w2 * X[0] - w0 * X[2];
+  const FP wz = w0 * X[1] - w1 * X[0];
+  const FP dot = w0 * X[0] + w1 * X[1] + w2 * X[2];
+  const FP p0 = a * X[0] + s * wx + c * dot * w0 + cam[3];
+  const FP p1 = a * X[1] + s * wy + c * dot * w1 + cam[4];
+  const FP p2 = a * X[2] + s * wz + c * dot * w2 + cam[5];
+  const FP xp = -p0 / p2;
+  const FP yp = -p1 / p2;
+  const FP n = xp * xp + yp * yp;
+  const FP d = FP(1) + n * (cam[7] + n * cam[8]);
+  r[0] = cam[6] * d * xp - o0;
+  r[1] = cam[6] * d * yp - o1;
+}
+
+// Analytic Jacobians: jc = d pred / d camera (2x9 row-major),
+// jp = d pred / d point (2x3 row-major). snavely.hpp:67-153.
+template <typename FP>
+__device__ inline void snavely_jacobians(const FP* cam, const FP* X, FP* jc, FP* jp) {
+  const FP w0 = cam[0], w1 = cam[1], w2 = cam[2];
+  const FP x0 = X[0], x1 = X[1], x2 = X[2];
+  const FP theta2 = w0 * w0 + w1 * w1 + w2 * w2;
+  FP a, s, c, s1, c2;
+  if (theta2 < taylor_threshold<FP>::value) {
+    const FP u = theta2;
+    a = FP(1) - u / FP(2) + u * u / FP(24);
+    s = FP(1) - u / FP(6) + u * u / FP(120);
+    c = FP(0.5) - u / FP(24) + u * u / FP(720);
+    s1 = -FP(1) / FP(3) + u / FP(30);
+    c2 = -FP(1) / FP(12) + u / FP(180);
+  } else {
+    const FP theta = sqrt(theta2);
+    FP sn, cs;
+    sin_cos(theta, &sn, &cs);
+    a = cs;
+    s = sn / theta;
+    c = (FP(1) - a) / theta2;
+    s1 = (a - s) / theta2;
+    c2 = (s - FP(2) * c) / theta2;
+  }
+  // R = a I + s [w]x + c w w^T
+  FP R[9];
+  R[0] = a + c * w0 * w0;
+  R[1] = -s * w2 + c * w0 * w1;
+  R[2] = s * w1 + c * w0 * w2;
+  R[3] = s * w2 + c * w1 * w0;
+  R[4] = a + c * w1 * w1;
+  R[5] = -s * w0 + c * w1 * w2;
+  R[6] = -s * w1 + c * w2 * w0;
+  R[7] = s * w0 + c * w2 * w1;
+  R[8] = a + c * w2 * w2;
+  // dy/dw = -s x w^T + s1 (w x x) w^T - s [x]x + c2 (w.x) w w^T + c (w x^T + (w.x) I)
+  const FP cr[3] = {w1 * x2 - w2 * x1, w2 * x0 - w0 * x2, w0 * x1 - w1 * x0};
+  const FP dt = w0 * x0 + w1 * x1 + w2 * x2;
+  const FP w[3] = {w0, w1, w2};
+  const FP x[3] = {x0, x1, x2};
+  const FP skx[9] = {FP(0), -x2, x1, x2, FP(0), -x0, -x1, x0, FP(0)};
+  FP Dw[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      Dw[3 * i + j] = -s * x[i] * w[j] + s1 * cr[i] * w[j] - s * skx[3 * i + j] + c2 * dt * w[i] * w[j] +
+                      c * (w[i] * x[j] + (i == j ? dt : FP(0)));
+  // P = R X + t
+  const FP P0 = R[0] * x0 + R[1] * x1 + R[2] * x2 + cam[3];
+  const FP P1 = R[3] * x0 + R[4] * x1 + R[5] * x2 + cam[4];
+  const FP P2 = R[6] * x0 + R[7] * x1 + R[8] * x2 + cam[5];
+  const FP iz = FP(1) / P2;
+  const FP p0 = -P0 * iz, p1 = -P1 * iz;
+  const FP n = p0 * p0 + p1 * p1;
+  const FP f = cam[6], k1 = cam[7], k2 = cam[8];
+  const FP dist = FP(1) + n * (k1 + n * k2);
+  // du/dp = f (dist I + 2 (k1 + 2 k2 n) p p^T); dp/dP = [[-iz,0,P0 iz^2],[0,-iz,P1 iz^2]]
+  const FP g = FP(2) * (k1 + FP(2) * k2 * n);
+  const FP A00 = f * (dist + g * p0 * p0), A01 = f * (g * p0 * p1);
+  const FP A10 = f * (g * p1 * p0), A11 = f * (dist + g * p1 * p1);
+  const FP iz2 = iz * iz;
+  const FP B02 = P0 * iz2, B12 = P1 * iz2;
+  FP U[6];  // du/dP 2x3
+  U[0] = -A00 * iz;
+  U[1] = -A01 * iz;
+  U[2] = A00 * B02 + A01 * B12;
+  U[3] = -A10 * iz;
+  U[4] = -A11 * iz;
+  U[5] = A10 * B02 + A11 * B12;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      jc[9 * r + j] = U[3 * r] * Dw[j] + U[3 * r + 1] * Dw[3 + j] + U[3 * r + 2] * Dw[6 + j];
+      jc[9 * r + 3 + j] = U[3 * r + j];
+      jp[3 * r + j] = U[3 * r] * R[j] + U[3 * r + 1] * R[3 + j] + U[3 * r + 2] * R[6 + j];
+    }
+  }
+  jc[6] = dist * p0;
+  jc[15] = dist * p1;
+  jc[7] = f * n * p0;
+  jc[16] = f * n * p1;
+  jc[8] = f * n * n * p0;
+  jc[17] = f * n * n * p1;
+}
+
+// Robust loss (loss.hpp:25-40): value rho(s) and IRLS weight rho'(s).
+template <typename FP>
+__device__ inline FP loss_value(int kind, FP delta, FP s) {
+  if (kind == 0) return s;
+  const FP d2 = delta * delta;
+  if (s <= d2) return s;
+  return FP(2) * delta * sqrt(s) - d2;
+}
+template <typename FP>
+__device__ inline FP loss_weight(int kind, FP delta, FP s) {
+  if (kind == 0) return FP(1);
+  const FP d2 = delta * delta;
+  if (s <= d2) return FP(1);
+  return delta / sqrt(s);
+}
+
+}  // namespace gb

@@ -1,0 +1,883 @@
+// Host orchestration and the C ABI (include/gb_bal.h).
+//
+// One handle = one user graph (cameras, points, observations) bound to one
+// CUDA device and one stream. gb_optimize uploads once, runs every LM
+// iteration as a captured CUDA graph whose kernels read and write the
+// device-resident State (no host decision inside an iteration), and writes
+// the refined parameters back into the user's AoS buffers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "activate.hpp"
+#include "gb_bal.h"
+#include "kernels.cuh"
+
+namespace gb {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NoDevice : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                         \
+  do {                                                                                                \
+    cudaError_t err__ = (x);                                                                          \
+    if (err__ != cudaSuccess)                                                                         \
+      throw CudaError(std::string("CUDA error ") + cudaGetErrorString(err__) + " at " #x);            \
+  } while (0)
+
+// ------------------------------------------------------------ user graph data
+struct GraphData {
+  int precision = GB_FP64;
+  int diff_mode = GB_ANALYTIC;
+  int device = 0;
+  void* cams = nullptr;
+  void* pts = nullptr;
+  uint64_t nc = 0, np = 0, ne = 0;
+  std::vector<uint8_t> cam_fixed, pt_fixed, level;
+  std::vector<uint32_t> cam_idx, pt_idx;
+  std::vector<double> obs;
+  int loss_kind = GB_LOSS_DEFAULT;
+  double huber = 1.0;
+  uint64_t revision = 1;
+};
+
+class SolverBase {
+ public:
+  virtual ~SolverBase() = default;
+  virtual void optimize(const gb_lm_config& cfg, gb_solve_report* rep, gb_iteration_record* recs, int max_recs) = 0;
+  virtual double residual_sum(int level, bool raw) = 0;
+  virtual void ls_linearize(int level, double cmin, double cmax, int damping, double* chi2, int64_t* n, void* b,
+                            void* diag, void* clamped, void* scaling, int32_t* finite) = 0;
+  virtual void ls_hvp(const void* v, void* out, double lambda) = 0;
+  virtual void ls_precond(double lambda, void* blocks, int32_t* fallbacks) = 0;
+  virtual void ls_solve_step(double lambda, const gb_pcg_config& pcg, void* dx, gb_pcg_stats* st, double* pred,
+                             int32_t* finite) = 0;
+  virtual void ls_jacobians(void* out) = 0;
+  virtual const Activation& activation() = 0;
+};
+
+// ------------------------------------------------------------- device memory
+class DBuf {
+ public:
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    bytes_ = 0;
+  }
+  void* alloc(size_t bytes) {
+    if (bytes <= bytes_ && p_) return p_;
+    release();
+    CK(cudaMalloc(&p_, bytes ? bytes : 1));
+    bytes_ = bytes;
+    return p_;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p_);
+  }
+
+ private:
+  void* p_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+template <typename T>
+T* upload(DBuf& buf, const std::vector<T>& v, cudaStream_t s) {
+  T* p = static_cast<T*>(buf.alloc(v.size() * sizeof(T)));
+  if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return p;
+}
+
+inline unsigned div_up(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+// --------------------------------------------------------------------- solver
+template <typename FP, typename SP>
+class Solver final : public SolverBase {
+  using A = arith_t<SP>;
+
+ public:
+  explicit Solver(GraphData& g) : g_(g) {
+    CK(cudaSetDevice(g_.device));
+    CK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+    st_ = static_cast<State<FP>*>(st_buf_.alloc(sizeof(State<FP>)));
+    CK(cudaMemsetAsync(st_, 0, sizeof(State<FP>), s_));
+  }
+  ~Solver() override {
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    if (pinned_) cudaFreeHost(pinned_);
+    if (flag_host_) cudaFreeHost(flag_host_);
+    cudaStreamDestroy(s_);
+  }
+
+  // current activation (the last level used; level 0 if never activated)
+  const Activation& activation() override {
+    ensure_structure(have_act_ ? act_level_ : 0);
+    return act_;
+  }
+
+  // ---------------------------------------------------------------- optimize
+  void optimize(const gb_lm_config& cfg, gb_solve_report* rep, gb_iteration_record* recs, int max_recs) override {
+    using Clock = std::chrono::steady_clock;
+    const auto t0 = Clock::now();
+    CK(cudaSetDevice(g_.device));
+    ensure_structure(cfg.level);
+    upload_params();
+    State<FP> hs{};
+    fill_config(hs, cfg);
+    CK(cudaMemcpyAsync(st_, &hs, sizeof(hs), cudaMemcpyHostToDevice, s_));
+    rec_buf_.alloc(sizeof(gb_iteration_record) * std::max(1, cfg.max_iterations));
+    dev_.recs = rec_buf_.as<gb_iteration_record>();
+    enqueue_linearize(1);
+    CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    const FP chi2 = hs.lin_chi2;
+    if (!std::isfinite(static_cast<double>(chi2)))
+      throw std::runtime_error("levenberg_marquardt: non-finite chi^2 at the initial parameters");
+
+    gb_solve_report r{};
+    r.initial_chi2 = r.final_chi2 = static_cast<double>(chi2);
+    r.free_dims = act_.free_dims;
+    r.residual_dims = static_cast<int64_t>(2 * act_.n_active);
+    r.active_factors = act_.n_active;
+    r.memory = memory_account();
+    r.termination = GB_TERM_MAX_ITERATIONS;
+    r.h2d_bytes = static_cast<double>(h2d_bytes_);
+    h2d_bytes_ = 0;
+    int nrec = 0;
+    if (act_.free_dims == 0) {
+      r.termination = GB_TERM_NO_FREE_PARAMETERS;
+    } else if (cfg.max_iterations > 0) {
+      // state: chi2, lambda0 (linear_system.hpp:94-99), nu = 2
+      hs.chi2 = chi2;
+      hs.lm_it = 0;
+      hs.terminated = 0;
+      hs.accepted_steps = 0;
+      CK(cudaMemcpyAsync(st_, &hs, sizeof(hs), cudaMemcpyHostToDevice, s_));
+      k_init_damping<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+      CK(cudaGetLastError());
+      build_iteration_graph(cfg.pcg.max_iterations);
+      r.setup_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+
+      std::vector<cudaEvent_t> ev(cfg.max_iterations + 1);
+      for (auto& e : ev) CK(cudaEventCreate(&e));
+      std::vector<cudaEvent_t> flag_ev(cfg.max_iterations);
+      for (auto& e : flag_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      if (!flag_host_) CK(cudaHostAlloc(reinterpret_cast<void**>(&flag_host_), 64 * sizeof(int), cudaHostAllocDefault));
+      int launched = 0;
+      for (int it = 0; it < cfg.max_iterations; ++it) {
+        CK(cudaEventRecord(ev[it], s_));
+        CK(cudaGraphLaunch(graph_exec_, s_));
+        ++launched;
+        CK(cudaMemcpyAsync(&flag_host_[it % 64], &st_->terminated, sizeof(int), cudaMemcpyDeviceToHost, s_));
+        CK(cudaEventRecord(flag_ev[it], s_));
+        // look one iteration behind: the device always has queued work
+        if (it >= 1) {
+          CK(cudaEventSynchronize(flag_ev[it - 1]));
+          if (flag_host_[(it - 1) % 64]) break;
+        }
+      }
+      CK(cudaEventRecord(ev[launched], s_));
+      CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
+      CK(cudaStreamSynchronize(s_));
+      nrec = hs.lm_it;
+      std::vector<gb_iteration_record> hr(std::max(nrec, 1));
+      if (nrec) CK(cudaMemcpy(hr.data(), dev_.recs, sizeof(gb_iteration_record) * nrec, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < nrec && i < launched; ++i) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+        hr[i].wall_seconds = ms * 1e-3;
+      }
+      for (auto& e : ev) cudaEventDestroy(e);
+      for (auto& e : flag_ev) cudaEventDestroy(e);
+      r.termination = hs.termination;
+      r.accepted_steps = hs.accepted_steps;
+      r.final_chi2 = static_cast<double>(hs.chi2);
+      if (recs)
+        for (int i = 0; i < std::min(nrec, max_recs); ++i) recs[i] = hr[i];
+      download_params();
+    }
+    r.iterations_run = nrec;
+    r.d2h_bytes = static_cast<double>(d2h_bytes_);
+    d2h_bytes_ = 0;
+    r.total_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+    if (rep) *rep = r;
+  }
+
+  double residual_sum(int level, bool raw) override {
+    CK(cudaSetDevice(g_.device));
+    ensure_structure(level);
+    upload_params();
+    if (raw)
+      k_chi2_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, dev_.x, 1);
+    else
+      k_chi2_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, dev_.x, 1);
+    CK(cudaGetLastError());
+    State<FP> hs;
+    CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    return static_cast<double>(hs.chi2_new);
+  }
+
+  // ------------------------------------------------ LinearSystem debug surface
+  void ls_linearize(int level, double cmin, double cmax, int damping, double* chi2, int64_t* n, void* b, void* diag,
+                    void* clamped, void* scaling, int32_t* finite) override {
+    CK(cudaSetDevice(g_.device));
+    ensure_structure(level);
+    upload_params();
+    gb_lm_config cfg;
+    gb_default_config(&cfg);
+    cfg.clamp_min = cmin;
+    cfg.clamp_max = cmax;
+    cfg.damping = damping;
+    State<FP> hs{};
+    fill_config(hs, cfg);
+    CK(cudaMemcpyAsync(st_, &hs, sizeof(hs), cudaMemcpyHostToDevice, s_));
+    enqueue_linearize(1);
+    CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    ls_state_ = hs;
+    ls_ready_ = true;
+    if (chi2) *chi2 = static_cast<double>(hs.lin_chi2);
+    if (n) *n = act_.free_dims;
+    if (finite) *finite = hs.lin_finite;
+    auto fetch = [&](const FP* src, void* dst) {
+      if (!dst) return;
+      std::vector<FP> h(ncols_);
+      CK(cudaMemcpy(h.data(), src, ncols_ * sizeof(FP), cudaMemcpyDeviceToHost));
+      FP* o = static_cast<FP*>(dst);
+      for (size_t i = 0; i < ref_to_int_.size(); ++i) o[i] = h[ref_to_int_[i]];
+    };
+    fetch(dev_.b, b);
+    fetch(dev_.clamped, clamped);
+    fetch(dev_.D, scaling);
+    if (diag) {
+      std::vector<FP> hc(45ull * act_.nc), hp(6ull * act_.np);
+      CK(cudaMemcpy(hc.data(), dev_.Hc, hc.size() * sizeof(FP), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(hp.data(), dev_.Hp, hp.size() * sizeof(FP), cudaMemcpyDeviceToHost));
+      FP* o = static_cast<FP*>(diag);
+      for (uint64_t c = 0; c < act_.nc; ++c)
+        if (act_.cam_col[c] >= 0)
+          for (int k = 0; k < 9; ++k) o[act_.cam_col[c] + k] = hc[45 * c + p9(k, k)];
+      for (uint64_t p = 0; p < act_.np; ++p)
+        if (act_.pt_col[p] >= 0)
+          for (int k = 0; k < 3; ++k) o[act_.pt_col[p] + k] = hp[6ull * act_.pt_rank[p] + p3(k, k)];
+    }
+  }
+
+  void need_ls() const {
+    if (!ls_ready_) throw std::logic_error("linear system not linearized (call gb_ls_linearize first)");
+  }
+
+  void begin_solve_state(double lambda, const gb_pcg_config* pcg) {
+    State<FP> hs = ls_state_;
+    hs.iter_active = 1;
+    hs.lambda_solve = static_cast<FP>(lambda);
+    hs.lambda = static_cast<FP>(lambda);
+    hs.pcg_done = hs.pcg_it = hs.pcg_conv = hs.pcg_zero = 0;
+    hs.pcg_relres = 0;
+    hs.fallbacks = 0;
+    if (pcg) {
+      hs.pcg_max_it = pcg->max_iterations;
+      hs.pcg_tol = pcg->tolerance;
+      hs.pcg_ratio = pcg->rejection_ratio;
+      hs.normalize_rhs = pcg->normalize_rhs;
+    }
+    CK(cudaMemcpyAsync(st_, &hs, sizeof(hs), cudaMemcpyHostToDevice, s_));
+  }
+
+  void ls_hvp(const void* v, void* out, double lambda) override {
+    need_ls();
+    begin_solve_state(lambda, nullptr);
+    std::vector<SP> hv(ncols_, narrow<SP>(0.0));
+    const SP* vin = static_cast<const SP*>(v);
+    for (size_t i = 0; i < ref_to_int_.size(); ++i) hv[ref_to_int_[i]] = vin[i];
+    CK(cudaMemcpyAsync(dev_.p, hv.data(), ncols_ * sizeof(SP), cudaMemcpyHostToDevice, s_));
+    Dev<FP, SP> d = dev_;
+    d.dbg_out = static_cast<A*>(dbg_buf_.alloc(ncols_ * sizeof(A)));
+    launch_hvp(d);
+    std::vector<A> h(ncols_);
+    CK(cudaMemcpyAsync(h.data(), d.dbg_out, ncols_ * sizeof(A), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    A* o = static_cast<A*>(out);
+    for (size_t i = 0; i < ref_to_int_.size(); ++i) o[i] = h[ref_to_int_[i]];
+  }
+
+  void ls_precond(double lambda, void* blocks, int32_t* fallbacks) override {
+    need_ls();
+    begin_solve_state(lambda, nullptr);
+    k_precond<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+    State<FP> hs;
+    std::vector<FP> mc(45ull * act_.nc), mp(6ull * act_.np);
+    CK(cudaMemcpyAsync(mc.data(), dev_.Mc, mc.size() * sizeof(FP), cudaMemcpyDeviceToHost, s_));
+    CK(cudaMemcpyAsync(mp.data(), dev_.Mp, mp.size() * sizeof(FP), cudaMemcpyDeviceToHost, s_));
+    CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    if (fallbacks) *fallbacks = hs.fallbacks;
+    if (!blocks) return;
+    FP* o = static_cast<FP*>(blocks);
+    uint64_t base = 0;
+    for (uint64_t c = 0; c < act_.nc; ++c) {
+      if (act_.cam_col[c] < 0) continue;
+      for (int i = 0; i < 9; ++i)
+        for (int j = 0; j < 9; ++j) o[base + 9 * i + j] = mc[45 * c + p9(i, j)];
+      base += 81;
+    }
+    for (uint64_t p = 0; p < act_.np; ++p) {
+      if (act_.pt_col[p] < 0) continue;
+      const uint64_t r = act_.pt_rank[p];
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) o[base + 3 * i + j] = mp[6 * r + p3(i, j)];
+      base += 9;
+    }
+  }
+
+  void ls_solve_step(double lambda, const gb_pcg_config& pcg, void* dx, gb_pcg_stats* stats, double* pred,
+                     int32_t* finite) override {
+    need_ls();
+    begin_solve_state(lambda, &pcg);
+    enqueue_solve(pcg.max_iterations);
+    State<FP> hs;
+    CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
+    std::vector<FP> h(ncols_);
+    CK(cudaMemcpyAsync(h.data(), dev_.dx, ncols_ * sizeof(FP), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    if (dx) {
+      FP* o = static_cast<FP*>(dx);
+      for (size_t i = 0; i < ref_to_int_.size(); ++i) o[i] = h[ref_to_int_[i]];
+    }
+    if (stats) *stats = gb_pcg_stats{hs.pcg_it, hs.pcg_relres, hs.pcg_conv};
+    if (pred) *pred = static_cast<double>(hs.pred);
+    if (finite) *finite = hs.step_finite;
+  }
+
+  void ls_jacobians(void* out) override {
+    need_ls();
+    if (!dev_.J) throw std::logic_error("dynamic mode stores no Jacobians");
+    const uint64_t na = act_.n_active;
+    std::vector<SP> h(24 * na);
+    CK(cudaMemcpy(h.data(), dev_.J, h.size() * sizeof(SP), cudaMemcpyDeviceToHost));
+    SP* o = static_cast<SP*>(out);
+    for (uint64_t d = 0; d < na; ++d) {
+      const uint64_t a = act_.d_a[d];
+      for (int k = 0; k < 24; ++k) o[24 * a + k] = h[k * na + d];
+    }
+  }
+
+ private:
+  // ------------------------------------------------------------ structure
+  void ensure_structure(int level) {
+    if (have_act_ && act_rev_ == g_.revision && act_level_ == level) return;
+    if (!g_.cams || !g_.pts) throw std::logic_error("cameras and points must be set before solving");
+    ActivationInput in;
+    in.nc = g_.nc;
+    in.np = g_.np;
+    in.ne = g_.ne;
+    in.cam = g_.cam_idx.data();
+    in.pt = g_.pt_idx.data();
+    in.level = g_.level.empty() ? nullptr : g_.level.data();
+    in.cam_fixed = g_.cam_fixed.empty() ? nullptr : g_.cam_fixed.data();
+    in.pt_fixed = g_.pt_fixed.empty() ? nullptr : g_.pt_fixed.data();
+    in.active_level = level;
+    activate(in, act_);
+    have_act_ = true;
+    act_rev_ = g_.revision;
+    act_level_ = level;
+    ls_ready_ = false;
+    if (graph_exec_) {
+      cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+    }
+    upload_structure();
+  }
+
+  void upload_structure() {
+    const uint64_t nc = act_.nc, np = act_.np, na = act_.n_active;
+    ncols_ = 9 * nc + 3 * np;
+    Dev<FP, SP>& d = dev_;
+    d = Dev<FP, SP>{};
+    d.nc = static_cast<uint32_t>(nc);
+    d.np = static_cast<uint32_t>(np);
+    d.na = static_cast<uint32_t>(na);
+    d.ntiles = act_.ntiles;
+    d.nparts = act_.nparts;
+    d.ncols = ncols_;
+    size_t h2d = 0;
+    auto up = [&](DBuf& buf, const auto& v) {
+      h2d += v.size() * sizeof(v[0]);
+      return upload(buf, v, s_);
+    };
+    // column free mask and the reference column map
+    std::vector<uint8_t> col_free(ncols_, 0);
+    ref_to_int_.assign(act_.free_dims, 0);
+    for (uint64_t c = 0; c < nc; ++c)
+      if (act_.cam_col[c] >= 0)
+        for (int k = 0; k < 9; ++k) {
+          col_free[9 * c + k] = 1;
+          ref_to_int_[act_.cam_col[c] + k] = 9 * c + k;
+        }
+    for (uint64_t p = 0; p < np; ++p)
+      if (act_.pt_col[p] >= 0)
+        for (int k = 0; k < 3; ++k) {
+          const uint64_t ic = 9 * nc + 3ull * act_.pt_rank[p] + k;
+          col_free[ic] = 1;
+          ref_to_int_[act_.pt_col[p] + k] = ic;
+        }
+    d.col_free = up(b_col_free_, col_free);
+    d.d_cam = up(b_dcam_, act_.d_cam);
+    d.d_lpt = up(b_dlpt_, act_.d_lpt);
+    std::vector<FP> obs(2 * na);
+    for (uint64_t e = 0; e < na; ++e) {
+      const uint64_t i = act_.active[act_.d_a[e]];
+      obs[e] = static_cast<FP>(g_.obs[2 * i]);
+      obs[na + e] = static_cast<FP>(g_.obs[2 * i + 1]);
+    }
+    d.d_obs = up(b_obs_, obs);
+    d.tile_ebeg = up(b_tile_ebeg_, act_.tile_ebeg);
+    d.tile_pbeg = up(b_tile_pbeg_, act_.tile_pbeg);
+    d.tile_chunk_base = up(b_tile_chunk_, act_.tile_chunk_base);
+    d.chunk_part_base = up(b_chunk_part_, act_.chunk_part_base);
+    d.pt_slot_off = up(b_pt_slot_off_, act_.pt_slot_off);
+    d.pt_slots = up(b_pt_slots_, act_.pt_slots);
+    d.cam_part_off = up(b_cam_part_off_, act_.cam_part_off);
+    d.cam_part_idx = up(b_cam_part_idx_, act_.cam_part_idx);
+    h2d_bytes_ += h2d;
+
+    const bool dyn = g_.diff_mode == GB_DYNAMIC;
+    d.J = dyn ? nullptr : static_cast<SP*>(b_J_.alloc(24 * na * sizeof(SP)));
+    d.w = g_.loss_kind == GB_LOSS_HUBER ? static_cast<FP*>(b_w_.alloc(na * sizeof(FP))) : nullptr;
+    d.loss_kind = g_.loss_kind;
+    d.huber = static_cast<FP>(g_.huber);
+    d.part = static_cast<FP*>(b_part_.alloc(std::max<uint64_t>(1, act_.nparts) * kLinVals * sizeof(FP)));
+    d.x = static_cast<FP*>(b_x_.alloc(ncols_ * sizeof(FP)));
+    d.x_new = static_cast<FP*>(b_xn_.alloc(ncols_ * sizeof(FP)));
+    d.b = static_cast<FP*>(b_b_.alloc(ncols_ * sizeof(FP)));
+    d.clamped = static_cast<FP*>(b_cl_.alloc(ncols_ * sizeof(FP)));
+    d.D = static_cast<FP*>(b_D_.alloc(ncols_ * sizeof(FP)));
+    d.dx = static_cast<FP*>(b_dx_.alloc(ncols_ * sizeof(FP)));
+    d.Hc = static_cast<FP*>(b_Hc_.alloc(45 * nc * sizeof(FP)));
+    d.Hp = static_cast<FP*>(b_Hp_.alloc(6 * np * sizeof(FP)));
+    d.Mc = static_cast<FP*>(b_Mc_.alloc(45 * nc * sizeof(FP)));
+    d.Mp = static_cast<FP*>(b_Mp_.alloc(6 * np * sizeof(FP)));
+    d.xs = static_cast<SP*>(b_xs_.alloc(ncols_ * sizeof(SP)));
+    d.r = static_cast<SP*>(b_r_.alloc(ncols_ * sizeof(SP)));
+    d.z = static_cast<SP*>(b_z_.alloc(ncols_ * sizeof(SP)));
+    d.p = static_cast<SP*>(b_p_.alloc(ncols_ * sizeof(SP)));
+    d.ap = static_cast<SP*>(b_ap_.alloc(ncols_ * sizeof(SP)));
+    d.tile_red = static_cast<FP*>(b_tr_.alloc(act_.ntiles * sizeof(FP)));
+    d.tile_red2 = static_cast<FP*>(b_tr2_.alloc(act_.ntiles * sizeof(FP)));
+    d.tile_flag = static_cast<int*>(b_tf_.alloc(act_.ntiles * sizeof(int)));
+    d.cam_red = static_cast<FP*>(b_cr_.alloc(std::max<uint64_t>(1, nc) * sizeof(FP)));
+    d.cam_red2 = static_cast<FP*>(b_cr2_.alloc(std::max<uint64_t>(1, nc) * sizeof(FP)));
+    d.cam_flag = static_cast<int*>(b_cf_.alloc(std::max<uint64_t>(1, nc) * sizeof(int)));
+    const uint64_t nblk = std::max<uint64_t>(vert_grid(), col_grid());
+    d.blk_red = static_cast<FP*>(b_br_.alloc(nblk * sizeof(FP)));
+    d.blk_red2 = static_cast<FP*>(b_br2_.alloc(nblk * sizeof(FP)));
+    d.blk_flag = static_cast<int*>(b_bf_.alloc(nblk * sizeof(int)));
+    d.st = st_;
+    d.recs = rec_buf_.as<gb_iteration_record>();
+    CK(cudaMemsetAsync(d.xs, 0, ncols_ * sizeof(SP), s_));
+    CK(cudaMemsetAsync(d.p, 0, ncols_ * sizeof(SP), s_));
+    if (pinned_) cudaFreeHost(pinned_);
+    pinned_ = nullptr;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&pinned_), std::max<uint64_t>(1, ncols_) * sizeof(FP), cudaHostAllocDefault));
+  }
+
+  void upload_params() {
+    const uint64_t nc = act_.nc, np = act_.np;
+    const FP* uc = static_cast<const FP*>(g_.cams);
+    const FP* up = static_cast<const FP*>(g_.pts);
+    CK(cudaStreamSynchronize(s_));  // pinned_ may still be in flight
+    std::memcpy(pinned_, uc, 9 * nc * sizeof(FP));
+    FP* dst = pinned_ + 9 * nc;
+    for (uint64_t i = 0; i < np; ++i) {
+      const uint64_t p = act_.pt_order[i];
+      dst[3 * i] = up[3 * p];
+      dst[3 * i + 1] = up[3 * p + 1];
+      dst[3 * i + 2] = up[3 * p + 2];
+    }
+    CK(cudaMemcpyAsync(dev_.x, pinned_, ncols_ * sizeof(FP), cudaMemcpyHostToDevice, s_));
+    h2d_bytes_ += ncols_ * sizeof(FP);
+  }
+
+  void download_params() {
+    const uint64_t nc = act_.nc, np = act_.np;
+    CK(cudaMemcpyAsync(pinned_, dev_.x, ncols_ * sizeof(FP), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    d2h_bytes_ += ncols_ * sizeof(FP);
+    FP* uc = static_cast<FP*>(g_.cams);
+    FP* up = static_cast<FP*>(g_.pts);
+    // fixed vertices are written back with their own bits (bit-identical)
+    std::memcpy(uc, pinned_, 9 * nc * sizeof(FP));
+    const FP* src = pinned_ + 9 * nc;
+    for (uint64_t i = 0; i < np; ++i) {
+      const uint64_t p = act_.pt_order[i];
+      up[3 * p] = src[3 * i];
+      up[3 * p + 1] = src[3 * i + 1];
+      up[3 * p + 2] = src[3 * i + 2];
+    }
+  }
+
+  void fill_config(State<FP>& hs, const gb_lm_config& cfg) {
+    hs.tol = cfg.tolerance;
+    hs.grad_tol = cfg.gradient_tolerance;
+    hs.lambda_max = cfg.lambda_max;
+    hs.tau = cfg.tau;
+    hs.pcg_tol = cfg.pcg.tolerance;
+    hs.pcg_ratio = cfg.pcg.rejection_ratio;
+    hs.pcg_max_it = cfg.pcg.max_iterations;
+    hs.normalize_rhs = cfg.pcg.normalize_rhs;
+    hs.clamp_min = cfg.clamp_min;
+    hs.clamp_max = cfg.clamp_max;
+    hs.before_scaling = cfg.damping == GB_DAMPING_BEFORE_SCALING;
+    hs.use_guard = cfg.use_rejection_guard;
+    hs.refresh_on_reject = cfg.refresh_on_reject;
+    hs.max_iterations = cfg.max_iterations;
+  }
+
+  // ------------------------------------------------------------- launches
+  unsigned vert_grid() const { return std::max(1u, div_up(static_cast<uint64_t>(act_.nc) + act_.np, 256)); }
+  unsigned col_grid() const { return std::max(1u, std::min(div_up(ncols_, 256), 148u * 8u)); }
+  unsigned cam_grid() const { return std::max(1u, div_up(act_.nc, kCamWarps)); }
+
+  void enqueue_linearize(int force) {
+    if (dev_.J)
+      k_lin_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, force);
+    else
+      k_lin_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, force);
+    CK(cudaGetLastError());
+    k_lin_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, force);
+    CK(cudaGetLastError());
+  }
+
+  void launch_hvp(const Dev<FP, SP>& d) {
+    if (d.J)
+      k_hvp_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
+    else
+      k_hvp_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
+    CK(cudaGetLastError());
+    k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d);
+    CK(cudaGetLastError());
+  }
+
+  // build_preconditioner + pcg_solve + unscale (linear_system.hpp:185-207)
+  void enqueue_solve(int pcg_max_it) {
+    k_precond<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+    k_rhs_norm<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+    k_pcg_init<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+    for (int k = 0; k < pcg_max_it; ++k) {
+      launch_hvp(dev_);
+      k_pcg_update<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+      CK(cudaGetLastError());
+      k_pcg_dir<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+      CK(cudaGetLastError());
+    }
+    k_step<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+  }
+
+  // One LM iteration (levenberg_marquardt.hpp:149-220) as a fixed kernel
+  // sequence; every kernel early-exits on the device flags it depends on.
+  void enqueue_iteration(int pcg_max_it) {
+    k_iter_begin<FP><<<1, 1, 0, s_>>>(st_, dev_.recs);
+    CK(cudaGetLastError());
+    enqueue_solve(pcg_max_it);
+    k_chi2_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, dev_.x_new, 0);
+    CK(cudaGetLastError());
+    k_decide<FP><<<1, 1, 0, s_>>>(st_, dev_.recs);
+    CK(cudaGetLastError());
+    k_commit<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+    enqueue_linearize(0);
+  }
+
+  void build_iteration_graph(int pcg_max_it) {
+    if (graph_exec_ && graph_pcg_it_ == pcg_max_it && graph_recs_ == dev_.recs) return;
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    graph_exec_ = nullptr;
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
+    enqueue_iteration(pcg_max_it);
+    CK(cudaStreamEndCapture(s_, &graph));
+    CK(cudaGraphInstantiate(&graph_exec_, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    graph_pcg_it_ = pcg_max_it;
+    graph_recs_ = dev_.recs;
+  }
+
+  gb_memory_account memory_account() const {
+    // analytic account, levenberg_marquardt.hpp:100-108 and README "Memory accounting"
+    struct LossFP {
+      int kind;
+      FP delta;
+    };
+    const uint64_t N = static_cast<uint64_t>(act_.free_dims);
+    gb_memory_account m{};
+    m.jacobian_bytes = g_.diff_mode == GB_DYNAMIC ? 0 : act_.n_active * 2 * 12 * sizeof(SP);
+    m.preconditioner_bytes = (81ull * act_.free_cams + 9ull * act_.free_pts) * sizeof(FP);
+    m.workspace_bytes = 5 * N * sizeof(SP) + 6 * N * sizeof(FP) + act_.n_active * (4 * sizeof(FP) + 2 * sizeof(A));
+    const uint64_t vtx = sizeof(uint64_t) + sizeof(void*) + 1 + sizeof(int64_t);
+    m.graph_bytes = g_.nc * (9 * sizeof(FP) + vtx) + g_.np * (3 * sizeof(FP) + vtx) +
+                    g_.ne * (2 * sizeof(uint32_t) + 2 * sizeof(FP) + 1 + 4 * sizeof(FP) + sizeof(LossFP) + 1);
+    return m;
+  }
+
+  GraphData& g_;
+  cudaStream_t s_ = nullptr;
+  Activation act_;
+  bool have_act_ = false;
+  uint64_t act_rev_ = 0;
+  int act_level_ = 0;
+  uint64_t ncols_ = 0;
+  std::vector<uint64_t> ref_to_int_;
+  Dev<FP, SP> dev_{};
+  State<FP>* st_ = nullptr;
+  State<FP> ls_state_{};
+  bool ls_ready_ = false;
+  FP* pinned_ = nullptr;
+  int* flag_host_ = nullptr;
+  size_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  int graph_pcg_it_ = -1;
+  gb_iteration_record* graph_recs_ = nullptr;
+  DBuf st_buf_, rec_buf_, dbg_buf_;
+  DBuf b_col_free_, b_dcam_, b_dlpt_, b_obs_, b_tile_ebeg_, b_tile_pbeg_, b_tile_chunk_, b_chunk_part_,
+      b_pt_slot_off_, b_pt_slots_, b_cam_part_off_, b_cam_part_idx_;
+  DBuf b_J_, b_w_, b_part_, b_x_, b_xn_, b_b_, b_cl_, b_D_, b_dx_, b_Hc_, b_Hp_, b_Mc_, b_Mp_, b_xs_, b_r_, b_z_, b_p_,
+      b_ap_, b_tr_, b_tr2_, b_tf_, b_cr_, b_cr2_, b_cf_, b_br_, b_br2_, b_bf_;
+};
+
+std::unique_ptr<SolverBase> make_solver(GraphData& g) {
+  switch (g.precision) {
+    case GB_FP64: return std::make_unique<Solver<double, double>>(g);
+    case GB_FP32: return std::make_unique<Solver<float, float>>(g);
+    case GB_FP32_BF16: return std::make_unique<Solver<float, bf16>>(g);
+  }
+  throw std::invalid_argument("invalid precision pair");
+}
+
+}  // namespace gb
+
+// ======================================================================= C ABI
+namespace {
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& what) {
+  g_err = what;
+  return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return GB_OK;
+  } catch (const gb::NoDevice& e) {
+    return set_err(GB_ERR_NO_DEVICE, e.what());
+  } catch (const gb::CudaError& e) {
+    return set_err(GB_ERR_CUDA, e.what());
+  } catch (const std::invalid_argument& e) {
+    return set_err(GB_ERR_INVALID_ARGUMENT, e.what());
+  } catch (const std::out_of_range& e) {
+    return set_err(GB_ERR_OUT_OF_RANGE, e.what());
+  } catch (const std::logic_error& e) {
+    return set_err(GB_ERR_LOGIC, e.what());
+  } catch (const std::runtime_error& e) {
+    return set_err(GB_ERR_RUNTIME, e.what());
+  } catch (const std::exception& e) {
+    return set_err(GB_ERR_RUNTIME, e.what());
+  }
+}
+}  // namespace
+
+struct gb_graph {
+  gb::GraphData data;
+  std::unique_ptr<gb::SolverBase> solver;
+  gb::SolverBase& get() {
+    if (!solver) solver = gb::make_solver(data);
+    return *solver;
+  }
+};
+
+extern "C" {
+
+void gb_default_config(gb_lm_config* c) {
+  c->max_iterations = 10;
+  c->tolerance = 1e-6;
+  c->level = 0;
+  c->tau = 1e-4;
+  c->pcg.max_iterations = 50;
+  c->pcg.tolerance = 1e-6;
+  c->pcg.rejection_ratio = 10.0;
+  c->pcg.normalize_rhs = 1;
+  c->clamp_min = 1e-6;
+  c->clamp_max = 1e32;
+  c->damping = GB_DAMPING_AFTER_SCALING;
+  c->use_rejection_guard = 1;
+  c->refresh_on_reject = 0;
+  c->lambda_max = 1e32;
+  c->gradient_tolerance = 1e-12;
+}
+
+const char* gb_last_error(void) { return g_err.c_str(); }
+
+int gb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+gb_graph* gb_create(int precision, int diff_mode, int device) {
+  gb_graph* out = nullptr;
+  const int rc = guarded([&] {
+    if (precision < GB_FP64 || precision > GB_FP32_BF16)
+      throw std::invalid_argument("invalid precision pair");
+    if (diff_mode < GB_ANALYTIC || diff_mode > GB_DYNAMIC) throw std::invalid_argument("unknown differentiation mode");
+    const int n = gb_device_count();
+    if (n == 0) throw gb::NoDevice("no CUDA device visible: the B200 solver has no CPU fallback");
+    if (device < 0 || device >= n) throw std::invalid_argument("invalid CUDA device ordinal");
+    auto* g = new gb_graph;
+    g->data.precision = precision;
+    g->data.diff_mode = diff_mode;
+    g->data.device = device;
+    out = g;
+  });
+  (void)rc;
+  return out;
+}
+
+void gb_destroy(gb_graph* g) { delete g; }
+
+int gb_set_cameras(gb_graph* g, void* params, uint64_t n, const uint8_t* fixed) {
+  return guarded([&] {
+    if (!params && n) throw std::invalid_argument("add_vertex: null handle");
+    g->data.cams = params;
+    g->data.nc = n;
+    g->data.cam_fixed.assign(fixed ? fixed : nullptr, fixed ? fixed + n : nullptr);
+    ++g->data.revision;
+  });
+}
+
+int gb_set_points(gb_graph* g, void* params, uint64_t n, const uint8_t* fixed) {
+  return guarded([&] {
+    if (!params && n) throw std::invalid_argument("add_vertex: null handle");
+    g->data.pts = params;
+    g->data.np = n;
+    g->data.pt_fixed.assign(fixed ? fixed : nullptr, fixed ? fixed + n : nullptr);
+    ++g->data.revision;
+  });
+}
+
+int gb_set_observations(gb_graph* g, uint64_t n, const uint32_t* cam, const uint32_t* pt, const void* observed,
+                        const uint8_t* level, int loss_kind, double huber_delta) {
+  return guarded([&] {
+    gb::GraphData& d = g->data;
+    if (n > 0xffffffffull) throw std::invalid_argument("more than 2^32 observations");
+    if (loss_kind != GB_LOSS_DEFAULT && loss_kind != GB_LOSS_HUBER) throw std::invalid_argument("unknown loss kind");
+    d.ne = n;
+    d.cam_idx.assign(cam, cam + n);
+    d.pt_idx.assign(pt, pt + n);
+    d.obs.resize(2 * n);
+    if (d.precision == GB_FP64) {
+      const double* o = static_cast<const double*>(observed);
+      std::copy(o, o + 2 * n, d.obs.begin());
+    } else {
+      const float* o = static_cast<const float*>(observed);
+      for (uint64_t i = 0; i < 2 * n; ++i) d.obs[i] = o[i];
+    }
+    d.level.assign(level ? level : nullptr, level ? level + n : nullptr);
+    d.loss_kind = loss_kind;
+    d.huber = huber_delta;
+    ++d.revision;
+  });
+}
+
+int gb_set_differentiation_mode(gb_graph* g, int mode) {
+  return guarded([&] {
+    if (mode < GB_ANALYTIC || mode > GB_DYNAMIC) throw std::invalid_argument("unknown differentiation mode");
+    if (mode != g->data.diff_mode) {
+      g->data.diff_mode = mode;
+      ++g->data.revision;
+    }
+  });
+}
+
+int gb_optimize(gb_graph* g, const gb_lm_config* cfg, gb_solve_report* report, gb_iteration_record* records,
+                int32_t max_records) {
+  return guarded([&] { g->get().optimize(*cfg, report, records, max_records); });
+}
+
+int gb_mse(gb_graph* g, double* out) {
+  return guarded([&] {
+    if (g->data.ne == 0) {
+      *out = 0.0;
+      return;
+    }
+    *out = g->get().residual_sum(0, true) / static_cast<double>(g->data.ne);
+  });
+}
+
+int gb_total_error(gb_graph* g, int level, double* out) {
+  return guarded([&] { *out = g->get().residual_sum(level, false); });
+}
+
+int gb_ls_linearize(gb_graph* g, int level, double cmin, double cmax, int damping, double* chi2, int64_t* n, void* b,
+                    void* diag, void* clamped, void* scaling, int32_t* finite) {
+  return guarded([&] { g->get().ls_linearize(level, cmin, cmax, damping, chi2, n, b, diag, clamped, scaling, finite); });
+}
+
+int gb_ls_hvp(gb_graph* g, const void* v, void* out, double lambda) {
+  return guarded([&] { g->get().ls_hvp(v, out, lambda); });
+}
+
+int gb_ls_preconditioner(gb_graph* g, double lambda, void* blocks, int32_t* fallbacks) {
+  return guarded([&] { g->get().ls_precond(lambda, blocks, fallbacks); });
+}
+
+int gb_ls_solve_step(gb_graph* g, double lambda, const gb_pcg_config* pcg, void* dx, gb_pcg_stats* stats, double* pred,
+                     int32_t* finite) {
+  return guarded([&] { g->get().ls_solve_step(lambda, *pcg, dx, stats, pred, finite); });
+}
+
+int gb_ls_jacobians(gb_graph* g, void* out) {
+  return guarded([&] { g->get().ls_jacobians(out); });
+}
+
+int gb_incidence(gb_graph* g, int descriptor, uint64_t* nseg, uint64_t* nitems, uint64_t* vos, uint64_t* offsets,
+                 uint32_t* items_factor, uint16_t* items_slot) {
+  return guarded([&] {
+    if (descriptor != 0 && descriptor != 1) throw std::out_of_range("incidence index");
+    const gb::Activation& a = g->get().activation();
+    const gb::Incidence& inc = descriptor == 0 ? a.cam_inc : a.pt_inc;
+    if (nseg) *nseg = inc.vertex_of_segment.size();
+    if (nitems) *nitems = inc.items.size();
+    if (vos) std::copy(inc.vertex_of_segment.begin(), inc.vertex_of_segment.end(), vos);
+    if (offsets) std::copy(inc.offsets.begin(), inc.offsets.end(), offsets);
+    if (items_factor) std::copy(inc.items.begin(), inc.items.end(), items_factor);
+    if (items_slot) std::fill(items_slot, items_slot + inc.items.size(), static_cast<uint16_t>(descriptor));
+  });
+}
+
+}  // extern "C"
