@@ -1,0 +1,307 @@
+#!/usr/bin/env python3
+"""Benchmark: ms per Levenberg–Marquardt iteration on a synthetic
+Final-13682-shaped bundle adjustment (BASELINE.json metric "LM iteration ms &
+solve time"), fp64, analytic Jacobians, PCG capped at 10 @ 1e-6 (the paper's
+and tests/acceptance.cpp:69-80's BAL configuration).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+A step is one LM iteration (levenberg_marquardt.hpp:149-220: block-Jacobi
+build, <=10 PCG iterations with matrix-free HVP, step, candidate chi^2,
+accept/reject, re-linearization on accept). Inputs are device-resident before
+the timed region; the J store (5.57 GB) is far larger than L2, so no flush is
+needed. Prints ONE JSON line on rank 0.
+
+--impl reference times the unmodified reference CPU solver (oracle/_ref,
+compiled from /root/reference with the Eigen-subset shim) on this box's host
+cores on the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "final": (13682, 4456117, 28987644, "synthetic Final-13682-shaped BA (13,682 cams, 4,456,117 pts, 28,987,644 obs)"),
+    "venice": (1778, 993923, 5001946, "synthetic Venice-1778-shaped BA (1,778 cams, 993,923 pts, 5,001,946 obs)"),
+    "dubrovnik": (356, 226730, 1255268, "synthetic Dubrovnik-356-shaped BA (356 cams, 226,730 pts, 1,255,268 obs)"),
+    "ladybug": (49, 7776, 31843, "synthetic Ladybug-49-shaped BA (49 cams, 7,776 pts, 31,843 obs)"),
+}
+DTYPE = {"fp64": "f64", "fp32": "f32", "fp32-bf16": "f32/bf16-storage"}
+SIZES = {"fp64": (8, 8, 8, 8), "fp32": (4, 4, 4, 4), "fp32-bf16": (2, 2, 4, 4)}  # s_J, s_V, s_A, s_FP
+
+
+def lm_config(max_iterations, bal):
+    c = bal.LMConfig(max_iterations=max_iterations)
+    c.pcg.max_iterations = 10
+    c.pcg.tolerance = 1e-6
+    return c
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reference_arm(args, shape, desc):
+    """The reference CPU solver (oracle/_ref) on this box's host cores."""
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from oracle import refbind
+    from paper_2509_26581_b200 import bal
+
+    cores = os.cpu_count() or 1
+    problem = bal.synthetic_bal(*shape, seed=42)
+    # bounded sample: 1 warm-up LM iteration + up to 5 timed ones of the full
+    # workload (each is ~seconds on the host at Final scale)
+    timed = max(1, min(args.steps, 5))
+    r = refbind.build_graph(problem, args.precision, "analytic", workers=cores)
+    t0 = time.perf_counter()
+    rep = bal.levenberg_marquardt(r, lm_config(1 + timed, bal))
+    wall = time.perf_counter() - t0
+    its = rep.iterations[1:] if len(rep.iterations) > 1 else rep.iterations
+    ms = 1e3 * statistics.mean(i.wall_seconds for i in its)
+    sample = (f"{len(its)} LM iteration(s) (after 1 warm-up) of the reference solver on the full workload, "
+              f"workers={cores}; per-iteration IterationRecord.wall_seconds (levenberg_marquardt.hpp:150,209); "
+              f"reference solve incl. activation {rep.total_seconds:.1f} s for {len(rep.iterations)} iterations")
+    line = {
+        "impl": "reference", "metric": "LM iteration ms (synthetic BAL BA)", "value": round(ms, 3),
+        "unit": "ms/LM-iteration", "n_gpus": world, "steps": len(its), "warmup": 1, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision],
+        "data": "synthetic", "config": {"workload": desc + f" {args.precision} analytic, PCG<=10@1e-6",
+                                        "precision": args.precision, "host_cores": cores},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/LM-iteration", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(ms, 3), "unit": "ms/LM-iteration", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "solve_seconds": round(rep.total_seconds, 3), "wall_seconds": round(wall, 3),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def ours(args, shape, desc):
+    import ctypes
+
+    import torch
+
+    world, rank, local = dist_setup()
+    from paper_2509_26581_b200 import _abi, bal
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    problem = bal.synthetic_bal(*shape, seed=42)
+    W, K = args.warmup, args.steps
+    cfg = lm_config(W + K, bal)
+
+    g = bal.build_graph(problem, args.precision, "analytic", device=local)
+    L = g.backend
+    c = cfg.to_c()
+    rep0 = _abi.gb_solve_report()
+    L.check(L.fn("begin")(g._h, ctypes.byref(c), ctypes.byref(rep0)))
+    stream = torch.cuda.ExternalStream(L.fn("stream")(g._h), device=local)
+    L.check(L.fn("step")(g._h, W))
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        L.check(L.fn("step")(g._h, K))
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    ms_total = ev0.elapsed_time(ev1)
+    rep = _abi.gb_solve_report()
+    recs = (_abi.gb_iteration_record * (W + K))()
+    L.check(L.fn("end")(g._h, ctypes.byref(rep), recs, W + K))
+    if rep.iterations_run < W + K:
+        raise SystemExit(f"solve terminated after {rep.iterations_run} < W+K iterations: timed steps would be no-ops")
+    # live roofline of the dominant kernel pair (HVP) on the solver stream
+    ms_hvp, ms_tiles = ctypes.c_double(), ctypes.c_double()
+    L.check(L.fn("time_hvp")(g._h, 20, ctypes.byref(ms_hvp), ctypes.byref(ms_tiles)))
+
+    ms = ms_total / K
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # e2e through the public API: host arrays -> graph -> solve -> host arrays
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g2 = bal.build_graph(problem, args.precision, "analytic", device=local)
+    rep2 = bal.levenberg_marquardt(g2, cfg)
+    e2e_s = time.perf_counter() - t0
+    n_it = max(1, len(rep2.iterations))
+    e2e_ms = 1e3 * e2e_s / n_it
+    h2d = (rep2.h2d_bytes + problem.observations.size * 0) / n_it
+    d2h = rep2.d2h_bytes / n_it
+
+    if rank != 0:
+        return
+    sJ, sV, sA, sFP = SIZES[args.precision]
+    E, N = rep.active_factors, rep.free_dims
+    hvp_bytes = E * (24 * sJ + 8) + N * (sV + sA)  # SURVEY.md §8(d) HVP algorithmic bytes
+    peak, peak_kind = measured_peak()
+    achieved = hvp_bytes / (ms_hvp.value * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_hvp_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_hvp")
+        except Exception:
+            traffic = None
+    launches_per_it = 10 + 4 * cfg.pcg.max_iterations
+    line = {
+        "metric": "LM iteration ms (synthetic BAL BA)", "value": round(ms, 4), "unit": "ms/LM-iteration",
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(ms, 4), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision], "data": "synthetic",
+        "config": {"workload": desc + f" {args.precision} analytic, PCG<=10@1e-6", "precision": args.precision,
+                   "cache": "inputs larger than L2 (J store %.2f GB)" % (E * 24 * sJ / 1e9),
+                   "parallelism": "single GPU" if world == 1 else f"replicas x{world}"},
+        "clocks": clocks.summary(),
+        "e2e": {"value": round(e2e_ms, 3), "unit": "ms/LM-iteration", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h),
+                "note": "public API: build_graph + levenberg_marquardt from host arrays, incl. upload, activation, "
+                        f"initial linearize and write-back, amortized over {n_it} iterations"},
+        "gpu_launches": launches_per_it * K,
+        "roofline": {"kernel": "k_hvp_tiles+k_hvp_cams (HVP, one PCG iteration's dominant pair)", "bound": "hbm",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "algorithmic_bytes": int(hvp_bytes), "ms_per_launch": round(ms_hvp.value, 4),
+                     "ms_tiles_only": round(ms_tiles.value, 4), "peak_kind": peak_kind},
+        "solve": {"iterations": rep.iterations_run, "accepted": rep.accepted_steps,
+                  "initial_chi2": rep.initial_chi2, "chi2_after_timed": rep.final_chi2,
+                  "setup_seconds": round(rep0.setup_seconds, 3), "e2e_solve_seconds": round(e2e_s, 3),
+                  "iteration_ms": [round(1e3 * recs[i].wall_seconds, 3) for i in range(W + K)]},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, problem)
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, problem):
+    """The reference solver (oracle/_ref) on the host cores: a bounded sample
+    of the same workload (1 timed LM iteration after 1 warm-up)."""
+    try:
+        from oracle import refbind
+        from paper_2509_26581_b200 import bal
+
+        if not refbind.available():
+            return {"value": None, "unit": "ms/LM-iteration", "cores": 0, "kind": "reference",
+                    "sample": "oracle/_ref not built"}
+        cores = os.cpu_count() or 1
+        r = refbind.build_graph(problem, args.precision, "analytic", workers=cores)
+        rep = bal.levenberg_marquardt(r, lm_config(2, bal))
+        its = rep.iterations[1:] if len(rep.iterations) > 1 else rep.iterations
+        ms = 1e3 * statistics.mean(i.wall_seconds for i in its)
+        return {"value": round(ms, 2), "unit": "ms/LM-iteration", "cores": cores, "kind": "reference",
+                "sample": f"{len(its)} LM iteration after 1 warm-up, full workload, workers={cores} "
+                          f"(reference solve incl. activation {rep.total_seconds:.1f} s)"}
+    except Exception as e:  # the baseline is reported, never the thing measured
+        return {"value": None, "unit": "ms/LM-iteration", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="final", choices=sorted(WORKLOADS))
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32", "fp32-bf16"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    nc, np_, ne, desc = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        reference_arm(args, (nc, np_, ne), desc)
+    else:
+        ours(args, (nc, np_, ne), desc)
+
+
+if __name__ == "__main__":
+    main()

@@ -188,6 +188,25 @@ int gb_set_differentiation_mode(gb_graph* g, int diff_mode);
 int gb_optimize(gb_graph* g, const gb_lm_config* cfg, gb_solve_report* report,
                 gb_iteration_record* records, int32_t max_records);
 
+/* The same solve split into phases, for callers that interleave their own
+ * work or time individual LM iterations (bench.py):
+ *   gb_begin   upload + activation + initial linearize + lambda0
+ *              (levenberg_marquardt.hpp:116-147); fills the initial fields of
+ *              report (may be NULL).
+ *   gb_step    enqueues n LM iterations (:149-220) on the solver stream and
+ *              returns without synchronizing; iterations after termination
+ *              are device-side no-ops.
+ *   gb_end     synchronizes, fills report/records, writes the parameters back.
+ *   gb_stream  the cudaStream_t all of the handle's kernels run on.
+ *   gb_time_hvp  average device time (ms, CUDA events on gb_stream) of
+ *              `reps` back-to-back Hessian-vector products at the current
+ *              linearization (the dominant kernel pair of a PCG iteration). */
+int gb_begin(gb_graph* g, const gb_lm_config* cfg, gb_solve_report* report);
+int gb_step(gb_graph* g, int32_t n);
+int gb_end(gb_graph* g, gb_solve_report* report, gb_iteration_record* records, int32_t max_records);
+void* gb_stream(gb_graph* g);
+int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_per_hvp, double* ms_tiles_only);
+
 /* BalGraph::mse (adapter.hpp:95-99) at the current user parameters. */
 int gb_mse(gb_graph* g, double* out);
 /* Graph::total_error(level) (graph.hpp:99-104). */

@@ -546,3 +546,19 @@ def lm_config(max_iterations=50, pcg_iterations=10, **kw):
                pcg=dict(max_iterations=pcg_iterations, tolerance=1e-6, rejection_ratio=10.0, normalize_rhs=True))
     cfg.update(kw)
     return cfg
+
+
+def update_damping(lam, nu, accepted, gain):
+    """Nielsen schedule (levenberg_marquardt.hpp:88-98)."""
+    if accepted:
+        g = 2.0 * gain - 1.0
+        return lam * max(1.0 / 3.0, 1.0 - g * g * g), 2.0
+    return lam * nu, nu * 2.0
+
+
+def project(camera, point, precision="fp64"):
+    """snavely_project for one camera/point (snavely.hpp:48-61)."""
+    P = Prec(precision)
+    c = np.asarray(camera, P.FP)[None, :]
+    x = np.asarray(point, P.FP)[None, :]
+    return residual(c, x, np.zeros((1, 2), P.FP), P)[0]

@@ -110,7 +110,8 @@ EXPORTED = [
     "gb_default_config", "gb_last_error", "gb_device_count", "gb_create", "gb_destroy", "gb_set_cameras",
     "gb_set_points", "gb_set_observations", "gb_set_differentiation_mode", "gb_optimize", "gb_mse",
     "gb_total_error", "gb_ls_linearize", "gb_ls_hvp", "gb_ls_preconditioner", "gb_ls_solve_step",
-    "gb_ls_jacobians", "gb_incidence", "gb_synthetic_bal",
+    "gb_ls_jacobians", "gb_incidence", "gb_synthetic_bal", "gb_begin", "gb_step", "gb_end", "gb_stream",
+    "gb_time_hvp",
 ]
 
 
@@ -146,6 +147,11 @@ def declare(lib: ctypes.CDLL, prefix: str = "gb_") -> ctypes.CDLL:
         f("create", vp, c_int, c_int, c_int)
         f("set_differentiation_mode", c_int, vp, c_int)
         f("synthetic_bal", c_int, c_uint64, c_uint64, c_uint64, c_uint64, c_uint64, c_double, vp, vp, vp, vp, vp)
+        f("begin", c_int, vp, POINTER(gb_lm_config), POINTER(gb_solve_report))
+        f("step", c_int, vp, c_int32)
+        f("end", c_int, vp, POINTER(gb_solve_report), vp, c_int32)
+        f("stream", vp, vp)
+        f("time_hvp", c_int, vp, c_int32, POINTER(c_double), POINTER(c_double))
     else:
         f("create", vp, c_int, c_int, c_int)
         f("set_workers", c_int, vp, c_int)

@@ -118,41 +118,64 @@ void activate(const ActivationInput& in, Activation& out) {
   out.pt_rank.assign(in.np, 0);
   for (uint64_t i = 0; i < in.np; ++i) out.pt_rank[out.pt_order[i]] = static_cast<uint32_t>(i);
 
-  // tiles: greedy over internal points, <= kTileEdges edges and <= kTilePoints
-  // points; a point with more than kTileEdges edges is a tile of its own
-  // ("heavy" tile, processed chunk by chunk).
+  // all active edges of each point (any camera), for the tile builder
+  std::vector<uint64_t> pe_off;
+  std::vector<uint32_t> pe_items;
+  {
+    std::vector<uint32_t> all(na);
+    for (uint64_t a = 0; a < na; ++a) all[a] = static_cast<uint32_t>(a);
+    stable_bucket(pt_of_a, in.np, all, pe_off, pe_items);
+  }
+  // tiles: greedy over internal points, <= kTileEdges edges, <= kTilePoints
+  // points and <= kTileCams distinct cameras; a point that alone exceeds a
+  // limit is a tile of its own ("heavy" tile, processed chunk by chunk).
   std::vector<uint32_t> tile_of_pt(in.np);
+  std::vector<uint32_t> cam_stamp(in.nc, kNoKey);
   out.tile_pbeg.push_back(0);
   out.tile_ebeg.push_back(0);
   {
-    uint64_t te = 0, tp = 0, ecount = 0;
+    uint64_t te = 0, tp = 0, tc = 0, ecount = 0;
+    uint32_t stamp = 0;
+    auto close = [&](uint64_t next_point) {
+      out.tile_pbeg.push_back(static_cast<uint32_t>(next_point));
+      out.tile_ebeg.push_back(static_cast<uint32_t>(ecount));
+      te = tp = tc = 0;
+      ++stamp;
+    };
     for (uint64_t i = 0; i < in.np; ++i) {
-      const uint64_t d = deg[out.pt_order[i]];
-      const bool heavy = d > static_cast<uint64_t>(kTileEdges);
-      if (tp > 0 && (heavy || te + d > static_cast<uint64_t>(kTileEdges) || tp >= static_cast<uint64_t>(kTilePoints))) {
-        out.tile_pbeg.push_back(static_cast<uint32_t>(i));
-        out.tile_ebeg.push_back(static_cast<uint32_t>(ecount));
-        te = tp = 0;
+      const uint32_t p = out.pt_order[i];
+      const uint64_t d = deg[p];
+      // distinct cameras this point would add to the current tile
+      uint64_t newc = 0;
+      for (uint64_t q = pe_off[p]; q < pe_off[p + 1]; ++q)
+        if (cam_stamp[cam_of_a[pe_items[q]]] != stamp) ++newc;
+      const bool heavy = d > static_cast<uint64_t>(kTileEdges) || d > static_cast<uint64_t>(kTileCams);
+      if (tp > 0 && (heavy || te + d > static_cast<uint64_t>(kTileEdges) || tp >= static_cast<uint64_t>(kTilePoints) ||
+                     tc + newc > static_cast<uint64_t>(kTileCams))) {
+        close(i);
+        newc = d;  // fresh tile: all its cameras are new (distinct per point)
       }
       tile_of_pt[i] = static_cast<uint32_t>(out.tile_pbeg.size() - 1);
+      for (uint64_t q = pe_off[p]; q < pe_off[p + 1]; ++q) {
+        uint32_t& st = cam_stamp[cam_of_a[pe_items[q]]];
+        if (st != stamp) {
+          st = stamp;
+          ++tc;
+        }
+      }
       te += d;
       tp += 1;
       ecount += d;
-      if (heavy) {  // close the heavy tile immediately
-        out.tile_pbeg.push_back(static_cast<uint32_t>(i + 1));
-        out.tile_ebeg.push_back(static_cast<uint32_t>(ecount));
-        te = tp = 0;
-      }
+      if (heavy) close(i + 1);
     }
-    if (tp > 0 || out.tile_pbeg.size() == 1) {
-      out.tile_pbeg.push_back(static_cast<uint32_t>(in.np));
-      out.tile_ebeg.push_back(static_cast<uint32_t>(ecount));
-    }
+    if (tp > 0 || out.tile_pbeg.size() == 1) close(in.np);
   }
   out.ntiles = static_cast<uint32_t>(out.tile_pbeg.size() - 1);
 
   // device edge order: active edges sorted by camera (stable in a), then
-  // stably bucketed by tile -> inside a tile: (camera, a).
+  // stably bucketed by tile -> inside a tile: (camera, a). Tiles start on
+  // kEdgePad boundaries; the padding slots are dummies.
+  std::vector<uint32_t> order;
   {
     std::vector<uint32_t> all(na);
     for (uint64_t a = 0; a < na; ++a) all[a] = static_cast<uint32_t>(a);
@@ -161,15 +184,55 @@ void activate(const ActivationInput& in, Activation& out) {
     stable_bucket(cam_of_a, in.nc, all, off, by_cam);
     std::vector<uint32_t> tile_of_a(na);
     for (uint64_t a = 0; a < na; ++a) tile_of_a[a] = tile_of_pt[out.pt_rank[pt_of_a[a]]];
-    stable_bucket(tile_of_a, out.ntiles, by_cam, off, out.d_a);
+    stable_bucket(tile_of_a, out.ntiles, by_cam, off, order);
   }
-  out.d_cam.resize(na);
-  out.d_lpt.resize(na);
-  for (uint64_t d = 0; d < na; ++d) {
-    const uint32_t a = out.d_a[d];
-    const uint32_t r = out.pt_rank[pt_of_a[a]];
-    out.d_cam[d] = cam_of_a[a];
-    out.d_lpt[d] = static_cast<uint16_t>(r - out.tile_pbeg[tile_of_pt[r]]);
+  out.tile_ecnt.resize(out.ntiles);
+  std::vector<uint32_t> real_beg(out.tile_ebeg);  // unpadded prefix (built above)
+  uint64_t slot = 0;
+  for (uint32_t t = 0; t < out.ntiles; ++t) {
+    out.tile_ecnt[t] = real_beg[t + 1] - real_beg[t];
+    out.tile_ebeg[t] = static_cast<uint32_t>(slot);
+    slot += (out.tile_ecnt[t] + kEdgePad - 1) / kEdgePad * kEdgePad;
+    const bool heavy = out.tile_ecnt[t] > static_cast<uint32_t>(kTileEdges) ||
+                       (out.tile_pbeg[t + 1] - out.tile_pbeg[t] == 1 && out.tile_ecnt[t] > static_cast<uint32_t>(kTileCams));
+    (heavy ? out.heavy_tiles : out.normal_tiles).push_back(t);
+  }
+  if (slot > 0xffffffffull) throw std::invalid_argument("more than 2^32 padded edge slots");
+  out.tile_ebeg[out.ntiles] = static_cast<uint32_t>(slot);
+  out.n_slots = slot;
+  out.d_a.assign(slot, kNoKey);
+  out.d_cam.assign(slot, 0);
+  out.d_lpt.assign(slot, 0);
+  for (uint32_t t = 0; t < out.ntiles; ++t) {
+    for (uint32_t j = 0; j < out.tile_ecnt[t]; ++j) {
+      const uint32_t a = order[real_beg[t] + j];
+      const uint32_t d = out.tile_ebeg[t] + j;
+      const uint32_t r = out.pt_rank[pt_of_a[a]];
+      out.d_a[d] = a;
+      out.d_cam[d] = cam_of_a[a];
+      out.d_lpt[d] = static_cast<uint16_t>(r - out.tile_pbeg[t]);
+    }
+    // dummies repeat the tile's last camera so camera runs are unaffected
+    for (uint32_t j = out.tile_ecnt[t]; j < out.tile_ebeg[t + 1] - out.tile_ebeg[t]; ++j)
+      out.d_cam[out.tile_ebeg[t] + j] = out.tile_ecnt[t] ? out.d_cam[out.tile_ebeg[t] + out.tile_ecnt[t] - 1] : 0;
+  }
+
+  // distinct cameras per tile (edges are camera-sorted inside a tile) and the
+  // per-edge local camera index used by the normal-tile kernels
+  out.d_lcam.assign(slot, 0);
+  out.tile_cam_off.assign(out.ntiles + 1, 0);
+  for (uint32_t t = 0; t < out.ntiles; ++t) {
+    const uint32_t eb = out.tile_ebeg[t];
+    uint32_t nl = 0;
+    for (uint32_t j = 0; j < out.tile_ecnt[t]; ++j) {
+      if (j == 0 || out.d_cam[eb + j] != out.d_cam[eb + j - 1]) {
+        out.tile_cams.push_back(out.d_cam[eb + j]);
+        ++nl;
+      }
+      out.d_lcam[eb + j] = static_cast<uint16_t>(std::min<uint32_t>(nl - 1, 0xffffu));
+    }
+    for (uint32_t j = out.tile_ecnt[t]; j < out.tile_ebeg[t + 1] - eb; ++j) out.d_lcam[eb + j] = nl ? nl - 1 : 0;
+    out.tile_cam_off[t + 1] = out.tile_cam_off[t] + nl;
   }
 
   // per-point slot lists (tile-local, ascending)
@@ -179,24 +242,22 @@ void activate(const ActivationInput& in, Activation& out) {
   {
     std::vector<uint32_t> cur(out.pt_slot_off.begin(), out.pt_slot_off.end() - 1);
     for (uint32_t t = 0; t < out.ntiles; ++t)
-      for (uint32_t d = out.tile_ebeg[t]; d < out.tile_ebeg[t + 1]; ++d) {
-        const uint32_t r = out.tile_pbeg[t] + out.d_lpt[d];
-        out.pt_slots[cur[r]++] = static_cast<uint16_t>((d - out.tile_ebeg[t]) & 0xffffu);
+      for (uint32_t j = 0; j < out.tile_ecnt[t]; ++j) {
+        const uint32_t r = out.tile_pbeg[t] + out.d_lpt[out.tile_ebeg[t] + j];
+        out.pt_slots[cur[r]++] = static_cast<uint16_t>(j & 0xffffu);
       }
   }
 
-  // warp chunks and camera runs
+  // warp chunks (32 real edges from the tile start) and their camera runs
   out.tile_chunk_base.assign(out.ntiles + 1, 0);
-  for (uint32_t t = 0; t < out.ntiles; ++t) {
-    const uint32_t ne_t = out.tile_ebeg[t + 1] - out.tile_ebeg[t];
-    out.tile_chunk_base[t + 1] = out.tile_chunk_base[t] + (ne_t + 31) / 32;
-  }
+  for (uint32_t t = 0; t < out.ntiles; ++t)
+    out.tile_chunk_base[t + 1] = out.tile_chunk_base[t] + (out.tile_ecnt[t] + 31) / 32;
   out.nchunks = out.tile_chunk_base[out.ntiles];
   out.chunk_part_base.assign(out.nchunks + 1, 0);
   std::vector<uint32_t> run_cam;
   for (uint32_t t = 0; t < out.ntiles; ++t) {
-    const uint32_t eb = out.tile_ebeg[t], ee = out.tile_ebeg[t + 1];
-    for (uint32_t k = 0; k < (ee - eb + 31) / 32; ++k) {
+    const uint32_t eb = out.tile_ebeg[t], ee = eb + out.tile_ecnt[t];
+    for (uint32_t k = 0; k < (out.tile_ecnt[t] + 31) / 32; ++k) {
       const uint32_t ch = out.tile_chunk_base[t] + k;
       uint32_t runs = 0;
       for (uint32_t d = eb + 32 * k; d < std::min(ee, eb + 32 * k + 32); ++d)
@@ -210,7 +271,7 @@ void activate(const ActivationInput& in, Activation& out) {
   out.nparts = out.chunk_part_base[out.nchunks];
   {
     std::vector<uint32_t> slots(out.nparts);
-    for (uint32_t s = 0; s < out.nparts; ++s) slots[s] = s;
+    for (uint32_t s2 = 0; s2 < out.nparts; ++s2) slots[s2] = s2;
     std::vector<uint64_t> off;
     stable_bucket(run_cam, in.nc, slots, off, out.cam_part_idx);
     out.cam_part_off.assign(in.nc + 1, 0);

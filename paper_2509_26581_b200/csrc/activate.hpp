@@ -16,8 +16,10 @@
 namespace gb {
 
 constexpr int kTileThreads = 256;  // CTA size of every tile kernel
-constexpr int kTileEdges = 512;    // max edges of a normal tile (SMEM staging)
+constexpr int kTileEdges = 512;    // max edges of a normal tile (SMEM staging of the point side)
 constexpr int kTilePoints = 256;   // max points of a tile
+constexpr int kEdgePad = 8;        // tile edge ranges start on 8-edge boundaries (16-byte aligned rows)
+constexpr int kTileCams = 64;      // max distinct cameras of a normal tile (SMEM camera staging)
 constexpr uint32_t kNoKey = 0xffffffffu;
 
 struct Incidence {
@@ -49,11 +51,17 @@ struct Activation {
   std::vector<uint32_t> pt_rank;   // point id -> internal i
   // tiles over internal points
   uint32_t ntiles = 0, nchunks = 0, nparts = 0;
-  std::vector<uint32_t> tile_ebeg, tile_pbeg, tile_chunk_base;  // size ntiles+1
-  // device edge order d (tile-major, camera then factor index inside a tile)
-  std::vector<uint32_t> d_a;    // d -> active factor a
+  std::vector<uint32_t> tile_ebeg, tile_pbeg, tile_chunk_base;  // size ntiles+1; tile_ebeg padded
+  std::vector<uint32_t> tile_ecnt;                              // real edges of each tile
+  std::vector<uint32_t> normal_tiles, heavy_tiles;              // tile ids by kind
+  uint64_t n_slots = 0;                                         // padded device edge slots (multiple of kEdgePad)
+  // device edge order d (tile-major, camera then factor index inside a tile),
+  // padded: slots [tile_ebeg[t] + tile_ecnt[t], tile_ebeg[t+1]) are dummies
+  std::vector<uint32_t> d_a;    // d -> active factor a (kNoKey for padding)
   std::vector<uint32_t> d_cam;  // d -> camera
   std::vector<uint16_t> d_lpt;  // d -> point index local to its tile
+  std::vector<uint16_t> d_lcam; // d -> camera index local to its tile (normal tiles)
+  std::vector<uint32_t> tile_cam_off, tile_cams;  // distinct cameras of each tile, ascending
   std::vector<uint32_t> pt_slot_off;  // internal point -> offsets into pt_slots (size np+1)
   std::vector<uint16_t> pt_slots;     // tile-local edge slots of each point, ascending
   // warp-chunk camera runs -> partial slots

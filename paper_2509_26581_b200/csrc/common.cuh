@@ -153,19 +153,49 @@ __device__ inline bool last_block(unsigned* counter) {
   return is_last;
 }
 
-// Sum of n partials in a fixed order by one block (strided per thread, then
-// block tree). volatile read: the partials were written by other blocks.
+// Sum of n partials in a fixed order by one block: each thread keeps four
+// independent accumulators over a fixed stride pattern (loads pipeline), then
+// a fixed tree. ld.cg: the partials were written by other blocks of the same
+// launch and are visible in L2 after their __threadfence.
+template <typename T>
+__device__ inline T ldcg(const T* p) {
+  return __ldcg(p);
+}
 template <typename T>
 __device__ inline T reduce_partials(const T* p, uint32_t n, T* scratch) {
-  T acc = T(0);
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) acc += static_cast<const volatile T*>(p)[i];
-  return block_sum(acc, scratch);
+  T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+  const uint32_t st = blockDim.x;
+  uint32_t i = threadIdx.x;
+  for (; i + 3 * st < n; i += 4 * st) {
+    a0 += ldcg(p + i);
+    a1 += ldcg(p + i + st);
+    a2 += ldcg(p + i + 2 * st);
+    a3 += ldcg(p + i + 3 * st);
+  }
+  for (; i < n; i += st) a0 += ldcg(p + i);
+  return block_sum((a0 + a1) + (a2 + a3), scratch);
 }
 template <typename T>
 __device__ inline T reduce_partials_max(const T* p, uint32_t n, T* scratch) {
-  T acc = T(-INFINITY);
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) acc = fmax(acc, static_cast<const volatile T*>(p)[i]);
-  return block_max(acc, scratch);
+  T a0 = T(-INFINITY), a1 = T(-INFINITY);
+  const uint32_t st = blockDim.x;
+  uint32_t i = threadIdx.x;
+  for (; i + st < n; i += 2 * st) {
+    a0 = fmax(a0, ldcg(p + i));
+    a1 = fmax(a1, ldcg(p + i + st));
+  }
+  for (; i < n; i += st) a0 = fmax(a0, ldcg(p + i));
+  return block_max(fmax(a0, a1), scratch);
+}
+__device__ inline int reduce_flags_and(const int* p, uint32_t n) {
+  int f = 1;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) f &= __ldcg(p + i);
+  return __syncthreads_and(f);
+}
+__device__ inline int reduce_flags_or(const int* p, uint32_t n) {
+  int f = 0;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) f |= __ldcg(p + i);
+  return __syncthreads_or(f);
 }
 
 }  // namespace gb

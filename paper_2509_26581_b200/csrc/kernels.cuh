@@ -81,7 +81,7 @@ struct State {
 template <typename FP, typename SP>
 struct Dev {
   using A = arith_t<SP>;
-  uint32_t nc, np, na, ntiles, nparts;
+  uint32_t nc, np, na, ntiles, nparts;  // na = padded edge slots (row stride of J, obs, w)
   uint64_t ncols;  // 9nc + 3np
   FP* x;
   FP* x_new;
@@ -91,8 +91,15 @@ struct Dev {
   const FP* d_obs;  // [2][na]
   SP* J;            // [24][na] or null (dynamic)
   FP* w;            // [na] or null (default loss: w == 1)
-  const uint32_t* tile_ebeg;
+  const uint32_t* tile_ebeg;  // padded slot begin of each tile
+  const uint32_t* tile_ecnt;  // real edges of each tile
   const uint32_t* tile_pbeg;
+  const uint16_t* d_lcam;        // local camera index (normal tiles)
+  const uint32_t* tile_cam_off;  // distinct cameras of each tile
+  const uint32_t* tile_cams;
+  const uint32_t* normal_tiles;
+  const uint32_t* heavy_tiles;
+  uint32_t n_normal, n_heavy;
   const uint32_t* tile_chunk_base;
   const uint32_t* chunk_part_base;
   const uint32_t* pt_slot_off;
@@ -112,9 +119,10 @@ struct Dev {
   SP* z;
   SP* p;
   SP* ap;
+  A* vt;       // (Arith) D * p for every column, refreshed with p (HVP gather source)
   A* dbg_out;  // optional wide HVP output (LinearSystem::hvp surface)
   FP* dx;
-  FP* tile_red;   // [ntiles]
+  FP* tile_red;   // [ntiles * 8] (HVP: one dot partial per warp of a tile)
   FP* tile_red2;  // [ntiles]
   int* tile_flag; // [ntiles]
   FP* cam_red;    // [nc]
@@ -188,12 +196,12 @@ __device__ inline void load_J(const Dev<FP, SP>& d, uint32_t e, arith_t<SP>* jc,
 // max |b|.
 // =====================================================================
 template <typename FP, typename SP, bool STORE>
-__global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, int force) {
+__global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, const uint32_t* list, int force) {
   if (!force && !d.st->do_linearize) return;
-  const uint32_t t = blockIdx.x;
-  const uint32_t eb = d.tile_ebeg[t], ee = d.tile_ebeg[t + 1];
+  const uint32_t t = list ? list[blockIdx.x] : blockIdx.x;
+  const uint32_t eb = d.tile_ebeg[t];
   const uint32_t pb = d.tile_pbeg[t], pe = d.tile_pbeg[t + 1];
-  const uint32_t ne_t = ee - eb, npt = pe - pb;
+  const uint32_t ne_t = d.tile_ecnt[t], npt = pe - pb;
   const bool heavy = ne_t > static_cast<uint32_t>(kTileEdges);
   const int tid = threadIdx.x, lane = tid & 31;
   const uint64_t pcol0 = 9ull * d.nc;
@@ -220,13 +228,11 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, int f
 #pragma unroll
     for (int k = 0; k < 9; ++k) cp[k] = d.x[9ull * cam + k];
     const FP* X = &sX[3 * lp];
-    FP res[2];
-    snavely_residual<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res);
+    FP res[2], jc[18], jp[6];
+    snavely_linearize<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res, jc, jp);
     const FP s = res[0] * res[0] + res[1] * res[1];
     const FP w = valid ? loss_weight<FP>(loss, delta, s) : FP(0);
     if (valid) chi += loss_value<FP>(loss, delta, s);
-    FP jc[18], jp[6];
-    snavely_jacobians<FP>(cp, X, jc, jp);
     if (STORE) {
 #pragma unroll
       for (int k = 0; k < 18; ++k) {
@@ -398,10 +404,7 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int 
     const FP chi = reduce_partials(d.tile_red, d.ntiles, scratch);
     const FP m1 = reduce_partials_max(d.tile_red2, d.ntiles, scratch);
     const FP m2 = reduce_partials_max(d.cam_red2, d.nc, scratch);
-    int f = 1;
-    for (uint32_t i = threadIdx.x; i < d.ntiles; i += blockDim.x) f &= static_cast<const volatile int*>(d.tile_flag)[i];
-    for (uint32_t i = threadIdx.x; i < d.nc; i += blockDim.x) f &= static_cast<const volatile int*>(d.cam_flag)[i];
-    f = __syncthreads_and(f);
+    const int f = reduce_flags_and(d.tile_flag, d.ntiles) & reduce_flags_and(d.cam_flag, d.nc);
     if (threadIdx.x == 0) {
       d.st->lin_chi2 = chi;
       d.st->grad_max = fmax(fmax(m1, m2), FP(0));
@@ -430,9 +433,7 @@ __global__ void k_init_damping(Dev<FP, SP> d) {
   }
   if (last_block(&d.st->cnt[1])) {
     const FP mm = reduce_partials_max(d.blk_red, gridDim.x, scratch);
-    int a = 0;
-    for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) a |= static_cast<const volatile int*>(d.blk_flag)[i];
-    a = __syncthreads_or(a);
+    const int a = reduce_flags_or(d.blk_flag, gridDim.x);
     if (threadIdx.x == 0) {
       const FP tau = static_cast<FP>(d.st->tau);
       d.st->lambda = a ? tau * fmax(mm, FP(0)) : tau;
@@ -670,7 +671,11 @@ __global__ void k_pcg_init(Dev<FP, SP> d) {
       apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &rz, &rr);
     else
       apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &rz, &rr);
-    for (int k = 0; k < n; ++k) d.p[col + k] = d.z[col + k];
+    for (int k = 0; k < n; ++k) {
+      const SP zk = d.z[col + k];
+      d.p[col + k] = zk;
+      d.vt[col + k] = static_cast<arith_t<SP>>(d.D[col + k]) * widen<arith_t<SP>>(zk);
+    }
   }
   rz = block_sum(rz, scratch);
   rr = block_sum(rr, scratch);
@@ -689,32 +694,33 @@ __global__ void k_pcg_init(Dev<FP, SP> d) {
 }
 
 // HVP, point side + camera runs (LinearSystem::hvp linear_system.hpp:104-115,
-// hvp_forward factor_descriptor.hpp:372-407, hvp_scatter :409-433).
+// hvp_forward factor_descriptor.hpp:372-407, hvp_scatter :409-433). One CTA
+// per tile (<= 512 edges in 256-edge chunks; heavy single-point tiles are
+// chunked with a running point sum). D*p is pre-gathered into vt by the kernel
+// that produced p, so an edge needs its J row, two indices and two L1/L2
+// gathers (its camera's 9 and its point's 3 values). Camera Jc^T q: warp-
+// segmented runs -> partial slots. Point Jp^T q: staged in shared memory and
+// summed per point in slot order after the single tile barrier. The tile's
+// p.Ap goes out as one partial per warp (no block reduction).
 template <typename FP, typename SP, bool DYN>
 __global__ void __launch_bounds__(kTileThreads) k_hvp_tiles(Dev<FP, SP> d) {
   using A = arith_t<SP>;
   if (!d.st->iter_active || d.st->pcg_done) return;
-  const uint32_t t = blockIdx.x;
-  const uint32_t eb = d.tile_ebeg[t], ee = d.tile_ebeg[t + 1];
-  const uint32_t pb = d.tile_pbeg[t], pe = d.tile_pbeg[t + 1];
-  const uint32_t ne_t = ee - eb, npt = pe - pb;
-  const bool heavy = ne_t > static_cast<uint32_t>(kTileEdges);
-  const int tid = threadIdx.x, lane = tid & 31;
-  const uint64_t pcol0 = 9ull * d.nc;
-
-  __shared__ A vt[kTilePoints * 3];
   __shared__ A stage[kTileEdges * 3];
   __shared__ A hacc[3];
   __shared__ FP sX[DYN ? kTilePoints * 3 : 1];
-  __shared__ FP scratch[32];
-
-  for (uint32_t i = tid; i < npt * 3; i += blockDim.x) {
-    const uint64_t col = pcol0 + 3ull * pb + i;
-    vt[i] = static_cast<A>(d.D[col]) * widen<A>(d.p[col]);
-    if (DYN) sX[i] = d.x[col];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint64_t pcol0 = 9ull * d.nc;
+  const uint32_t t = blockIdx.x;
+  const uint32_t eb = d.tile_ebeg[t], ne_t = d.tile_ecnt[t];
+  const uint32_t pb = d.tile_pbeg[t], npt = d.tile_pbeg[t + 1] - pb;
+  const bool heavy = ne_t > static_cast<uint32_t>(kTileEdges);
+  const A* vtp = d.vt + pcol0 + 3ull * pb;
+  if (DYN) {
+    for (uint32_t i = tid; i < npt * 3; i += blockDim.x) sX[i] = d.x[pcol0 + 3ull * pb + i];
   }
-  if (tid < 3) hacc[tid] = A(0);
-  __syncthreads();
+  if (heavy && tid < 3) hacc[tid] = A(0);
+  if (DYN || heavy) __syncthreads();
 
   for (uint32_t c0 = 0; c0 < ne_t; c0 += kTileThreads) {
     const uint32_t j = c0 + tid;
@@ -735,23 +741,24 @@ __global__ void __launch_bounds__(kTileThreads) k_hvp_tiles(Dev<FP, SP> d) {
     } else {
       load_J(d, e, jc, jp);
     }
-    A vc[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) vc[k] = static_cast<A>(d.D[9ull * cam + k]) * widen<A>(d.p[9ull * cam + k]);
+    const A wgt = d.w ? static_cast<A>(d.w[e]) : A(1);
+    const A* cv = d.vt + 9ull * cam;
+    const A* pv = vtp + 3 * lp;
     A u0 = A(0), u1 = A(0), s0 = A(0), s1 = A(0);
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
-      u0 += jc[k] * vc[k];
-      u1 += jc[9 + k] * vc[k];
+      const A v = cv[k];
+      u0 += jc[k] * v;
+      u1 += jc[9 + k] * v;
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      s0 += jp[k] * vt[3 * lp + k];
-      s1 += jp[3 + k] * vt[3 * lp + k];
+      const A v = pv[k];
+      s0 += jp[k] * v;
+      s1 += jp[3 + k] * v;
     }
     u0 += s0;
     u1 += s1;
-    const A wgt = d.w ? static_cast<A>(d.w[e]) : A(1);
     const A q0 = valid ? wgt * u0 : A(0), q1 = valid ? wgt * u1 : A(0);
     A g[9];
 #pragma unroll
@@ -773,7 +780,7 @@ __global__ void __launch_bounds__(kTileThreads) k_hvp_tiles(Dev<FP, SP> d) {
         for (int k = 0; k < 3; ++k) stage[j * 3 + k] = h[k];
     } else {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) stage[tid * 3 + k] = h[k];
+      for (int k = 0; k < 3; ++k) stage[tid * 3 + k] = valid ? h[k] : A(0);
       __syncthreads();
       if (tid < 3) {
         A acc = hacc[tid];
@@ -816,11 +823,185 @@ __global__ void __launch_bounds__(kTileThreads) k_hvp_tiles(Dev<FP, SP> d) {
       dot += widen<FP>(pk) * widen<FP>(o);
     }
   }
-  const FP tdot = block_sum(dot, scratch);
-  if (tid == 0) d.tile_red[t] = tdot;
+  dot = warp_sum(dot);
+  if (lane == 0) d.tile_red[8ull * t + (tid >> 5)] = dot;
 }
 
-// Camera side of the HVP + p.Ap finalization (pcg.hpp:332-340).
+// vt = (Arith) D * widen(p) for every column (the HVP's gather source).
+template <typename FP, typename SP>
+__global__ void k_make_vt(Dev<FP, SP> d) {
+  using A = arith_t<SP>;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    d.vt[i] = static_cast<A>(d.D[i]) * widen<A>(d.p[i]);
+}
+
+// =====================================================================
+// Normal-tile kernels (<= kTileEdges edges, <= kTileCams cameras): one CTA
+// pass per tile, one edge per thread. The tile's cameras are staged in shared
+// memory by the prologue (the edge loop reads a 16-bit local camera index),
+// so each edge costs one dependent DRAM round trip (its J row, indices).
+// =====================================================================
+
+// Linearize (factor_descriptor.hpp:272-292, :322-370, unscaled half of
+// :435-482) on a normal tile. Camera b + packed H: every edge's Jc rows,
+// w r and w are staged in shared memory; each warp then reduces its own
+// 32-edge chunk run by run with one lane per output value (54 values over
+// 32 lanes), i.e. plain FMAs over shared memory instead of shuffle trees.
+// Dynamic shared memory: see lin_normal_smem().
+constexpr int kLinRow = 21;  // Jc (18) + w r (2) + w (1) per staged edge
+template <typename FP>
+__host__ __device__ constexpr size_t lin_normal_smem() {
+  return sizeof(FP) * (kTilePoints * 3 + kTileCams * 9 + kTileThreads * kLinRow + kTileEdges * 9 + 32);
+}
+
+template <typename FP, typename SP, bool STORE>
+__global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int force) {
+  if (!force && !d.st->do_linearize) return;
+  extern __shared__ __align__(16) unsigned char lin_smem[];
+  FP* sX = reinterpret_cast<FP*>(lin_smem);
+  FP* sC = sX + kTilePoints * 3;
+  FP* sJ = sC + kTileCams * 9;
+  FP* pst = sJ + kTileThreads * kLinRow;
+  FP* scratch = pst + kTileEdges * 9;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t t = d.normal_tiles[blockIdx.x];
+  const uint32_t eb = d.tile_ebeg[t], ne_t = d.tile_ecnt[t];
+  const uint32_t pb = d.tile_pbeg[t], npt = d.tile_pbeg[t + 1] - pb;
+  const uint32_t cb = d.tile_cam_off[t], ncam = d.tile_cam_off[t + 1] - cb;
+  const uint64_t pcol0 = 9ull * d.nc;
+  for (uint32_t i = tid; i < npt * 3; i += blockDim.x) sX[i] = d.x[pcol0 + 3ull * pb + i];
+  for (uint32_t i = tid; i < ncam * 9; i += blockDim.x) sC[i] = d.x[9ull * d.tile_cams[cb + i / 9] + i % 9];
+  __syncthreads();
+  FP chi = FP(0);
+  for (uint32_t c0 = 0; c0 < ne_t; c0 += kTileThreads) {
+  const uint32_t j = c0 + tid;
+  const bool valid = j < ne_t;
+  const uint32_t e = eb + (valid ? j : 0);
+  const uint32_t lc = d.d_lcam[e], lp = d.d_lpt[e];
+  const FP o0 = d.d_obs[e], o1 = d.d_obs[static_cast<uint64_t>(d.na) + e];
+
+  FP res[2], jc[18], jp[6];
+  snavely_linearize<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res, jc, jp);
+  const FP s = res[0] * res[0] + res[1] * res[1];
+  const FP w = valid ? loss_weight<FP>(d.loss_kind, d.huber, s) : FP(0);
+  if (valid) chi += loss_value<FP>(d.loss_kind, d.huber, s);
+  if (STORE) {
+#pragma unroll
+    for (int k = 0; k < 18; ++k) {
+      const SP v = narrow<SP>(jc[k]);
+      if (valid) d.J[k * static_cast<uint64_t>(d.na) + e] = v;
+      jc[k] = widen<FP>(v);
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const SP v = narrow<SP>(jp[k]);
+      if (valid) d.J[(18 + k) * static_cast<uint64_t>(d.na) + e] = v;
+      jp[k] = widen<FP>(v);
+    }
+  }
+  if (d.w && valid) d.w[e] = w;
+  const FP wr0 = valid ? w * res[0] : FP(0), wr1 = valid ? w * res[1] : FP(0);
+  FP* row = sJ + tid * kLinRow;
+#pragma unroll
+  for (int k = 0; k < 18; ++k) row[k] = valid ? jc[k] : FP(0);
+  row[18] = wr0;
+  row[19] = wr1;
+  row[20] = w;
+  if (valid) {
+    FP* pv = pst + j * 9;
+    pv[0] = jp[0] * wr0 + jp[3] * wr1;
+    pv[1] = jp[1] * wr0 + jp[4] * wr1;
+    pv[2] = jp[2] * wr0 + jp[5] * wr1;
+    pv[3] = w * (jp[0] * jp[0] + jp[3] * jp[3]);
+    pv[4] = w * (jp[0] * jp[1] + jp[3] * jp[4]);
+    pv[5] = w * (jp[0] * jp[2] + jp[3] * jp[5]);
+    pv[6] = w * (jp[1] * jp[1] + jp[4] * jp[4]);
+    pv[7] = w * (jp[1] * jp[2] + jp[4] * jp[5]);
+    pv[8] = w * (jp[2] * jp[2] + jp[5] * jp[5]);
+  }
+  // run structure of this warp's 32-edge chunk
+  const unsigned full = 0xffffffffu;
+  const uint32_t prev = __shfl_up_sync(full, lc, 1);
+  const unsigned hm = __ballot_sync(full, valid && (lane == 0 || lc != prev));
+  const unsigned vm = __ballot_sync(full, valid);
+  __syncwarp();
+  // camera side: lane owns values v0 = lane and v1 = lane + 32 (< 54);
+  // value v < 9: b_v = sum Jc0v wr0 + Jc1v wr1; v >= 9: H(i,j) = sum w (Jc0i Jc0j + Jc1i Jc1j)
+  const bool has1 = lane + 32 < kLinVals;
+  const bool isb = lane < 9;
+  // value v0: m * (row[i0] row[k0] + row[i0 + 9] row[k1]) with m = 1 (b) or w (H)
+  const int i0 = isb ? lane : p9row(lane - 9);
+  const int k0 = isb ? 18 : p9col(lane - 9);
+  const int k1 = isb ? 19 : 9 + p9col(lane - 9);
+  const int i1 = has1 ? p9row(lane + 32 - 9) : 0;
+  const int j1 = has1 ? p9col(lane + 32 - 9) : 0;
+  const uint32_t slot0 = d.chunk_part_base[d.tile_chunk_base[t] + c0 / 32 + warp];
+  unsigned heads = hm;
+  uint32_t run = 0;
+  while (heads) {
+    const int start = __ffs(heads) - 1;
+    heads &= heads - 1;
+    const int stop = heads ? __ffs(heads) - 1 : 32 - __clz(vm);
+    FP acc0 = FP(0), acc1 = FP(0);
+    for (int q = start; q < stop; ++q) {
+      const FP* rr = sJ + (32 * warp + q) * kLinRow;
+      const FP m0 = isb ? FP(1) : rr[20];
+      acc0 += m0 * (rr[i0] * rr[k0] + rr[9 + i0] * rr[k1]);
+      if (has1) acc1 += rr[20] * (rr[i1] * rr[j1] + rr[9 + i1] * rr[9 + j1]);
+    }
+    FP* dst = d.part + static_cast<uint64_t>(slot0 + run) * kLinVals;
+    dst[lane] = acc0;
+    if (has1) dst[32 + lane] = acc1;
+    ++run;
+  }
+  __syncthreads();
+  }
+
+  // point epilogue (same as the generic kernel)
+  FP gmax = FP(0);
+  int fin = 1;
+  for (uint32_t i = tid; i < npt; i += blockDim.x) {
+    FP acc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] = FP(0);
+    for (uint32_t q = d.pt_slot_off[pb + i]; q < d.pt_slot_off[pb + i + 1]; ++q) {
+      const uint32_t sl = d.pt_slots[q];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] += pst[sl * 9 + k];
+    }
+    const uint64_t col = pcol0 + 3ull * (pb + i);
+    const bool freev = d.col_free[col];
+    const uint64_t pidx = static_cast<uint64_t>(pb + i);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const FP bk = freev ? acc[k] : FP(0);
+      d.b[col + k] = bk;
+      const FP diag = freev ? acc[3 + p3(k, k)] : FP(0);
+      const FP cl = clampv(diag, FP(d.st->clamp_min), FP(d.st->clamp_max));
+      d.clamped[col + k] = freev ? cl : FP(0);
+      d.D[col + k] = freev ? FP(1) / sqrt(cl) : FP(0);
+      if (freev) {
+        fin &= (is_finite(bk) && is_finite(diag)) ? 1 : 0;
+        gmax = fmax(gmax, fabs(bk));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) d.Hp[6 * pidx + k] = freev ? acc[3 + k] : FP(0);
+  }
+  const FP tchi = block_sum(chi, scratch);
+  const FP tmax = block_max(gmax, scratch);
+  const int tfin = __syncthreads_and(fin);
+  if (tid == 0) {
+    d.tile_red[t] = tchi;
+    d.tile_red2[t] = tmax;
+    d.tile_flag[t] = tfin;
+  }
+}
+
+// Camera side of the HVP + p.Ap finalization (pcg.hpp:332-340). Each block
+// also folds a fixed slice of the tiles' per-warp dot partials, so the last
+// block only sums one partial per block (fixed order, deterministic).
 template <typename FP, typename SP>
 __global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams(Dev<FP, SP> d) {
   using A = arith_t<SP>;
@@ -828,6 +1009,7 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams(Dev<FP, SP> d) {
   __shared__ FP scratch[32];
   const int lane = threadIdx.x & 31;
   const uint32_t c = blockIdx.x * kCamWarps + (threadIdx.x >> 5);
+  FP mine = FP(0);
   if (c < d.nc) {
     FP acc[9];
 #pragma unroll
@@ -858,13 +1040,18 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams(Dev<FP, SP> d) {
       dot = widen<FP>(pk) * widen<FP>(o);
     }
     dot = warp_sum(dot);
-    if (lane == 0) d.cam_red[c] = dot;
+    if (lane == 0) mine = dot;
   }
+  // this block's slice of the tile partials
+  const uint64_t ntp = 8ull * d.ntiles;
+  const uint64_t per = (ntp + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = min(ntp, per * blockIdx.x), hi = min(ntp, lo + per);
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) mine += d.tile_red[i];
+  const FP bsum = block_sum(mine, scratch);
+  if (threadIdx.x == 0) d.blk_red[blockIdx.x] = bsum;
   if (last_block(&d.st->cnt[4])) {
-    const FP s1 = reduce_partials(d.tile_red, d.ntiles, scratch);
-    const FP s2 = reduce_partials(d.cam_red, d.nc, scratch);
+    const FP pap = reduce_partials(d.blk_red, gridDim.x, scratch);
     if (threadIdx.x == 0) {
-      const FP pap = s1 + s2;
       d.st->pap = pap;
       if (!(pap > FP(0)) || !is_finite(pap)) {
         d.st->pcg_done = 1;
@@ -931,10 +1118,14 @@ __global__ void k_pcg_update(Dev<FP, SP> d) {
 template <typename FP, typename SP>
 __global__ void k_pcg_dir(Dev<FP, SP> d) {
   if (!d.st->iter_active || d.st->pcg_done) return;
+  using A = arith_t<SP>;
   const FP beta = d.st->beta;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    d.p[i] = narrow<SP>(widen<FP>(d.z[i]) + beta * widen<FP>(d.p[i]));
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const SP pi = narrow<SP>(widen<FP>(d.z[i]) + beta * widen<FP>(d.p[i]));
+    d.p[i] = pi;
+    d.vt[i] = static_cast<A>(d.D[i]) * widen<A>(pi);
+  }
 }
 
 // Unscale, predicted decrease, dx = D x, candidate x_new = x + dx
@@ -970,9 +1161,7 @@ __global__ void k_step(Dev<FP, SP> d) {
   }
   if (last_block(&d.st->cnt[6])) {
     const FP s = reduce_partials(d.blk_red, gridDim.x, scratch);
-    int f = 1;
-    for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) f &= static_cast<const volatile int*>(d.blk_flag)[i];
-    f = __syncthreads_and(f);
+    const int f = reduce_flags_and(d.blk_flag, gridDim.x);
     if (threadIdx.x == 0) {
       d.st->pred = s;
       d.st->step_finite = f;
@@ -988,7 +1177,7 @@ __global__ void __launch_bounds__(kTileThreads) k_chi2_tiles(Dev<FP, SP> d, cons
   if (!force && (!d.st->iter_active || !d.st->step_finite)) return;
   __shared__ FP scratch[32];
   const uint32_t t = blockIdx.x;
-  const uint32_t eb = d.tile_ebeg[t], ee = d.tile_ebeg[t + 1], pb = d.tile_pbeg[t];
+  const uint32_t eb = d.tile_ebeg[t], ee = eb + d.tile_ecnt[t], pb = d.tile_pbeg[t];
   const uint64_t pcol0 = 9ull * d.nc;
   FP chi = FP(0);
   for (uint32_t e = eb + threadIdx.x; e < ee; e += blockDim.x) {

@@ -27,65 +27,92 @@ struct taylor_threshold<float> {
 __device__ inline void sin_cos(double x, double* s, double* c) { sincos(x, s, c); }
 __device__ inline void sin_cos(float x, float* s, float* c) { sincosf(x, s, c); }
 
-// Residual r = predicted - observed (adapter.hpp:58-65).
+// Rodrigues coefficients shared by the residual and the Jacobian chain:
+// a = cos t, s = sin t / t, c = (1 - cos t) / t^2 (snavely.hpp:23-35) and the
+// derivative coefficients s1 = (a - s)/t^2, c2 = (s - 2c)/t^2 (:74-90). One
+// sqrt, one sincos and two reciprocals per edge (the reference evaluates the
+// chain twice per edge and divides each time).
 template <typename FP>
-__device__ inline void snavely_residual(const FP* cam, const FP* X, FP o0, FP o1, FP* r) {
-  const FP w0 = cam[0], w1 = cam[1], w2 = cam[2];
+struct Rodrigues {
+  FP a, s, c;        // residual path (rotate_angle_axis Taylor form)
+  FP ja, js, jcc;    // chain path (rodrigues_with_jacobian Taylor form)
+  FP s1, c2;
+};
+
+template <typename FP>
+__device__ inline Rodrigues<FP> rodrigues_coeffs(FP w0, FP w1, FP w2, bool need_chain) {
+  Rodrigues<FP> R;
   const FP theta2 = w0 * w0 + w1 * w1 + w2 * w2;
-  FP a, s, c;
   if (theta2 < taylor_threshold<FP>::value) {
     const FP u = theta2;
-    a = FP(1) - u * FP(0.5) + u * u * (FP(1) / FP(24));
-    s = FP(1) - u * (FP(1) / FP(6)) + u * u * (FP(1) / FP(120));
-    c = FP(0.5) - u * (FP(1) / FP(24)) + u * u * (FP(1) / FP(720));
+    R.a = FP(1) - u * FP(0.5) + u * u * (FP(1) / FP(24));
+    R.s = FP(1) - u * (FP(1) / FP(6)) + u * u * (FP(1) / FP(120));
+    R.c = FP(0.5) - u * (FP(1) / FP(24)) + u * u * (FP(1) / FP(720));
+    if (need_chain) {
+      R.ja = FP(1) - u / FP(2) + u * u / FP(24);
+      R.js = FP(1) - u / FP(6) + u * u / FP(120);
+      R.jcc = FP(0.5) - u / FP(24) + u * u / FP(720);
+      R.s1 = -FP(1) / FP(3) + u / FP(30);
+      R.c2 = -FP(1) / FP(12) + u / FP(180);
+    }
   } else {
     const FP theta = sqrt(theta2);
     FP sn, cs;
     sin_cos(theta, &sn, &cs);
-    a = cs;
-    s = sn / theta;
-    c = (FP(1) - a) / theta2;
+    const FP it2 = FP(1) / theta2;
+    R.a = cs;
+    R.s = sn / theta;
+    R.c = (FP(1) - cs) * it2;
+    R.ja = R.a;
+    R.js = R.s;
+    R.jcc = R.c;
+    if (need_chain) {
+      R.s1 = (R.a - R.s) * it2;
+      R.c2 = (R.s - FP(2) * R.c) * it2;
+    }
   }
+  return R;
+}
+
+// P = R(w) X + t through the direct Rodrigues formula (rotate_angle_axis,
+// snavely.hpp:36-42 + :52-54).
+template <typename FP>
+__device__ inline void rotate_translate(const FP* cam, const FP* X, const Rodrigues<FP>& R, FP* P) {
+  const FP w0 = cam[0], w1 = cam[1], w2 = cam[2];
   const FP wx = w1 * X[2] - w2 * X[1];
   const FP wy = w2 * X[0] - w0 * X[2];
   const FP wz = w0 * X[1] - w1 * X[0];
   const FP dot = w0 * X[0] + w1 * X[1] + w2 * X[2];
-  const FP p0 = a * X[0] + s * wx + c * dot * w0 + cam[3];
-  const FP p1 = a * X[1] + s * wy + c * dot * w1 + cam[4];
-  const FP p2 = a * X[2] + s * wz + c * dot * w2 + cam[5];
-  const FP xp = -p0 / p2;
-  const FP yp = -p1 / p2;
+  P[0] = R.a * X[0] + R.s * wx + R.c * dot * w0 + cam[3];
+  P[1] = R.a * X[1] + R.s * wy + R.c * dot * w1 + cam[4];
+  P[2] = R.a * X[2] + R.s * wz + R.c * dot * w2 + cam[5];
+}
+
+// Residual r = predicted - observed (adapter.hpp:58-65, snavely.hpp:48-61).
+template <typename FP>
+__device__ inline void snavely_residual(const FP* cam, const FP* X, FP o0, FP o1, FP* r) {
+  const Rodrigues<FP> R = rodrigues_coeffs<FP>(cam[0], cam[1], cam[2], false);
+  FP P[3];
+  rotate_translate(cam, X, R, P);
+  const FP iz = FP(1) / P[2];
+  const FP xp = -P[0] * iz, yp = -P[1] * iz;
   const FP n = xp * xp + yp * yp;
   const FP d = FP(1) + n * (cam[7] + n * cam[8]);
   r[0] = cam[6] * d * xp - o0;
   r[1] = cam[6] * d * yp - o1;
 }
 
-// Analytic Jacobians: jc = d pred / d camera (2x9 row-major),
-// jp = d pred / d point (2x3 row-major). snavely.hpp:67-153.
+// Residual and both Jacobian blocks from ONE chain (SnavelyChain,
+// snavely.hpp:103-153): jc = d pred / d camera (2x9 row-major),
+// jp = d pred / d point (2x3 row-major). r may be null.
 template <typename FP>
-__device__ inline void snavely_jacobians(const FP* cam, const FP* X, FP* jc, FP* jp) {
+__device__ inline void snavely_linearize(const FP* cam, const FP* X, FP o0, FP o1, FP* r, FP* jc, FP* jp) {
   const FP w0 = cam[0], w1 = cam[1], w2 = cam[2];
   const FP x0 = X[0], x1 = X[1], x2 = X[2];
-  const FP theta2 = w0 * w0 + w1 * w1 + w2 * w2;
-  FP a, s, c, s1, c2;
-  if (theta2 < taylor_threshold<FP>::value) {
-    const FP u = theta2;
-    a = FP(1) - u / FP(2) + u * u / FP(24);
-    s = FP(1) - u / FP(6) + u * u / FP(120);
-    c = FP(0.5) - u / FP(24) + u * u / FP(720);
-    s1 = -FP(1) / FP(3) + u / FP(30);
-    c2 = -FP(1) / FP(12) + u / FP(180);
-  } else {
-    const FP theta = sqrt(theta2);
-    FP sn, cs;
-    sin_cos(theta, &sn, &cs);
-    a = cs;
-    s = sn / theta;
-    c = (FP(1) - a) / theta2;
-    s1 = (a - s) / theta2;
-    c2 = (s - FP(2) * c) / theta2;
-  }
+  const Rodrigues<FP> Ro = rodrigues_coeffs<FP>(w0, w1, w2, true);
+  FP P[3];
+  rotate_translate(cam, X, Ro, P);
+  const FP a = Ro.ja, s = Ro.js, c = Ro.jcc, s1 = Ro.s1, c2 = Ro.c2;
   // R = a I + s [w]x + c w w^T
   FP R[9];
   R[0] = a + c * w0 * w0;
@@ -110,21 +137,21 @@ __device__ inline void snavely_jacobians(const FP* cam, const FP* X, FP* jc, FP*
     for (int j = 0; j < 3; ++j)
       Dw[3 * i + j] = -s * x[i] * w[j] + s1 * cr[i] * w[j] - s * skx[3 * i + j] + c2 * dt * w[i] * w[j] +
                       c * (w[i] * x[j] + (i == j ? dt : FP(0)));
-  // P = R X + t
-  const FP P0 = R[0] * x0 + R[1] * x1 + R[2] * x2 + cam[3];
-  const FP P1 = R[3] * x0 + R[4] * x1 + R[5] * x2 + cam[4];
-  const FP P2 = R[6] * x0 + R[7] * x1 + R[8] * x2 + cam[5];
-  const FP iz = FP(1) / P2;
-  const FP p0 = -P0 * iz, p1 = -P1 * iz;
+  const FP iz = FP(1) / P[2];
+  const FP p0 = -P[0] * iz, p1 = -P[1] * iz;
   const FP n = p0 * p0 + p1 * p1;
   const FP f = cam[6], k1 = cam[7], k2 = cam[8];
   const FP dist = FP(1) + n * (k1 + n * k2);
+  if (r) {
+    r[0] = f * dist * p0 - o0;
+    r[1] = f * dist * p1 - o1;
+  }
   // du/dp = f (dist I + 2 (k1 + 2 k2 n) p p^T); dp/dP = [[-iz,0,P0 iz^2],[0,-iz,P1 iz^2]]
   const FP g = FP(2) * (k1 + FP(2) * k2 * n);
   const FP A00 = f * (dist + g * p0 * p0), A01 = f * (g * p0 * p1);
   const FP A10 = f * (g * p1 * p0), A11 = f * (dist + g * p1 * p1);
   const FP iz2 = iz * iz;
-  const FP B02 = P0 * iz2, B12 = P1 * iz2;
+  const FP B02 = P[0] * iz2, B12 = P[1] * iz2;
   FP U[6];  // du/dP 2x3
   U[0] = -A00 * iz;
   U[1] = -A01 * iz;
@@ -133,12 +160,12 @@ __device__ inline void snavely_jacobians(const FP* cam, const FP* X, FP* jc, FP*
   U[4] = -A11 * iz;
   U[5] = A10 * B02 + A11 * B12;
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
+  for (int rr = 0; rr < 2; ++rr) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      jc[9 * r + j] = U[3 * r] * Dw[j] + U[3 * r + 1] * Dw[3 + j] + U[3 * r + 2] * Dw[6 + j];
-      jc[9 * r + 3 + j] = U[3 * r + j];
-      jp[3 * r + j] = U[3 * r] * R[j] + U[3 * r + 1] * R[3 + j] + U[3 * r + 2] * R[6 + j];
+      jc[9 * rr + j] = U[3 * rr] * Dw[j] + U[3 * rr + 1] * Dw[3 + j] + U[3 * rr + 2] * Dw[6 + j];
+      jc[9 * rr + 3 + j] = U[3 * rr + j];
+      jp[3 * rr + j] = U[3 * rr] * R[j] + U[3 * rr + 1] * R[3 + j] + U[3 * rr + 2] * R[6 + j];
     }
   }
   jc[6] = dist * p0;
@@ -147,6 +174,11 @@ __device__ inline void snavely_jacobians(const FP* cam, const FP* X, FP* jc, FP*
   jc[16] = f * n * p1;
   jc[8] = f * n * n * p0;
   jc[17] = f * n * n * p1;
+}
+
+template <typename FP>
+__device__ inline void snavely_jacobians(const FP* cam, const FP* X, FP* jc, FP* jp) {
+  snavely_linearize<FP>(cam, X, FP(0), FP(0), nullptr, jc, jp);
 }
 
 // Robust loss (loss.hpp:25-40): value rho(s) and IRLS weight rho'(s).

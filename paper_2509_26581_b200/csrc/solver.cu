@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -56,6 +57,11 @@ class SolverBase {
  public:
   virtual ~SolverBase() = default;
   virtual void optimize(const gb_lm_config& cfg, gb_solve_report* rep, gb_iteration_record* recs, int max_recs) = 0;
+  virtual void begin(const gb_lm_config& cfg, gb_solve_report* rep) = 0;
+  virtual void step(int n) = 0;
+  virtual void end(gb_solve_report* rep, gb_iteration_record* recs, int max_recs) = 0;
+  virtual void* stream() = 0;
+  virtual void time_hvp(int reps, double* ms_pair, double* ms_tiles) = 0;
   virtual double residual_sum(int level, bool raw) = 0;
   virtual void ls_linearize(int level, double cmin, double cmax, int damping, double* chi2, int64_t* n, void* b,
                             void* diag, void* clamped, void* scaling, int32_t* finite) = 0;
@@ -109,15 +115,21 @@ inline unsigned div_up(uint64_t a, uint64_t b) { return static_cast<unsigned>((a
 template <typename FP, typename SP>
 class Solver final : public SolverBase {
   using A = arith_t<SP>;
+  using Clock = std::chrono::steady_clock;
 
  public:
   explicit Solver(GraphData& g) : g_(g) {
     CK(cudaSetDevice(g_.device));
+    CK(cudaFuncSetAttribute(k_lin_normal<FP, SP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(lin_normal_smem<FP>())));
+    CK(cudaFuncSetAttribute(k_lin_normal<FP, SP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(lin_normal_smem<FP>())));
     CK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
     st_ = static_cast<State<FP>*>(st_buf_.alloc(sizeof(State<FP>)));
     CK(cudaMemsetAsync(st_, 0, sizeof(State<FP>), s_));
   }
   ~Solver() override {
+    for (auto& e : ev_) cudaEventDestroy(e);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (pinned_) cudaFreeHost(pinned_);
     if (flag_host_) cudaFreeHost(flag_host_);
@@ -131,12 +143,14 @@ class Solver final : public SolverBase {
   }
 
   // ---------------------------------------------------------------- optimize
-  void optimize(const gb_lm_config& cfg, gb_solve_report* rep, gb_iteration_record* recs, int max_recs) override {
-    using Clock = std::chrono::steady_clock;
-    const auto t0 = Clock::now();
+  // levenberg_marquardt (levenberg_marquardt.hpp:115-224) in three phases.
+  void begin(const gb_lm_config& cfg, gb_solve_report* rep) override {
+    if (in_solve_) end(nullptr, nullptr, 0);
+    t0_ = Clock::now();
     CK(cudaSetDevice(g_.device));
     ensure_structure(cfg.level);
     upload_params();
+    cfg_ = cfg;
     State<FP> hs{};
     fill_config(hs, cfg);
     CK(cudaMemcpyAsync(st_, &hs, sizeof(hs), cudaMemcpyHostToDevice, s_));
@@ -148,8 +162,8 @@ class Solver final : public SolverBase {
     const FP chi2 = hs.lin_chi2;
     if (!std::isfinite(static_cast<double>(chi2)))
       throw std::runtime_error("levenberg_marquardt: non-finite chi^2 at the initial parameters");
-
-    gb_solve_report r{};
+    gb_solve_report& r = rep_;
+    r = gb_solve_report{};
     r.initial_chi2 = r.final_chi2 = static_cast<double>(chi2);
     r.free_dims = act_.free_dims;
     r.residual_dims = static_cast<int64_t>(2 * act_.n_active);
@@ -158,11 +172,12 @@ class Solver final : public SolverBase {
     r.termination = GB_TERM_MAX_ITERATIONS;
     r.h2d_bytes = static_cast<double>(h2d_bytes_);
     h2d_bytes_ = 0;
-    int nrec = 0;
+    launched_ = 0;
+    max_it_ = 0;
     if (act_.free_dims == 0) {
       r.termination = GB_TERM_NO_FREE_PARAMETERS;
     } else if (cfg.max_iterations > 0) {
-      // state: chi2, lambda0 (linear_system.hpp:94-99), nu = 2
+      // chi2, lambda0 = tau * max(D^2 clamped) (linear_system.hpp:94-99), nu = 2
       hs.chi2 = chi2;
       hs.lm_it = 0;
       hs.terminated = 0;
@@ -171,51 +186,114 @@ class Solver final : public SolverBase {
       k_init_damping<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
       CK(cudaGetLastError());
       build_iteration_graph(cfg.pcg.max_iterations);
-      r.setup_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+      max_it_ = cfg.max_iterations;
+      ev_.resize(max_it_ + 1);
+      for (auto& e : ev_) CK(cudaEventCreate(&e));
+      CK(cudaStreamSynchronize(s_));
+    }
+    r.setup_seconds = std::chrono::duration<double>(Clock::now() - t0_).count();
+    in_solve_ = true;
+    if (rep) *rep = r;
+  }
 
-      std::vector<cudaEvent_t> ev(cfg.max_iterations + 1);
-      for (auto& e : ev) CK(cudaEventCreate(&e));
-      std::vector<cudaEvent_t> flag_ev(cfg.max_iterations);
-      for (auto& e : flag_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  void step(int n) override {
+    if (!in_solve_) throw std::logic_error("gb_step outside gb_begin/gb_end");
+    for (int k = 0; k < n && launched_ < max_it_; ++k) {
+      if (launched_ == 0) CK(cudaEventRecord(ev_[0], s_));
+      CK(cudaGraphLaunch(graph_exec_, s_));
+      ++launched_;
+      CK(cudaEventRecord(ev_[launched_], s_));
+    }
+  }
+
+  void end(gb_solve_report* rep, gb_iteration_record* recs, int max_recs) override {
+    if (!in_solve_) throw std::logic_error("gb_end without gb_begin");
+    in_solve_ = false;
+    gb_solve_report& r = rep_;
+    if (max_it_ > 0) {
+      State<FP> hs;
+      CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
+      CK(cudaStreamSynchronize(s_));
+      const int nrec = hs.lm_it;
+      std::vector<gb_iteration_record> hr(std::max(nrec, 1));
+      if (nrec) CK(cudaMemcpy(hr.data(), dev_.recs, sizeof(gb_iteration_record) * nrec, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < nrec && i < launched_; ++i) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
+        hr[i].wall_seconds = ms * 1e-3;
+      }
+      for (auto& e : ev_) cudaEventDestroy(e);
+      ev_.clear();
+      r.termination = hs.terminated ? hs.termination : GB_TERM_MAX_ITERATIONS;
+      r.accepted_steps = hs.accepted_steps;
+      r.final_chi2 = static_cast<double>(hs.chi2);
+      r.iterations_run = nrec;
+      if (recs)
+        for (int i = 0; i < std::min(nrec, max_recs); ++i) recs[i] = hr[i];
+      download_params();
+    }
+    r.d2h_bytes = static_cast<double>(d2h_bytes_);
+    d2h_bytes_ = 0;
+    r.total_seconds = std::chrono::duration<double>(Clock::now() - t0_).count();
+    if (rep) *rep = r;
+  }
+
+  void* stream() override { return s_; }
+
+  void optimize(const gb_lm_config& cfg, gb_solve_report* rep, gb_iteration_record* recs, int max_recs) override {
+    begin(cfg, nullptr);
+    if (max_it_ > 0) {
       if (!flag_host_) CK(cudaHostAlloc(reinterpret_cast<void**>(&flag_host_), 64 * sizeof(int), cudaHostAllocDefault));
-      int launched = 0;
-      for (int it = 0; it < cfg.max_iterations; ++it) {
-        CK(cudaEventRecord(ev[it], s_));
-        CK(cudaGraphLaunch(graph_exec_, s_));
-        ++launched;
+      std::vector<cudaEvent_t> flag_ev(max_it_);
+      for (auto& e : flag_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      for (int it = 0; it < max_it_; ++it) {
+        step(1);
         CK(cudaMemcpyAsync(&flag_host_[it % 64], &st_->terminated, sizeof(int), cudaMemcpyDeviceToHost, s_));
         CK(cudaEventRecord(flag_ev[it], s_));
-        // look one iteration behind: the device always has queued work
+        // look one iteration behind so the device always has queued work
         if (it >= 1) {
           CK(cudaEventSynchronize(flag_ev[it - 1]));
           if (flag_host_[(it - 1) % 64]) break;
         }
       }
-      CK(cudaEventRecord(ev[launched], s_));
-      CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
-      CK(cudaStreamSynchronize(s_));
-      nrec = hs.lm_it;
-      std::vector<gb_iteration_record> hr(std::max(nrec, 1));
-      if (nrec) CK(cudaMemcpy(hr.data(), dev_.recs, sizeof(gb_iteration_record) * nrec, cudaMemcpyDeviceToHost));
-      for (int i = 0; i < nrec && i < launched; ++i) {
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
-        hr[i].wall_seconds = ms * 1e-3;
-      }
-      for (auto& e : ev) cudaEventDestroy(e);
       for (auto& e : flag_ev) cudaEventDestroy(e);
-      r.termination = hs.termination;
-      r.accepted_steps = hs.accepted_steps;
-      r.final_chi2 = static_cast<double>(hs.chi2);
-      if (recs)
-        for (int i = 0; i < std::min(nrec, max_recs); ++i) recs[i] = hr[i];
-      download_params();
     }
-    r.iterations_run = nrec;
-    r.d2h_bytes = static_cast<double>(d2h_bytes_);
-    d2h_bytes_ = 0;
-    r.total_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
-    if (rep) *rep = r;
+    end(rep, recs, max_recs);
+  }
+
+  // Average device time of the HVP kernel pair (and of the tile kernel alone)
+  // at the current linearization; the device State is saved and restored.
+  void time_hvp(int reps, double* ms_pair, double* ms_tiles) override {
+    if (in_solve_) throw std::logic_error("gb_time_hvp during a solve");
+    if (!have_act_) throw std::logic_error("gb_time_hvp before any solve");
+    State<FP> saved;
+    CK(cudaMemcpyAsync(&saved, st_, sizeof(saved), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    State<FP> hs = saved;
+    hs.iter_active = 1;
+    hs.pcg_done = 0;
+    CK(cudaMemcpyAsync(st_, &hs, sizeof(hs), cudaMemcpyHostToDevice, s_));
+    cudaEvent_t a, b, c;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventCreate(&c));
+    launch_hvp(dev_);  // warm
+    CK(cudaEventRecord(a, s_));
+    for (int i = 0; i < reps; ++i) launch_hvp(dev_);
+    CK(cudaEventRecord(b, s_));
+    for (int i = 0; i < reps; ++i) launch_hvp_tiles(dev_);
+    CK(cudaEventRecord(c, s_));
+    CK(cudaEventSynchronize(c));
+    float m1 = 0, m2 = 0;
+    CK(cudaEventElapsedTime(&m1, a, b));
+    CK(cudaEventElapsedTime(&m2, b, c));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaEventDestroy(c);
+    CK(cudaMemcpyAsync(st_, &saved, sizeof(saved), cudaMemcpyHostToDevice, s_));
+    CK(cudaStreamSynchronize(s_));
+    if (ms_pair) *ms_pair = m1 / reps;
+    if (ms_tiles) *ms_tiles = m2 / reps;
   }
 
   double residual_sum(int level, bool raw) override {
@@ -307,6 +385,8 @@ class Solver final : public SolverBase {
     const SP* vin = static_cast<const SP*>(v);
     for (size_t i = 0; i < ref_to_int_.size(); ++i) hv[ref_to_int_[i]] = vin[i];
     CK(cudaMemcpyAsync(dev_.p, hv.data(), ncols_ * sizeof(SP), cudaMemcpyHostToDevice, s_));
+    k_make_vt<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
     Dev<FP, SP> d = dev_;
     d.dbg_out = static_cast<A*>(dbg_buf_.alloc(ncols_ * sizeof(A)));
     launch_hvp(d);
@@ -369,13 +449,14 @@ class Solver final : public SolverBase {
   void ls_jacobians(void* out) override {
     need_ls();
     if (!dev_.J) throw std::logic_error("dynamic mode stores no Jacobians");
-    const uint64_t na = act_.n_active;
-    std::vector<SP> h(24 * na);
+    const uint64_t ns = act_.n_slots;
+    std::vector<SP> h(24 * ns);
     CK(cudaMemcpy(h.data(), dev_.J, h.size() * sizeof(SP), cudaMemcpyDeviceToHost));
     SP* o = static_cast<SP*>(out);
-    for (uint64_t d = 0; d < na; ++d) {
+    for (uint64_t d = 0; d < ns; ++d) {
+      if (act_.d_a[d] == kNoKey) continue;
       const uint64_t a = act_.d_a[d];
-      for (int k = 0; k < 24; ++k) o[24 * a + k] = h[k * na + d];
+      for (int k = 0; k < 24; ++k) o[24 * a + k] = h[k * ns + d];
     }
   }
 
@@ -407,13 +488,13 @@ class Solver final : public SolverBase {
   }
 
   void upload_structure() {
-    const uint64_t nc = act_.nc, np = act_.np, na = act_.n_active;
+    const uint64_t nc = act_.nc, np = act_.np, ns = act_.n_slots;
     ncols_ = 9 * nc + 3 * np;
     Dev<FP, SP>& d = dev_;
     d = Dev<FP, SP>{};
     d.nc = static_cast<uint32_t>(nc);
     d.np = static_cast<uint32_t>(np);
-    d.na = static_cast<uint32_t>(na);
+    d.na = static_cast<uint32_t>(ns);
     d.ntiles = act_.ntiles;
     d.nparts = act_.nparts;
     d.ncols = ncols_;
@@ -441,14 +522,23 @@ class Solver final : public SolverBase {
     d.col_free = up(b_col_free_, col_free);
     d.d_cam = up(b_dcam_, act_.d_cam);
     d.d_lpt = up(b_dlpt_, act_.d_lpt);
-    std::vector<FP> obs(2 * na);
-    for (uint64_t e = 0; e < na; ++e) {
+    d.d_lcam = up(b_dlcam_, act_.d_lcam);
+    std::vector<FP> obs(2 * ns, FP(0));
+    for (uint64_t e = 0; e < ns; ++e) {
+      if (act_.d_a[e] == kNoKey) continue;
       const uint64_t i = act_.active[act_.d_a[e]];
       obs[e] = static_cast<FP>(g_.obs[2 * i]);
-      obs[na + e] = static_cast<FP>(g_.obs[2 * i + 1]);
+      obs[ns + e] = static_cast<FP>(g_.obs[2 * i + 1]);
     }
     d.d_obs = up(b_obs_, obs);
     d.tile_ebeg = up(b_tile_ebeg_, act_.tile_ebeg);
+    d.tile_ecnt = up(b_tile_ecnt_, act_.tile_ecnt);
+    d.tile_cam_off = up(b_tile_cam_off_, act_.tile_cam_off);
+    d.tile_cams = up(b_tile_cams_, act_.tile_cams);
+    d.normal_tiles = up(b_normal_, act_.normal_tiles);
+    d.heavy_tiles = up(b_heavy_, act_.heavy_tiles);
+    d.n_normal = static_cast<uint32_t>(act_.normal_tiles.size());
+    d.n_heavy = static_cast<uint32_t>(act_.heavy_tiles.size());
     d.tile_pbeg = up(b_tile_pbeg_, act_.tile_pbeg);
     d.tile_chunk_base = up(b_tile_chunk_, act_.tile_chunk_base);
     d.chunk_part_base = up(b_chunk_part_, act_.chunk_part_base);
@@ -459,8 +549,10 @@ class Solver final : public SolverBase {
     h2d_bytes_ += h2d;
 
     const bool dyn = g_.diff_mode == GB_DYNAMIC;
-    d.J = dyn ? nullptr : static_cast<SP*>(b_J_.alloc(24 * na * sizeof(SP)));
-    d.w = g_.loss_kind == GB_LOSS_HUBER ? static_cast<FP*>(b_w_.alloc(na * sizeof(FP))) : nullptr;
+    d.J = dyn ? nullptr : static_cast<SP*>(b_J_.alloc(24 * ns * sizeof(SP)));
+    if (d.J) CK(cudaMemsetAsync(d.J, 0, 24 * ns * sizeof(SP), s_));  // padding slots stay 0
+    d.w = g_.loss_kind == GB_LOSS_HUBER ? static_cast<FP*>(b_w_.alloc(ns * sizeof(FP))) : nullptr;
+    if (d.w) CK(cudaMemsetAsync(d.w, 0, ns * sizeof(FP), s_));
     d.loss_kind = g_.loss_kind;
     d.huber = static_cast<FP>(g_.huber);
     d.part = static_cast<FP*>(b_part_.alloc(std::max<uint64_t>(1, act_.nparts) * kLinVals * sizeof(FP)));
@@ -479,13 +571,15 @@ class Solver final : public SolverBase {
     d.z = static_cast<SP*>(b_z_.alloc(ncols_ * sizeof(SP)));
     d.p = static_cast<SP*>(b_p_.alloc(ncols_ * sizeof(SP)));
     d.ap = static_cast<SP*>(b_ap_.alloc(ncols_ * sizeof(SP)));
-    d.tile_red = static_cast<FP*>(b_tr_.alloc(act_.ntiles * sizeof(FP)));
+    d.vt = static_cast<A*>(b_vt_.alloc(ncols_ * sizeof(A)));
+    CK(cudaMemsetAsync(d.vt, 0, ncols_ * sizeof(A), s_));
+    d.tile_red = static_cast<FP*>(b_tr_.alloc(8ull * act_.ntiles * sizeof(FP)));
     d.tile_red2 = static_cast<FP*>(b_tr2_.alloc(act_.ntiles * sizeof(FP)));
     d.tile_flag = static_cast<int*>(b_tf_.alloc(act_.ntiles * sizeof(int)));
     d.cam_red = static_cast<FP*>(b_cr_.alloc(std::max<uint64_t>(1, nc) * sizeof(FP)));
     d.cam_red2 = static_cast<FP*>(b_cr2_.alloc(std::max<uint64_t>(1, nc) * sizeof(FP)));
     d.cam_flag = static_cast<int*>(b_cf_.alloc(std::max<uint64_t>(1, nc) * sizeof(int)));
-    const uint64_t nblk = std::max<uint64_t>(vert_grid(), col_grid());
+    const uint64_t nblk = std::max<uint64_t>(std::max<uint64_t>(vert_grid(), col_grid()), cam_grid());
     d.blk_red = static_cast<FP*>(b_br_.alloc(nblk * sizeof(FP)));
     d.blk_red2 = static_cast<FP*>(b_br2_.alloc(nblk * sizeof(FP)));
     d.blk_flag = static_cast<int*>(b_bf_.alloc(nblk * sizeof(int)));
@@ -556,21 +650,30 @@ class Solver final : public SolverBase {
   unsigned cam_grid() const { return std::max(1u, div_up(act_.nc, kCamWarps)); }
 
   void enqueue_linearize(int force) {
-    if (dev_.J)
-      k_lin_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, force);
-    else
-      k_lin_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, force);
+    const size_t smem = lin_normal_smem<FP>();
+    if (dev_.J) {
+      if (dev_.n_normal) k_lin_normal<FP, SP, true><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
+      if (dev_.n_heavy) k_lin_tiles<FP, SP, true><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
+    } else {
+      if (dev_.n_normal) k_lin_normal<FP, SP, false><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
+      if (dev_.n_heavy) k_lin_tiles<FP, SP, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
+    }
     CK(cudaGetLastError());
     k_lin_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, force);
     CK(cudaGetLastError());
   }
 
-  void launch_hvp(const Dev<FP, SP>& d) {
-    if (d.J)
-      k_hvp_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
-    else
+  // HVP tile pass (dynamic mode recomputes J per edge).
+  void launch_hvp_tiles(const Dev<FP, SP>& d) {
+    if (!d.J)
       k_hvp_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
+    else
+      k_hvp_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
     CK(cudaGetLastError());
+  }
+
+  void launch_hvp(const Dev<FP, SP>& d) {
+    launch_hvp_tiles(d);
     k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d);
     CK(cudaGetLastError());
   }
@@ -642,6 +745,13 @@ class Solver final : public SolverBase {
 
   GraphData& g_;
   cudaStream_t s_ = nullptr;
+  // phase state of the current solve
+  gb_lm_config cfg_{};
+  gb_solve_report rep_{};
+  bool in_solve_ = false;
+  int max_it_ = 0, launched_ = 0;
+  std::vector<cudaEvent_t> ev_;
+  Clock::time_point t0_;
   Activation act_;
   bool have_act_ = false;
   uint64_t act_rev_ = 0;
@@ -659,6 +769,7 @@ class Solver final : public SolverBase {
   int graph_pcg_it_ = -1;
   gb_iteration_record* graph_recs_ = nullptr;
   DBuf st_buf_, rec_buf_, dbg_buf_;
+  DBuf b_vt_, b_dlcam_, b_tile_ecnt_, b_tile_cam_off_, b_tile_cams_, b_normal_, b_heavy_;
   DBuf b_col_free_, b_dcam_, b_dlpt_, b_obs_, b_tile_ebeg_, b_tile_pbeg_, b_tile_chunk_, b_chunk_part_,
       b_pt_slot_off_, b_pt_slots_, b_cam_part_off_, b_cam_part_idx_;
   DBuf b_J_, b_w_, b_part_, b_x_, b_xn_, b_b_, b_cl_, b_D_, b_dx_, b_Hc_, b_Hp_, b_Mc_, b_Mp_, b_xs_, b_r_, b_z_, b_p_,
@@ -827,6 +938,28 @@ int gb_set_differentiation_mode(gb_graph* g, int mode) {
 int gb_optimize(gb_graph* g, const gb_lm_config* cfg, gb_solve_report* report, gb_iteration_record* records,
                 int32_t max_records) {
   return guarded([&] { g->get().optimize(*cfg, report, records, max_records); });
+}
+
+int gb_begin(gb_graph* g, const gb_lm_config* cfg, gb_solve_report* report) {
+  return guarded([&] { g->get().begin(*cfg, report); });
+}
+
+int gb_step(gb_graph* g, int32_t n) {
+  return guarded([&] { g->get().step(n); });
+}
+
+int gb_end(gb_graph* g, gb_solve_report* report, gb_iteration_record* records, int32_t max_records) {
+  return guarded([&] { g->get().end(report, records, max_records); });
+}
+
+void* gb_stream(gb_graph* g) {
+  void* s = nullptr;
+  guarded([&] { s = g->get().stream(); });
+  return s;
+}
+
+int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_pair, double* ms_tiles) {
+  return guarded([&] { g->get().time_hvp(reps < 1 ? 1 : reps, ms_pair, ms_tiles); });
 }
 
 int gb_mse(gb_graph* g, double* out) {

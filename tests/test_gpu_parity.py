@@ -152,10 +152,22 @@ def test_lm_parity_fp64(gpu, ref, ladybug):
 
 @pytest.mark.parametrize("precision", ["fp32", "fp32-bf16"])
 def test_lm_parity_low_precision(gpu, ref, ladybug, precision):
-    g, r, ra, rb = run_pair(ladybug, ref, precision)
+    # At tolerance 1e-4 (resolvable in float) the LM trace is decided by the
+    # algorithm: same iteration count and accept pattern as the reference.
+    cfg = bal_cfg()
+    cfg.tolerance = 1e-4
+    g, r, ra, rb = run_pair(ladybug, ref, precision, cfg=cfg)
+    assert ra.termination == rb.termination
     assert len(ra.iterations) == len(rb.iterations)
+    assert [i.accepted for i in ra.iterations] == [i.accepted for i in rb.iterations]
     assert abs(ra.final_chi2 - rb.final_chi2) <= 1e-4 * rb.final_chi2
     assert ra.memory == rb.memory
+    # At the BAL config's 1e-6 the reference's own float chi^2 (a sequential
+    # sum) carries ~3e-6 relative rounding noise, so the last accept/terminate
+    # decision is noise-decided (a faithful numpy restatement also differs by
+    # one iteration, tests/test_oracle_cpu.py); cost parity still holds.
+    g, r, ra, rb = run_pair(ladybug, ref, precision)
+    assert abs(ra.final_chi2 - rb.final_chi2) <= 1e-4 * rb.final_chi2
 
 
 def test_lm_parity_dynamic(gpu, ref, ladybug):
@@ -209,3 +221,26 @@ def test_tiny_and_heavy_tiles(gpu, ref):
     for prob in (bal.synthetic_bal(*TINY, seed=11), p):
         g, r, ra, rb = run_pair(prob, ref, cfg=bal_cfg(12))
         assert_trace_parity(ra, rb, 1e-6)
+
+
+def test_stepping_api_matches_optimize(gpu, ladybug):
+    import ctypes
+
+    from paper_2509_26581_b200 import _abi
+
+    cfg = bal_cfg(8)
+    g1 = bal.build_graph(ladybug, "fp64")
+    r1 = bal.levenberg_marquardt(g1, cfg)
+    g2 = bal.build_graph(ladybug, "fp64")
+    L = g2.backend
+    c = cfg.to_c()
+    L.check(L.fn("begin")(g2._h, ctypes.byref(c), None))
+    for _ in range(8):
+        L.check(L.fn("step")(g2._h, 1))
+    rep = _abi.gb_solve_report()
+    L.check(L.fn("end")(g2._h, ctypes.byref(rep), None, 0))
+    assert rep.final_chi2 == r1.final_chi2 and rep.iterations_run == len(r1.iterations)
+    assert np.array_equal(g1.points, g2.points)
+    ms = ctypes.c_double()
+    L.check(L.fn("time_hvp")(g2._h, 3, ctypes.byref(ms), None))
+    assert ms.value > 0
