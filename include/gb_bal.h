@@ -207,6 +207,27 @@ int gb_end(gb_graph* g, gb_solve_report* report, gb_iteration_record* records, i
 void* gb_stream(gb_graph* g);
 int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_per_hvp, double* ms_tiles_only);
 
+/* ---- multi-GPU sharding (no reference counterpart: the reference is a
+ * single-process CPU solver) -------------------------------
+ * One process (or host thread) per shard. Every rank registers the FULL
+ * problem; the solve shards it into contiguous point-tile ranges balanced by
+ * edge count, replicates the cameras, and allreduces the camera-sized vectors
+ * and PCG scalars every PCG iteration. After gb_optimize every rank holds the
+ * complete refined cameras and points.
+ *   kind 0: NCCL; id = the 128-byte ncclUniqueId from gb_nccl_unique_id on
+ *           rank 0, shared with the other ranks out of band.
+ *   kind 1: in-process loopback (ranks are host threads on one GPU; for
+ *           testing the sharded path on a single device); id = uint64 key.
+ * gb_shard_plan (host only) reports each rank's [tile0,tile1), [point0,point1)
+ * (internal order), edge count and (optionally) the owner rank of every point
+ * for `world` ranks. world == 1 with kind 0 runs the collective code path on
+ * a single rank. */
+int gb_nccl_unique_id(void* out128);
+int gb_set_distributed(gb_graph* g, int world, int rank, int kind, const void* id);
+int gb_shard_plan(uint64_t num_cameras, uint64_t num_points, uint64_t n, const uint32_t* camera_index,
+                  const uint32_t* point_index, int world, uint32_t* tiles_out, uint32_t* points_out,
+                  uint64_t* edges_out, uint32_t* point_owner);
+
 /* BalGraph::mse (adapter.hpp:95-99) at the current user parameters. */
 int gb_mse(gb_graph* g, double* out);
 /* Graph::total_error(level) (graph.hpp:99-104). */

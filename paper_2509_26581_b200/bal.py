@@ -314,6 +314,15 @@ class BalGraph:
         self._levels = np.ascontiguousarray(levels, dtype=np.uint8)
         self._bind()
 
+    # -- sharding (multi-GPU)
+    def set_distributed(self, world: int, rank: int, kind: str = "nccl", uid: bytes = b""):
+        """Shard this graph over `world` ranks (this handle is `rank`). kind
+        'nccl': uid = nccl_unique_id() from rank 0; kind 'loopback': ranks are
+        host threads of this process on one GPU, uid = an 8-byte group key."""
+        buf = ctypes.create_string_buffer(bytes(uid).ljust(128, b"\0"), 128)
+        self.backend.check(self.backend.fn("set_distributed")(self._h, world, rank, 0 if kind == "nccl" else 1, buf))
+        self._bind()
+
     # -- objective
     def mse(self) -> float:
         out = ctypes.c_double()
@@ -384,6 +393,28 @@ class BalGraph:
                                                         vos.ctypes.data, off.ctypes.data, itf.ctypes.data,
                                                         its.ctypes.data))
         return vos, off, itf, its
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes) through the library's runtime-loaded NCCL."""
+    buf = ctypes.create_string_buffer(128)
+    Backend(_abi.lib(), "gb_").check(_abi.lib().gb_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_plan(problem: BALProblem, world: int):
+    """Per-rank tile/point ranges, edge counts and point owners (host only)."""
+    L = _abi.lib()
+    tiles = np.zeros(2 * world, np.uint32)
+    pts = np.zeros(2 * world, np.uint32)
+    edges = np.zeros(world, np.uint64)
+    owner = np.zeros(problem.num_points, np.uint32)
+    cam = np.ascontiguousarray(problem.camera_index, np.uint32)
+    pt = np.ascontiguousarray(problem.point_index, np.uint32)
+    Backend(L, "gb_").check(L.gb_shard_plan(problem.num_cameras, problem.num_points, cam.shape[0], cam.ctypes.data,
+                                            pt.ctypes.data, world, tiles.ctypes.data, pts.ctypes.data,
+                                            edges.ctypes.data, owner.ctypes.data))
+    return tiles.reshape(world, 2), pts.reshape(world, 2), edges, owner
 
 
 def build_graph(problem: BALProblem, precision: str = "fp64", diff_mode: str = "analytic",

@@ -50,6 +50,38 @@ void build_incidence(uint64_t nvert, const std::vector<uint32_t>& vert_of_a, con
   }
 }
 
+
+// warp chunks (32 real edges from the tile start), their camera runs and the
+// camera -> partial-slot CSR (slot order)
+void build_partial_plan(Activation& out) {
+  out.tile_chunk_base.assign(out.ntiles + 1, 0);
+  for (uint32_t t = 0; t < out.ntiles; ++t)
+    out.tile_chunk_base[t + 1] = out.tile_chunk_base[t] + (out.tile_ecnt[t] + 31) / 32;
+  out.nchunks = out.tile_chunk_base[out.ntiles];
+  out.chunk_part_base.assign(out.nchunks + 1, 0);
+  std::vector<uint32_t> run_cam;
+  for (uint32_t t = 0; t < out.ntiles; ++t) {
+    const uint32_t eb = out.tile_ebeg[t], ee = eb + out.tile_ecnt[t];
+    for (uint32_t k = 0; k < (out.tile_ecnt[t] + 31) / 32; ++k) {
+      const uint32_t ch = out.tile_chunk_base[t] + k;
+      uint32_t runs = 0;
+      for (uint32_t d = eb + 32 * k; d < std::min(ee, eb + 32 * k + 32); ++d)
+        if (d == eb + 32 * k || out.d_cam[d] != out.d_cam[d - 1]) {
+          ++runs;
+          run_cam.push_back(out.d_cam[d]);
+        }
+      out.chunk_part_base[ch + 1] = out.chunk_part_base[ch] + runs;
+    }
+  }
+  out.nparts = out.chunk_part_base[out.nchunks];
+  std::vector<uint32_t> slots(out.nparts);
+  for (uint32_t s2 = 0; s2 < out.nparts; ++s2) slots[s2] = s2;
+  std::vector<uint64_t> off;
+  stable_bucket(run_cam, out.nc, slots, off, out.cam_part_idx);
+  out.cam_part_off.assign(out.nc + 1, 0);
+  for (uint64_t c = 0; c <= out.nc; ++c) out.cam_part_off[c] = static_cast<uint32_t>(off[c]);
+}
+
 }  // namespace
 
 void activate(const ActivationInput& in, Activation& out) {
@@ -248,35 +280,74 @@ void activate(const ActivationInput& in, Activation& out) {
       }
   }
 
-  // warp chunks (32 real edges from the tile start) and their camera runs
-  out.tile_chunk_base.assign(out.ntiles + 1, 0);
-  for (uint32_t t = 0; t < out.ntiles; ++t)
-    out.tile_chunk_base[t + 1] = out.tile_chunk_base[t] + (out.tile_ecnt[t] + 31) / 32;
-  out.nchunks = out.tile_chunk_base[out.ntiles];
-  out.chunk_part_base.assign(out.nchunks + 1, 0);
-  std::vector<uint32_t> run_cam;
-  for (uint32_t t = 0; t < out.ntiles; ++t) {
-    const uint32_t eb = out.tile_ebeg[t], ee = eb + out.tile_ecnt[t];
-    for (uint32_t k = 0; k < (out.tile_ecnt[t] + 31) / 32; ++k) {
-      const uint32_t ch = out.tile_chunk_base[t] + k;
-      uint32_t runs = 0;
-      for (uint32_t d = eb + 32 * k; d < std::min(ee, eb + 32 * k + 32); ++d)
-        if (d == eb + 32 * k || out.d_cam[d] != out.d_cam[d - 1]) {
-          ++runs;
-          run_cam.push_back(out.d_cam[d]);
-        }
-      out.chunk_part_base[ch + 1] = out.chunk_part_base[ch] + runs;
-    }
+  build_partial_plan(out);
+}
+
+}  // namespace gb
+
+namespace gb {
+
+void shard_range(const Activation& full, int world, int rank, uint32_t* tile0, uint32_t* tile1, uint32_t* point0,
+                 uint32_t* point1) {
+  const uint64_t total = full.n_slots;
+  auto bound = [&](int r) -> uint32_t {
+    if (r <= 0) return 0;
+    if (r >= world) return full.ntiles;
+    const uint64_t target = total * static_cast<uint64_t>(r) / static_cast<uint64_t>(world);
+    // first tile whose slot begin reaches the target
+    return static_cast<uint32_t>(std::lower_bound(full.tile_ebeg.begin(), full.tile_ebeg.end() - 1, target) -
+                                 full.tile_ebeg.begin());
+  };
+  *tile0 = bound(rank);
+  *tile1 = std::max(*tile0, bound(rank + 1));
+  *point0 = full.tile_pbeg[*tile0];
+  *point1 = full.tile_pbeg[*tile1];
+}
+
+void shard(const Activation& full, int world, int rank, Activation& out) {
+  if (world <= 1) {
+    out = full;
+    return;
   }
-  out.nparts = out.chunk_part_base[out.nchunks];
-  {
-    std::vector<uint32_t> slots(out.nparts);
-    for (uint32_t s2 = 0; s2 < out.nparts; ++s2) slots[s2] = s2;
-    std::vector<uint64_t> off;
-    stable_bucket(run_cam, in.nc, slots, off, out.cam_part_idx);
-    out.cam_part_off.assign(in.nc + 1, 0);
-    for (uint64_t c = 0; c <= in.nc; ++c) out.cam_part_off[c] = static_cast<uint32_t>(off[c]);
+  uint32_t t0, t1, p0, p1;
+  shard_range(full, world, rank, &t0, &t1, &p0, &p1);
+  out = Activation();
+  out.nc = full.nc;
+  out.np = p1 - p0;
+  out.n_active = full.n_active;
+  out.active = full.active;
+  out.level = full.level;
+  out.free_cams = full.free_cams;
+  out.free_pts = full.free_pts;
+  out.free_dims = full.free_dims;
+  out.cam_col = full.cam_col;
+  out.pt_col = full.pt_col;
+  out.cam_inc = full.cam_inc;
+  out.pt_inc = full.pt_inc;
+  out.pt_order.assign(full.pt_order.begin() + p0, full.pt_order.begin() + p1);
+  out.pt_rank = full.pt_rank;  // global internal ranks (debug surface only)
+  out.ntiles = t1 - t0;
+  const uint32_t s0 = full.tile_ebeg[t0], s1 = full.tile_ebeg[t1];
+  out.n_slots = s1 - s0;
+  for (uint32_t t = t0; t <= t1; ++t) {
+    out.tile_ebeg.push_back(full.tile_ebeg[t] - s0);
+    out.tile_pbeg.push_back(full.tile_pbeg[t] - p0);
+    out.tile_cam_off.push_back(full.tile_cam_off[t] - full.tile_cam_off[t0]);
   }
+  out.tile_ecnt.assign(full.tile_ecnt.begin() + t0, full.tile_ecnt.begin() + t1);
+  out.tile_cams.assign(full.tile_cams.begin() + full.tile_cam_off[t0], full.tile_cams.begin() + full.tile_cam_off[t1]);
+  for (uint32_t t : full.normal_tiles)
+    if (t >= t0 && t < t1) out.normal_tiles.push_back(t - t0);
+  for (uint32_t t : full.heavy_tiles)
+    if (t >= t0 && t < t1) out.heavy_tiles.push_back(t - t0);
+  out.d_a.assign(full.d_a.begin() + s0, full.d_a.begin() + s1);
+  out.d_cam.assign(full.d_cam.begin() + s0, full.d_cam.begin() + s1);
+  out.d_lpt.assign(full.d_lpt.begin() + s0, full.d_lpt.begin() + s1);
+  out.d_lcam.assign(full.d_lcam.begin() + s0, full.d_lcam.begin() + s1);
+  const uint32_t q0 = full.pt_slot_off[p0];
+  for (uint32_t i = p0; i <= p1; ++i) out.pt_slot_off.push_back(full.pt_slot_off[i] - q0);
+  out.pt_slots.assign(full.pt_slots.begin() + q0, full.pt_slots.begin() + full.pt_slot_off[p1]);
+  build_partial_plan(out);
 }
 
 }  // namespace gb

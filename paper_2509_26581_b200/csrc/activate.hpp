@@ -73,4 +73,12 @@ struct Activation {
 // Throws std::invalid_argument on out-of-range indices.
 void activate(const ActivationInput& in, Activation& out);
 
+// Rank `rank` of `world`: a contiguous range of tiles balanced by edge slots,
+// with its points and edges; cameras stay global (replicated). Incidence,
+// columns and counts stay global. shard_range reports [tile0, tile1) and
+// [point0, point1) in the full activation's internal order.
+void shard_range(const Activation& full, int world, int rank, uint32_t* tile0, uint32_t* tile1, uint32_t* point0,
+                 uint32_t* point1);
+void shard(const Activation& full, int world, int rank, Activation& out);
+
 }  // namespace gb

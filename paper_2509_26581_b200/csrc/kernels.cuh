@@ -135,7 +135,100 @@ struct Dev {
   gb_iteration_record* recs;
   int loss_kind;
   FP huber;
+  // sharding: world ranks own disjoint point tiles; cameras
+  // are replicated and counted in dot products on rank 0 only. world > 1:
+  // every reduction site writes a per-rank partial into red/redmax, the host
+  // allreduces it, and a finalize kernel applies the decision.
+  int world, rank, dist;  // dist: a reducer is attached (even with world == 1)
+  FP* red;     // SUM partials (layout: kRed* below)
+  FP* redmax;  // MAX partials
 };
+
+// red layout: [0, 54 nc) camera sums (linearize b+H / HVP J^T q), then scalars
+template <typename FP, typename SP>
+__host__ __device__ inline uint64_t red_scalars(const Dev<FP, SP>& d) {
+  return 54ull * d.nc + 8;
+}
+enum RedSlot : int {
+  kRedLinChi = 0, kRedLinFail, kRedDampAny, kRedRhs, kRedFallback, kRedInitRz, kRedInitRr, kRedHvpDot,
+  kRedUpdRz, kRedUpdRr, kRedStepPred, kRedStepFail, kRedChi, kRedCount
+};
+enum RedMaxSlot : int { kRedMaxLin = 0, kRedMaxDamp, kRedMaxCount };
+
+// columns counted in dot products / norms on this rank (cameras: rank 0 only)
+template <typename FP, typename SP>
+__device__ inline bool counted(const Dev<FP, SP>& d, uint64_t col) {
+  return d.rank == 0 || col >= 9ull * d.nc;
+}
+
+// ---- decisions, shared by the fused last blocks (world == 1) and the
+// finalize kernels (world > 1)
+template <typename FP>
+__device__ inline void fin_lin(State<FP>* st, FP chi, bool all_finite, FP gmax) {
+  st->lin_chi2 = chi;
+  st->grad_max = fmax(gmax, FP(0));
+  st->lin_finite = (all_finite && is_finite(chi)) ? 1 : 0;
+}
+template <typename FP>
+__device__ inline void fin_damp(State<FP>* st, FP m, bool any) {
+  const FP tau = static_cast<FP>(st->tau);
+  st->lambda = any ? tau * fmax(m, FP(0)) : tau;
+  st->nu = FP(2);
+}
+template <typename FP>
+__device__ inline void fin_rhs(State<FP>* st, FP s) {  // pcg.hpp:303-311
+  const FP nrm = sqrt(s);
+  st->rhs_norm = nrm;
+  if (!(nrm > FP(0))) {
+    st->pcg_done = 1;
+    st->pcg_zero = 1;
+    st->pcg_conv = is_finite(nrm) ? 1 : 0;
+    st->pcg_relres = 0.0;
+  }
+  st->scale = st->normalize_rhs ? FP(1) / nrm : FP(1);
+  st->ref_norm = st->normalize_rhs ? FP(1) : nrm;
+  st->unscale = st->normalize_rhs ? nrm : FP(1);
+}
+template <typename FP>
+__device__ inline void fin_init(State<FP>* st, FP rz, FP rr) {  // pcg.hpp:326-329
+  if (!st->pcg_done) {
+    st->rho = rz;
+    st->pcg_relres = static_cast<double>(sqrt(rr) / st->ref_norm);
+  }
+}
+template <typename FP>
+__device__ inline void fin_hvp(State<FP>* st, FP pap) {  // pcg.hpp:334-340
+  st->pap = pap;
+  if (!(pap > FP(0)) || !is_finite(pap)) {
+    st->pcg_done = 1;
+    st->pcg_conv = 0;
+  } else {
+    st->alpha = st->rho / pap;
+  }
+}
+template <typename FP>
+__device__ inline void fin_upd(State<FP>* st, FP rz, FP rr) {  // pcg.hpp:345-359
+  st->pcg_it += 1;
+  const FP res = sqrt(rr);
+  const double rel = static_cast<double>(res / st->ref_norm);
+  st->pcg_relres = rel;
+  if (!isfinite(rel)) {
+    st->pcg_done = 1;
+    st->pcg_conv = 0;
+  } else if (res <= static_cast<FP>(st->pcg_tol) * st->ref_norm) {
+    st->pcg_done = 1;
+    st->pcg_conv = 1;
+  } else {
+    st->beta = rz / st->rho;
+    st->rho = rz;
+  }
+}
+template <typename FP>
+__device__ inline void fin_step(State<FP>* st, FP pred, bool finite) {
+  st->pred = pred;
+  st->step_finite = finite ? 1 : 0;
+}
+
 
 // ------------------------------------------------------------------ helpers
 
@@ -358,18 +451,51 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, const
 // Camera side of the linearization: sum each camera's partial slots (slot
 // order), write b_c, packed H_c, clamped diagonal and D; the last block
 // finalizes chi^2, finiteness and max |b| (linear_system.hpp:67-90).
+// phase 0: fused (world == 1); phase 1: per-rank camera sums and tile
+// scalars into red/redmax; phase 2: camera b/H/D from the allreduced sums and
+// the finalize.
 template <typename FP, typename SP>
-__global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int force) {
+__global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int force, int phase) {
   if (!force && !d.st->do_linearize) return;
   __shared__ FP scratch[32];
   const int lane = threadIdx.x & 31;
   const uint32_t c = blockIdx.x * kCamWarps + (threadIdx.x >> 5);
+  if (phase == 1) {
+    if (c < d.nc) {
+      FP a0 = FP(0), a1 = FP(0);
+      for (uint32_t q = d.cam_part_off[c]; q < d.cam_part_off[c + 1]; ++q) {
+        const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * kLinVals;
+        a0 += src[lane];
+        if (lane < kLinVals - 32) a1 += src[32 + lane];
+      }
+      d.red[54ull * c + lane] = a0;
+      if (lane < kLinVals - 32) d.red[54ull * c + 32 + lane] = a1;
+    }
+    if (last_block(&d.st->cnt[0])) {
+      const FP chi = reduce_partials(d.tile_red, d.ntiles, scratch);
+      const FP m1 = reduce_partials_max(d.tile_red2, d.ntiles, scratch);
+      int bad = 0;
+      for (uint32_t i = threadIdx.x; i < d.ntiles; i += blockDim.x) bad += __ldcg(d.tile_flag + i) ? 0 : 1;
+      bad = __syncthreads_count(bad > 0);
+      if (threadIdx.x == 0) {
+        d.red[red_scalars(d) + kRedLinChi] = chi;
+        d.red[red_scalars(d) + kRedLinFail] = FP(bad);
+        d.redmax[kRedMaxLin] = m1;
+      }
+    }
+    return;
+  }
   if (c < d.nc) {
     FP a0 = FP(0), a1 = FP(0);
-    for (uint32_t q = d.cam_part_off[c]; q < d.cam_part_off[c + 1]; ++q) {
-      const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * kLinVals;
-      a0 += src[lane];
-      if (lane < kLinVals - 32) a1 += src[32 + lane];
+    if (phase == 0) {
+      for (uint32_t q = d.cam_part_off[c]; q < d.cam_part_off[c + 1]; ++q) {
+        const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * kLinVals;
+        a0 += src[lane];
+        if (lane < kLinVals - 32) a1 += src[32 + lane];
+      }
+    } else {
+      a0 = d.red[54ull * c + lane];
+      if (lane < kLinVals - 32) a1 = d.red[54ull * c + 32 + lane];
     }
     const bool freev = d.col_free[9ull * c];
     // value v lives in lane v (a0) or lane v-32 (a1)
@@ -401,14 +527,16 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int 
     }
   }
   if (last_block(&d.st->cnt[0])) {
-    const FP chi = reduce_partials(d.tile_red, d.ntiles, scratch);
-    const FP m1 = reduce_partials_max(d.tile_red2, d.ntiles, scratch);
     const FP m2 = reduce_partials_max(d.cam_red2, d.nc, scratch);
-    const int f = reduce_flags_and(d.tile_flag, d.ntiles) & reduce_flags_and(d.cam_flag, d.nc);
-    if (threadIdx.x == 0) {
-      d.st->lin_chi2 = chi;
-      d.st->grad_max = fmax(fmax(m1, m2), FP(0));
-      d.st->lin_finite = (f && is_finite(chi)) ? 1 : 0;
+    const int fc = reduce_flags_and(d.cam_flag, d.nc);
+    if (phase == 0) {
+      const FP chi = reduce_partials(d.tile_red, d.ntiles, scratch);
+      const FP m1 = reduce_partials_max(d.tile_red2, d.ntiles, scratch);
+      const int f = reduce_flags_and(d.tile_flag, d.ntiles) & fc;
+      if (threadIdx.x == 0) fin_lin(d.st, chi, f != 0, fmax(m1, m2));
+    } else if (threadIdx.x == 0) {
+      const FP* rs = d.red + red_scalars(d);
+      fin_lin(d.st, rs[kRedLinChi], fc != 0 && rs[kRedLinFail] == FP(0), fmax(d.redmax[kRedMaxLin], m2));
     }
   }
 }
@@ -421,7 +549,7 @@ __global__ void k_init_damping(Dev<FP, SP> d) {
   bool any = false;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    if (d.col_free[i]) {
+    if (d.col_free[i] && counted(d, i)) {
       any = true;
       m = fmax(m, d.D[i] * d.D[i] * d.clamped[i]);
     }
@@ -435,9 +563,12 @@ __global__ void k_init_damping(Dev<FP, SP> d) {
     const FP mm = reduce_partials_max(d.blk_red, gridDim.x, scratch);
     const int a = reduce_flags_or(d.blk_flag, gridDim.x);
     if (threadIdx.x == 0) {
-      const FP tau = static_cast<FP>(d.st->tau);
-      d.st->lambda = a ? tau * fmax(mm, FP(0)) : tau;
-      d.st->nu = FP(2);
+      if (!d.dist) {
+        fin_damp(d.st, mm, a != 0);
+      } else {
+        d.redmax[kRedMaxDamp] = mm;
+        d.red[red_scalars(d) + kRedDampAny] = FP(a ? 1 : 0);
+      }
     }
   }
 }
@@ -574,7 +705,7 @@ __device__ inline void precond_vertex(const Dev<FP, SP>& d, const FP* H, FP* M, 
     for (int i = 0; i < N; ++i)
 #pragma unroll
       for (int j = i; j < N; ++j, ++q) out[q] = (i == j) ? FP(1) / diag[i] : FP(0);
-    atomicAdd(&d.st->fallbacks, 1);
+    if (d.rank == 0 || N == 3) atomicAdd(&d.st->fallbacks, 1);  // replicated camera blocks counted once
   }
 #pragma unroll
   for (int k = 0; k < NP; ++k) M[k] = out[k];
@@ -626,25 +757,19 @@ __global__ void k_rhs_norm(Dev<FP, SP> d) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const FP rhs = -d.D[i] * d.b[i];
-    acc += rhs * rhs;
+    if (counted(d, i)) acc += rhs * rhs;
   }
   acc = block_sum(acc, scratch);
   if (threadIdx.x == 0) d.blk_red[blockIdx.x] = acc;
   if (last_block(&d.st->cnt[2])) {
     const FP s = reduce_partials(d.blk_red, gridDim.x, scratch);
     if (threadIdx.x == 0) {
-      State<FP>* st = d.st;
-      const FP nrm = sqrt(s);
-      st->rhs_norm = nrm;
-      if (!(nrm > FP(0))) {
-        st->pcg_done = 1;
-        st->pcg_zero = 1;
-        st->pcg_conv = is_finite(nrm) ? 1 : 0;
-        st->pcg_relres = 0.0;
+      if (!d.dist) {
+        fin_rhs(d.st, s);
+      } else {
+        d.red[red_scalars(d) + kRedRhs] = s;
+        d.red[red_scalars(d) + kRedFallback] = FP(d.st->fallbacks);
       }
-      st->scale = st->normalize_rhs ? FP(1) / nrm : FP(1);
-      st->ref_norm = st->normalize_rhs ? FP(1) : nrm;
-      st->unscale = st->normalize_rhs ? nrm : FP(1);
     }
   }
 }
@@ -667,10 +792,15 @@ __global__ void k_pcg_init(Dev<FP, SP> d) {
       d.r[col + k] = narrow<SP>(rhs * scale);
       d.xs[col + k] = narrow<SP>(FP(0));
     }
+    FP lrz = FP(0), lrr = FP(0);
     if (cam)
-      apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &rz, &rr);
+      apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &lrz, &lrr);
     else
-      apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &rz, &rr);
+      apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &lrz, &lrr);
+    if (counted(d, col)) {
+      rz += lrz;
+      rr += lrr;
+    }
     for (int k = 0; k < n; ++k) {
       const SP zk = d.z[col + k];
       d.p[col + k] = zk;
@@ -686,9 +816,13 @@ __global__ void k_pcg_init(Dev<FP, SP> d) {
   if (last_block(&d.st->cnt[3])) {
     const FP srz = reduce_partials(d.blk_red, gridDim.x, scratch);
     const FP srr = reduce_partials(d.blk_red2, gridDim.x, scratch);
-    if (threadIdx.x == 0 && !d.st->pcg_done) {
-      d.st->rho = srz;
-      d.st->pcg_relres = static_cast<double>(sqrt(srr) / d.st->ref_norm);
+    if (threadIdx.x == 0) {
+      if (!d.dist) {
+        fin_init(d.st, srz, srr);
+      } else {
+        d.red[red_scalars(d) + kRedInitRz] = srz;
+        d.red[red_scalars(d) + kRedInitRr] = srr;
+      }
     }
   }
 }
@@ -1002,8 +1136,11 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
 // Camera side of the HVP + p.Ap finalization (pcg.hpp:332-340). Each block
 // also folds a fixed slice of the tiles' per-warp dot partials, so the last
 // block only sums one partial per block (fixed order, deterministic).
+// phase 0: fused (world == 1). phase 1: per-rank camera J^T q sums -> red[0,
+// 9nc) and the local point dot -> red[9nc]. phase 2: ap_c from the allreduced
+// sums, camera dot, pAp = camera dot + reduced point dot.
 template <typename FP, typename SP>
-__global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams(Dev<FP, SP> d) {
+__global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams(Dev<FP, SP> d, int phase) {
   using A = arith_t<SP>;
   if (!d.st->iter_active || d.st->pcg_done) return;
   __shared__ FP scratch[32];
@@ -1014,52 +1151,95 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams(Dev<FP, SP> d) {
     FP acc[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc[k] = FP(0);
-    for (uint32_t q = d.cam_part_off[c] + lane; q < d.cam_part_off[c + 1]; q += 32) {
-      const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * 9;
+    if (phase != 2) {
+      for (uint32_t q = d.cam_part_off[c] + lane; q < d.cam_part_off[c + 1]; q += 32) {
+        const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * 9;
 #pragma unroll
-      for (int k = 0; k < 9; ++k) acc[k] += src[k];
+        for (int k = 0; k < 9; ++k) acc[k] += src[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] = warp_sum(acc[k]);
     }
+    if (phase == 1) {
+      if (lane < 9) {
+        FP a = acc[0];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) acc[k] = warp_sum(acc[k]);
-    FP dot = FP(0);
-    const bool freev = d.col_free[9ull * c];
-    if (lane < 9) {
-      const uint64_t col = 9ull * c + lane;
-      FP a = acc[0];
+        for (int k = 1; k < 9; ++k)
+          if (lane == k) a = acc[k];
+        d.red[9ull * c + lane] = a;
+      }
+    } else {
+      FP dot = FP(0);
+      const bool freev = d.col_free[9ull * c];
+      if (lane < 9) {
+        const uint64_t col = 9ull * c + lane;
+        FP a = acc[0];
 #pragma unroll
-      for (int k = 1; k < 9; ++k)
-        if (lane == k) a = acc[k];
-      const FP Dk = d.D[col];
-      const A damp = d.st->before_scaling ? static_cast<A>(d.st->lambda_solve * Dk * Dk)
-                                          : static_cast<A>(d.st->lambda_solve);
-      const SP pk = d.p[col];
-      const A out = freev ? damp * widen<A>(pk) + static_cast<A>(Dk) * static_cast<A>(a) : A(0);
-      const SP o = narrow<SP>(out);
-      d.ap[col] = o;
-      if (d.dbg_out) d.dbg_out[col] = out;
-      dot = widen<FP>(pk) * widen<FP>(o);
+        for (int k = 1; k < 9; ++k)
+          if (lane == k) a = acc[k];
+        if (phase == 2) a = d.red[col];
+        const FP Dk = d.D[col];
+        const A damp = d.st->before_scaling ? static_cast<A>(d.st->lambda_solve * Dk * Dk)
+                                            : static_cast<A>(d.st->lambda_solve);
+        const SP pk = d.p[col];
+        const A out = freev ? damp * widen<A>(pk) + static_cast<A>(Dk) * static_cast<A>(a) : A(0);
+        const SP o = narrow<SP>(out);
+        d.ap[col] = o;
+        if (d.dbg_out) d.dbg_out[col] = out;
+        dot = widen<FP>(pk) * widen<FP>(o);
+      }
+      dot = warp_sum(dot);
+      if (lane == 0) mine = dot;
     }
-    dot = warp_sum(dot);
-    if (lane == 0) mine = dot;
   }
-  // this block's slice of the tile partials
-  const uint64_t ntp = 8ull * d.ntiles;
-  const uint64_t per = (ntp + gridDim.x - 1) / gridDim.x;
-  const uint64_t lo = min(ntp, per * blockIdx.x), hi = min(ntp, lo + per);
-  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) mine += d.tile_red[i];
+  if (phase != 2) {  // this block's slice of the tiles' point dot partials
+    const uint64_t ntp = 8ull * d.ntiles;
+    const uint64_t per = (ntp + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = min(ntp, per * blockIdx.x), hi = min(ntp, lo + per);
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) mine += d.tile_red[i];
+  }
   const FP bsum = block_sum(mine, scratch);
   if (threadIdx.x == 0) d.blk_red[blockIdx.x] = bsum;
   if (last_block(&d.st->cnt[4])) {
-    const FP pap = reduce_partials(d.blk_red, gridDim.x, scratch);
+    const FP tot = reduce_partials(d.blk_red, gridDim.x, scratch);
     if (threadIdx.x == 0) {
-      d.st->pap = pap;
-      if (!(pap > FP(0)) || !is_finite(pap)) {
-        d.st->pcg_done = 1;
-        d.st->pcg_conv = 0;
-      } else {
-        d.st->alpha = d.st->rho / pap;
-      }
+      if (phase == 0) fin_hvp(d.st, tot);
+      else if (phase == 1) d.red[9ull * d.nc] = tot;
+      else fin_hvp(d.st, tot + d.red[9ull * d.nc]);
     }
+  }
+}
+
+// Finalize kernels for world > 1 (one thread; inputs already allreduced).
+template <typename FP, typename SP>
+__global__ void k_fin(Dev<FP, SP> d, int site) {
+  State<FP>* st = d.st;
+  const FP* rs = d.red + red_scalars(d);
+  switch (site) {
+    case 0:  // init damping
+      fin_damp(st, d.redmax[kRedMaxDamp], rs[kRedDampAny] > FP(0));
+      break;
+    case 1:  // rhs norm + fallback count
+      if (!st->iter_active) return;
+      st->fallbacks = static_cast<int>(rs[kRedFallback]);
+      fin_rhs(st, rs[kRedRhs]);
+      break;
+    case 2:  // pcg init
+      if (!st->iter_active) return;
+      fin_init(st, rs[kRedInitRz], rs[kRedInitRr]);
+      break;
+    case 3:  // pcg update
+      if (!st->iter_active || st->pcg_done) return;
+      fin_upd(st, rs[kRedUpdRz], rs[kRedUpdRr]);
+      break;
+    case 4:  // step
+      if (!st->iter_active) return;
+      fin_step(st, rs[kRedStepPred], rs[kRedStepFail] == FP(0));
+      break;
+    case 5:  // candidate chi^2
+      if (!st->iter_active || !st->step_finite) return;
+      st->chi2_new = rs[kRedChi];
+      break;
   }
 }
 
@@ -1080,10 +1260,15 @@ __global__ void k_pcg_update(Dev<FP, SP> d) {
       d.xs[col + k] = narrow<SP>(widen<FP>(d.xs[col + k]) + alpha * widen<FP>(d.p[col + k]));
       d.r[col + k] = narrow<SP>(widen<FP>(d.r[col + k]) - alpha * widen<FP>(d.ap[col + k]));
     }
+    FP lrz = FP(0), lrr = FP(0);
     if (cam)
-      apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &rz, &rr);
+      apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &lrz, &lrr);
     else
-      apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &rz, &rr);
+      apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &lrz, &lrr);
+    if (counted(d, col)) {
+      rz += lrz;
+      rr += lrr;
+    }
   }
   rz = block_sum(rz, scratch);
   rr = block_sum(rr, scratch);
@@ -1095,20 +1280,11 @@ __global__ void k_pcg_update(Dev<FP, SP> d) {
     const FP srz = reduce_partials(d.blk_red, gridDim.x, scratch);
     const FP srr = reduce_partials(d.blk_red2, gridDim.x, scratch);
     if (threadIdx.x == 0) {
-      State<FP>* st = d.st;
-      st->pcg_it += 1;
-      const FP res = sqrt(srr);
-      const double rel = static_cast<double>(res / st->ref_norm);
-      st->pcg_relres = rel;
-      if (!isfinite(rel)) {
-        st->pcg_done = 1;
-        st->pcg_conv = 0;
-      } else if (res <= static_cast<FP>(st->pcg_tol) * st->ref_norm) {
-        st->pcg_done = 1;
-        st->pcg_conv = 1;
+      if (!d.dist) {
+        fin_upd(d.st, srz, srr);
       } else {
-        st->beta = srz / st->rho;
-        st->rho = srz;
+        d.red[red_scalars(d) + kRedUpdRz] = srz;
+        d.red[red_scalars(d) + kRedUpdRr] = srr;
       }
     }
   }
@@ -1146,7 +1322,7 @@ __global__ void k_step(Dev<FP, SP> d) {
     const FP xsi = zero ? FP(0) : widen<FP>(d.xs[i]) * unscale;
     const FP rhs = -Di * d.b[i];
     const FP damp = before ? lam * Di * Di : lam;
-    pred += xsi * (damp * xsi + rhs);
+    if (counted(d, i)) pred += xsi * (damp * xsi + rhs);
     const FP dxi = Di * xsi;
     d.dx[i] = dxi;
     if (!is_finite(dxi)) fin = 0;
@@ -1163,8 +1339,12 @@ __global__ void k_step(Dev<FP, SP> d) {
     const FP s = reduce_partials(d.blk_red, gridDim.x, scratch);
     const int f = reduce_flags_and(d.blk_flag, gridDim.x);
     if (threadIdx.x == 0) {
-      d.st->pred = s;
-      d.st->step_finite = f;
+      if (!d.dist) {
+        fin_step(d.st, s, f != 0);
+      } else {
+        d.red[red_scalars(d) + kRedStepPred] = s;
+        d.red[red_scalars(d) + kRedStepFail] = f ? FP(0) : FP(1);
+      }
     }
   }
 }
@@ -1195,7 +1375,12 @@ __global__ void __launch_bounds__(kTileThreads) k_chi2_tiles(Dev<FP, SP> d, cons
   if (threadIdx.x == 0) d.tile_red[t] = chi;
   if (last_block(&d.st->cnt[7])) {
     const FP s = reduce_partials(d.tile_red, d.ntiles, scratch);
-    if (threadIdx.x == 0) d.st->chi2_new = s;
+    if (threadIdx.x == 0) {
+      if (!d.dist || force)
+        d.st->chi2_new = s;
+      else
+        d.red[red_scalars(d) + kRedChi] = s;
+    }
   }
 }
 

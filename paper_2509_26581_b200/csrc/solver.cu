@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "activate.hpp"
+#include "dist.hpp"
 #include "gb_bal.h"
 #include "kernels.cuh"
 
@@ -51,6 +52,9 @@ struct GraphData {
   int loss_kind = GB_LOSS_DEFAULT;
   double huber = 1.0;
   uint64_t revision = 1;
+  std::shared_ptr<Reducer> reducer;  // null: single GPU
+  int world() const { return reducer ? reducer->world() : 1; }
+  int rank() const { return reducer ? reducer->rank() : 0; }
 };
 
 class SolverBase {
@@ -185,7 +189,18 @@ class Solver final : public SolverBase {
       CK(cudaMemcpyAsync(st_, &hs, sizeof(hs), cudaMemcpyHostToDevice, s_));
       k_init_damping<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
       CK(cudaGetLastError());
-      build_iteration_graph(cfg.pcg.max_iterations);
+      if (dist()) {
+        allreduce(dev_.redmax + kRedMaxDamp, 1, true);
+        allreduce(red_s() + kRedDampAny, 1);
+        fin(0);
+      }
+      pcg_max_it_ = cfg.pcg.max_iterations;
+      if (!dist() || g_.reducer->capturable()) {
+        build_iteration_graph(cfg.pcg.max_iterations);
+      } else if (graph_exec_) {
+        cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+      }
       max_it_ = cfg.max_iterations;
       ev_.resize(max_it_ + 1);
       for (auto& e : ev_) CK(cudaEventCreate(&e));
@@ -200,7 +215,10 @@ class Solver final : public SolverBase {
     if (!in_solve_) throw std::logic_error("gb_step outside gb_begin/gb_end");
     for (int k = 0; k < n && launched_ < max_it_; ++k) {
       if (launched_ == 0) CK(cudaEventRecord(ev_[0], s_));
-      CK(cudaGraphLaunch(graph_exec_, s_));
+      if (graph_exec_)
+        CK(cudaGraphLaunch(graph_exec_, s_));
+      else
+        enqueue_iteration(pcg_max_it_);
       ++launched_;
       CK(cudaEventRecord(ev_[launched_], s_));
     }
@@ -305,6 +323,7 @@ class Solver final : public SolverBase {
     else
       k_chi2_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, dev_.x, 1);
     CK(cudaGetLastError());
+    if (dist()) allreduce(&st_->chi2_new, 1);
     State<FP> hs;
     CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
     CK(cudaStreamSynchronize(s_));
@@ -315,6 +334,7 @@ class Solver final : public SolverBase {
   void ls_linearize(int level, double cmin, double cmax, int damping, double* chi2, int64_t* n, void* b, void* diag,
                     void* clamped, void* scaling, int32_t* finite) override {
     CK(cudaSetDevice(g_.device));
+    need_single();
     ensure_structure(level);
     upload_params();
     gb_lm_config cfg;
@@ -359,6 +379,9 @@ class Solver final : public SolverBase {
 
   void need_ls() const {
     if (!ls_ready_) throw std::logic_error("linear system not linearized (call gb_ls_linearize first)");
+  }
+  void need_single() const {
+    if (g_.world() > 1) throw std::logic_error("the LinearSystem inspection surface needs world == 1");
   }
 
   void begin_solve_state(double lambda, const gb_pcg_config* pcg) {
@@ -475,7 +498,22 @@ class Solver final : public SolverBase {
     in.cam_fixed = g_.cam_fixed.empty() ? nullptr : g_.cam_fixed.data();
     in.pt_fixed = g_.pt_fixed.empty() ? nullptr : g_.pt_fixed.data();
     in.active_level = level;
-    activate(in, act_);
+    if (g_.reducer) {
+      Activation full;
+      activate(in, full);
+      full_np_ = full.np;
+      full_pt_order_ = full.pt_order;
+      shard_p0_.assign(g_.world() + 1, 0);
+      for (int r = 0; r < g_.world(); ++r) {
+        uint32_t t0, t1, p0, p1;
+        shard_range(full, g_.world(), r, &t0, &t1, &p0, &p1);
+        shard_p0_[r] = p0;
+        shard_p0_[r + 1] = p1;
+      }
+      shard(full, g_.world(), g_.rank(), act_);
+    } else {
+      activate(in, act_);
+    }
     have_act_ = true;
     act_rev_ = g_.revision;
     act_level_ = level;
@@ -512,13 +550,16 @@ class Solver final : public SolverBase {
           col_free[9 * c + k] = 1;
           ref_to_int_[act_.cam_col[c] + k] = 9 * c + k;
         }
-    for (uint64_t p = 0; p < np; ++p)
-      if (act_.pt_col[p] >= 0)
-        for (int k = 0; k < 3; ++k) {
-          const uint64_t ic = 9 * nc + 3ull * act_.pt_rank[p] + k;
-          col_free[ic] = 1;
-          ref_to_int_[act_.pt_col[p] + k] = ic;
-        }
+    // local internal point i (this shard) -> point id p = pt_order[i]
+    for (uint64_t i = 0; i < np; ++i) {
+      const uint64_t p = act_.pt_order[i];
+      if (act_.pt_col[p] < 0) continue;
+      for (int k = 0; k < 3; ++k) {
+        const uint64_t ic = 9 * nc + 3 * i + k;
+        col_free[ic] = 1;
+        ref_to_int_[act_.pt_col[p] + k] = ic;  // meaningful for world == 1 (debug surface)
+      }
+    }
     d.col_free = up(b_col_free_, col_free);
     d.d_cam = up(b_dcam_, act_.d_cam);
     d.d_lpt = up(b_dlpt_, act_.d_lpt);
@@ -585,6 +626,13 @@ class Solver final : public SolverBase {
     d.blk_flag = static_cast<int*>(b_bf_.alloc(nblk * sizeof(int)));
     d.st = st_;
     d.recs = rec_buf_.as<gb_iteration_record>();
+    d.world = g_.world();
+    d.rank = g_.rank();
+    d.dist = g_.reducer ? 1 : 0;
+    d.red = static_cast<FP*>(b_red_.alloc((54ull * nc + 8 + kRedCount + 8) * sizeof(FP)));
+    d.redmax = static_cast<FP*>(b_redmax_.alloc(8 * sizeof(FP)));
+    CK(cudaMemsetAsync(d.red, 0, (54ull * nc + 8 + kRedCount + 8) * sizeof(FP), s_));
+    CK(cudaMemsetAsync(d.redmax, 0, 8 * sizeof(FP), s_));
     CK(cudaMemsetAsync(d.xs, 0, ncols_ * sizeof(SP), s_));
     CK(cudaMemsetAsync(d.p, 0, ncols_ * sizeof(SP), s_));
     if (pinned_) cudaFreeHost(pinned_);
@@ -610,6 +658,10 @@ class Solver final : public SolverBase {
   }
 
   void download_params() {
+    if (dist()) {
+      download_params_sharded();
+      return;
+    }
     const uint64_t nc = act_.nc, np = act_.np;
     CK(cudaMemcpyAsync(pinned_, dev_.x, ncols_ * sizeof(FP), cudaMemcpyDeviceToHost, s_));
     CK(cudaStreamSynchronize(s_));
@@ -624,6 +676,33 @@ class Solver final : public SolverBase {
       up[3 * p] = src[3 * i];
       up[3 * p + 1] = src[3 * i + 1];
       up[3 * p + 2] = src[3 * i + 2];
+    }
+  }
+
+  // every rank ends with every point: each shard broadcasts its internal point
+  // range (bit-exact copies, fixed points included)
+  void download_params_sharded() {
+    const uint64_t nc = act_.nc;
+    FP* xall = static_cast<FP*>(b_xall_.alloc(std::max<uint64_t>(1, 3 * full_np_) * sizeof(FP)));
+    const int me = g_.rank();
+    CK(cudaMemcpyAsync(xall + 3ull * shard_p0_[me], dev_.x + 9 * nc, 3ull * act_.np * sizeof(FP),
+                       cudaMemcpyDeviceToDevice, s_));
+    for (int r = 0; r < g_.world(); ++r) {
+      const uint64_t n = 3ull * (shard_p0_[r + 1] - shard_p0_[r]);
+      if (n) g_.reducer->broadcast(xall + 3ull * shard_p0_[r], n * sizeof(FP), r, s_);
+    }
+    std::vector<FP> hc(9 * nc), hp(3 * full_np_);
+    CK(cudaMemcpyAsync(hc.data(), dev_.x, hc.size() * sizeof(FP), cudaMemcpyDeviceToHost, s_));
+    CK(cudaMemcpyAsync(hp.data(), xall, hp.size() * sizeof(FP), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    d2h_bytes_ += (hc.size() + hp.size()) * sizeof(FP);
+    std::memcpy(g_.cams, hc.data(), hc.size() * sizeof(FP));
+    FP* up = static_cast<FP*>(g_.pts);
+    for (uint64_t i = 0; i < full_np_; ++i) {
+      const uint64_t p = full_pt_order_[i];
+      up[3 * p] = hp[3 * i];
+      up[3 * p + 1] = hp[3 * i + 1];
+      up[3 * p + 2] = hp[3 * i + 2];
     }
   }
 
@@ -649,6 +728,17 @@ class Solver final : public SolverBase {
   unsigned col_grid() const { return std::max(1u, std::min(div_up(ncols_, 256), 148u * 8u)); }
   unsigned cam_grid() const { return std::max(1u, div_up(act_.nc, kCamWarps)); }
 
+  // ---- collectives (world > 1)
+  bool dist() const { return static_cast<bool>(g_.reducer); }
+  void allreduce(FP* p, size_t n, bool max = false) {
+    g_.reducer->allreduce(p, n, static_cast<int>(sizeof(FP)), max, s_);
+  }
+  FP* red_s() const { return dev_.red + red_scalars(dev_); }
+  void fin(int site) {
+    k_fin<FP, SP><<<1, 1, 0, s_>>>(dev_, site);
+    CK(cudaGetLastError());
+  }
+
   void enqueue_linearize(int force) {
     const size_t smem = lin_normal_smem<FP>();
     if (dev_.J) {
@@ -659,7 +749,15 @@ class Solver final : public SolverBase {
       if (dev_.n_heavy) k_lin_tiles<FP, SP, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
     }
     CK(cudaGetLastError());
-    k_lin_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, force);
+    if (!dist()) {
+      k_lin_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, force, 0);
+    } else {
+      k_lin_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, force, 1);
+      CK(cudaGetLastError());
+      allreduce(dev_.red, red_scalars(dev_) + 2);
+      allreduce(dev_.redmax + kRedMaxLin, 1, true);
+      k_lin_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, force, 2);
+    }
     CK(cudaGetLastError());
   }
 
@@ -674,7 +772,14 @@ class Solver final : public SolverBase {
 
   void launch_hvp(const Dev<FP, SP>& d) {
     launch_hvp_tiles(d);
-    k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d);
+    if (!dist()) {
+      k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 0);
+    } else {
+      k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 1);
+      CK(cudaGetLastError());
+      allreduce(d.red, 9ull * d.nc + 1);
+      k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 2);
+    }
     CK(cudaGetLastError());
   }
 
@@ -684,17 +789,33 @@ class Solver final : public SolverBase {
     CK(cudaGetLastError());
     k_rhs_norm<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
     CK(cudaGetLastError());
+    if (dist()) {
+      allreduce(red_s() + kRedRhs, 2);
+      fin(1);
+    }
     k_pcg_init<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
     CK(cudaGetLastError());
+    if (dist()) {
+      allreduce(red_s() + kRedInitRz, 2);
+      fin(2);
+    }
     for (int k = 0; k < pcg_max_it; ++k) {
       launch_hvp(dev_);
       k_pcg_update<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
       CK(cudaGetLastError());
+      if (dist()) {
+        allreduce(red_s() + kRedUpdRz, 2);
+        fin(3);
+      }
       k_pcg_dir<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
       CK(cudaGetLastError());
     }
     k_step<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
     CK(cudaGetLastError());
+    if (dist()) {
+      allreduce(red_s() + kRedStepPred, 2);
+      fin(4);
+    }
   }
 
   // One LM iteration (levenberg_marquardt.hpp:149-220) as a fixed kernel
@@ -705,6 +826,10 @@ class Solver final : public SolverBase {
     enqueue_solve(pcg_max_it);
     k_chi2_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, dev_.x_new, 0);
     CK(cudaGetLastError());
+    if (dist()) {
+      allreduce(red_s() + kRedChi, 1);
+      fin(5);
+    }
     k_decide<FP><<<1, 1, 0, s_>>>(st_, dev_.recs);
     CK(cudaGetLastError());
     k_commit<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
@@ -749,7 +874,7 @@ class Solver final : public SolverBase {
   gb_lm_config cfg_{};
   gb_solve_report rep_{};
   bool in_solve_ = false;
-  int max_it_ = 0, launched_ = 0;
+  int max_it_ = 0, launched_ = 0, pcg_max_it_ = 0;
   std::vector<cudaEvent_t> ev_;
   Clock::time_point t0_;
   Activation act_;
@@ -758,6 +883,8 @@ class Solver final : public SolverBase {
   int act_level_ = 0;
   uint64_t ncols_ = 0;
   std::vector<uint64_t> ref_to_int_;
+  uint64_t full_np_ = 0;
+  std::vector<uint32_t> full_pt_order_, shard_p0_;
   Dev<FP, SP> dev_{};
   State<FP>* st_ = nullptr;
   State<FP> ls_state_{};
@@ -769,6 +896,7 @@ class Solver final : public SolverBase {
   int graph_pcg_it_ = -1;
   gb_iteration_record* graph_recs_ = nullptr;
   DBuf st_buf_, rec_buf_, dbg_buf_;
+  DBuf b_red_, b_redmax_, b_xall_;
   DBuf b_vt_, b_dlcam_, b_tile_ecnt_, b_tile_cam_off_, b_tile_cams_, b_normal_, b_heavy_;
   DBuf b_col_free_, b_dcam_, b_dlpt_, b_obs_, b_tile_ebeg_, b_tile_pbeg_, b_tile_chunk_, b_chunk_part_,
       b_pt_slot_off_, b_pt_slots_, b_cam_part_off_, b_cam_part_idx_;
@@ -960,6 +1088,51 @@ void* gb_stream(gb_graph* g) {
 
 int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_pair, double* ms_tiles) {
   return guarded([&] { g->get().time_hvp(reps < 1 ? 1 : reps, ms_pair, ms_tiles); });
+}
+
+int gb_nccl_unique_id(void* out128) {
+  return guarded([&] { gb::nccl_unique_id(out128); });
+}
+
+int gb_set_distributed(gb_graph* g, int world, int rank, int kind, const void* id) {
+  return guarded([&] {
+    if (world < 1) {
+      g->data.reducer.reset();
+    } else {
+      if (cudaSetDevice(g->data.device) != cudaSuccess) throw gb::CudaError("cudaSetDevice failed");
+      g->data.reducer = gb::make_reducer(kind, world, rank, id);
+    }
+    g->solver.reset();
+    ++g->data.revision;
+  });
+}
+
+int gb_shard_plan(uint64_t num_cameras, uint64_t num_points, uint64_t n, const uint32_t* camera_index,
+                  const uint32_t* point_index, int world, uint32_t* tiles_out, uint32_t* points_out,
+                  uint64_t* edges_out, uint32_t* point_owner) {
+  return guarded([&] {
+    gb::ActivationInput in;
+    in.nc = num_cameras;
+    in.np = num_points;
+    in.ne = n;
+    in.cam = camera_index;
+    in.pt = point_index;
+    gb::Activation full;
+    gb::activate(in, full);
+    for (int r = 0; r < world; ++r) {
+      uint32_t t0, t1, p0, p1;
+      gb::shard_range(full, world, r, &t0, &t1, &p0, &p1);
+      tiles_out[2 * r] = t0;
+      tiles_out[2 * r + 1] = t1;
+      points_out[2 * r] = p0;
+      points_out[2 * r + 1] = p1;
+      uint64_t e = 0;
+      for (uint32_t t = t0; t < t1; ++t) e += full.tile_ecnt[t];
+      edges_out[r] = e;
+      if (point_owner)
+        for (uint32_t i = p0; i < p1; ++i) point_owner[full.pt_order[i]] = static_cast<uint32_t>(r);
+    }
+  });
 }
 
 int gb_mse(gb_graph* g, double* out) {

@@ -1,0 +1,96 @@
+"""The sharded (multi-GPU) solve path on one device.
+
+gpurun provides one GPU, so the K-rank path runs as K host threads of this
+process on the same device with the in-process loopback reducer (rank-order
+reductions, the same kernels, partial/allreduce/finalize sites and final point
+gather as under NCCL). NCCL itself is exercised with a one-rank communicator
+(collective code path, NCCL calls captured into the iteration CUDA graph).
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from paper_2509_26581_b200 import bal
+
+pytestmark = pytest.mark.gpu
+
+LADYBUG = (49, 7776, 31843)
+
+
+def cfg(its=50):
+    c = bal.LMConfig(max_iterations=its)
+    c.pcg.max_iterations = 10
+    return c
+
+
+def solve_sharded(problem, world, precision="fp64", key=1234, its=50):
+    graphs = [bal.build_graph(problem, precision) for _ in range(world)]
+    for r, g in enumerate(graphs):
+        g.set_distributed(world, r, "loopback", int(key).to_bytes(8, "little"))
+    reps = [None] * world
+    errs = []
+
+    def run(r):
+        try:
+            reps[r] = bal.levenberg_marquardt(graphs[r], cfg(its))
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    assert not errs, errs
+    return graphs, reps
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_loopback_shards_match_single_gpu(gpu, world):
+    p = bal.synthetic_bal(*LADYBUG, seed=42)
+    g1 = bal.build_graph(p, "fp64")
+    r1 = bal.levenberg_marquardt(g1, cfg())
+    graphs, reps = solve_sharded(p, world, key=100 + world)
+    for g, r in zip(graphs, reps):
+        assert r.termination == r1.termination and len(r.iterations) == len(r1.iterations)
+        assert abs(r.final_chi2 - r1.final_chi2) <= 1e-9 * r1.final_chi2
+        assert np.linalg.norm(g.points - g1.points) <= 1e-7 * np.linalg.norm(g1.points)
+        assert np.linalg.norm(g.cameras - g1.cameras) <= 1e-7 * np.linalg.norm(g1.cameras)
+        assert r.memory == r1.memory and r.free_dims == r1.free_dims
+    # every rank ends with the same bits (replicated cameras, gathered points)
+    for g in graphs[1:]:
+        assert np.array_equal(g.cameras.view(np.uint64), graphs[0].cameras.view(np.uint64))
+        assert np.array_equal(g.points.view(np.uint64), graphs[0].points.view(np.uint64))
+
+
+def test_loopback_shards_fixed_and_heavy(gpu, ref):
+    p = bal.synthetic_bal(520, 30, 30 * 520, seed=7)  # heavy single-point tiles
+    fixed_c = np.zeros(520, bool)
+    fixed_c[:5] = True
+    graphs = [bal.build_graph(p, "fp64") for _ in range(2)]
+    for r, g in enumerate(graphs):
+        g.set_fixed(cameras=fixed_c)
+        g.set_distributed(2, r, "loopback", (777).to_bytes(8, "little"))
+    reps = [None, None]
+    th = [threading.Thread(target=lambda r=r: reps.__setitem__(r, bal.levenberg_marquardt(graphs[r], cfg(12))))
+          for r in range(2)]
+    [t.start() for t in th]
+    [t.join(600) for t in th]
+    rr = ref.build_graph(p, "fp64", workers=4)
+    rr.set_fixed(cameras=fixed_c)
+    rb = bal.levenberg_marquardt(rr, cfg(12))
+    assert len(reps[0].iterations) == len(rb.iterations)
+    assert abs(reps[0].final_chi2 - rb.final_chi2) <= 1e-6 * rb.final_chi2
+    assert np.array_equal(graphs[0].cameras[:5].view(np.uint64), p.cameras[:5].view(np.uint64))
+
+
+def test_nccl_single_rank_collective_path(gpu):
+    p = bal.synthetic_bal(*LADYBUG, seed=42)
+    g1 = bal.build_graph(p, "fp64")
+    r1 = bal.levenberg_marquardt(g1, cfg())
+    g = bal.build_graph(p, "fp64")
+    g.set_distributed(1, 0, "nccl", bal.nccl_unique_id())
+    r = bal.levenberg_marquardt(g, cfg())
+    assert len(r.iterations) == len(r1.iterations)
+    assert abs(r.final_chi2 - r1.final_chi2) <= 1e-12 * r1.final_chi2
