@@ -228,6 +228,11 @@ int gb_shard_plan(uint64_t num_cameras, uint64_t num_points, uint64_t n, const u
                   const uint32_t* point_index, int world, uint32_t* tiles_out, uint32_t* points_out,
                   uint64_t* edges_out, uint32_t* point_owner);
 
+/* Test hook: runs the device activation and the host reference activation
+ * (activate.cpp, the same rules) and compares every structure bit for bit.
+ * GB_OK or GB_ERR_LOGIC naming the first differing array. */
+int gb_activation_selfcheck(gb_graph* g, int level);
+
 /* BalGraph::mse (adapter.hpp:95-99) at the current user parameters. */
 int gb_mse(gb_graph* g, double* out);
 /* Graph::total_error(level) (graph.hpp:99-104). */

@@ -51,6 +51,57 @@ void build_incidence(uint64_t nvert, const std::vector<uint32_t>& vert_of_a, con
 }
 
 
+// Greedy tile partition over internal-point degrees (shared by the host and
+// the device activation): <= kTileEdges edges and <= kTilePoints points per
+// tile; a point with more than kTileEdges edges is a tile of its own.
+// tile_ebeg here is the UNPADDED edge prefix.
+}  // namespace
+
+void greedy_tiles(const std::vector<uint32_t>& deg_int, std::vector<uint32_t>& tile_pbeg,
+                  std::vector<uint32_t>& tile_ebeg, std::vector<uint32_t>& tile_of_pt) {
+  const uint64_t np = deg_int.size();
+  tile_pbeg.assign(1, 0);
+  tile_ebeg.assign(1, 0);
+  tile_of_pt.resize(np);
+  uint64_t te = 0, tp = 0, ecount = 0;
+  for (uint64_t i = 0; i < np; ++i) {
+    const uint64_t d = deg_int[i];
+    const bool heavy = d > static_cast<uint64_t>(kTileEdges);
+    if (tp > 0 && (heavy || te + d > static_cast<uint64_t>(kTileEdges) || tp >= static_cast<uint64_t>(kTilePoints))) {
+      tile_pbeg.push_back(static_cast<uint32_t>(i));
+      tile_ebeg.push_back(static_cast<uint32_t>(ecount));
+      te = tp = 0;
+    }
+    tile_of_pt[i] = static_cast<uint32_t>(tile_pbeg.size() - 1);
+    te += d;
+    tp += 1;
+    ecount += d;
+    if (heavy) {
+      tile_pbeg.push_back(static_cast<uint32_t>(i + 1));
+      tile_ebeg.push_back(static_cast<uint32_t>(ecount));
+      te = tp = 0;
+    }
+  }
+  if (tp > 0 || tile_pbeg.size() == 1) {
+    tile_pbeg.push_back(static_cast<uint32_t>(np));
+    tile_ebeg.push_back(static_cast<uint32_t>(ecount));
+  }
+}
+
+// normal tiles: <= kTileEdges edges and <= kTileCams distinct cameras (the
+// shared-memory kernels); everything else goes through the generic kernels
+void classify_tiles(Activation& out) {
+  out.normal_tiles.clear();
+  out.heavy_tiles.clear();
+  for (uint32_t t = 0; t < out.ntiles; ++t) {
+    const bool heavy = out.tile_ecnt[t] > static_cast<uint32_t>(kTileEdges) ||
+                       out.tile_cam_off[t + 1] - out.tile_cam_off[t] > static_cast<uint32_t>(kTileCams);
+    (heavy ? out.heavy_tiles : out.normal_tiles).push_back(t);
+  }
+}
+
+namespace {
+
 // warp chunks (32 real edges from the tile start), their camera runs and the
 // camera -> partial-slot CSR (slot order)
 void build_partial_plan(Activation& out) {
@@ -150,58 +201,14 @@ void activate(const ActivationInput& in, Activation& out) {
   out.pt_rank.assign(in.np, 0);
   for (uint64_t i = 0; i < in.np; ++i) out.pt_rank[out.pt_order[i]] = static_cast<uint32_t>(i);
 
-  // all active edges of each point (any camera), for the tile builder
-  std::vector<uint64_t> pe_off;
-  std::vector<uint32_t> pe_items;
-  {
-    std::vector<uint32_t> all(na);
-    for (uint64_t a = 0; a < na; ++a) all[a] = static_cast<uint32_t>(a);
-    stable_bucket(pt_of_a, in.np, all, pe_off, pe_items);
-  }
-  // tiles: greedy over internal points, <= kTileEdges edges, <= kTilePoints
-  // points and <= kTileCams distinct cameras; a point that alone exceeds a
-  // limit is a tile of its own ("heavy" tile, processed chunk by chunk).
-  std::vector<uint32_t> tile_of_pt(in.np);
-  std::vector<uint32_t> cam_stamp(in.nc, kNoKey);
-  out.tile_pbeg.push_back(0);
-  out.tile_ebeg.push_back(0);
-  {
-    uint64_t te = 0, tp = 0, tc = 0, ecount = 0;
-    uint32_t stamp = 0;
-    auto close = [&](uint64_t next_point) {
-      out.tile_pbeg.push_back(static_cast<uint32_t>(next_point));
-      out.tile_ebeg.push_back(static_cast<uint32_t>(ecount));
-      te = tp = tc = 0;
-      ++stamp;
-    };
-    for (uint64_t i = 0; i < in.np; ++i) {
-      const uint32_t p = out.pt_order[i];
-      const uint64_t d = deg[p];
-      // distinct cameras this point would add to the current tile
-      uint64_t newc = 0;
-      for (uint64_t q = pe_off[p]; q < pe_off[p + 1]; ++q)
-        if (cam_stamp[cam_of_a[pe_items[q]]] != stamp) ++newc;
-      const bool heavy = d > static_cast<uint64_t>(kTileEdges) || d > static_cast<uint64_t>(kTileCams);
-      if (tp > 0 && (heavy || te + d > static_cast<uint64_t>(kTileEdges) || tp >= static_cast<uint64_t>(kTilePoints) ||
-                     tc + newc > static_cast<uint64_t>(kTileCams))) {
-        close(i);
-        newc = d;  // fresh tile: all its cameras are new (distinct per point)
-      }
-      tile_of_pt[i] = static_cast<uint32_t>(out.tile_pbeg.size() - 1);
-      for (uint64_t q = pe_off[p]; q < pe_off[p + 1]; ++q) {
-        uint32_t& st = cam_stamp[cam_of_a[pe_items[q]]];
-        if (st != stamp) {
-          st = stamp;
-          ++tc;
-        }
-      }
-      te += d;
-      tp += 1;
-      ecount += d;
-      if (heavy) close(i + 1);
-    }
-    if (tp > 0 || out.tile_pbeg.size() == 1) close(in.np);
-  }
+  // tiles: greedy over internal points, <= kTileEdges edges and <= kTilePoints
+  // points; a point with more than kTileEdges edges is a tile of its own
+  // ("heavy" tile, processed chunk by chunk). Only degrees are needed, so the
+  // device activation runs the same loop on the host over the degree array.
+  std::vector<uint32_t> deg_int(in.np);
+  for (uint64_t i = 0; i < in.np; ++i) deg_int[i] = deg[out.pt_order[i]];
+  std::vector<uint32_t> tile_of_pt;
+  greedy_tiles(deg_int, out.tile_pbeg, out.tile_ebeg, tile_of_pt);
   out.ntiles = static_cast<uint32_t>(out.tile_pbeg.size() - 1);
 
   // device edge order: active edges sorted by camera (stable in a), then
@@ -225,9 +232,6 @@ void activate(const ActivationInput& in, Activation& out) {
     out.tile_ecnt[t] = real_beg[t + 1] - real_beg[t];
     out.tile_ebeg[t] = static_cast<uint32_t>(slot);
     slot += (out.tile_ecnt[t] + kEdgePad - 1) / kEdgePad * kEdgePad;
-    const bool heavy = out.tile_ecnt[t] > static_cast<uint32_t>(kTileEdges) ||
-                       (out.tile_pbeg[t + 1] - out.tile_pbeg[t] == 1 && out.tile_ecnt[t] > static_cast<uint32_t>(kTileCams));
-    (heavy ? out.heavy_tiles : out.normal_tiles).push_back(t);
   }
   if (slot > 0xffffffffull) throw std::invalid_argument("more than 2^32 padded edge slots");
   out.tile_ebeg[out.ntiles] = static_cast<uint32_t>(slot);
@@ -266,6 +270,7 @@ void activate(const ActivationInput& in, Activation& out) {
     for (uint32_t j = out.tile_ecnt[t]; j < out.tile_ebeg[t + 1] - eb; ++j) out.d_lcam[eb + j] = nl ? nl - 1 : 0;
     out.tile_cam_off[t + 1] = out.tile_cam_off[t] + nl;
   }
+  classify_tiles(out);
 
   // per-point slot lists (tile-local, ascending)
   out.pt_slot_off.assign(in.np + 1, 0);
@@ -350,4 +355,10 @@ void shard(const Activation& full, int world, int rank, Activation& out) {
   build_partial_plan(out);
 }
 
+}  // namespace gb
+
+namespace gb {
+void build_incidence_host(uint64_t nvert, const std::vector<uint32_t>& vert_of_a, const uint8_t* fixed, Incidence& inc) {
+  build_incidence(nvert, vert_of_a, fixed, inc);
+}
 }  // namespace gb

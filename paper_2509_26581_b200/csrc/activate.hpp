@@ -81,4 +81,11 @@ void shard_range(const Activation& full, int world, int rank, uint32_t* tile0, u
                  uint32_t* point1);
 void shard(const Activation& full, int world, int rank, Activation& out);
 
+// building blocks shared with the device activation (activate_dev.cuh)
+void greedy_tiles(const std::vector<uint32_t>& deg_int, std::vector<uint32_t>& tile_pbeg,
+                  std::vector<uint32_t>& tile_ebeg, std::vector<uint32_t>& tile_of_pt);
+void classify_tiles(Activation& out);
+// FactorDescriptor::build_incidence for one slot (factor_descriptor.hpp:710-753)
+void build_incidence_host(uint64_t nvert, const std::vector<uint32_t>& vert_of_a, const uint8_t* fixed, Incidence& inc);
+
 }  // namespace gb

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "activate.hpp"
+#include "activate_dev.cuh"
 #include "dist.hpp"
 #include "gb_bal.h"
 #include "kernels.cuh"
@@ -75,6 +76,7 @@ class SolverBase {
                              int32_t* finite) = 0;
   virtual void ls_jacobians(void* out) = 0;
   virtual const Activation& activation() = 0;
+  virtual std::string selfcheck(int level) = 0;
 };
 
 // ------------------------------------------------------------- device memory
@@ -135,7 +137,6 @@ class Solver final : public SolverBase {
   ~Solver() override {
     for (auto& e : ev_) cudaEventDestroy(e);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-    if (pinned_) cudaFreeHost(pinned_);
     if (flag_host_) cudaFreeHost(flag_host_);
     cudaStreamDestroy(s_);
   }
@@ -143,7 +144,44 @@ class Solver final : public SolverBase {
   // current activation (the last level used; level 0 if never activated)
   const Activation& activation() override {
     ensure_structure(have_act_ ? act_level_ : 0);
+    ensure_host_plan();
     return act_;
+  }
+
+  // device activation == host activation, array by array (empty string = ok)
+  std::string selfcheck(int level) override {
+    CK(cudaSetDevice(g_.device));
+    if (g_.reducer) throw std::logic_error("selfcheck applies to the single-GPU (device-activated) path");
+    have_act_ = false;
+    ensure_structure(level);
+    Activation h;
+    activate(activation_input(level), h);
+    std::string err;
+    auto cmp = [&](const char* name, const auto* dptr, const auto& hv) {
+      using T = typename std::decay_t<decltype(hv)>::value_type;
+      std::vector<T> got(hv.size());
+      if (!hv.empty()) CK(cudaMemcpy(got.data(), dptr, hv.size() * sizeof(T), cudaMemcpyDeviceToHost));
+      if (got != hv && err.empty()) err = std::string("mismatch in ") + name;
+    };
+    if (h.ntiles != act_.ntiles || h.n_slots != act_.n_slots || h.nparts != act_.nparts || h.nchunks != act_.nchunks ||
+        h.n_active != act_.n_active)
+      return "count mismatch";
+    if (h.tile_ebeg != act_.tile_ebeg || h.tile_pbeg != act_.tile_pbeg || h.tile_ecnt != act_.tile_ecnt ||
+        h.tile_chunk_base != act_.tile_chunk_base || h.normal_tiles != act_.normal_tiles ||
+        h.heavy_tiles != act_.heavy_tiles || h.tile_cam_off != act_.tile_cam_off)
+      return "tile plan mismatch";
+    cmp("pt_order", pt_order_dev_, h.pt_order);
+    cmp("d_a", b_da_.as<uint32_t>(), h.d_a);
+    cmp("d_cam", dev_.d_cam, h.d_cam);
+    cmp("d_lpt", dev_.d_lpt, h.d_lpt);
+    cmp("d_lcam", dev_.d_lcam, h.d_lcam);
+    cmp("tile_cams", dev_.tile_cams, h.tile_cams);
+    cmp("chunk_part_base", dev_.chunk_part_base, h.chunk_part_base);
+    cmp("pt_slot_off", dev_.pt_slot_off, h.pt_slot_off);
+    cmp("pt_slots", dev_.pt_slots, h.pt_slots);
+    cmp("cam_part_off", dev_.cam_part_off, h.cam_part_off);
+    cmp("cam_part_idx", dev_.cam_part_idx, h.cam_part_idx);
+    return err;
   }
 
   // ---------------------------------------------------------------- optimize
@@ -336,6 +374,7 @@ class Solver final : public SolverBase {
     CK(cudaSetDevice(g_.device));
     need_single();
     ensure_structure(level);
+    ensure_host_plan();
     upload_params();
     gb_lm_config cfg;
     gb_default_config(&cfg);
@@ -485,9 +524,7 @@ class Solver final : public SolverBase {
 
  private:
   // ------------------------------------------------------------ structure
-  void ensure_structure(int level) {
-    if (have_act_ && act_rev_ == g_.revision && act_level_ == level) return;
-    if (!g_.cams || !g_.pts) throw std::logic_error("cameras and points must be set before solving");
+  ActivationInput activation_input(int level) const {
     ActivationInput in;
     in.nc = g_.nc;
     in.np = g_.np;
@@ -498,7 +535,15 @@ class Solver final : public SolverBase {
     in.cam_fixed = g_.cam_fixed.empty() ? nullptr : g_.cam_fixed.data();
     in.pt_fixed = g_.pt_fixed.empty() ? nullptr : g_.pt_fixed.data();
     in.active_level = level;
-    if (g_.reducer) {
+    return in;
+  }
+
+  void ensure_structure(int level) {
+    if (have_act_ && act_rev_ == g_.revision && act_level_ == level) return;
+    if (!g_.cams || !g_.pts) throw std::logic_error("cameras and points must be set before solving");
+    host_plan_ = false;
+    if (g_.reducer) {  // sharded: host activation + slicing (tested on CPU and by the loopback suite)
+      const ActivationInput in = activation_input(level);
       Activation full;
       activate(in, full);
       full_np_ = full.np;
@@ -511,8 +556,10 @@ class Solver final : public SolverBase {
         shard_p0_[r + 1] = p1;
       }
       shard(full, g_.world(), g_.rank(), act_);
+      host_plan_ = true;
+      upload_structure_host();
     } else {
-      activate(in, act_);
+      device_structure(level);
     }
     have_act_ = true;
     act_rev_ = g_.revision;
@@ -522,44 +569,62 @@ class Solver final : public SolverBase {
       cudaGraphExecDestroy(graph_exec_);
       graph_exec_ = nullptr;
     }
-    upload_structure();
+    allocate_work();
   }
 
-  void upload_structure() {
-    const uint64_t nc = act_.nc, np = act_.np, ns = act_.n_slots;
-    ncols_ = 9 * nc + 3 * np;
+  // The host activation (activate.cpp) for the debug surface of a device-
+  // activated graph: identical structures (gb_activation_selfcheck), plus the
+  // reference column map and incidence CSRs.
+  void ensure_host_plan() {
+    if (host_plan_) return;
+    activate(activation_input(act_level_), act_);
+    host_plan_ = true;
+    build_ref_map();
+  }
+
+  void build_ref_map() {
+    const uint64_t nc = act_.nc, np = act_.np;
+    ref_to_int_.assign(act_.free_dims, 0);
+    for (uint64_t c = 0; c < nc; ++c)
+      if (act_.cam_col[c] >= 0)
+        for (int k = 0; k < 9; ++k) ref_to_int_[act_.cam_col[c] + k] = 9 * c + k;
+    for (uint64_t i = 0; i < np; ++i) {
+      const uint64_t p = act_.pt_order[i];
+      if (act_.pt_col[p] >= 0)
+        for (int k = 0; k < 3; ++k) ref_to_int_[act_.pt_col[p] + k] = 9 * nc + 3 * i + k;
+    }
+  }
+
+  void set_counts() {
     Dev<FP, SP>& d = dev_;
-    d = Dev<FP, SP>{};
-    d.nc = static_cast<uint32_t>(nc);
-    d.np = static_cast<uint32_t>(np);
-    d.na = static_cast<uint32_t>(ns);
+    ncols_ = 9 * act_.nc + 3 * act_.np;
+    d.nc = static_cast<uint32_t>(act_.nc);
+    d.np = static_cast<uint32_t>(act_.np);
+    d.na = static_cast<uint32_t>(act_.n_slots);
     d.ntiles = act_.ntiles;
     d.nparts = act_.nparts;
     d.ncols = ncols_;
+  }
+
+  // ---- host activation -> device arrays (sharded path)
+  void upload_structure_host() {
+    const uint64_t nc = act_.nc, np = act_.np, ns = act_.n_slots;
+    dev_ = Dev<FP, SP>{};
+    set_counts();
+    Dev<FP, SP>& d = dev_;
     size_t h2d = 0;
     auto up = [&](DBuf& buf, const auto& v) {
       h2d += v.size() * sizeof(v[0]);
       return upload(buf, v, s_);
     };
-    // column free mask and the reference column map
     std::vector<uint8_t> col_free(ncols_, 0);
-    ref_to_int_.assign(act_.free_dims, 0);
     for (uint64_t c = 0; c < nc; ++c)
       if (act_.cam_col[c] >= 0)
-        for (int k = 0; k < 9; ++k) {
-          col_free[9 * c + k] = 1;
-          ref_to_int_[act_.cam_col[c] + k] = 9 * c + k;
-        }
-    // local internal point i (this shard) -> point id p = pt_order[i]
-    for (uint64_t i = 0; i < np; ++i) {
-      const uint64_t p = act_.pt_order[i];
-      if (act_.pt_col[p] < 0) continue;
-      for (int k = 0; k < 3; ++k) {
-        const uint64_t ic = 9 * nc + 3 * i + k;
-        col_free[ic] = 1;
-        ref_to_int_[act_.pt_col[p] + k] = ic;  // meaningful for world == 1 (debug surface)
-      }
-    }
+        for (int k = 0; k < 9; ++k) col_free[9 * c + k] = 1;
+    for (uint64_t i = 0; i < np; ++i)  // local internal point i -> point id pt_order[i]
+      if (act_.pt_col[act_.pt_order[i]] >= 0)
+        for (int k = 0; k < 3; ++k) col_free[9 * nc + 3 * i + k] = 1;
+    if (g_.world() == 1) build_ref_map();
     d.col_free = up(b_col_free_, col_free);
     d.d_cam = up(b_dcam_, act_.d_cam);
     d.d_lpt = up(b_dlpt_, act_.d_lpt);
@@ -587,8 +652,230 @@ class Solver final : public SolverBase {
     d.pt_slots = up(b_pt_slots_, act_.pt_slots);
     d.cam_part_off = up(b_cam_part_off_, act_.cam_part_off);
     d.cam_part_idx = up(b_cam_part_idx_, act_.cam_part_idx);
+    pt_order_dev_ = up(b_pt_order_, act_.pt_order);
     h2d_bytes_ += h2d;
+  }
 
+  // ---- device activation (single GPU): activate_dev.cuh
+  template <typename T>
+  T* scratch(DBuf& b, uint64_t n) {
+    return static_cast<T*>(b.alloc(std::max<uint64_t>(1, n) * sizeof(T)));
+  }
+  template <typename T>
+  T* to_dev(DBuf& b, const std::vector<T>& v) {
+    h2d_bytes_ += v.size() * sizeof(T);
+    return upload(b, v, s_);
+  }
+  void cub_scan_excl(const uint32_t* in, uint32_t* out, uint64_t n) {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, static_cast<int64_t>(n), s_));
+    CK(cub::DeviceScan::ExclusiveSum(b_cub_.alloc(tmp), tmp, in, out, static_cast<int64_t>(n), s_));
+  }
+  void cub_scan_incl(const uint32_t* in, uint32_t* out, uint64_t n) {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out, static_cast<int64_t>(n), s_));
+    CK(cub::DeviceScan::InclusiveSum(b_cub_.alloc(tmp), tmp, in, out, static_cast<int64_t>(n), s_));
+  }
+  template <typename K>
+  void cub_sort(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, int end_bit) {
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, static_cast<int64_t>(n), 0, end_bit, s_));
+    CK(cub::DeviceRadixSort::SortPairs(b_cub_.alloc(tmp), tmp, kin, kout, vin, vout, static_cast<int64_t>(n), 0,
+                                       end_bit, s_));
+  }
+  unsigned grid_for(uint64_t n) const {
+    return std::max(1u, std::min(div_up(n, 256), 148u * 16u));
+  }
+
+  void device_structure(int level) {
+    using namespace actdev;
+    const uint64_t nc = g_.nc, np = g_.np, ne = g_.ne;
+    act_ = Activation();
+    act_.nc = nc;
+    act_.np = np;
+    act_.level = level;
+    // columns (vertex_descriptor.hpp:115-126) - host, O(nc + np)
+    for (uint64_t c = 0; c < nc; ++c) act_.free_cams += (g_.cam_fixed.empty() || !g_.cam_fixed[c]) ? 1 : 0;
+    for (uint64_t p = 0; p < np; ++p) act_.free_pts += (g_.pt_fixed.empty() || !g_.pt_fixed[p]) ? 1 : 0;
+    act_.free_dims = 9 * act_.free_cams + 3 * act_.free_pts;
+
+    DBuf s_cam, s_pt, s_lvl, s_cfix, s_pfix, s_obs, s_flag, s_pos, s_cam_a, s_pt_a, s_entry, s_key, s_key2, s_val, s_val2,
+        s_rank, s_deg, s_degi, s_rb, s_k64, s_k64b, s_order, s_pkey, s_pval, s_pkey2, s_pval2, s_hc, s_hr, s_ic, s_ir,
+        s_runcam, s_runcam2, s_slots, s_cnt, s_bad;
+    const uint32_t* cam = to_dev(s_cam, g_.cam_idx);
+    const uint32_t* pt = to_dev(s_pt, g_.pt_idx);
+    const uint8_t* lvl = g_.level.empty() ? nullptr : to_dev(s_lvl, g_.level);
+    const uint8_t* cfix = g_.cam_fixed.empty() ? nullptr : to_dev(s_cfix, g_.cam_fixed);
+    const uint8_t* pfix = g_.pt_fixed.empty() ? nullptr : to_dev(s_pfix, g_.pt_fixed);
+    const double* obs = to_dev(s_obs, g_.obs);
+    uint32_t* flag = scratch<uint32_t>(s_flag, ne + 1);
+    uint32_t* pos = scratch<uint32_t>(s_pos, ne + 1);
+    int* bad = scratch<int>(s_bad, 1);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), s_));
+    CK(cudaMemsetAsync(flag + ne, 0, sizeof(uint32_t), s_));
+    k_flags<<<grid_for(ne), 256, 0, s_>>>(ne, cam, pt, lvl, level, static_cast<uint32_t>(nc), static_cast<uint32_t>(np),
+                                          flag, bad);
+    CK(cudaGetLastError());
+    cub_scan_excl(flag, pos, ne + 1);
+    uint32_t na32 = 0;
+    int hbad = 0;
+    CK(cudaMemcpyAsync(&na32, pos + ne, sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    if (hbad) {  // reproduce the exact diagnostic (resolve_slots, factor_descriptor.hpp:549-558)
+      Activation tmp;
+      activate(activation_input(level), tmp);
+    }
+    const uint64_t na = na32;
+    act_.n_active = na;
+    uint32_t* cam_a = scratch<uint32_t>(s_cam_a, na);
+    uint32_t* pt_a = scratch<uint32_t>(s_pt_a, na);
+    uint32_t* entry_a = scratch<uint32_t>(s_entry, na);
+    k_compact<<<grid_for(ne), 256, 0, s_>>>(ne, flag, pos, cam, pt, cam_a, pt_a, entry_a);
+    // internal point order: stable sort by smallest active camera
+    uint32_t* key = scratch<uint32_t>(s_key, np);
+    uint32_t* key2 = scratch<uint32_t>(s_key2, np);
+    uint32_t* val = scratch<uint32_t>(s_val, np);
+    uint32_t* deg = scratch<uint32_t>(s_deg, np);
+    k_fill_u32<<<grid_for(np), 256, 0, s_>>>(np, static_cast<uint32_t>(nc), key);
+    CK(cudaMemsetAsync(deg, 0, std::max<uint64_t>(1, np) * sizeof(uint32_t), s_));
+    k_iota<<<grid_for(np), 256, 0, s_>>>(np, val);
+    k_point_stats<<<grid_for(na), 256, 0, s_>>>(na, cam_a, pt_a, key, deg);
+    CK(cudaGetLastError());
+    uint32_t* pt_order = static_cast<uint32_t*>(b_pt_order_.alloc(std::max<uint64_t>(1, np) * sizeof(uint32_t)));
+    cub_sort<uint32_t>(key, key2, val, pt_order, np, bits_for(nc + 1));
+    pt_order_dev_ = pt_order;
+    uint32_t* rank = scratch<uint32_t>(s_rank, np);
+    uint32_t* degi = scratch<uint32_t>(s_degi, np + 1);
+    CK(cudaMemsetAsync(degi + np, 0, sizeof(uint32_t), s_));
+    k_rank<<<grid_for(np), 256, 0, s_>>>(np, pt_order, deg, rank, degi);
+    CK(cudaGetLastError());
+    std::vector<uint32_t> hdeg(np);
+    if (np) CK(cudaMemcpyAsync(hdeg.data(), degi, np * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    // tiles: the host greedy over degrees (activate.cpp greedy_tiles)
+    std::vector<uint32_t> real_beg, tile_of_pt;
+    greedy_tiles(hdeg, act_.tile_pbeg, real_beg, tile_of_pt);
+    act_.ntiles = static_cast<uint32_t>(act_.tile_pbeg.size() - 1);
+    const uint32_t T = act_.ntiles;
+    act_.tile_ecnt.resize(T);
+    act_.tile_ebeg.assign(T + 1, 0);
+    act_.tile_chunk_base.assign(T + 1, 0);
+    uint64_t slot = 0;
+    for (uint32_t t = 0; t < T; ++t) {
+      act_.tile_ecnt[t] = real_beg[t + 1] - real_beg[t];
+      act_.tile_ebeg[t] = static_cast<uint32_t>(slot);
+      slot += (act_.tile_ecnt[t] + kEdgePad - 1) / kEdgePad * kEdgePad;
+      act_.tile_chunk_base[t + 1] = act_.tile_chunk_base[t] + (act_.tile_ecnt[t] + 31) / 32;
+    }
+    if (slot > 0xffffffffull) throw std::invalid_argument("more than 2^32 padded edge slots");
+    act_.tile_ebeg[T] = static_cast<uint32_t>(slot);
+    act_.n_slots = slot;
+    act_.nchunks = act_.tile_chunk_base[T];
+    const uint64_t ns = slot;
+    dev_ = Dev<FP, SP>{};
+    set_counts();
+    Dev<FP, SP>& d = dev_;
+    d.tile_pbeg = to_dev(b_tile_pbeg_, act_.tile_pbeg);
+    d.tile_ebeg = to_dev(b_tile_ebeg_, act_.tile_ebeg);
+    d.tile_ecnt = to_dev(b_tile_ecnt_, act_.tile_ecnt);
+    d.tile_chunk_base = to_dev(b_tile_chunk_, act_.tile_chunk_base);
+    const uint32_t* rb = to_dev(s_rb, real_beg);
+    // device edge order: stable sort by (tile, camera) over factor order
+    uint64_t* k64 = scratch<uint64_t>(s_k64, na);
+    uint64_t* k64b = scratch<uint64_t>(s_k64b, na);
+    uint32_t* vals = scratch<uint32_t>(s_val2, na);
+    uint32_t* order = scratch<uint32_t>(s_order, na);
+    k_edge_keys<<<grid_for(na), 256, 0, s_>>>(na, cam_a, pt_a, rank, d.tile_pbeg, T, k64, vals);
+    CK(cudaGetLastError());
+    cub_sort<uint64_t>(k64, k64b, vals, order, na, 32 + bits_for(T));
+    // padded slot arrays
+    uint32_t* d_a = static_cast<uint32_t*>(b_da_.alloc(std::max<uint64_t>(1, ns) * sizeof(uint32_t)));
+    uint32_t* d_cam = static_cast<uint32_t*>(b_dcam_.alloc(std::max<uint64_t>(1, ns) * sizeof(uint32_t)));
+    uint16_t* d_lpt = static_cast<uint16_t*>(b_dlpt_.alloc(std::max<uint64_t>(1, ns) * sizeof(uint16_t)));
+    uint16_t* d_lcam = static_cast<uint16_t*>(b_dlcam_.alloc(std::max<uint64_t>(1, ns) * sizeof(uint16_t)));
+    FP* d_obs = static_cast<FP*>(b_obs_.alloc(std::max<uint64_t>(1, 2 * ns) * sizeof(FP)));
+    CK(cudaMemsetAsync(d_a, 0xff, std::max<uint64_t>(1, ns) * sizeof(uint32_t), s_));
+    CK(cudaMemsetAsync(d_lpt, 0, std::max<uint64_t>(1, ns) * sizeof(uint16_t), s_));
+    CK(cudaMemsetAsync(d_obs, 0, std::max<uint64_t>(1, 2 * ns) * sizeof(FP), s_));
+    uint32_t* pkey = scratch<uint32_t>(s_pkey, na);
+    uint32_t* pval = scratch<uint32_t>(s_pval, na);
+    uint32_t* hc = scratch<uint32_t>(s_hc, na);
+    uint32_t* hr = scratch<uint32_t>(s_hr, na);
+    k_place<FP><<<grid_for(na), 256, 0, s_>>>(na, k64b, order, cam_a, pt_a, entry_a, rank, rb, d.tile_ebeg,
+                                               d.tile_pbeg, obs, ns, d_a, d_cam, d_lpt, d_obs, pkey, pval, hc, hr);
+    CK(cudaGetLastError());
+    uint32_t* ic = scratch<uint32_t>(s_ic, na);
+    uint32_t* ir = scratch<uint32_t>(s_ir, na);
+    cub_scan_incl(hc, ic, na);
+    cub_scan_incl(hr, ir, na);
+    uint32_t* tile_cam_off = static_cast<uint32_t*>(b_tile_cam_off_.alloc((T + 1) * sizeof(uint32_t)));
+    uint32_t* chunk_part_base =
+        static_cast<uint32_t*>(b_chunk_part_.alloc((act_.nchunks + 1) * sizeof(uint32_t)));
+    k_tile_offsets<<<grid_for(T + 1), 256, 0, s_>>>(T, na, rb, d.tile_ecnt, d.tile_chunk_base, ic, ir, tile_cam_off,
+                                                     chunk_part_base);
+    CK(cudaGetLastError());
+    act_.tile_cam_off.resize(T + 1);
+    CK(cudaMemcpyAsync(act_.tile_cam_off.data(), tile_cam_off, (T + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
+    uint32_t nparts = 0;
+    CK(cudaMemcpyAsync(&nparts, chunk_part_base + act_.nchunks, sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    act_.nparts = nparts;
+    d.nparts = nparts;
+    const uint32_t ncams_total = act_.tile_cam_off[T];
+    uint32_t* tile_cams = static_cast<uint32_t*>(b_tile_cams_.alloc(std::max<uint32_t>(1, ncams_total) * sizeof(uint32_t)));
+    uint32_t* run_cam = scratch<uint32_t>(s_runcam, nparts);
+    k_runs<<<grid_for(na), 256, 0, s_>>>(na, k64b, rb, d.tile_ebeg, tile_cam_off, hc, ic, hr, ir, d_lcam, tile_cams,
+                                          run_cam);
+    k_pad<<<grid_for(T), 256, 0, s_>>>(T, d.tile_ebeg, d.tile_ecnt, d_cam, d_lcam);
+    CK(cudaGetLastError());
+    // per-point slot lists: stable sort of (point rank, slot) + degree scan
+    uint32_t* pkey2 = scratch<uint32_t>(s_pkey2, na);
+    uint32_t* pval2 = scratch<uint32_t>(s_pval2, na);
+    cub_sort<uint32_t>(pkey, pkey2, pval, pval2, na, bits_for(np));
+    uint16_t* pt_slots = static_cast<uint16_t*>(b_pt_slots_.alloc(std::max<uint64_t>(1, na) * sizeof(uint16_t)));
+    k_u32_to_u16<<<grid_for(na), 256, 0, s_>>>(na, pval2, pt_slots);
+    uint32_t* pt_slot_off = static_cast<uint32_t*>(b_pt_slot_off_.alloc((np + 1) * sizeof(uint32_t)));
+    cub_scan_excl(degi, pt_slot_off, np + 1);
+    // camera -> partial-slot CSR
+    uint32_t* slots = scratch<uint32_t>(s_slots, nparts);
+    uint32_t* runcam2 = scratch<uint32_t>(s_runcam2, nparts);
+    k_iota<<<grid_for(nparts), 256, 0, s_>>>(nparts, slots);
+    uint32_t* cam_part_idx = static_cast<uint32_t*>(b_cam_part_idx_.alloc(std::max<uint32_t>(1, nparts) * sizeof(uint32_t)));
+    cub_sort<uint32_t>(run_cam, runcam2, slots, cam_part_idx, nparts, bits_for(nc));
+    uint32_t* cnt = scratch<uint32_t>(s_cnt, nc + 1);
+    CK(cudaMemsetAsync(cnt, 0, (nc + 1) * sizeof(uint32_t), s_));
+    k_hist<<<grid_for(nparts), 256, 0, s_>>>(nparts, run_cam, cnt);
+    uint32_t* cam_part_off = static_cast<uint32_t*>(b_cam_part_off_.alloc((nc + 1) * sizeof(uint32_t)));
+    cub_scan_excl(cnt, cam_part_off, nc + 1);
+    // columns: free mask in internal order
+    uint8_t* col_free = static_cast<uint8_t*>(b_col_free_.alloc(std::max<uint64_t>(1, ncols_)));
+    k_col_free<<<grid_for(ncols_), 256, 0, s_>>>(static_cast<uint32_t>(nc), static_cast<uint32_t>(np), cfix, pfix,
+                                                 pt_order, col_free);
+    CK(cudaGetLastError());
+    classify_tiles(act_);
+    d.normal_tiles = to_dev(b_normal_, act_.normal_tiles);
+    d.heavy_tiles = to_dev(b_heavy_, act_.heavy_tiles);
+    d.n_normal = static_cast<uint32_t>(act_.normal_tiles.size());
+    d.n_heavy = static_cast<uint32_t>(act_.heavy_tiles.size());
+    d.d_cam = d_cam;
+    d.d_lpt = d_lpt;
+    d.d_lcam = d_lcam;
+    d.d_obs = d_obs;
+    d.tile_cam_off = tile_cam_off;
+    d.tile_cams = tile_cams;
+    d.chunk_part_base = chunk_part_base;
+    d.pt_slot_off = pt_slot_off;
+    d.pt_slots = pt_slots;
+    d.cam_part_off = cam_part_off;
+    d.cam_part_idx = cam_part_idx;
+    d.col_free = col_free;
+    CK(cudaStreamSynchronize(s_));  // scratch buffers are released on return
+  }
+
+  void allocate_work() {
+    const uint64_t nc = act_.nc, np = act_.np, ns = act_.n_slots;
+    Dev<FP, SP>& d = dev_;
     const bool dyn = g_.diff_mode == GB_DYNAMIC;
     d.J = dyn ? nullptr : static_cast<SP*>(b_J_.alloc(24 * ns * sizeof(SP)));
     if (d.J) CK(cudaMemsetAsync(d.J, 0, 24 * ns * sizeof(SP), s_));  // padding slots stay 0
@@ -635,25 +922,27 @@ class Solver final : public SolverBase {
     CK(cudaMemsetAsync(d.redmax, 0, 8 * sizeof(FP), s_));
     CK(cudaMemsetAsync(d.xs, 0, ncols_ * sizeof(SP), s_));
     CK(cudaMemsetAsync(d.p, 0, ncols_ * sizeof(SP), s_));
-    if (pinned_) cudaFreeHost(pinned_);
-    pinned_ = nullptr;
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&pinned_), std::max<uint64_t>(1, ncols_) * sizeof(FP), cudaHostAllocDefault));
+    b_ptstage_.alloc(std::max<uint64_t>(1, 3 * np) * sizeof(FP));
   }
 
+  // user AoS -> internal order on the device (cameras copied as is)
   void upload_params() {
     const uint64_t nc = act_.nc, np = act_.np;
-    const FP* uc = static_cast<const FP*>(g_.cams);
-    const FP* up = static_cast<const FP*>(g_.pts);
-    CK(cudaStreamSynchronize(s_));  // pinned_ may still be in flight
-    std::memcpy(pinned_, uc, 9 * nc * sizeof(FP));
-    FP* dst = pinned_ + 9 * nc;
-    for (uint64_t i = 0; i < np; ++i) {
-      const uint64_t p = act_.pt_order[i];
-      dst[3 * i] = up[3 * p];
-      dst[3 * i + 1] = up[3 * p + 1];
-      dst[3 * i + 2] = up[3 * p + 2];
+    FP* stage = b_ptstage_.as<FP>();
+    CK(cudaMemcpyAsync(dev_.x, g_.cams, 9 * nc * sizeof(FP), cudaMemcpyHostToDevice, s_));
+    if (dist()) {  // the shard's own points only
+      std::vector<FP> loc(3 * np);
+      const FP* up = static_cast<const FP*>(g_.pts);
+      for (uint64_t i = 0; i < np; ++i)
+        for (int k = 0; k < 3; ++k) loc[3 * i + k] = up[3ull * act_.pt_order[i] + k];
+      CK(cudaMemcpyAsync(dev_.x + 9 * nc, loc.data(), loc.size() * sizeof(FP), cudaMemcpyHostToDevice, s_));
+      CK(cudaStreamSynchronize(s_));
+    } else {
+      CK(cudaMemcpyAsync(stage, g_.pts, 3 * np * sizeof(FP), cudaMemcpyHostToDevice, s_));
+      actdev::k_gather_points<FP><<<grid_for(3 * np), 256, 0, s_>>>(static_cast<uint32_t>(np), pt_order_dev_, stage,
+                                                                    dev_.x + 9 * nc);
+      CK(cudaGetLastError());
     }
-    CK(cudaMemcpyAsync(dev_.x, pinned_, ncols_ * sizeof(FP), cudaMemcpyHostToDevice, s_));
     h2d_bytes_ += ncols_ * sizeof(FP);
   }
 
@@ -663,20 +952,15 @@ class Solver final : public SolverBase {
       return;
     }
     const uint64_t nc = act_.nc, np = act_.np;
-    CK(cudaMemcpyAsync(pinned_, dev_.x, ncols_ * sizeof(FP), cudaMemcpyDeviceToHost, s_));
+    FP* stage = b_ptstage_.as<FP>();
+    actdev::k_scatter_points<FP><<<grid_for(3 * np), 256, 0, s_>>>(static_cast<uint32_t>(np), pt_order_dev_,
+                                                                   dev_.x + 9 * nc, stage);
+    CK(cudaGetLastError());
+    // fixed vertices are written back with their own bits (bit-identical)
+    CK(cudaMemcpyAsync(g_.cams, dev_.x, 9 * nc * sizeof(FP), cudaMemcpyDeviceToHost, s_));
+    CK(cudaMemcpyAsync(g_.pts, stage, 3 * np * sizeof(FP), cudaMemcpyDeviceToHost, s_));
     CK(cudaStreamSynchronize(s_));
     d2h_bytes_ += ncols_ * sizeof(FP);
-    FP* uc = static_cast<FP*>(g_.cams);
-    FP* up = static_cast<FP*>(g_.pts);
-    // fixed vertices are written back with their own bits (bit-identical)
-    std::memcpy(uc, pinned_, 9 * nc * sizeof(FP));
-    const FP* src = pinned_ + 9 * nc;
-    for (uint64_t i = 0; i < np; ++i) {
-      const uint64_t p = act_.pt_order[i];
-      up[3 * p] = src[3 * i];
-      up[3 * p + 1] = src[3 * i + 1];
-      up[3 * p + 2] = src[3 * i + 2];
-    }
   }
 
   // every rank ends with every point: each shard broadcasts its internal point
@@ -889,14 +1173,15 @@ class Solver final : public SolverBase {
   State<FP>* st_ = nullptr;
   State<FP> ls_state_{};
   bool ls_ready_ = false;
-  FP* pinned_ = nullptr;
   int* flag_host_ = nullptr;
   size_t h2d_bytes_ = 0, d2h_bytes_ = 0;
   cudaGraphExec_t graph_exec_ = nullptr;
   int graph_pcg_it_ = -1;
   gb_iteration_record* graph_recs_ = nullptr;
   DBuf st_buf_, rec_buf_, dbg_buf_;
-  DBuf b_red_, b_redmax_, b_xall_;
+  DBuf b_red_, b_redmax_, b_xall_, b_pt_order_, b_da_, b_cub_, b_ptstage_;
+  uint32_t* pt_order_dev_ = nullptr;
+  bool host_plan_ = false;
   DBuf b_vt_, b_dlcam_, b_tile_ecnt_, b_tile_cam_off_, b_tile_cams_, b_normal_, b_heavy_;
   DBuf b_col_free_, b_dcam_, b_dlpt_, b_obs_, b_tile_ebeg_, b_tile_pbeg_, b_tile_chunk_, b_chunk_part_,
       b_pt_slot_off_, b_pt_slots_, b_cam_part_off_, b_cam_part_idx_;
@@ -1132,6 +1417,13 @@ int gb_shard_plan(uint64_t num_cameras, uint64_t num_points, uint64_t n, const u
       if (point_owner)
         for (uint32_t i = p0; i < p1; ++i) point_owner[full.pt_order[i]] = static_cast<uint32_t>(r);
     }
+  });
+}
+
+int gb_activation_selfcheck(gb_graph* g, int level) {
+  return guarded([&] {
+    const std::string e = g->get().selfcheck(level);
+    if (!e.empty()) throw std::logic_error("device activation differs from host activation: " + e);
   });
 }
 

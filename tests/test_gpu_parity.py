@@ -244,3 +244,17 @@ def test_stepping_api_matches_optimize(gpu, ladybug):
     ms = ctypes.c_double()
     L.check(L.fn("time_hvp")(g2._h, 3, ctypes.byref(ms), None))
     assert ms.value > 0
+
+
+def test_device_activation_matches_host(gpu):
+    from paper_2509_26581_b200 import _abi
+
+    rng = np.random.default_rng(3)
+    cases = [bal.synthetic_bal(*LADYBUG, seed=42), bal.synthetic_bal(520, 30, 30 * 520, seed=7),
+             bal.synthetic_bal(*TINY, seed=5), bal.synthetic_bal(200, 5000, 25000, seed=4, zipf=1.1)]
+    for i, p in enumerate(cases):
+        g = bal.build_graph(p, "fp64")
+        if i == 0:
+            g.set_fixed(cameras=rng.random(p.num_cameras) < 0.1, points=rng.random(p.num_points) < 0.05)
+            g.set_levels((rng.random(p.num_observations) < 0.05).astype(np.uint8))
+        g.backend.check(_abi.lib().gb_activation_selfcheck(g._h, 0))
