@@ -288,7 +288,7 @@ __device__ inline void load_J(const Dev<FP, SP>& d, uint32_t e, arith_t<SP>* jc,
 // shared memory. Point epilogue: clamp, D = 1/sqrt(clamped), finiteness,
 // max |b|.
 // =====================================================================
-template <typename FP, typename SP, bool STORE>
+template <typename FP, typename SP, bool STORE, bool AUTO>
 __global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, const uint32_t* list, int force) {
   if (!force && !d.st->do_linearize) return;
   const uint32_t t = list ? list[blockIdx.x] : blockIdx.x;
@@ -322,7 +322,12 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, const
     for (int k = 0; k < 9; ++k) cp[k] = d.x[9ull * cam + k];
     const FP* X = &sX[3 * lp];
     FP res[2], jc[18], jp[6];
-    snavely_linearize<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res, jc, jp);
+    if (AUTO) {
+      snavely_residual<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res);
+      snavely_jacobians_auto<FP>(cp, X, jc, jp);
+    } else {
+      snavely_linearize<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res, jc, jp);
+    }
     const FP s = res[0] * res[0] + res[1] * res[1];
     const FP w = valid ? loss_weight<FP>(loss, delta, s) : FP(0);
     if (valid) chi += loss_value<FP>(loss, delta, s);
@@ -836,8 +841,8 @@ __global__ void k_pcg_init(Dev<FP, SP> d) {
 // segmented runs -> partial slots. Point Jp^T q: staged in shared memory and
 // summed per point in slot order after the single tile barrier. The tile's
 // p.Ap goes out as one partial per warp (no block reduction).
-template <typename FP, typename SP, bool DYN>
-__global__ void __launch_bounds__(kTileThreads) k_hvp_tiles(Dev<FP, SP> d) {
+template <typename FP, typename SP, bool DYN, int MINB = 1>
+__global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d) {
   using A = arith_t<SP>;
   if (!d.st->iter_active || d.st->pcg_done) return;
   __shared__ A stage[kTileEdges * 3];
@@ -989,7 +994,7 @@ __host__ __device__ constexpr size_t lin_normal_smem() {
   return sizeof(FP) * (kTilePoints * 3 + kTileCams * 9 + kTileThreads * kLinRow + kTileEdges * 9 + 32);
 }
 
-template <typename FP, typename SP, bool STORE>
+template <typename FP, typename SP, bool STORE, bool AUTO>
 __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int force) {
   if (!force && !d.st->do_linearize) return;
   extern __shared__ __align__(16) unsigned char lin_smem[];
@@ -1016,7 +1021,12 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
   const FP o0 = d.d_obs[e], o1 = d.d_obs[static_cast<uint64_t>(d.na) + e];
 
   FP res[2], jc[18], jp[6];
-  snavely_linearize<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res, jc, jp);
+  if (AUTO) {
+    snavely_residual<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res);
+    snavely_jacobians_auto<FP>(&sC[9 * lc], &sX[3 * lp], jc, jp);
+  } else {
+    snavely_linearize<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res, jc, jp);
+  }
   const FP s = res[0] * res[0] + res[1] * res[1];
   const FP w = valid ? loss_weight<FP>(d.loss_kind, d.huber, s) : FP(0);
   if (valid) chi += loss_value<FP>(d.loss_kind, d.huber, s);

@@ -181,6 +181,112 @@ __device__ inline void snavely_jacobians(const FP* cam, const FP* X, FP* jc, FP*
   snavely_linearize<FP>(cam, X, FP(0), FP(0), nullptr, jc, jp);
 }
 
+// ---- Auto differentiation (DifferentiationMode::Auto) ----------------------
+// Forward-mode dual numbers with one infinitesimal (dual.hpp:13-99) and the
+// residual evaluated generically (snavely_project + rotate_angle_axis,
+// snavely.hpp:18-61): one pass per Jacobian column, the residual recomputed
+// per column exactly like FactorDescriptor::jacobian_auto_slot
+// (factor_descriptor.hpp:610-624).
+template <typename T>
+struct Dual {
+  T v, d;
+};
+template <typename T>
+__device__ inline Dual<T> operator+(Dual<T> a, Dual<T> b) { return {a.v + b.v, a.d + b.d}; }
+template <typename T>
+__device__ inline Dual<T> operator-(Dual<T> a, Dual<T> b) { return {a.v - b.v, a.d - b.d}; }
+template <typename T>
+__device__ inline Dual<T> operator*(Dual<T> a, Dual<T> b) { return {a.v * b.v, a.v * b.d + a.d * b.v}; }
+template <typename T>
+__device__ inline Dual<T> operator/(Dual<T> a, Dual<T> b) {
+  const T inv = T(1) / b.v;
+  return {a.v * inv, (a.d - a.v * inv * b.d) * inv};
+}
+template <typename T>
+__device__ inline Dual<T> operator-(Dual<T> a) { return {-a.v, -a.d}; }
+template <typename T>
+__device__ inline Dual<T> operator+(Dual<T> a, T b) { return {a.v + b, a.d}; }
+template <typename T>
+__device__ inline Dual<T> operator+(T a, Dual<T> b) { return {a + b.v, b.d}; }
+template <typename T>
+__device__ inline Dual<T> operator-(Dual<T> a, T b) { return {a.v - b, a.d}; }
+template <typename T>
+__device__ inline Dual<T> operator-(T a, Dual<T> b) { return {a - b.v, -b.d}; }
+template <typename T>
+__device__ inline Dual<T> operator*(Dual<T> a, T b) { return {a.v * b, a.d * b}; }
+template <typename T>
+__device__ inline Dual<T> operator*(T a, Dual<T> b) { return {a * b.v, a * b.d}; }
+template <typename T>
+__device__ inline Dual<T> dsqrt(Dual<T> a) {
+  const T s = sqrt(a.v);
+  return {s, a.d / (T(2) * s)};
+}
+template <typename T>
+__device__ inline void dsincos(Dual<T> a, Dual<T>* sn, Dual<T>* cs) {
+  T s, c;
+  sin_cos(a.v, &s, &c);
+  *sn = {s, c * a.d};
+  *cs = {c, -s * a.d};
+}
+
+template <typename FP>
+__device__ inline void snavely_project_dual(const Dual<FP>* camera, const Dual<FP>* X, Dual<FP>* predicted) {
+  using D = Dual<FP>;
+  const D* omega = camera;
+  const D theta2 = omega[0] * omega[0] + omega[1] * omega[1] + omega[2] * omega[2];
+  D a, s, c;
+  if (theta2.v < taylor_threshold<FP>::value) {
+    const D u = theta2;
+    a = FP(1) - u * FP(0.5) + u * u * (FP(1) / FP(24));
+    s = FP(1) - u * (FP(1) / FP(6)) + u * u * (FP(1) / FP(120));
+    c = FP(0.5) - u * (FP(1) / FP(24)) + u * u * (FP(1) / FP(720));
+  } else {
+    const D theta = dsqrt(theta2);
+    D sn, cs;
+    dsincos(theta, &sn, &cs);
+    a = cs;
+    s = sn / theta;
+    c = (FP(1) - a) / theta2;
+  }
+  const D wx = omega[1] * X[2] - omega[2] * X[1];
+  const D wy = omega[2] * X[0] - omega[0] * X[2];
+  const D wz = omega[0] * X[1] - omega[1] * X[0];
+  const D dot = omega[0] * X[0] + omega[1] * X[1] + omega[2] * X[2];
+  D p0 = a * X[0] + s * wx + c * dot * omega[0];
+  D p1 = a * X[1] + s * wy + c * dot * omega[1];
+  D p2 = a * X[2] + s * wz + c * dot * omega[2];
+  p0 = p0 + camera[3];
+  p1 = p1 + camera[4];
+  p2 = p2 + camera[5];
+  const D xp = -p0 / p2;
+  const D yp = -p1 / p2;
+  const D n = xp * xp + yp * yp;
+  const D distortion = FP(1) + n * (camera[7] + n * camera[8]);
+  predicted[0] = camera[6] * distortion * xp;
+  predicted[1] = camera[6] * distortion * yp;
+}
+
+// jc (2x9) and jp (2x3) by 12 dual passes
+template <typename FP>
+__device__ inline void snavely_jacobians_auto(const FP* cam, const FP* X, FP* jc, FP* jp) {
+#pragma unroll 1
+  for (int k = 0; k < 12; ++k) {
+    Dual<FP> c[9], x[3], pred[2];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) c[i] = {cam[i], i == k ? FP(1) : FP(0)};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) x[i] = {X[i], 9 + i == k ? FP(1) : FP(0)};
+    snavely_project_dual<FP>(c, x, pred);
+    if (k < 9) {
+      jc[k] = pred[0].d;
+      jc[9 + k] = pred[1].d;
+    } else {
+      jp[k - 9] = pred[0].d;
+      jp[3 + k - 9] = pred[1].d;
+    }
+  }
+}
+
 // Robust loss (loss.hpp:25-40): value rho(s) and IRLS weight rho'(s).
 template <typename FP>
 __device__ inline FP loss_value(int kind, FP delta, FP s) {

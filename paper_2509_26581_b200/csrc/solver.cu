@@ -126,9 +126,12 @@ class Solver final : public SolverBase {
  public:
   explicit Solver(GraphData& g) : g_(g) {
     CK(cudaSetDevice(g_.device));
-    CK(cudaFuncSetAttribute(k_lin_normal<FP, SP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (const char* e = std::getenv("GB_HVP_MINB")) hvp_minb_ = std::atoi(e);
+    CK(cudaFuncSetAttribute(k_lin_normal<FP, SP, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(lin_normal_smem<FP>())));
-    CK(cudaFuncSetAttribute(k_lin_normal<FP, SP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_lin_normal<FP, SP, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(lin_normal_smem<FP>())));
+    CK(cudaFuncSetAttribute(k_lin_normal<FP, SP, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(lin_normal_smem<FP>())));
     CK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
     st_ = static_cast<State<FP>*>(st_buf_.alloc(sizeof(State<FP>)));
@@ -1025,12 +1028,19 @@ class Solver final : public SolverBase {
 
   void enqueue_linearize(int force) {
     const size_t smem = lin_normal_smem<FP>();
-    if (dev_.J) {
-      if (dev_.n_normal) k_lin_normal<FP, SP, true><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
-      if (dev_.n_heavy) k_lin_tiles<FP, SP, true><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
+    const bool aut = g_.diff_mode == GB_AUTO;
+    if (dev_.J && aut) {  // Auto: stored J from dual-number passes (factor_descriptor.hpp:610-624)
+      if (dev_.n_normal) k_lin_normal<FP, SP, true, true><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
+      if (dev_.n_heavy)
+        k_lin_tiles<FP, SP, true, true><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
+    } else if (dev_.J) {
+      if (dev_.n_normal) k_lin_normal<FP, SP, true, false><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
+      if (dev_.n_heavy)
+        k_lin_tiles<FP, SP, true, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
     } else {
-      if (dev_.n_normal) k_lin_normal<FP, SP, false><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
-      if (dev_.n_heavy) k_lin_tiles<FP, SP, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
+      if (dev_.n_normal) k_lin_normal<FP, SP, false, false><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
+      if (dev_.n_heavy)
+        k_lin_tiles<FP, SP, false, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
     }
     CK(cudaGetLastError());
     if (!dist()) {
@@ -1049,8 +1059,10 @@ class Solver final : public SolverBase {
   void launch_hvp_tiles(const Dev<FP, SP>& d) {
     if (!d.J)
       k_hvp_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
+    else if (hvp_minb_ == 4)
+      k_hvp_tiles<FP, SP, false, 4><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
     else
-      k_hvp_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
+      k_hvp_tiles<FP, SP, false, 1><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
     CK(cudaGetLastError());
   }
 
@@ -1182,6 +1194,7 @@ class Solver final : public SolverBase {
   DBuf b_red_, b_redmax_, b_xall_, b_pt_order_, b_da_, b_cub_, b_ptstage_;
   uint32_t* pt_order_dev_ = nullptr;
   bool host_plan_ = false;
+  int hvp_minb_ = 4;  // occupancy hint of the HVP tile kernel (A/B: GB_HVP_MINB=1 -> 80 regs, 3 CTAs/SM)
   DBuf b_vt_, b_dlcam_, b_tile_ecnt_, b_tile_cam_off_, b_tile_cams_, b_normal_, b_heavy_;
   DBuf b_col_free_, b_dcam_, b_dlpt_, b_obs_, b_tile_ebeg_, b_tile_pbeg_, b_tile_chunk_, b_chunk_part_,
       b_pt_slot_off_, b_pt_slots_, b_cam_part_off_, b_cam_part_idx_;

@@ -258,3 +258,18 @@ def test_device_activation_matches_host(gpu):
             g.set_fixed(cameras=rng.random(p.num_cameras) < 0.1, points=rng.random(p.num_points) < 0.05)
             g.set_levels((rng.random(p.num_observations) < 0.05).astype(np.uint8))
         g.backend.check(_abi.lib().gb_activation_selfcheck(g._h, 0))
+
+
+def test_auto_mode_parity(gpu, ref, ladybug):
+    # DifferentiationMode::Auto: dual-number Jacobians (factor_descriptor.hpp:610-624);
+    # analytic vs auto < 1e-12 (tests/test_bal.cpp:243-244), traces vs the reference's auto run
+    ga, ra = pair(ladybug, ref, mode="auto")
+    ga.ls_linearize(0)
+    ra.ls_linearize(0)
+    ja, jr = ga.ls_jacobians(LADYBUG[2]), ra.ls_jacobians(LADYBUG[2])
+    assert rel(ja, jr) <= 1e-13
+    gn, _ = pair(ladybug, ref)
+    gn.ls_linearize(0)
+    assert rel(ja, gn.ls_jacobians(LADYBUG[2])) <= 1e-12
+    g, r, a1, b1 = run_pair(ladybug, ref, mode="auto")
+    assert_trace_parity(a1, b1, 1e-6)
