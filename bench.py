@@ -180,6 +180,8 @@ def ours(args, shape, desc):
         torch.distributed.broadcast_object_list(obj, src=0)
         uid = obj[0]
     g = bal.build_graph(problem, args.precision, "analytic", device=local)
+    if args.solver != "pcg":
+        g.set_linear_solver(args.solver)
     if world > 1:
         g.set_distributed(world, rank, "nccl", uid)
     L = g.backend
@@ -223,6 +225,8 @@ def ours(args, shape, desc):
         torch.distributed.barrier()
     t0 = time.perf_counter()
     g2 = bal.build_graph(problem, args.precision, "analytic", device=local)
+    if args.solver != "pcg":
+        g2.set_linear_solver(args.solver)
     if world > 1:
         g2.set_distributed(world, rank, "nccl", obj[0])
     rep2 = bal.levenberg_marquardt(g2, cfg)
@@ -258,7 +262,8 @@ def ours(args, shape, desc):
         "metric": "LM iteration ms (synthetic BAL BA)", "value": round(ms, 4), "unit": "ms/LM-iteration",
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(ms, 4), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision], "data": "synthetic",
-        "config": {"workload": desc + f" {args.precision} analytic, PCG<=10@1e-6", "precision": args.precision,
+        "config": {"workload": desc + f" {args.precision} analytic, PCG<=10@1e-6" +
+                   ("" if args.solver == "pcg" else f", {args.solver} linear solver"), "precision": args.precision,
                    "cache": "inputs larger than L2 (J store %.2f GB)" % (E * 24 * sJ / 1e9),
                    "parallelism": "single GPU" if world == 1 else
                    f"{world} GPUs: point-tile shards, replicated cameras, NCCL allreduce per PCG iteration"},
@@ -313,6 +318,8 @@ def main():
     ap.add_argument("--workload", default="final", choices=sorted(WORKLOADS))
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32", "fp32-bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solver", default="pcg", choices=["pcg", "schur"],
+                    help="pcg = the reference algorithm (headline); schur = Schur-complement mode")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -55,6 +55,9 @@ extern "C" {
 /* factor_descriptor.hpp:37 DampingPlacement */
 #define GB_DAMPING_AFTER_SCALING 0
 #define GB_DAMPING_BEFORE_SCALING 1
+/* linear solver of the LM step (gb_set_linear_solver) */
+#define GB_SOLVER_PCG 0   /* matrix-free PCG on the full system (the reference, linear_system.hpp:185-207) */
+#define GB_SOLVER_SCHUR 1 /* Schur complement onto the cameras (north star (c); no reference counterpart) */
 /* levenberg_marquardt.hpp:28-35 Termination */
 #define GB_TERM_MAX_ITERATIONS 0
 #define GB_TERM_TOLERANCE_REACHED 1
@@ -175,6 +178,12 @@ int gb_set_points(gb_graph* g, void* params_fp, uint64_t n, const uint8_t* fixed
 int gb_set_observations(gb_graph* g, uint64_t n, const uint32_t* camera_index,
                         const uint32_t* point_index, const void* observed_fp,
                         const uint8_t* level, int loss_kind, double huber_delta);
+/* Linear solver of every LM step: GB_SOLVER_PCG (default, the reference's
+ * algorithm) or GB_SOLVER_SCHUR: points are eliminated with their exact 3x3
+ * blocks, PCG (same pcg_solve semantics and config) runs on the reduced camera
+ * system S = A_cc - A_cp A_pp^-1 A_pc with block-Jacobi on S's camera blocks,
+ * and the points are back-substituted. Stored-Jacobian modes, single GPU. */
+int gb_set_linear_solver(gb_graph* g, int solver);
 /* FactorDescriptor::set_differentiation_mode (factor_descriptor.hpp:230-235). */
 int gb_set_differentiation_mode(gb_graph* g, int diff_mode);
 

@@ -562,3 +562,124 @@ def project(camera, point, precision="fp64"):
     c = np.asarray(camera, P.FP)[None, :]
     x = np.asarray(point, P.FP)[None, :]
     return residual(c, x, np.zeros((1, 2), P.FP), P)[0]
+
+
+# ------------------------------------------------------------ Schur mode
+# Not in the reference (SPEC.md:164, 366 non-goal; PAPER.md:561 future work):
+# this is the CPU statement of the device Schur-complement solver mode
+# (SURVEY.md §8 f-1), checked against a dense oracle in the tests. On the
+# scaled, damped system A = D H D + Lambda (linear_system.hpp:104-115) with
+# camera (c) / point (p) blocks:
+#   S = A_cc - A_cp A_pp^-1 A_pc,  r_c = rhs_c - A_cp A_pp^-1 rhs_p
+#   S x_c = r_c by pcg_solve with block-Jacobi on S's camera blocks,
+#   x_p = A_pp^-1 (rhs_p - A_pc x_c); pred and dx as in solve_step.
+class SchurSystem:
+    def __init__(self, ls: LinearSystem):
+        self.ls = ls
+        g = ls.g
+        a = g.active
+        self.cam = g.cam_idx[a]
+        self.pt = g.pt_idx[a]
+        nfc = int(np.sum(~g.cam_fixed))
+        self.nfc = nfc
+        self.ccol = g.cam_col[self.cam]
+        self.pcol = g.pt_col[self.pt]
+
+    def _parts(self, lam):
+        ls, g = self.ls, self.ls.g
+        T = g.P.FP
+        D = ls.D
+        Jc, Jp = ls.Jc.astype(T), ls.Jp.astype(T)
+        ok_c = self.ccol >= 0
+        ok_p = self.pcol >= 0
+        cc = np.where(ok_c[:, None], self.ccol[:, None] + np.arange(9), 0)
+        pc = np.where(ok_p[:, None], self.pcol[:, None] + np.arange(3), 0)
+        Jtc = np.where(ok_c[:, None, None], Jc * D[cc][:, None, :], 0)
+        Jtp = np.where(ok_p[:, None, None], Jp * D[pc][:, None, :], 0)
+        w = ls.w.astype(T)
+        lamv = (T(lam) * D * D) if ls.before else np.full(g.N, T(lam))
+        N = g.N
+        npf = (N - 9 * self.nfc) // 3
+        App = np.zeros((npf, 3, 3), T)
+        pidx = np.where(ok_p, (self.pcol - 9 * self.nfc) // 3, 0)
+        np.add.at(App, pidx[ok_p], (w[:, None, None] * np.einsum("eri,erj->eij", Jtp, Jtp))[ok_p])
+        App[:, np.arange(3), np.arange(3)] += lamv[9 * self.nfc:].reshape(npf, 3)
+        Ainv = np.linalg.inv(App.astype(np.float64)).astype(T)
+        return Jtc, Jtp, w, lamv, pidx, ok_c, ok_p, Ainv, cc, pc
+
+    def operator(self, lam):
+        Jtc, Jtp, w, lamv, pidx, ok_c, ok_p, Ainv, cc, pc = self._parts(lam)
+        nfc, T = self.nfc, self.ls.g.P.FP
+
+        def S(v):  # camera-sized
+            vv = np.zeros(self.ls.g.N, T)
+            vv[: 9 * nfc] = v
+            u = np.einsum("erc,ec->er", Jtc, vv[cc] * ok_c[:, None])
+            q = w[:, None] * u
+            y = np.zeros((Ainv.shape[0], 3), T)
+            np.add.at(y, pidx[ok_p], np.einsum("erc,er->ec", Jtp, q)[ok_p])
+            z = np.einsum("pij,pj->pi", Ainv, y)
+            u2 = np.einsum("erc,ec->er", Jtp, z[pidx] * ok_p[:, None])
+            g = np.einsum("erc,er->ec", Jtc, w[:, None] * (u - u2))
+            out = lamv[: 9 * nfc] * v
+            np.add.at(out, cc[ok_c].ravel(), g[ok_c].ravel())
+            return out
+
+        return S
+
+    def solve_step(self, lam, pcg):
+        ls, g = self.ls, self.ls.g
+        T = g.P.FP
+        Jtc, Jtp, w, lamv, pidx, ok_c, ok_p, Ainv, cc, pc = self._parts(lam)
+        nfc = self.nfc
+        rhs = (-ls.D * ls.b).astype(T)
+        rc, rp = rhs[: 9 * nfc], rhs[9 * nfc:].reshape(-1, 3)
+        zp = np.einsum("pij,pj->pi", Ainv, rp)
+        u2 = np.einsum("erc,ec->er", Jtp, zp[pidx] * ok_p[:, None])
+        gc = np.einsum("erc,er->ec", Jtc, w[:, None] * u2)
+        r = rc.copy()
+        np.add.at(r, cc[ok_c].ravel(), -gc[ok_c].ravel())
+        # block-Jacobi of S: A_cc(c) - sum_e B_e A_pp^-1 B_e^T, B_e = w Jtc^T Jtp
+        Scc = np.zeros((nfc, 9, 9), T)
+        cidx = np.where(ok_c, self.ccol // 9, 0)
+        np.add.at(Scc, cidx[ok_c], (w[:, None, None] * np.einsum("eri,erj->eij", Jtc, Jtc))[ok_c])
+        B = w[:, None, None] * np.einsum("eri,erj->eij", Jtc, Jtp)
+        corr = np.einsum("eij,ejk,elk->eil", B, Ainv[pidx], B)
+        sel = ok_c & ok_p
+        np.add.at(Scc, cidx[sel], -corr[sel])
+        Scc[:, np.arange(9), np.arange(9)] += lamv[: 9 * nfc].reshape(nfc, 9)
+        Minv = np.linalg.inv(Scc.astype(np.float64)).astype(T)
+
+        def M(v):
+            return g.P.narrow(np.einsum("kij,kj->ki", Minv, v.astype(T).reshape(nfc, 9)).reshape(-1))
+
+        xc, stats = pcg_solve(self.operator(lam), M, r, pcg, g.P)
+        xx = np.zeros(g.N, T)
+        xx[: 9 * nfc] = xc
+        u = np.einsum("erc,ec->er", Jtc, xx[cc] * ok_c[:, None])
+        y = np.zeros_like(rp)
+        np.add.at(y, pidx[ok_p], np.einsum("erc,er->ec", Jtp, w[:, None] * u)[ok_p])
+        xp = np.einsum("pij,pj->pi", Ainv, rp - y)
+        x = np.concatenate([xc, xp.reshape(-1)]).astype(T)
+        damp = T(lam) * ls.D * ls.D if ls.before else T(lam)
+        pred = seqsum(x * (damp * x + rhs), T)
+        dx = (ls.D * x).astype(T)
+        return dx, stats, pred, bool(np.all(np.isfinite(dx)))
+
+    def dense(self, lam):
+        """Dense A, S, r_c and the exact Schur solution (the dense oracle)."""
+        ls, g = self.ls, self.ls.g
+        N, nfc = g.N, self.nfc
+        A = np.zeros((N, N))
+        I = np.eye(N)
+        for k in range(N):
+            A[:, k] = ls.hvp(I[k].astype(g.P.FP), lam)
+        rhs = -ls.D * ls.b
+        c = slice(0, 9 * nfc)
+        p = slice(9 * nfc, N)
+        Spp = np.linalg.inv(A[p, p])
+        S = A[c, c] - A[c, p] @ Spp @ A[p, c]
+        r = rhs[c] - A[c, p] @ Spp @ rhs[p]
+        xc = np.linalg.solve(S, r)
+        xp = Spp @ (rhs[p] - A[p, c] @ xc)
+        return A, S, r, np.concatenate([xc, xp]), rhs

@@ -314,6 +314,14 @@ class BalGraph:
         self._levels = np.ascontiguousarray(levels, dtype=np.uint8)
         self._bind()
 
+    # -- linear solver of the LM step
+    def set_linear_solver(self, solver: str = "pcg"):
+        """'pcg' (the reference's full-system PCG) or 'schur' (Schur complement
+        onto the cameras, back-substituted points; device path only)."""
+        if solver not in ("pcg", "schur"):
+            raise ValueError(f"unknown linear solver: {solver}")
+        self.backend.check(self.backend.fn("set_linear_solver")(self._h, 0 if solver == "pcg" else 1))
+
     # -- sharding (multi-GPU; SURVEY.md §8e)
     def set_distributed(self, world: int, rank: int, kind: str = "nccl", uid: bytes = b""):
         """Shard this graph over `world` ranks (this handle is `rank`). kind

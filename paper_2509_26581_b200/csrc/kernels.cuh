@@ -61,6 +61,7 @@ struct State {
   double tol, grad_tol, lambda_max, tau, pcg_tol, pcg_ratio;
   double clamp_min, clamp_max;
   int max_iterations, pcg_max_it, normalize_rhs, before_scaling, use_guard, refresh_on_reject;
+  int schur;  // linear solver: 0 full-system PCG (reference), 1 Schur complement on the cameras
   // PCG
   FP rho, pap, alpha, beta, rhs_norm, scale, unscale, ref_norm;
   double pcg_relres;
@@ -120,6 +121,8 @@ struct Dev {
   SP* p;
   SP* ap;
   A* vt;       // (Arith) D * p for every column, refreshed with p (HVP gather source)
+  FP* rc;      // Schur: reduced camera rhs (9nc)
+  FP* xp;      // Schur: back-substituted point step (3np), unscaled
   A* dbg_out;  // optional wide HVP output (LinearSystem::hvp surface)
   FP* dx;
   FP* tile_red;   // [ntiles * 8] (HVP: one dot partial per warp of a tile)
@@ -721,6 +724,7 @@ __global__ void k_precond(Dev<FP, SP> d) {
   if (!d.st->iter_active) return;
   const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (v < d.nc) {
+    if (d.st->schur) return;  // k_schur_pre_cams
     const uint64_t col = 9 * v;
     precond_vertex<FP, SP, 9>(d, d.Hc + 45 * v, d.Mc + 45 * v, col, d.col_free[col]);
   } else if (v < static_cast<uint64_t>(d.nc) + d.np) {
@@ -761,7 +765,8 @@ __global__ void k_rhs_norm(Dev<FP, SP> d) {
   FP acc = FP(0);
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const FP rhs = -d.D[i] * d.b[i];
+    if (d.st->schur && i >= 9ull * d.nc) break;
+    const FP rhs = d.st->schur ? d.rc[i] : -d.D[i] * d.b[i];
     if (counted(d, i)) acc += rhs * rhs;
   }
   acc = block_sum(acc, scratch);
@@ -788,12 +793,12 @@ __global__ void k_pcg_init(Dev<FP, SP> d) {
   FP rz = FP(0), rr = FP(0);
   const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t nv = static_cast<uint64_t>(d.nc) + d.np;
-  if (v < nv) {
+  if (v < nv && !(d.st->schur && v >= d.nc)) {
     const bool cam = v < d.nc;
     const int n = cam ? 9 : 3;
     const uint64_t col = cam ? 9 * v : 9ull * d.nc + 3 * (v - d.nc);
     for (int k = 0; k < n; ++k) {
-      const FP rhs = -d.D[col + k] * d.b[col + k];
+      const FP rhs = d.st->schur ? d.rc[col + k] : -d.D[col + k] * d.b[col + k];
       d.r[col + k] = narrow<SP>(rhs * scale);
       d.xs[col + k] = narrow<SP>(FP(0));
     }
@@ -1261,7 +1266,7 @@ __global__ void k_pcg_update(Dev<FP, SP> d) {
   const FP alpha = d.st->alpha;
   FP rz = FP(0), rr = FP(0);
   const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  const uint64_t nv = static_cast<uint64_t>(d.nc) + d.np;
+  const uint64_t nv = d.st->schur ? static_cast<uint64_t>(d.nc) : static_cast<uint64_t>(d.nc) + d.np;
   if (v < nv) {
     const bool cam = v < d.nc;
     const int n = cam ? 9 : 3;
@@ -1306,7 +1311,8 @@ __global__ void k_pcg_dir(Dev<FP, SP> d) {
   if (!d.st->iter_active || d.st->pcg_done) return;
   using A = arith_t<SP>;
   const FP beta = d.st->beta;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
+  const uint64_t n = d.st->schur ? 9ull * d.nc : d.ncols;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const SP pi = narrow<SP>(widen<FP>(d.z[i]) + beta * widen<FP>(d.p[i]));
     d.p[i] = pi;
@@ -1329,7 +1335,8 @@ __global__ void k_step(Dev<FP, SP> d) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const FP Di = d.D[i];
-    const FP xsi = zero ? FP(0) : widen<FP>(d.xs[i]) * unscale;
+    const bool ptcol = i >= 9ull * d.nc;
+    const FP xsi = (d.st->schur && ptcol) ? d.xp[i - 9ull * d.nc] : (zero ? FP(0) : widen<FP>(d.xs[i]) * unscale);
     const FP rhs = -Di * d.b[i];
     const FP damp = before ? lam * Di * Di : lam;
     if (counted(d, i)) pred += xsi * (damp * xsi + rhs);
@@ -1392,6 +1399,309 @@ __global__ void __launch_bounds__(kTileThreads) k_chi2_tiles(Dev<FP, SP> d, cons
         d.red[red_scalars(d) + kRedChi] = s;
     }
   }
+}
+
+
+// =====================================================================
+// Schur-complement solver mode (no reference counterpart: SPEC.md:164,366
+// non-goal, PAPER.md:561 future work; CPU statement + dense oracle in
+// oracle/restatement.py SchurSystem). Scaled damped system A = D H D + L:
+//   S = A_cc - A_cp A_pp^-1 A_pc (cameras), r_c = rhs_c - A_cp A_pp^-1 rhs_p,
+//   PCG on S with block-Jacobi of S's camera blocks, x_p by back-substitution.
+// Every kernel is a tile pass with the point blocks local to the tile; the
+// A_pp^-1 are the point preconditioner blocks (k_precond, exact LLT).
+// =====================================================================
+
+// packed 3x3 symmetric (p3 layout) times vector
+template <typename T, typename M>
+__device__ inline void sym3_mul(const M* m, const T* v, T* out) {
+  out[0] = T(m[0]) * v[0] + T(m[1]) * v[1] + T(m[2]) * v[2];
+  out[1] = T(m[1]) * v[0] + T(m[3]) * v[1] + T(m[4]) * v[2];
+  out[2] = T(m[2]) * v[0] + T(m[4]) * v[1] + T(m[5]) * v[2];
+}
+
+// camera blocks of S: per edge E = B A_pp^-1 B^T with B = w Jc~^T Jp~ (9x3)
+template <typename FP, typename SP>
+__global__ void __launch_bounds__(kTileThreads) k_schur_pre_tiles(Dev<FP, SP> d) {
+  if (!d.st->iter_active) return;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint64_t pcol0 = 9ull * d.nc;
+  const uint32_t t = blockIdx.x;
+  const uint32_t eb = d.tile_ebeg[t], ne_t = d.tile_ecnt[t], pb = d.tile_pbeg[t];
+  for (uint32_t c0 = 0; c0 < ne_t; c0 += kTileThreads) {
+    const uint32_t j = c0 + tid;
+    const bool valid = j < ne_t;
+    const uint32_t e = eb + (valid ? j : 0);
+    const uint32_t cam = d.d_cam[e];
+    const uint64_t pid = pb + d.d_lpt[e];
+    const uint64_t pcol = pcol0 + 3 * pid;
+    FP jc[18], jp[6];
+#pragma unroll
+    for (int k = 0; k < 18; ++k) jc[k] = widen<FP>(d.J[k * static_cast<uint64_t>(d.na) + e]) * d.D[9ull * cam + (k % 9)];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) jp[k] = widen<FP>(d.J[(18 + k) * static_cast<uint64_t>(d.na) + e]) * d.D[pcol + (k % 3)];
+    const FP w = d.w ? d.w[e] : FP(1);
+    const bool on = valid && d.col_free[pcol];
+    FP B[27], C[27];
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) B[3 * i + k] = on ? w * (jc[i] * jp[k] + jc[9 + i] * jp[3 + k]) : FP(0);
+    const FP* M = d.Mp + 6 * pid;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) sym3_mul<FP, FP>(M, &B[3 * i], &C[3 * i]);
+    const uint32_t chunk = d.tile_chunk_base[t] + (c0 + (tid & ~31)) / 32;
+    const RunInfo ri = run_info(cam, valid, d.chunk_part_base[chunk]);
+#pragma unroll
+    for (int g = 0; g < 5; ++g) {
+      FP v[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const int q = 9 * g + k;
+        const int a = p9row(q), bb = p9col(q);
+        v[k] = C[3 * a] * B[3 * bb] + C[3 * a + 1] * B[3 * bb + 1] + C[3 * a + 2] * B[3 * bb + 2];
+      }
+      seg_reduce<FP, 9>(v, lane, ri.run_end);
+      if (ri.head) {
+        FP* dst = d.part + static_cast<uint64_t>(ri.slot) * kLinVals + 9 * g;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) dst[k] = v[k];
+      }
+    }
+  }
+}
+
+// S_c = D H_cc D + L - sum(E), LLT inverse -> Mc (fallback like k_precond)
+template <typename FP, typename SP>
+__global__ void k_schur_pre_cams(Dev<FP, SP> d) {
+  if (!d.st->iter_active) return;
+  const uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (c >= d.nc) return;
+  const uint64_t col = 9 * c;
+  FP* Mo = d.Mc + 45 * c;
+  if (!d.col_free[col]) {
+    for (int k = 0; k < 45; ++k) Mo[k] = FP(0);
+    return;
+  }
+  const FP lam = d.st->lambda_solve;
+  FP Dv[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Dv[k] = d.D[col + k];
+  FP B[45];
+  int q = 0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = i; j < 9; ++j, ++q) {
+      B[q] = Dv[i] * d.Hc[45 * c + q] * Dv[j];
+      if (i == j) B[q] += d.st->before_scaling ? lam * Dv[i] * Dv[i] : lam;
+    }
+  for (uint32_t s2 = d.cam_part_off[c]; s2 < d.cam_part_off[c + 1]; ++s2) {
+    const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[s2]) * kLinVals;
+#pragma unroll
+    for (int k = 0; k < 45; ++k) B[k] -= src[k];
+  }
+  FP out[45];
+  if (!chol_inverse<FP, 9>(B, out)) {
+    q = 0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+      for (int j = i; j < 9; ++j, ++q) out[q] = (i == j) ? FP(1) / clampv(B[q], FP(d.st->clamp_min), FP(d.st->clamp_max)) : FP(0);
+    atomicAdd(&d.st->fallbacks, 1);
+  }
+#pragma unroll
+  for (int k = 0; k < 45; ++k) Mo[k] = out[k];
+}
+
+// Shared tile pass: phase 1 y_p = sum_e Jp~^T w Jc~ v_c (points, in SMEM).
+// mode 0 (S v): z_p = A_pp^-1 y_p, then per edge g = Jc~^T w (Jc~ v - Jp~ z).
+// mode 1 (rhs): z_p = A_pp^-1 rhs_p (no phase 1), g = Jc~^T w Jp~ z.
+// mode 2 (back-substitution): x_p = A_pp^-1 (rhs_p - y_p) -> xp (no phase 2).
+// vt holds (Arith) D * v for the camera columns.
+template <typename FP, typename SP, int MODE>
+__global__ void __launch_bounds__(kTileThreads) k_schur_tiles(Dev<FP, SP> d) {
+  using A = arith_t<SP>;
+  if (!d.st->iter_active) return;
+  if (MODE == 0 && d.st->pcg_done) return;
+  __shared__ A stage[kTileEdges * 3];
+  __shared__ A usm[kTileEdges * 2];
+  __shared__ A zt[kTilePoints * 3];
+  __shared__ A hacc[3];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint64_t pcol0 = 9ull * d.nc;
+  const uint32_t t = blockIdx.x;
+  const uint32_t eb = d.tile_ebeg[t], ne_t = d.tile_ecnt[t];
+  const uint32_t pb = d.tile_pbeg[t], npt = d.tile_pbeg[t + 1] - pb;
+  const bool heavy = ne_t > static_cast<uint32_t>(kTileEdges);
+  if (tid < 3) hacc[tid] = A(0);
+  __syncthreads();
+  if (MODE != 1) {  // phase 1: y_p
+    for (uint32_t c0 = 0; c0 < ne_t; c0 += kTileThreads) {
+      const uint32_t j = c0 + tid;
+      const bool valid = j < ne_t;
+      const uint32_t e = eb + (valid ? j : 0);
+      const uint32_t cam = d.d_cam[e];
+      A jc[18], jp[6];
+      load_J(d, e, jc, jp);
+      const A* cv = d.vt + 9ull * cam;
+      A u0 = A(0), u1 = A(0);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        u0 += jc[k] * cv[k];
+        u1 += jc[9 + k] * cv[k];
+      }
+      const A wgt = d.w ? static_cast<A>(d.w[e]) : A(1);
+      const A q0 = valid ? wgt * u0 : A(0), q1 = valid ? wgt * u1 : A(0);
+      if (!heavy && valid) {
+        usm[2 * j] = u0;
+        usm[2 * j + 1] = u1;
+      }
+      A h[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) h[k] = jp[k] * q0 + jp[3 + k] * q1;
+      if (!heavy) {
+        if (valid)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) stage[j * 3 + k] = h[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) stage[tid * 3 + k] = h[k];
+        __syncthreads();
+        if (tid < 3) {
+          A acc = hacc[tid];
+          const uint32_t nvalid = min(static_cast<uint32_t>(kTileThreads), ne_t - c0);
+          for (uint32_t q = 0; q < nvalid; ++q) acc += stage[q * 3 + tid];
+          hacc[tid] = acc;
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+  // per point: z (modes 0, 1) or x_p (mode 2)
+  for (uint32_t i = tid; i < npt; i += blockDim.x) {
+    const uint64_t pid = pb + i;
+    const uint64_t col = pcol0 + 3 * pid;
+    const bool freev = d.col_free[col];
+    FP y[3] = {FP(0), FP(0), FP(0)};
+    if (MODE != 1) {
+      A acc[3];
+      if (heavy) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] = hacc[k];
+      } else {
+        acc[0] = acc[1] = acc[2] = A(0);
+        for (uint32_t q = d.pt_slot_off[pid]; q < d.pt_slot_off[pid + 1]; ++q) {
+          const uint32_t sl = d.pt_slots[q];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) acc[k] += stage[sl * 3 + k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) y[k] = d.D[col + k] * static_cast<FP>(acc[k]);  // Jp~^T = D_p Jp^T
+    }
+    FP rhs[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) rhs[k] = -d.D[col + k] * d.b[col + k];
+    FP src[3], z[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) src[k] = MODE == 0 ? y[k] : (MODE == 1 ? rhs[k] : rhs[k] - y[k]);
+    sym3_mul<FP, FP>(d.Mp + 6 * pid, src, z);
+    if (MODE == 2) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) d.xp[3 * pid + k] = freev ? z[k] : FP(0);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) zt[3 * i + k] = freev ? static_cast<A>(d.D[col + k] * z[k]) : A(0);
+    }
+  }
+  if (MODE == 2) return;
+  __syncthreads();
+  // phase 2: camera contributions
+  for (uint32_t c0 = 0; c0 < ne_t; c0 += kTileThreads) {
+    const uint32_t j = c0 + tid;
+    const bool valid = j < ne_t;
+    const uint32_t e = eb + (valid ? j : 0);
+    const uint32_t cam = d.d_cam[e];
+    const uint32_t lp = d.d_lpt[e];
+    A jc[18], jp[6];
+    load_J(d, e, jc, jp);
+    A u0 = A(0), u1 = A(0);
+    if (MODE == 0) {
+      if (!heavy) {
+        u0 = usm[2 * j];
+        u1 = usm[2 * j + 1];
+      } else {
+        const A* cv = d.vt + 9ull * cam;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          u0 += jc[k] * cv[k];
+          u1 += jc[9 + k] * cv[k];
+        }
+      }
+    }
+    A v0 = A(0), v1 = A(0);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      v0 += jp[k] * zt[3 * lp + k];
+      v1 += jp[3 + k] * zt[3 * lp + k];
+    }
+    const A wgt = d.w ? static_cast<A>(d.w[e]) : A(1);
+    const A q0 = valid ? wgt * (MODE == 0 ? u0 - v0 : v0) : A(0);
+    const A q1 = valid ? wgt * (MODE == 0 ? u1 - v1 : v1) : A(0);
+    A g[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) g[k] = jc[k] * q0 + jc[9 + k] * q1;
+    const uint32_t chunk = d.tile_chunk_base[t] + (c0 + (tid & ~31)) / 32;
+    const RunInfo ri = run_info(cam, valid, d.chunk_part_base[chunk]);
+    seg_reduce<A, 9>(g, lane, ri.run_end);
+    if (ri.head) {
+      FP* dst = d.part + static_cast<uint64_t>(ri.slot) * 9;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) dst[k] = static_cast<FP>(g[k]);
+    }
+  }
+  if (MODE == 0 && tid < 8) d.tile_red[8ull * t + tid] = FP(0);  // no point columns in the Schur PCG
+}
+
+// r_c = rhs_c - D_c * sum(partials)
+template <typename FP, typename SP>
+__global__ void __launch_bounds__(32 * kCamWarps) k_schur_rhs_cams(Dev<FP, SP> d) {
+  if (!d.st->iter_active) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t c = blockIdx.x * kCamWarps + (threadIdx.x >> 5);
+  if (c >= d.nc) return;
+  FP acc[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) acc[k] = FP(0);
+  for (uint32_t q = d.cam_part_off[c] + lane; q < d.cam_part_off[c + 1]; q += 32) {
+    const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * 9;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] += src[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) acc[k] = warp_sum(acc[k]);
+  if (lane < 9) {
+    const uint64_t col = 9ull * c + lane;
+    FP a = acc[0];
+#pragma unroll
+    for (int k = 1; k < 9; ++k)
+      if (lane == k) a = acc[k];
+    d.rc[col] = d.col_free[col] ? -d.D[col] * d.b[col] - d.D[col] * a : FP(0);
+  }
+}
+
+// vt (cameras) = D * x_c after the Schur PCG (x_c unscaled), for back-substitution
+template <typename FP, typename SP>
+__global__ void k_schur_xc(Dev<FP, SP> d) {
+  using A = arith_t<SP>;
+  if (!d.st->iter_active) return;
+  const FP unscale = d.st->unscale;
+  const bool zero = d.st->pcg_zero;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < 9ull * d.nc;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    d.vt[i] = static_cast<A>(d.D[i] * (zero ? FP(0) : widen<FP>(d.xs[i]) * unscale));
 }
 
 // Accept / reject, Nielsen damping, termination, per-iteration record

@@ -53,6 +53,7 @@ struct GraphData {
   int loss_kind = GB_LOSS_DEFAULT;
   double huber = 1.0;
   uint64_t revision = 1;
+  int linear_solver = GB_SOLVER_PCG;
   std::shared_ptr<Reducer> reducer;  // null: single GPU
   int world() const { return reducer ? reducer->world() : 1; }
   int rank() const { return reducer ? reducer->rank() : 0; }
@@ -434,6 +435,7 @@ class Solver final : public SolverBase {
     hs.pcg_done = hs.pcg_it = hs.pcg_conv = hs.pcg_zero = 0;
     hs.pcg_relres = 0;
     hs.fallbacks = 0;
+    hs.schur = g_.linear_solver == GB_SOLVER_SCHUR ? 1 : 0;
     if (pcg) {
       hs.pcg_max_it = pcg->max_iterations;
       hs.pcg_tol = pcg->tolerance;
@@ -904,6 +906,8 @@ class Solver final : public SolverBase {
     d.ap = static_cast<SP*>(b_ap_.alloc(ncols_ * sizeof(SP)));
     d.vt = static_cast<A*>(b_vt_.alloc(ncols_ * sizeof(A)));
     CK(cudaMemsetAsync(d.vt, 0, ncols_ * sizeof(A), s_));
+    d.rc = static_cast<FP*>(b_rc_.alloc(std::max<uint64_t>(1, 9 * nc) * sizeof(FP)));
+    d.xp = static_cast<FP*>(b_xp_.alloc(std::max<uint64_t>(1, 3 * np) * sizeof(FP)));
     d.tile_red = static_cast<FP*>(b_tr_.alloc(8ull * act_.ntiles * sizeof(FP)));
     d.tile_red2 = static_cast<FP*>(b_tr2_.alloc(act_.ntiles * sizeof(FP)));
     d.tile_flag = static_cast<int*>(b_tf_.alloc(act_.ntiles * sizeof(int)));
@@ -1008,6 +1012,10 @@ class Solver final : public SolverBase {
     hs.use_guard = cfg.use_rejection_guard;
     hs.refresh_on_reject = cfg.refresh_on_reject;
     hs.max_iterations = cfg.max_iterations;
+    hs.schur = g_.linear_solver == GB_SOLVER_SCHUR ? 1 : 0;
+    if (hs.schur && g_.diff_mode == GB_DYNAMIC)
+      throw std::invalid_argument("Schur mode needs stored Jacobians (analytic or auto)");
+    if (hs.schur && g_.reducer) throw std::logic_error("Schur mode is single-GPU in this build");
   }
 
   // ------------------------------------------------------------- launches
@@ -1079,8 +1087,36 @@ class Solver final : public SolverBase {
     CK(cudaGetLastError());
   }
 
+  // Schur mode (kernels.cuh k_schur_*): camera blocks of S, reduced rhs, PCG
+  // on the cameras, back-substitution of the points, step.
+  void enqueue_solve_schur(int pcg_max_it) {
+    k_precond<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);  // point blocks = A_pp^-1
+    k_schur_pre_tiles<FP, SP><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_);
+    k_schur_pre_cams<FP, SP><<<div_up(act_.nc, 128), 128, 0, s_>>>(dev_);
+    k_schur_tiles<FP, SP, 1><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_);
+    k_schur_rhs_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_);
+    k_rhs_norm<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+    k_pcg_init<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+    for (int k = 0; k < pcg_max_it; ++k) {
+      k_schur_tiles<FP, SP, 0><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_);
+      k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, 0);
+      k_pcg_update<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+      k_pcg_dir<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+      CK(cudaGetLastError());
+    }
+    k_schur_xc<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+    k_schur_tiles<FP, SP, 2><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_);
+    k_step<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+  }
+
   // build_preconditioner + pcg_solve + unscale (linear_system.hpp:185-207)
   void enqueue_solve(int pcg_max_it) {
+    if (g_.linear_solver == GB_SOLVER_SCHUR) {
+      enqueue_solve_schur(pcg_max_it);
+      return;
+    }
     k_precond<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
     CK(cudaGetLastError());
     k_rhs_norm<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
@@ -1191,6 +1227,7 @@ class Solver final : public SolverBase {
   int graph_pcg_it_ = -1;
   gb_iteration_record* graph_recs_ = nullptr;
   DBuf st_buf_, rec_buf_, dbg_buf_;
+  DBuf b_rc_, b_xp_;
   DBuf b_red_, b_redmax_, b_xall_, b_pt_order_, b_da_, b_cub_, b_ptstage_;
   uint32_t* pt_order_dev_ = nullptr;
   bool host_plan_ = false;
@@ -1348,6 +1385,14 @@ int gb_set_observations(gb_graph* g, uint64_t n, const uint32_t* cam, const uint
     d.loss_kind = loss_kind;
     d.huber = huber_delta;
     ++d.revision;
+  });
+}
+
+int gb_set_linear_solver(gb_graph* g, int solver) {
+  return guarded([&] {
+    if (solver != GB_SOLVER_PCG && solver != GB_SOLVER_SCHUR) throw std::invalid_argument("unknown linear solver");
+    g->data.linear_solver = solver;
+    if (g->solver) g->solver.reset();
   });
 }
 

@@ -283,3 +283,27 @@ def test_reference_memory_account_ratios(ref):
     assert acc[("fp32", "analytic")]["jacobian_bytes"] == 500 * 24 * 4
     assert acc[("fp32-bf16", "analytic")]["jacobian_bytes"] * 2 == acc[("fp32", "analytic")]["jacobian_bytes"]
     assert acc[("fp64", "dynamic")]["jacobian_bytes"] == 0
+
+
+# --------------------------------------------- Schur mode (its own oracle)
+def test_schur_restatement_against_dense():
+    p = bal.synthetic_bal(6, 40, 200, seed=12)
+    g = R.build_graph(p, "fp64")
+    R.activate(g, 0)
+    ls = R.LinearSystem(g)
+    ls.linearize()
+    sch = R.SchurSystem(ls)
+    lam = 0.05
+    A, S, r, xdense, rhs = sch.dense(lam)
+    Sop = sch.operator(lam)
+    nc9 = 9 * sch.nfc
+    E = np.eye(nc9)
+    Smf = np.stack([Sop(E[k]) for k in range(nc9)], 1)
+    assert np.linalg.norm(Smf - S) <= 1e-10 * np.linalg.norm(S)
+    # converged Schur PCG == dense solve of the full damped system
+    pcg = dict(max_iterations=200, tolerance=1e-13, rejection_ratio=10, normalize_rhs=True)
+    dx, st, pred, fin = sch.solve_step(lam, pcg)
+    x = np.linalg.solve(A, rhs)
+    assert np.allclose(xdense, x, rtol=1e-9, atol=1e-12)
+    assert np.linalg.norm(dx - ls.D * x) <= 1e-8 * np.linalg.norm(ls.D * x)
+    assert st["converged"]

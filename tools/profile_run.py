@@ -15,10 +15,13 @@ ap.add_argument("--workload", default="final")
 ap.add_argument("--precision", default="fp64")
 ap.add_argument("--mode", default="analytic")
 ap.add_argument("--iters", type=int, default=2)
+ap.add_argument("--solver", default="pcg")
 a = ap.parse_args()
 nc, np_, ne, _ = WORKLOADS[a.workload]
 p = bal.synthetic_bal(nc, np_, ne, seed=42)
 g = bal.build_graph(p, a.precision, a.mode)
+if a.solver != "pcg":
+    g.set_linear_solver(a.solver)
 c = lm_config(a.iters, bal).to_c()
 L = g.backend
 L.check(L.fn("begin")(g._h, ctypes.byref(c), None))
