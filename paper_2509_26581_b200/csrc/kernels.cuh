@@ -16,6 +16,8 @@
 //             summed per point in slot order inside the tile.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "activate.hpp"
 #include "common.cuh"
 #include "gb_bal.h"
@@ -722,15 +724,18 @@ __device__ inline void precond_vertex(const Dev<FP, SP>& d, const FP* H, FP* M, 
 template <typename FP, typename SP>
 __global__ void k_precond(Dev<FP, SP> d) {
   if (!d.st->iter_active) return;
-  const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (v < d.nc) {
-    if (d.st->schur) return;  // k_schur_pre_cams
-    const uint64_t col = 9 * v;
-    precond_vertex<FP, SP, 9>(d, d.Hc + 45 * v, d.Mc + 45 * v, col, d.col_free[col]);
-  } else if (v < static_cast<uint64_t>(d.nc) + d.np) {
-    const uint64_t i = v - d.nc;
-    const uint64_t col = 9ull * d.nc + 3 * i;
-    precond_vertex<FP, SP, 3>(d, d.Hp + 6 * i, d.Mp + 6 * i, col, d.col_free[col]);
+  const uint64_t nv = static_cast<uint64_t>(d.nc) + d.np;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (v < d.nc) {
+      if (d.st->schur) continue;  // k_schur_pre_cams
+      const uint64_t col = 9 * v;
+      precond_vertex<FP, SP, 9>(d, d.Hc + 45 * v, d.Mc + 45 * v, col, d.col_free[col]);
+    } else {
+      const uint64_t i = v - d.nc;
+      const uint64_t col = 9ull * d.nc + 3 * i;
+      precond_vertex<FP, SP, 3>(d, d.Hp + 6 * i, d.Mp + 6 * i, col, d.col_free[col]);
+    }
   }
 }
 
@@ -791,9 +796,9 @@ __global__ void k_pcg_init(Dev<FP, SP> d) {
   __shared__ FP scratch[32];
   const FP scale = d.st->scale;
   FP rz = FP(0), rr = FP(0);
-  const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  const uint64_t nv = static_cast<uint64_t>(d.nc) + d.np;
-  if (v < nv && !(d.st->schur && v >= d.nc)) {
+  const uint64_t nv = d.st->schur ? static_cast<uint64_t>(d.nc) : static_cast<uint64_t>(d.nc) + d.np;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const bool cam = v < d.nc;
     const int n = cam ? 9 : 3;
     const uint64_t col = cam ? 9 * v : 9ull * d.nc + 3 * (v - d.nc);
@@ -1258,6 +1263,27 @@ __global__ void k_fin(Dev<FP, SP> d, int site) {
   }
 }
 
+// x += alpha p; r -= alpha Ap; z = M r for one vertex; rr, rz partials
+template <typename FP, typename SP>
+__device__ inline void pcg_update_vertex(const Dev<FP, SP>& d, uint64_t v, FP alpha, FP* rz, FP* rr) {
+  const bool cam = v < d.nc;
+  const int n = cam ? 9 : 3;
+  const uint64_t col = cam ? 9 * v : 9ull * d.nc + 3 * (v - d.nc);
+  for (int k = 0; k < n; ++k) {
+    d.xs[col + k] = narrow<SP>(widen<FP>(d.xs[col + k]) + alpha * widen<FP>(d.p[col + k]));
+    d.r[col + k] = narrow<SP>(widen<FP>(d.r[col + k]) - alpha * widen<FP>(d.ap[col + k]));
+  }
+  FP lrz = FP(0), lrr = FP(0);
+  if (cam)
+    apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &lrz, &lrr);
+  else
+    apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &lrz, &lrr);
+  if (counted(d, col)) {
+    *rz += lrz;
+    *rr += lrr;
+  }
+}
+
 // x += alpha p; r -= alpha Ap; z = M r; rr, rz (pcg.hpp:340-357)
 template <typename FP, typename SP>
 __global__ void k_pcg_update(Dev<FP, SP> d) {
@@ -1265,26 +1291,10 @@ __global__ void k_pcg_update(Dev<FP, SP> d) {
   __shared__ FP scratch[32];
   const FP alpha = d.st->alpha;
   FP rz = FP(0), rr = FP(0);
-  const uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t nv = d.st->schur ? static_cast<uint64_t>(d.nc) : static_cast<uint64_t>(d.nc) + d.np;
-  if (v < nv) {
-    const bool cam = v < d.nc;
-    const int n = cam ? 9 : 3;
-    const uint64_t col = cam ? 9 * v : 9ull * d.nc + 3 * (v - d.nc);
-    for (int k = 0; k < n; ++k) {
-      d.xs[col + k] = narrow<SP>(widen<FP>(d.xs[col + k]) + alpha * widen<FP>(d.p[col + k]));
-      d.r[col + k] = narrow<SP>(widen<FP>(d.r[col + k]) - alpha * widen<FP>(d.ap[col + k]));
-    }
-    FP lrz = FP(0), lrr = FP(0);
-    if (cam)
-      apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &lrz, &lrr);
-    else
-      apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &lrz, &lrr);
-    if (counted(d, col)) {
-      rz += lrz;
-      rr += lrr;
-    }
-  }
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    pcg_update_vertex(d, v, alpha, &rz, &rr);
   rz = block_sum(rz, scratch);
   rr = block_sum(rr, scratch);
   if (threadIdx.x == 0) {
@@ -1302,6 +1312,60 @@ __global__ void k_pcg_update(Dev<FP, SP> d) {
         d.red[red_scalars(d) + kRedUpdRr] = srr;
       }
     }
+  }
+}
+
+// Fused PCG step for the single-GPU path (cooperative launch): update
+// (pcg.hpp:340-357), grid barrier, every block reduces the same partials in
+// the same order (so beta and the stop decision agree everywhere), then
+// p = z + beta p and vt = D p (pcg.hpp:358-361). Block 0 writes the state.
+template <typename FP, typename SP>
+__global__ void __launch_bounds__(256) k_pcg_step(Dev<FP, SP> d) {
+  using A = arith_t<SP>;
+  State<FP>* st = d.st;
+  if (!st->iter_active || st->pcg_done) return;
+  __shared__ FP scratch[32];
+  const FP alpha = st->alpha, rho = st->rho, ref = st->ref_norm;
+  const FP tol = static_cast<FP>(st->pcg_tol);
+  const bool schur = st->schur;
+  FP rz = FP(0), rr = FP(0);
+  const uint64_t nv = schur ? static_cast<uint64_t>(d.nc) : static_cast<uint64_t>(d.nc) + d.np;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv; v += stride)
+    pcg_update_vertex(d, v, alpha, &rz, &rr);
+  rz = block_sum(rz, scratch);
+  rr = block_sum(rr, scratch);
+  if (threadIdx.x == 0) {
+    d.blk_red[blockIdx.x] = rz;
+    d.blk_red2[blockIdx.x] = rr;
+  }
+  cooperative_groups::this_grid().sync();
+  const FP srz = reduce_partials(d.blk_red, gridDim.x, scratch);
+  const FP srr = reduce_partials(d.blk_red2, gridDim.x, scratch);
+  const FP res = sqrt(srr);
+  const double rel = static_cast<double>(res / ref);
+  const bool stop = !isfinite(rel) || res <= tol * ref;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->pcg_it += 1;
+    st->pcg_relres = rel;
+    if (!isfinite(rel)) {
+      st->pcg_done = 1;
+      st->pcg_conv = 0;
+    } else if (res <= tol * ref) {
+      st->pcg_done = 1;
+      st->pcg_conv = 1;
+    } else {
+      st->beta = srz / rho;
+      st->rho = srz;
+    }
+  }
+  if (stop) return;
+  const FP beta = srz / rho;
+  const uint64_t n = schur ? 9ull * d.nc : d.ncols;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const SP pi = narrow<SP>(widen<FP>(d.z[i]) + beta * widen<FP>(d.p[i]));
+    d.p[i] = pi;
+    d.vt[i] = static_cast<A>(d.D[i]) * widen<A>(pi);
   }
 }
 

@@ -128,6 +128,13 @@ class Solver final : public SolverBase {
   explicit Solver(GraphData& g) : g_(g) {
     CK(cudaSetDevice(g_.device));
     if (const char* e = std::getenv("GB_HVP_MINB")) hvp_minb_ = std::atoi(e);
+    {
+      int sms = 0, per = 0;
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g_.device));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_step<FP, SP>, 256, 0));
+      coop_grid_ = static_cast<unsigned>(std::max(1, sms * std::max(1, per)));
+      if (const char* e = std::getenv("GB_PCG_FUSED")) fused_pcg_ = std::atoi(e) != 0;
+    }
     CK(cudaFuncSetAttribute(k_lin_normal<FP, SP, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(lin_normal_smem<FP>())));
     CK(cudaFuncSetAttribute(k_lin_normal<FP, SP, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -914,7 +921,8 @@ class Solver final : public SolverBase {
     d.cam_red = static_cast<FP*>(b_cr_.alloc(std::max<uint64_t>(1, nc) * sizeof(FP)));
     d.cam_red2 = static_cast<FP*>(b_cr2_.alloc(std::max<uint64_t>(1, nc) * sizeof(FP)));
     d.cam_flag = static_cast<int*>(b_cf_.alloc(std::max<uint64_t>(1, nc) * sizeof(int)));
-    const uint64_t nblk = std::max<uint64_t>(std::max<uint64_t>(vert_grid(), col_grid()), cam_grid());
+    const uint64_t nblk =
+        std::max<uint64_t>(std::max<uint64_t>(std::max<uint64_t>(vert_grid(), col_grid()), cam_grid()), coop_grid_);
     d.blk_red = static_cast<FP*>(b_br_.alloc(nblk * sizeof(FP)));
     d.blk_red2 = static_cast<FP*>(b_br2_.alloc(nblk * sizeof(FP)));
     d.blk_flag = static_cast<int*>(b_bf_.alloc(nblk * sizeof(int)));
@@ -1019,6 +1027,7 @@ class Solver final : public SolverBase {
   }
 
   // ------------------------------------------------------------- launches
+  // one vertex per thread (memory-level parallelism beats grid-stride reuse here)
   unsigned vert_grid() const { return std::max(1u, div_up(static_cast<uint64_t>(act_.nc) + act_.np, 256)); }
   unsigned col_grid() const { return std::max(1u, std::min(div_up(ncols_, 256), 148u * 8u)); }
   unsigned cam_grid() const { return std::max(1u, div_up(act_.nc, kCamWarps)); }
@@ -1101,14 +1110,31 @@ class Solver final : public SolverBase {
     for (int k = 0; k < pcg_max_it; ++k) {
       k_schur_tiles<FP, SP, 0><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_);
       k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, 0);
-      k_pcg_update<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
-      k_pcg_dir<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+      if (fused_pcg_) {
+        launch_pcg_step();
+      } else {
+        k_pcg_update<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+        k_pcg_dir<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+      }
       CK(cudaGetLastError());
     }
     k_schur_xc<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
     k_schur_tiles<FP, SP, 2><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_);
     k_step<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
     CK(cudaGetLastError());
+  }
+
+  void launch_pcg_step() {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(coop_grid_);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s_;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_pcg_step<FP, SP>, dev_));
   }
 
   // build_preconditioner + pcg_solve + unscale (linear_system.hpp:185-207)
@@ -1133,6 +1159,10 @@ class Solver final : public SolverBase {
     }
     for (int k = 0; k < pcg_max_it; ++k) {
       launch_hvp(dev_);
+      if (!dist() && fused_pcg_) {
+        launch_pcg_step();
+        continue;
+      }
       k_pcg_update<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
       CK(cudaGetLastError());
       if (dist()) {
@@ -1231,6 +1261,8 @@ class Solver final : public SolverBase {
   DBuf b_red_, b_redmax_, b_xall_, b_pt_order_, b_da_, b_cub_, b_ptstage_;
   uint32_t* pt_order_dev_ = nullptr;
   bool host_plan_ = false;
+  unsigned coop_grid_ = 148 * 8;  // co-resident blocks of k_pcg_step (cooperative launch)
+  bool fused_pcg_ = false;  // GB_PCG_FUSED=1: cooperative k_pcg_step (measured slower: 358 vs 335 us at Final)
   int hvp_minb_ = 4;  // occupancy hint of the HVP tile kernel (A/B: GB_HVP_MINB=1 -> 80 regs, 3 CTAs/SM)
   DBuf b_vt_, b_dlcam_, b_tile_ecnt_, b_tile_cam_off_, b_tile_cams_, b_normal_, b_heavy_;
   DBuf b_col_free_, b_dcam_, b_dlpt_, b_obs_, b_tile_ebeg_, b_tile_pbeg_, b_tile_chunk_, b_chunk_part_,

@@ -273,3 +273,16 @@ def test_auto_mode_parity(gpu, ref, ladybug):
     assert rel(ja, gn.ls_jacobians(LADYBUG[2])) <= 1e-12
     g, r, a1, b1 = run_pair(ladybug, ref, mode="auto")
     assert_trace_parity(a1, b1, 1e-6)
+
+
+def test_large_problem_trace_parity(gpu, ref):
+    # > 1 M columns: every vertex-, column- and tile-grid covers the whole
+    # problem (small cases fit in one grid wave and would hide coverage bugs)
+    p = bal.synthetic_bal(60, 400_000, 2_000_000, seed=8)
+    cfg = bal_cfg(3)
+    g = bal.build_graph(p, "fp64")
+    ra = bal.levenberg_marquardt(g, cfg)
+    r = ref.build_graph(p, "fp64", workers=16)
+    rb = bal.levenberg_marquardt(r, cfg)
+    assert [i.pcg_iterations for i in ra.iterations] == [i.pcg_iterations for i in rb.iterations]
+    assert_trace_parity(ra, rb, 1e-6)
