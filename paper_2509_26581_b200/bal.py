@@ -56,6 +56,23 @@ def dtypes(precision: str):
     raise ValueError(f"invalid precision pair: {precision}")
 
 
+def bf16_bits(x) -> np.ndarray:
+    """float -> bfloat16 storage bits, RNE with the quiet-NaN encoding of
+    bfloat16::round_from (bfloat16.hpp:25-33)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    nan = np.isnan(np.asarray(x, dtype=np.float32))
+    r[nan] = (((u[nan] >> 16) & 0x8000) | 0x7FC0).astype(np.uint16)
+    return r
+
+
+def _to_storage(v, sp):
+    """Values in the storage type SP (bf16 storage = uint16 bits)."""
+    if sp is np.uint16 and np.asarray(v).dtype != np.uint16:
+        return bf16_bits(v)
+    return np.ascontiguousarray(v, dtype=sp)
+
+
 # --------------------------------------------------------------------- configs
 @dataclass
 class PCGConfig:
@@ -361,7 +378,7 @@ class BalGraph:
         return dict(chi2=chi.value, b=b, diag=diag, clamped=cl, scaling=D, finite=bool(fin.value), n=N)
 
     def ls_hvp(self, v, lam):
-        v = np.ascontiguousarray(v, dtype=self.SP)
+        v = _to_storage(v, self.SP)
         out = np.zeros(v.shape[0], self.A)
         self.backend.check(self.backend.fn("ls_hvp")(self._h, v.ctypes.data, out.ctypes.data, float(lam)))
         return out

@@ -89,6 +89,14 @@ __host__ __device__ inline To widen(bf16 x) {
   return static_cast<To>(u32_as_f32(static_cast<uint32_t>(x.bits) << 16));
 }
 
+// Explicitly rounded multiply / fused multiply-add: the factored Jacobian
+// store rebuilds J entries in the HVP with exactly the
+// operations linearize used, so these must not be left to FMA contraction.
+__device__ inline double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ inline float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ inline double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ inline float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
 template <typename T>
 __host__ __device__ inline bool is_finite(T x) {
   return isfinite(x);

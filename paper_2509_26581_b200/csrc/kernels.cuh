@@ -92,7 +92,14 @@ struct Dev {
   const uint32_t* d_cam;
   const uint16_t* d_lpt;
   const FP* d_obs;  // [2][na]
-  SP* J;            // [24][na] or null (dynamic)
+  SP* J;            // [24][na] full store, [16][na] factored store (jfact), or null (dynamic)
+  FP* Rf;           // [nc][10] factored store: R (row-major 3x3) and f per camera
+  int jfact;        // 1: factored J store (analytic mode, SP == FP), DESIGN.md §2
+  // pipelined HVP (hvp_pipe.cuh): tile records and per-tile camera copies
+  const uint32_t* tile_meta;  // [n_normal][12]
+  uint32_t ntcams;            // tile_cam_off[ntiles]
+  arith_t<SP>* tcv;           // [ntcams][9]  D*p of each tile's cameras
+  FP* tcr;                    // [ntcams][10] R, f of each tile's cameras (factored store)
   FP* w;            // [na] or null (default loss: w == 1)
   const uint32_t* tile_ebeg;  // padded slot begin of each tile
   const uint32_t* tile_ecnt;  // real edges of each tile
@@ -252,6 +259,69 @@ __device__ inline void seg_reduce(T (&v)[K], int lane, int run_end) {
   }
 }
 
+// Camera-run sums of 9 values over a 32-edge warp chunk whose runs are
+// contiguous lane ranges (edges sorted by camera inside a tile), written to
+// the run's partial slot. Per run: lanes outside it contribute 0, then a
+// 5-stage transpose reduction (xor 16/8/4/2/1 exchanging 5/3/2/1/1 values,
+// i.e. 12 shuffles instead of seg_reduce's 45) leaves value k of the run
+// total in the two lanes 2m, 2m+1 of a fixed m(k). Fixed association order,
+// so results are deterministic. heads/vm: ballots of run heads / valid lanes.
+__device__ inline int rr9_slot(int lane) {
+  const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
+  const int q = b2 ? (b1 ? -1 : 2) : b1;                 // position in the stage-2 list
+  const int p = q < 0 ? -1 : (b3 ? (q == 2 ? -1 : 3 + q) : q);  // position in the stage-1 list
+  if (p < 0) return -1;
+  return b4 ? (p < 4 ? 5 + p : -1) : p;
+}
+
+template <typename T, typename Out>
+__device__ inline void run_reduce9_store(const T (&g)[9], int lane, unsigned heads, unsigned vm, uint32_t slot0,
+                                         Out* part) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  const int myslot = (lane & 1) ? -1 : rr9_slot(lane);
+  const unsigned full = 0xffffffffu;
+  uint32_t r = 0;
+  while (heads) {
+    const int start = __ffs(heads) - 1;
+    heads &= heads - 1;
+    const int stop = heads ? __ffs(heads) - 1 : 32 - __clz(vm);
+    const bool in = lane >= start && lane < stop;
+    T a[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) a[k] = in ? g[k] : T(0);
+    T k1[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const T hi = i < 4 ? a[5 + i] : T(0);
+      k1[i] = b4 ? hi : a[i];
+      const T snd = b4 ? a[i] : hi;
+      k1[i] += __shfl_xor_sync(full, snd, 16);
+    }
+    T k2[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const T hi = i < 2 ? k1[3 + i] : T(0);
+      k2[i] = b3 ? hi : k1[i];
+      const T snd = b3 ? k1[i] : hi;
+      k2[i] += __shfl_xor_sync(full, snd, 8);
+    }
+    T k3[2];
+    {
+      k3[0] = b2 ? k2[2] : k2[0];
+      k3[1] = b2 ? T(0) : k2[1];
+      const T s0 = b2 ? k2[0] : k2[2];
+      const T s1 = b2 ? k2[1] : T(0);
+      k3[0] += __shfl_xor_sync(full, s0, 4);
+      k3[1] += __shfl_xor_sync(full, s1, 4);
+    }
+    T v = b1 ? k3[1] : k3[0];
+    v += __shfl_xor_sync(full, b1 ? k3[0] : k3[1], 2);
+    v += __shfl_xor_sync(full, v, 1);
+    if (myslot >= 0) part[static_cast<uint64_t>(slot0 + r) * 9 + myslot] = static_cast<Out>(v);
+    ++r;
+  }
+}
+
 struct RunInfo {
   bool head;
   int run_end;
@@ -272,15 +342,80 @@ __device__ inline RunInfo run_info(uint32_t cam, bool valid, uint32_t chunk_slot
   return ri;
 }
 
+// Factored J store (analytic mode with SP == FP): per edge 16
+// rows [Jc(:,0:3) row 0 | row 1 | U = du/dP (2x3) | dist | n | p0 | p1];
+// per camera Rf = [R | f]. The rebuilt entries are bit-identical to the
+// chain's (same explicitly rounded operations, snavely.cuh), so the stored
+// operator is exactly J; it moves 16 instead of 24 values per edge.
+constexpr int kJFactRows = 16;
+
 template <typename FP, typename SP>
-__device__ inline void load_J(const Dev<FP, SP>& d, uint32_t e, arith_t<SP>* jc, arith_t<SP>* jp) {
+__device__ inline void store_J(const Dev<FP, SP>& d, uint32_t e, const FP* jc, const FP* jp, const FP* fac) {
+  const uint64_t na = d.na;
+  if (d.jfact) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      d.J[k * na + e] = narrow<SP>(jc[k]);
+      d.J[(3 + k) * na + e] = narrow<SP>(jc[9 + k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 10; ++k) d.J[(6 + k) * na + e] = narrow<SP>(fac[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 18; ++k) d.J[k * na + e] = narrow<SP>(jc[k]);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) d.J[(18 + k) * na + e] = narrow<SP>(jp[k]);
+  }
+}
+
+template <typename FP, typename SP>
+__device__ inline void load_J(const Dev<FP, SP>& d, uint32_t e, uint32_t cam, arith_t<SP>* jc, arith_t<SP>* jp) {
   using A = arith_t<SP>;
   const SP* J = d.J;
   const uint64_t na = d.na;
+  if constexpr (std::is_same<SP, FP>::value) {
+    if (d.jfact) {
+      FP U[6], R[9];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        jc[k] = J[k * na + e];
+        jc[9 + k] = J[(3 + k) * na + e];
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) U[k] = J[(6 + k) * na + e];
+      const FP dist = J[12 * na + e], n = J[13 * na + e], p0 = J[14 * na + e], p1 = J[15 * na + e];
+      const FP* rf = d.Rf + 10ull * cam;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) R[k] = rf[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        jc[3 + k] = U[k];
+        jc[12 + k] = U[3 + k];
+      }
+      point_block<FP>(U, R, jp);
+      intrinsic_cols<FP>(dist, n, p0, p1, rf[9], jc);
+      return;
+    }
+  }
 #pragma unroll
   for (int k = 0; k < 18; ++k) jc[k] = widen<A>(J[k * na + e]);
 #pragma unroll
   for (int k = 0; k < 6; ++k) jp[k] = widen<A>(J[(18 + k) * na + e]);
+}
+
+// Full 24-value rows from either store (LinearSystem accessor surface).
+template <typename FP, typename SP>
+__global__ void k_expand_J(Dev<FP, SP> d, SP* out) {
+  using A = arith_t<SP>;
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < d.na;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    A jc[18], jp[6];
+    load_J(d, static_cast<uint32_t>(e), d.d_cam[e], jc, jp);
+#pragma unroll
+    for (int k = 0; k < 18; ++k) out[k * static_cast<uint64_t>(d.na) + e] = narrow<SP>(jc[k]);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) out[(18 + k) * static_cast<uint64_t>(d.na) + e] = narrow<SP>(jp[k]);
+  }
 }
 
 // =====================================================================
@@ -326,29 +461,22 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, const
 #pragma unroll
     for (int k = 0; k < 9; ++k) cp[k] = d.x[9ull * cam + k];
     const FP* X = &sX[3 * lp];
-    FP res[2], jc[18], jp[6];
+    FP res[2], jc[18], jp[6], fac[10];
     if (AUTO) {
       snavely_residual<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res);
       snavely_jacobians_auto<FP>(cp, X, jc, jp);
     } else {
-      snavely_linearize<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res, jc, jp);
+      snavely_linearize<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res, jc, jp, fac);
     }
     const FP s = res[0] * res[0] + res[1] * res[1];
     const FP w = valid ? loss_weight<FP>(loss, delta, s) : FP(0);
     if (valid) chi += loss_value<FP>(loss, delta, s);
     if (STORE) {
+      if (valid) store_J(d, e, jc, jp, fac);
 #pragma unroll
-      for (int k = 0; k < 18; ++k) {
-        const SP v = narrow<SP>(jc[k]);
-        if (valid) d.J[k * static_cast<uint64_t>(d.na) + e] = v;
-        jc[k] = widen<FP>(v);
-      }
+      for (int k = 0; k < 18; ++k) jc[k] = widen<FP>(narrow<SP>(jc[k]));
 #pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        const SP v = narrow<SP>(jp[k]);
-        if (valid) d.J[(18 + k) * static_cast<uint64_t>(d.na) + e] = v;
-        jp[k] = widen<FP>(v);
-      }
+      for (int k = 0; k < 6; ++k) jp[k] = widen<FP>(narrow<SP>(jp[k]));
     }
     if (d.w && valid) d.w[e] = w;
     const FP wr0 = w * res[0], wr1 = w * res[1];
@@ -494,6 +622,14 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int 
       }
     }
     return;
+  }
+  if (c < d.nc && d.jfact && lane == 0) {  // factored J store: R and f per camera
+    FP cp[9], rf[10];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) cp[k] = d.x[9ull * c + k];
+    camera_factor<FP>(cp, rf);
+#pragma unroll
+    for (int k = 0; k < 10; ++k) d.Rf[10ull * c + k] = rf[k];
   }
   if (c < d.nc) {
     FP a0 = FP(0), a1 = FP(0);
@@ -852,7 +988,7 @@ __global__ void k_pcg_init(Dev<FP, SP> d) {
 // summed per point in slot order after the single tile barrier. The tile's
 // p.Ap goes out as one partial per warp (no block reduction).
 template <typename FP, typename SP, bool DYN, int MINB = 1>
-__global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d) {
+__global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d, const uint32_t* list) {
   using A = arith_t<SP>;
   if (!d.st->iter_active || d.st->pcg_done) return;
   __shared__ A stage[kTileEdges * 3];
@@ -860,7 +996,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d)
   __shared__ FP sX[DYN ? kTilePoints * 3 : 1];
   const int tid = threadIdx.x, lane = tid & 31;
   const uint64_t pcol0 = 9ull * d.nc;
-  const uint32_t t = blockIdx.x;
+  const uint32_t t = list ? list[blockIdx.x] : blockIdx.x;
   const uint32_t eb = d.tile_ebeg[t], ne_t = d.tile_ecnt[t];
   const uint32_t pb = d.tile_pbeg[t], npt = d.tile_pbeg[t + 1] - pb;
   const bool heavy = ne_t > static_cast<uint32_t>(kTileEdges);
@@ -888,7 +1024,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d)
 #pragma unroll
       for (int k = 0; k < 6; ++k) jp[k] = static_cast<A>(fjp[k]);
     } else {
-      load_J(d, e, jc, jp);
+      load_J(d, e, cam, jc, jp);
     }
     const A wgt = d.w ? static_cast<A>(d.w[e]) : A(1);
     const A* cv = d.vt + 9ull * cam;
@@ -913,12 +1049,11 @@ __global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d)
 #pragma unroll
     for (int k = 0; k < 9; ++k) g[k] = jc[k] * q0 + jc[9 + k] * q1;
     const uint32_t chunk = d.tile_chunk_base[t] + (c0 + (tid & ~31)) / 32;
-    const RunInfo ri = run_info(cam, valid, d.chunk_part_base[chunk]);
-    seg_reduce<A, 9>(g, lane, ri.run_end);
-    if (ri.head) {
-      FP* dst = d.part + static_cast<uint64_t>(ri.slot) * 9;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) dst[k] = static_cast<FP>(g[k]);
+    {
+      const uint32_t prev = __shfl_up_sync(0xffffffffu, cam, 1);
+      const unsigned hm = __ballot_sync(0xffffffffu, valid && (lane == 0 || cam != prev));
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      run_reduce9_store<A, FP>(g, lane, hm, vm, hm ? d.chunk_part_base[chunk] : 0u, d.part);
     }
     A h[3];
 #pragma unroll
@@ -1030,29 +1165,22 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
   const uint32_t lc = d.d_lcam[e], lp = d.d_lpt[e];
   const FP o0 = d.d_obs[e], o1 = d.d_obs[static_cast<uint64_t>(d.na) + e];
 
-  FP res[2], jc[18], jp[6];
+  FP res[2], jc[18], jp[6], fac[10];
   if (AUTO) {
     snavely_residual<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res);
     snavely_jacobians_auto<FP>(&sC[9 * lc], &sX[3 * lp], jc, jp);
   } else {
-    snavely_linearize<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res, jc, jp);
+    snavely_linearize<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res, jc, jp, fac);
   }
   const FP s = res[0] * res[0] + res[1] * res[1];
   const FP w = valid ? loss_weight<FP>(d.loss_kind, d.huber, s) : FP(0);
   if (valid) chi += loss_value<FP>(d.loss_kind, d.huber, s);
   if (STORE) {
+    if (valid) store_J(d, e, jc, jp, fac);
 #pragma unroll
-    for (int k = 0; k < 18; ++k) {
-      const SP v = narrow<SP>(jc[k]);
-      if (valid) d.J[k * static_cast<uint64_t>(d.na) + e] = v;
-      jc[k] = widen<FP>(v);
-    }
+    for (int k = 0; k < 18; ++k) jc[k] = widen<FP>(narrow<SP>(jc[k]));
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      const SP v = narrow<SP>(jp[k]);
-      if (valid) d.J[(18 + k) * static_cast<uint64_t>(d.na) + e] = v;
-      jp[k] = widen<FP>(v);
-    }
+    for (int k = 0; k < 6; ++k) jp[k] = widen<FP>(narrow<SP>(jp[k]));
   }
   if (d.w && valid) d.w[e] = w;
   const FP wr0 = valid ? w * res[0] : FP(0), wr1 = valid ? w * res[1] : FP(0);
@@ -1500,10 +1628,14 @@ __global__ void __launch_bounds__(kTileThreads) k_schur_pre_tiles(Dev<FP, SP> d)
     const uint64_t pid = pb + d.d_lpt[e];
     const uint64_t pcol = pcol0 + 3 * pid;
     FP jc[18], jp[6];
+    {
+      arith_t<SP> ja[18], pa[6];
+      load_J(d, e, cam, ja, pa);
 #pragma unroll
-    for (int k = 0; k < 18; ++k) jc[k] = widen<FP>(d.J[k * static_cast<uint64_t>(d.na) + e]) * d.D[9ull * cam + (k % 9)];
+      for (int k = 0; k < 18; ++k) jc[k] = static_cast<FP>(ja[k]) * d.D[9ull * cam + (k % 9)];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) jp[k] = widen<FP>(d.J[(18 + k) * static_cast<uint64_t>(d.na) + e]) * d.D[pcol + (k % 3)];
+      for (int k = 0; k < 6; ++k) jp[k] = static_cast<FP>(pa[k]) * d.D[pcol + (k % 3)];
+    }
     const FP w = d.w ? d.w[e] : FP(1);
     const bool on = valid && d.col_free[pcol];
     FP B[27], C[27];
@@ -1607,7 +1739,7 @@ __global__ void __launch_bounds__(kTileThreads) k_schur_tiles(Dev<FP, SP> d) {
       const uint32_t e = eb + (valid ? j : 0);
       const uint32_t cam = d.d_cam[e];
       A jc[18], jp[6];
-      load_J(d, e, jc, jp);
+      load_J(d, e, cam, jc, jp);
       const A* cv = d.vt + 9ull * cam;
       A u0 = A(0), u1 = A(0);
 #pragma unroll
@@ -1690,7 +1822,7 @@ __global__ void __launch_bounds__(kTileThreads) k_schur_tiles(Dev<FP, SP> d) {
     const uint32_t cam = d.d_cam[e];
     const uint32_t lp = d.d_lpt[e];
     A jc[18], jp[6];
-    load_J(d, e, jc, jp);
+    load_J(d, e, cam, jc, jp);
     A u0 = A(0), u1 = A(0);
     if (MODE == 0) {
       if (!heavy) {

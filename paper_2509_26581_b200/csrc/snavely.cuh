@@ -105,25 +105,66 @@ __device__ inline void snavely_residual(const FP* cam, const FP* X, FP o0, FP o1
 // Residual and both Jacobian blocks from ONE chain (SnavelyChain,
 // snavely.hpp:103-153): jc = d pred / d camera (2x9 row-major),
 // jp = d pred / d point (2x3 row-major). r may be null.
+// R = a I + s [w]x + c w w^T (rodrigues_with_jacobian, snavely.hpp:67-101),
+// explicitly rounded: the factored J store rebuilds the point block from this
+// per-camera matrix, so linearize and the HVP must produce identical bits.
 template <typename FP>
-__device__ inline void snavely_linearize(const FP* cam, const FP* X, FP o0, FP o1, FP* r, FP* jc, FP* jp) {
+__device__ inline void rotation_matrix(const Rodrigues<FP>& Ro, FP w0, FP w1, FP w2, FP* R) {
+  const FP a = Ro.ja, s = Ro.js, c = Ro.jcc;
+  const FP c0 = mul_rn(c, w0), c1 = mul_rn(c, w1), c2 = mul_rn(c, w2);
+  R[0] = fma_rn(c0, w0, a);
+  R[1] = fma_rn(c0, w1, -mul_rn(s, w2));
+  R[2] = fma_rn(c0, w2, mul_rn(s, w1));
+  R[3] = fma_rn(c1, w0, mul_rn(s, w2));
+  R[4] = fma_rn(c1, w1, a);
+  R[5] = fma_rn(c1, w2, -mul_rn(s, w0));
+  R[6] = fma_rn(c2, w0, -mul_rn(s, w1));
+  R[7] = fma_rn(c2, w1, mul_rn(s, w0));
+  R[8] = fma_rn(c2, w2, a);
+}
+
+// Point block jp = du/dP . R (snavely.hpp:150-153), 2x3 row-major.
+template <typename FP>
+__device__ inline void point_block(const FP* U, const FP* R, FP* jp) {
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      jp[3 * rr + j] = fma_rn(U[3 * rr + 2], R[6 + j], fma_rn(U[3 * rr + 1], R[3 + j], mul_rn(U[3 * rr], R[j])));
+}
+
+// Intrinsics columns of the camera block: [d p | f n p | f n^2 p]
+// (snavely.hpp:122-128).
+template <typename FP>
+__device__ inline void intrinsic_cols(FP dist, FP n, FP p0, FP p1, FP f, FP* jc) {
+  const FP fn = mul_rn(f, n), fnn = mul_rn(fn, n);
+  jc[6] = mul_rn(dist, p0);
+  jc[15] = mul_rn(dist, p1);
+  jc[7] = mul_rn(fn, p0);
+  jc[16] = mul_rn(fn, p1);
+  jc[8] = mul_rn(fnn, p0);
+  jc[17] = mul_rn(fnn, p1);
+}
+
+// Per-camera record of the factored J store: R (9) and f.
+template <typename FP>
+__device__ inline void camera_factor(const FP* cam, FP* rf) {
+  const Rodrigues<FP> Ro = rodrigues_coeffs<FP>(cam[0], cam[1], cam[2], true);
+  rotation_matrix<FP>(Ro, cam[0], cam[1], cam[2], rf);
+  rf[9] = cam[6];
+}
+
+template <typename FP>
+__device__ inline void snavely_linearize(const FP* cam, const FP* X, FP o0, FP o1, FP* r, FP* jc, FP* jp,
+                                         FP* fac = nullptr) {
   const FP w0 = cam[0], w1 = cam[1], w2 = cam[2];
   const FP x0 = X[0], x1 = X[1], x2 = X[2];
   const Rodrigues<FP> Ro = rodrigues_coeffs<FP>(w0, w1, w2, true);
   FP P[3];
   rotate_translate(cam, X, Ro, P);
-  const FP a = Ro.ja, s = Ro.js, c = Ro.jcc, s1 = Ro.s1, c2 = Ro.c2;
-  // R = a I + s [w]x + c w w^T
+  const FP s = Ro.js, c = Ro.jcc, s1 = Ro.s1, c2 = Ro.c2;
   FP R[9];
-  R[0] = a + c * w0 * w0;
-  R[1] = -s * w2 + c * w0 * w1;
-  R[2] = s * w1 + c * w0 * w2;
-  R[3] = s * w2 + c * w1 * w0;
-  R[4] = a + c * w1 * w1;
-  R[5] = -s * w0 + c * w1 * w2;
-  R[6] = -s * w1 + c * w2 * w0;
-  R[7] = s * w0 + c * w2 * w1;
-  R[8] = a + c * w2 * w2;
+  rotation_matrix<FP>(Ro, w0, w1, w2, R);
   // dy/dw = -s x w^T + s1 (w x x) w^T - s [x]x + c2 (w.x) w w^T + c (w x^T + (w.x) I)
   const FP cr[3] = {w1 * x2 - w2 * x1, w2 * x0 - w0 * x2, w0 * x1 - w1 * x0};
   const FP dt = w0 * x0 + w1 * x1 + w2 * x2;
@@ -165,15 +206,18 @@ __device__ inline void snavely_linearize(const FP* cam, const FP* X, FP o0, FP o
     for (int j = 0; j < 3; ++j) {
       jc[9 * rr + j] = U[3 * rr] * Dw[j] + U[3 * rr + 1] * Dw[3 + j] + U[3 * rr + 2] * Dw[6 + j];
       jc[9 * rr + 3 + j] = U[3 * rr + j];
-      jp[3 * rr + j] = U[3 * rr] * R[j] + U[3 * rr + 1] * R[3 + j] + U[3 * rr + 2] * R[6 + j];
     }
   }
-  jc[6] = dist * p0;
-  jc[15] = dist * p1;
-  jc[7] = f * n * p0;
-  jc[16] = f * n * p1;
-  jc[8] = f * n * n * p0;
-  jc[17] = f * n * n * p1;
+  point_block<FP>(U, R, jp);
+  intrinsic_cols<FP>(dist, n, p0, p1, f, jc);
+  if (fac) {  // factored store: U (6), dist, n, p0, p1
+#pragma unroll
+    for (int k = 0; k < 6; ++k) fac[k] = U[k];
+    fac[6] = dist;
+    fac[7] = n;
+    fac[8] = p0;
+    fac[9] = p1;
+  }
 }
 
 template <typename FP>

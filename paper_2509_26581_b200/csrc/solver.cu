@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -22,6 +23,7 @@
 #include "dist.hpp"
 #include "gb_bal.h"
 #include "kernels.cuh"
+#include "hvp_pipe.cuh"
 
 namespace gb {
 
@@ -83,6 +85,7 @@ class SolverBase {
 // ------------------------------------------------------------- device memory
 class DBuf {
  public:
+  static constexpr size_t kSlack = 64;
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
@@ -95,7 +98,7 @@ class DBuf {
   void* alloc(size_t bytes) {
     if (bytes <= bytes_ && p_) return p_;
     release();
-    CK(cudaMalloc(&p_, bytes ? bytes : 1));
+    CK(cudaMalloc(&p_, bytes + kSlack));  // slack: 16-byte-widened bulk copies may read past the end
     bytes_ = bytes;
     return p_;
   }
@@ -118,6 +121,27 @@ T* upload(DBuf& buf, const std::vector<T>& v, cudaStream_t s) {
 
 inline unsigned div_up(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 
+// Setup phase timer: GB_TIMING=1 prints "[gb] phase ms" lines to stderr
+// (synchronizing the stream at each mark, so only for diagnosis).
+struct PhaseTimer {
+  using Clock = std::chrono::steady_clock;
+  bool on = false;
+  cudaStream_t s = nullptr;
+  Clock::time_point t;
+  explicit PhaseTimer(cudaStream_t st) : s(st) {
+    const char* e = std::getenv("GB_TIMING");
+    on = e && *e && *e != '0';
+    t = Clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto n = Clock::now();
+    std::fprintf(stderr, "[gb] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 // --------------------------------------------------------------------- solver
 template <typename FP, typename SP>
 class Solver final : public SolverBase {
@@ -131,6 +155,7 @@ class Solver final : public SolverBase {
     {
       int sms = 0, per = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g_.device));
+      sms_ = static_cast<uint32_t>(sms);
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_step<FP, SP>, 256, 0));
       coop_grid_ = static_cast<unsigned>(std::max(1, sms * std::max(1, per)));
       if (const char* e = std::getenv("GB_PCG_FUSED")) fused_pcg_ = std::atoi(e) != 0;
@@ -201,8 +226,11 @@ class Solver final : public SolverBase {
     if (in_solve_) end(nullptr, nullptr, 0);
     t0_ = Clock::now();
     CK(cudaSetDevice(g_.device));
+    PhaseTimer pt(s_);
     ensure_structure(cfg.level);
+    pt.mark("begin: structure");
     upload_params();
+    pt.mark("begin: upload params");
     cfg_ = cfg;
     State<FP> hs{};
     fill_config(hs, cfg);
@@ -212,6 +240,7 @@ class Solver final : public SolverBase {
     enqueue_linearize(1);
     CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
     CK(cudaStreamSynchronize(s_));
+    pt.mark("begin: initial linearize");
     const FP chi2 = hs.lin_chi2;
     if (!std::isfinite(static_cast<double>(chi2)))
       throw std::runtime_error("levenberg_marquardt: non-finite chi^2 at the initial parameters");
@@ -254,6 +283,7 @@ class Solver final : public SolverBase {
       ev_.resize(max_it_ + 1);
       for (auto& e : ev_) CK(cudaEventCreate(&e));
       CK(cudaStreamSynchronize(s_));
+      pt.mark("begin: damping + graph capture");
     }
     r.setup_seconds = std::chrono::duration<double>(Clock::now() - t0_).count();
     in_solve_ = true;
@@ -525,7 +555,14 @@ class Solver final : public SolverBase {
     if (!dev_.J) throw std::logic_error("dynamic mode stores no Jacobians");
     const uint64_t ns = act_.n_slots;
     std::vector<SP> h(24 * ns);
-    CK(cudaMemcpy(h.data(), dev_.J, h.size() * sizeof(SP), cudaMemcpyDeviceToHost));
+    {
+      DBuf full;
+      SP* fj = static_cast<SP*>(full.alloc(24 * ns * sizeof(SP)));
+      k_expand_J<FP, SP><<<grid_for(ns), 256, 0, s_>>>(dev_, fj);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(h.data(), fj, h.size() * sizeof(SP), cudaMemcpyDeviceToHost, s_));
+      CK(cudaStreamSynchronize(s_));
+    }
     SP* o = static_cast<SP*>(out);
     for (uint64_t d = 0; d < ns; ++d) {
       if (act_.d_a[d] == kNoKey) continue;
@@ -581,7 +618,9 @@ class Solver final : public SolverBase {
       cudaGraphExecDestroy(graph_exec_);
       graph_exec_ = nullptr;
     }
+    PhaseTimer pt(s_);
     allocate_work();
+    pt.mark("allocate work");
   }
 
   // The host activation (activate.cpp) for the debug surface of a device-
@@ -711,6 +750,7 @@ class Solver final : public SolverBase {
     for (uint64_t p = 0; p < np; ++p) act_.free_pts += (g_.pt_fixed.empty() || !g_.pt_fixed[p]) ? 1 : 0;
     act_.free_dims = 9 * act_.free_cams + 3 * act_.free_pts;
 
+    PhaseTimer ptm(s_);
     DBuf s_cam, s_pt, s_lvl, s_cfix, s_pfix, s_obs, s_flag, s_pos, s_cam_a, s_pt_a, s_entry, s_key, s_key2, s_val, s_val2,
         s_rank, s_deg, s_degi, s_rb, s_k64, s_k64b, s_order, s_pkey, s_pval, s_pkey2, s_pval2, s_hc, s_hr, s_ic, s_ir,
         s_runcam, s_runcam2, s_slots, s_cnt, s_bad;
@@ -720,6 +760,7 @@ class Solver final : public SolverBase {
     const uint8_t* cfix = g_.cam_fixed.empty() ? nullptr : to_dev(s_cfix, g_.cam_fixed);
     const uint8_t* pfix = g_.pt_fixed.empty() ? nullptr : to_dev(s_pfix, g_.pt_fixed);
     const double* obs = to_dev(s_obs, g_.obs);
+    ptm.mark("act: h2d edges");
     uint32_t* flag = scratch<uint32_t>(s_flag, ne + 1);
     uint32_t* pos = scratch<uint32_t>(s_pos, ne + 1);
     int* bad = scratch<int>(s_bad, 1);
@@ -766,8 +807,10 @@ class Solver final : public SolverBase {
     if (np) CK(cudaMemcpyAsync(hdeg.data(), degi, np * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
     CK(cudaStreamSynchronize(s_));
     // tiles: the host greedy over degrees (activate.cpp greedy_tiles)
+    ptm.mark("act: compact + point order");
     std::vector<uint32_t> real_beg, tile_of_pt;
     greedy_tiles(hdeg, act_.tile_pbeg, real_beg, tile_of_pt);
+    ptm.mark("act: host greedy tiles");
     act_.ntiles = static_cast<uint32_t>(act_.tile_pbeg.size() - 1);
     const uint32_t T = act_.ntiles;
     act_.tile_ecnt.resize(T);
@@ -832,6 +875,7 @@ class Solver final : public SolverBase {
     uint32_t nparts = 0;
     CK(cudaMemcpyAsync(&nparts, chunk_part_base + act_.nchunks, sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
     CK(cudaStreamSynchronize(s_));
+    ptm.mark("act: edge sort + place");
     act_.nparts = nparts;
     d.nparts = nparts;
     const uint32_t ncams_total = act_.tile_cam_off[T];
@@ -883,18 +927,46 @@ class Solver final : public SolverBase {
     d.cam_part_idx = cam_part_idx;
     d.col_free = col_free;
     CK(cudaStreamSynchronize(s_));  // scratch buffers are released on return
+    ptm.mark("act: runs, slots, csr");
   }
 
   void allocate_work() {
     const uint64_t nc = act_.nc, np = act_.np, ns = act_.n_slots;
     Dev<FP, SP>& d = dev_;
     const bool dyn = g_.diff_mode == GB_DYNAMIC;
-    d.J = dyn ? nullptr : static_cast<SP*>(b_J_.alloc(24 * ns * sizeof(SP)));
-    if (d.J) CK(cudaMemsetAsync(d.J, 0, 24 * ns * sizeof(SP), s_));  // padding slots stay 0
+    // factored J store: analytic mode with SP == FP; GB_JFACT=0 disables
+    d.jfact = (!dyn && g_.diff_mode == GB_ANALYTIC && std::is_same<SP, FP>::value) ? 1 : 0;
+    if (const char* e = std::getenv("GB_JFACT")) d.jfact = d.jfact && std::atoi(e) != 0;
+    const uint64_t jrows = d.jfact ? kJFactRows : 24;
+    d.J = dyn ? nullptr : static_cast<SP*>(b_J_.alloc(jrows * ns * sizeof(SP)));
+    if (d.J) CK(cudaMemsetAsync(d.J, 0, jrows * ns * sizeof(SP), s_));  // padding slots stay 0
+    d.Rf = d.jfact ? static_cast<FP*>(b_Rf_.alloc(std::max<uint64_t>(1, 10 * nc) * sizeof(FP))) : nullptr;
     d.w = g_.loss_kind == GB_LOSS_HUBER ? static_cast<FP*>(b_w_.alloc(ns * sizeof(FP))) : nullptr;
     if (d.w) CK(cudaMemsetAsync(d.w, 0, ns * sizeof(FP), s_));
     d.loss_kind = g_.loss_kind;
     d.huber = static_cast<FP>(g_.huber);
+    // bulk-copy pipelined HVP (hvp_pipe.cuh): stored J, >= 2 stages in shared memory; GB_HVP_PIPE=0 disables
+    {
+      int optin = 0;
+      CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g_.device));
+      pipe_ = pipe_layout<FP, SP>(d.jfact ? kJFactRows : 24, d.w != nullptr, static_cast<uint32_t>(optin));
+      pipe_ok_ = d.J != nullptr && pipe_.stages >= 2 && d.n_normal > 0;
+      if (const char* e = std::getenv("GB_HVP_PIPE")) pipe_ok_ = pipe_ok_ && std::atoi(e) != 0;
+      d.tile_meta = nullptr;
+      d.tcv = nullptr;
+      d.tcr = nullptr;
+      d.ntcams = act_.tile_cam_off.empty() ? 0 : act_.tile_cam_off.back();
+      if (pipe_ok_) {
+        CK(cudaFuncSetAttribute(k_hvp_pipe<FP, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(pipe_.total_bytes)));
+        uint32_t* meta = static_cast<uint32_t*>(b_tmeta_.alloc(12ull * d.n_normal * sizeof(uint32_t)));
+        k_tile_meta<FP, SP><<<grid_for(d.n_normal), 256, 0, s_>>>(d, meta);
+        CK(cudaGetLastError());
+        d.tile_meta = meta;
+        d.tcv = static_cast<A*>(b_tcv_.alloc(std::max<uint64_t>(1, 9ull * d.ntcams) * sizeof(A)));
+        d.tcr = d.jfact ? static_cast<FP*>(b_tcr_.alloc(std::max<uint64_t>(1, 10ull * d.ntcams) * sizeof(FP))) : nullptr;
+      }
+    }
     d.part = static_cast<FP*>(b_part_.alloc(std::max<uint64_t>(1, act_.nparts) * kLinVals * sizeof(FP)));
     d.x = static_cast<FP*>(b_x_.alloc(ncols_ * sizeof(FP)));
     d.x_new = static_cast<FP*>(b_xn_.alloc(ncols_ * sizeof(FP)));
@@ -1070,16 +1142,25 @@ class Solver final : public SolverBase {
       k_lin_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, force, 2);
     }
     CK(cudaGetLastError());
+    if (pipe_ok_ && dev_.tcr) {
+      k_tcam_rf<FP, SP><<<grid_for(10ull * dev_.ntcams), 256, 0, s_>>>(dev_, force);
+      CK(cudaGetLastError());
+    }
   }
 
   // HVP tile pass (dynamic mode recomputes J per edge).
   void launch_hvp_tiles(const Dev<FP, SP>& d) {
-    if (!d.J)
-      k_hvp_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
-    else if (hvp_minb_ == 4)
-      k_hvp_tiles<FP, SP, false, 4><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
-    else
-      k_hvp_tiles<FP, SP, false, 1><<<act_.ntiles, kTileThreads, 0, s_>>>(d);
+    if (!d.J) {
+      k_hvp_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(d, nullptr);
+    } else if (pipe_ok_) {  // normal tiles through the bulk-copy pipeline, heavy tiles one CTA each
+      k_tcam_vt<FP, SP><<<grid_for(9ull * d.ntcams), 256, 0, s_>>>(d);
+      k_hvp_pipe<FP, SP><<<std::min<uint32_t>(d.n_normal, sms_), kPipeThreads, pipe_.total_bytes, s_>>>(d, pipe_);
+      if (d.n_heavy) k_hvp_tiles<FP, SP, false, 1><<<d.n_heavy, kTileThreads, 0, s_>>>(d, d.heavy_tiles);
+    } else if (hvp_minb_ == 4) {
+      k_hvp_tiles<FP, SP, false, 4><<<act_.ntiles, kTileThreads, 0, s_>>>(d, nullptr);
+    } else {
+      k_hvp_tiles<FP, SP, false, 1><<<act_.ntiles, kTileThreads, 0, s_>>>(d, nullptr);
+    }
     CK(cudaGetLastError());
   }
 
@@ -1267,7 +1348,11 @@ class Solver final : public SolverBase {
   DBuf b_vt_, b_dlcam_, b_tile_ecnt_, b_tile_cam_off_, b_tile_cams_, b_normal_, b_heavy_;
   DBuf b_col_free_, b_dcam_, b_dlpt_, b_obs_, b_tile_ebeg_, b_tile_pbeg_, b_tile_chunk_, b_chunk_part_,
       b_pt_slot_off_, b_pt_slots_, b_cam_part_off_, b_cam_part_idx_;
-  DBuf b_J_, b_w_, b_part_, b_x_, b_xn_, b_b_, b_cl_, b_D_, b_dx_, b_Hc_, b_Hp_, b_Mc_, b_Mp_, b_xs_, b_r_, b_z_, b_p_,
+  PipeLayout pipe_{};
+  bool pipe_ok_ = false;
+  uint32_t sms_ = 148;
+  DBuf b_tmeta_, b_tcv_, b_tcr_;
+  DBuf b_J_, b_Rf_, b_w_, b_part_, b_x_, b_xn_, b_b_, b_cl_, b_D_, b_dx_, b_Hc_, b_Hp_, b_Mc_, b_Mp_, b_xs_, b_r_, b_z_, b_p_,
       b_ap_, b_tr_, b_tr2_, b_tf_, b_cr_, b_cr2_, b_cf_, b_br_, b_br2_, b_bf_;
 };
 

@@ -83,6 +83,56 @@ def test_jacobians_parity(gpu, ref, ladybug):
     assert rel(ja, jb) <= 1e-12
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_factored_jacobian_store_bit_exact(gpu, ladybug, monkeypatch, precision):
+    """The factored J store (16 values per edge + R, f per camera; DESIGN.md
+    §2) rebuilds exactly the chain's J: bit-identical to the full 24-value
+    store, and the HVP / LM trace through it is bit-identical too."""
+    out = {}
+    for jf in ("1", "0"):
+        monkeypatch.setenv("GB_JFACT", jf)
+        g = bal.build_graph(ladybug, precision, "analytic")
+        n = g.ls_linearize(0)["n"]
+        v = np.random.default_rng(3).standard_normal(n)
+        out[jf] = (g.ls_jacobians(LADYBUG[2]), g.ls_hvp(v, 1e-3))
+        g2 = bal.build_graph(ladybug, precision, "analytic")
+        rep = bal.levenberg_marquardt(g2, bal_cfg(8))
+        out[jf] += ([(i.chi2_after, i.lambda_, i.pcg_iterations) for i in rep.iterations], g2.cameras.copy())
+    a, b = out["1"], out["0"]
+    assert np.array_equal(a[0].view(np.uint8), b[0].view(np.uint8))
+    assert np.array_equal(a[1], b[1])
+    assert a[2] == b[2]
+    assert np.array_equal(a[3], b[3])
+
+
+@pytest.mark.parametrize("precision,mode,huber", [("fp64", "analytic", None), ("fp64", "auto", None),
+                                                 ("fp32", "analytic", 2.0), ("fp32-bf16", "analytic", None)])
+def test_pipelined_hvp_bit_exact(gpu, monkeypatch, precision, mode, huber):
+    """The bulk-copy pipelined HVP (hvp_pipe.cuh) keeps k_hvp_tiles' arithmetic
+    and association order: bit-identical HVP and LM trace with it on and off.
+    Problem sized to give several tiles per CTA (ring wrap-around) and heavy
+    tiles (a point seen by > 512 cameras)."""
+    probs = [bal.synthetic_bal(900, 60000, 330000, seed=11), bal.synthetic_bal(900, 60000, 330000, seed=12, zipf=1.2)]
+    for p in probs:
+        _pipe_vs_tiles(monkeypatch, p, precision, mode, huber)
+
+
+def _pipe_vs_tiles(monkeypatch, p, precision, mode, huber):
+    out = {}
+    for pipe in ("1", "0"):
+        monkeypatch.setenv("GB_HVP_PIPE", pipe)
+        g = bal.build_graph(p, precision, mode, huber)
+        n = g.ls_linearize(0)["n"]
+        v = np.random.default_rng(4).standard_normal(n)
+        h = g.ls_hvp(v, 1e-3)
+        g2 = bal.build_graph(p, precision, mode, huber)
+        rep = bal.levenberg_marquardt(g2, bal_cfg(4))
+        out[pipe] = (h, [(i.chi2_after, i.lambda_, i.pcg_iterations) for i in rep.iterations], g2.points.copy())
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert out["1"][1] == out["0"][1]
+    assert np.array_equal(out["1"][2], out["0"][2])
+
+
 @pytest.mark.parametrize("mode", ["analytic", "dynamic"])
 def test_hvp_parity(gpu, ref, ladybug, mode):
     g, r = pair(ladybug, ref, mode=mode)
