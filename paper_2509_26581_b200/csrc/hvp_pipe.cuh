@@ -2,17 +2,20 @@
 // linear_system.hpp:104-115; hvp_forward factor_descriptor.hpp:372-407 and
 // hvp_scatter :409-433).
 //
-// Same arithmetic, association order and outputs as k_hvp_tiles (so results
-// are bit-identical), restructured for HBM bandwidth: one persistent CTA per
-// SM, a producer warp and 16 consumer warps (one edge per consumer thread).
-// The producer streams every byte a tile needs into a ring of shared-memory
+// Same arithmetic and association order as k_hvp_tiles (results are
+// bit-identical), restructured for HBM bandwidth: one persistent CTA per SM,
+// a producer warp and 16 consumer warps (one edge per consumer thread). The
+// producer streams every byte a tile needs into a ring of shared-memory
 // stages with 1-D bulk async copies (cp.async.bulk, completion counted on an
-// mbarrier): the J rows (SoA, one contiguous run per row), local camera and
-// point indices, Huber weights, the chunk partial-slot bases, the tile's
-// point slot lists, and the tile's p, D and free masks. It also gathers the
-// tile's cameras (D*p and, for the factored store, R and f) into the stage.
-// Consumers therefore touch global memory only to write partial slots, ap
-// and the per-warp dot partials, while the next stages' copies are in flight.
+// mbarrier). Small scattered copies are what limits a bulk-copy stream (a
+// measured ~30-90 ns each, tools/tma_bench.cu), so a tile needs only
+// rows + 4 copies: its J rows (SoA, one contiguous run per row), a static
+// per-tile "aux" blob (edge camera/point indices, point slot lists, chunk
+// partial-slot bases, free mask; built once per activation), a per-
+// linearization "lin" blob (point D, camera R f, Huber weights), the tile's
+// p (contiguous in the internal point order) and the tile's camera D*p copy
+// (tcv, refreshed before each HVP). Consumers touch global memory only to
+// write partial slots, ap and the per-warp dot partials.
 #pragma once
 
 #include <algorithm>
@@ -25,45 +28,86 @@ constexpr int kPipeConsumers = kTileEdges;          // one consumer thread per e
 constexpr int kPipeThreads = kPipeConsumers + 32;   // + one producer warp
 constexpr int kPipeMaxStages = 4;
 
+__host__ __device__ constexpr uint32_t r16(uint64_t b) { return static_cast<uint32_t>((b + 15) / 16 * 16); }
+
+// byte stride of one J row (and of one contribution row) in shared memory
+template <typename T>
+__host__ __device__ constexpr uint32_t pipe_jstride() {
+  return static_cast<uint32_t>(kTileEdges * sizeof(T) + 16);
+}
+
+// Section offsets inside a tile's aux blob (static) and lin blob (per
+// linearization); identical on the host (sizes) and the device (reads).
+struct AuxSec {
+  uint32_t lcam, lpt, psl, pso, cpb, cf, bytes;
+};
+__host__ __device__ inline AuxSec aux_sections(uint32_t ne, uint32_t npt) {
+  const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad, nch = (ne + 31) / 32;
+  AuxSec a;
+  a.lcam = 0;
+  a.lpt = a.lcam + r16(2ull * ne8);
+  a.psl = a.lpt + r16(2ull * ne8);
+  a.pso = a.psl + r16(2ull * ne);
+  a.cpb = a.pso + r16(2ull * (npt + 1));
+  a.cf = a.cpb + r16(4ull * nch);
+  a.bytes = a.cf + r16(3ull * npt);
+  return a;
+}
+struct LinSec {
+  uint32_t D, cr, w, bytes;
+};
+template <typename FP>
+__host__ __device__ inline LinSec lin_sections(uint32_t ne, uint32_t npt, uint32_t ncam, bool fact, bool huber) {
+  const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad;
+  LinSec l;
+  l.D = 0;
+  l.cr = l.D + r16(sizeof(FP) * 3ull * npt);
+  l.w = l.cr + (fact ? r16(sizeof(FP) * 10ull * ncam) : 0u);
+  l.bytes = l.w + (huber ? r16(sizeof(FP) * 1ull * ne8) : 0u);
+  return l;
+}
+
 // byte offsets inside one stage (all 16-byte aligned)
 struct PipeLayout {
-  uint32_t hdr, J, lcam, lpt, w, cpb, camv, camr, pso, psl, p, D, cf;
+  uint32_t hdr, J, aux, lin, p, camv;
   uint32_t stage_bytes, fixed_bytes, total_bytes;
   int stages, rows;
+  int dbg;  // experiments only (GB_PIPE_DBG): 1 skip camera reduction, 2 skip epilogue, 4 skip edge math,
+            // 16 copy only the J rows
 };
 
 template <typename FP, typename SP>
-inline PipeLayout pipe_layout(int rows, bool huber, uint32_t smem_budget) {
+inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_budget) {
   using A = arith_t<SP>;
   PipeLayout L{};
   uint32_t o = 0;
   auto take = [&](uint64_t bytes) {
     const uint32_t r = o;
-    o += static_cast<uint32_t>((bytes + 15) / 16 * 16);
+    o += r16(bytes);
     return r;
   };
   L.rows = rows;
   L.hdr = take(16 * 4);
-  L.J = take(static_cast<uint64_t>(rows) * kTileEdges * sizeof(SP));
-  L.lcam = take(kTileEdges * 2);
-  L.lpt = take(kTileEdges * 2);
-  L.w = huber ? take(kTileEdges * sizeof(FP)) : 0;
-  L.cpb = take((kTileEdges / 32 + 1) * 4 + 32);
-  L.camv = take(kTileCams * 9 * sizeof(A) + 32);
-  L.camr = take(kTileCams * 10 * sizeof(FP) + 32);
-  L.pso = take((kTilePoints + 1) * 4 + 32);
-  L.psl = take(kTileEdges * 2 + 32);
+  // J rows at a padded stride (bank spread); rows 0..11 are reused for the
+  // edges' camera (9) and point (3) contributions when sizeof(SP) == sizeof(A)
+  L.J = take(static_cast<uint64_t>(rows) * pipe_jstride<SP>());
+  L.aux = take(aux_sections(kTileEdges, kTilePoints).bytes);
+  L.lin = take(lin_sections<FP>(kTileEdges, kTilePoints, kTileCams, fact, huber).bytes);
   L.p = take(kTilePoints * 3 * sizeof(SP) + 32);
-  L.D = take(kTilePoints * 3 * sizeof(FP) + 32);
-  L.cf = take(kTilePoints * 3 + 32);
+  L.camv = take(kTileCams * 9 * sizeof(A) + 32);
   L.stage_bytes = o;
-  // after the stages: 2 mbarriers per stage, the point staging (kTileEdges x 3 A)
-  L.fixed_bytes = 2 * kPipeMaxStages * 8 + static_cast<uint32_t>((kTileEdges * 3 * sizeof(A) + 15) / 16 * 16);
+  // after the stages: 2 mbarriers per stage, then (bf16 storage only) a
+  // separate 12-row staging for the camera / point contributions
+  L.fixed_bytes = 2 * kPipeMaxStages * 8 +
+                  (sizeof(SP) == sizeof(A) ? 0u : static_cast<uint32_t>(12 * pipe_jstride<A>()));
   const uint32_t avail = smem_budget > L.fixed_bytes ? smem_budget - L.fixed_bytes : 0;
   L.stages = static_cast<int>(std::min<uint32_t>(kPipeMaxStages, avail / L.stage_bytes));
   L.total_bytes = L.stages * L.stage_bytes + L.fixed_bytes;
   return L;
 }
+
+// tile record, one per normal tile (list order)
+enum TileMeta : int { kMT = 0, kMEb, kMNe, kMPb, kMNpt, kMCb, kMNcam, kMCh0, kMAux16, kMLin16, kMCount = 12 };
 
 // ---- PTX helpers: mbarrier + 1-D bulk async copy global -> shared
 __device__ inline uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -115,22 +159,21 @@ __device__ inline Span span16(const void* p, uint64_t bytes) {
   return Span{reinterpret_cast<const char*>(lo), static_cast<uint32_t>(hi - lo), static_cast<uint32_t>(a - lo)};
 }
 
-enum PipeHdr : int { kHT = 0, kHNe, kHNpt, kHNcam, kHDcpb, kHDpso, kHDpsl, kHDp, kHDD, kHDcf, kHNe8, kHPb, kHDcv, kHDcr };
+enum PipeHdr : int { kHT = 0, kHNe, kHNpt, kHNcam, kHDp, kHDcv, kHPb };
 
 template <typename FP, typename SP>
 __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, PipeLayout L) {
   using A = arith_t<SP>;
-  if (!d.st->iter_active || d.st->pcg_done) return;
+  if (!L.dbg && (!d.st->iter_active || d.st->pcg_done)) return;
   extern __shared__ __align__(128) unsigned char pipe_smem[];
   const int S = L.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(pipe_smem + S * L.stage_bytes);
   uint64_t* empty = full + kPipeMaxStages;
-  A* hstage = reinterpret_cast<A*>(empty + kPipeMaxStages);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);   // producer lane 0 (arrive + expect_tx)
-      mbar_init(&empty[s], 1);  // consumer thread 0 after the tile's last barrier
+      mbar_init(&empty[s], kPipeConsumers / 32);  // every consumer warp, when done with the stage
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -148,7 +191,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       const uint32_t my = base + lane * gridDim.x;
       uint4 m0 = make_uint4(0, 0, 0, 0), m1 = m0, m2 = m0;
       if (my < ntiles) {
-        const uint4* r = reinterpret_cast<const uint4*>(d.tile_meta + 12ull * my);
+        const uint4* r = reinterpret_cast<const uint4*>(d.tile_meta + static_cast<uint64_t>(kMCount) * my);
         m0 = r[0];
         m1 = r[1];
         m2 = r[2];
@@ -158,70 +201,43 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         const uint32_t t = __shfl_sync(0xffffffffu, m0.x, k), eb = __shfl_sync(0xffffffffu, m0.y, k);
         const uint32_t ne = __shfl_sync(0xffffffffu, m0.z, k), pb = __shfl_sync(0xffffffffu, m0.w, k);
         const uint32_t npt = __shfl_sync(0xffffffffu, m1.x, k), cb = __shfl_sync(0xffffffffu, m1.y, k);
-        const uint32_t ncam = __shfl_sync(0xffffffffu, m1.z, k), ch0 = __shfl_sync(0xffffffffu, m1.w, k);
-        const uint32_t ps0 = __shfl_sync(0xffffffffu, m2.x, k);
+        const uint32_t ncam = __shfl_sync(0xffffffffu, m1.z, k);
+        const uint64_t aux16 = __shfl_sync(0xffffffffu, m2.x, k), lin16 = __shfl_sync(0xffffffffu, m2.y, k);
         const int s = static_cast<int>(i % S);
         if (i >= static_cast<uint32_t>(S)) mbar_wait(&empty[s], ((i / S) - 1) & 1);
         unsigned char* st = pipe_smem + s * L.stage_bytes;
-        const uint32_t nch = (ne + 31) / 32;
         const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad;
-        const uint64_t pc = pcol0 + 3ull * pb;
-        const Span s_cpb = span16(d.chunk_part_base + ch0, 4ull * nch);
-        const Span s_pso = span16(d.pt_slot_off + pb, 4ull * (npt + 1));
-        const Span s_psl = span16(d.pt_slots + ps0, 2ull * ne);
-        const Span s_p = span16(d.p + pc, sizeof(SP) * 3ull * npt);
-        const Span s_D = span16(d.D + pc, sizeof(FP) * 3ull * npt);
-        const Span s_cf = span16(d.col_free + pc, 3ull * npt);
+        const AuxSec as = aux_sections(ne, npt);
+        const LinSec ls = lin_sections<FP>(ne, npt, ncam, d.jfact != 0, d.w != nullptr);
+        const Span s_p = span16(d.p + pcol0 + 3ull * pb, sizeof(SP) * 3ull * npt);
         const Span s_cv = span16(d.tcv + 9ull * cb, sizeof(A) * 9ull * ncam);
-        const Span s_cr = span16(d.tcr + 10ull * cb, sizeof(FP) * 10ull * ncam);
-        const bool fact = d.jfact != 0;
+        const bool small = !(L.dbg & 16);  // experiments: 16 = J rows only
         const uint32_t jrow = ne8 * static_cast<uint32_t>(sizeof(SP));
-        const uint32_t total = L.rows * jrow + 2 * (ne8 * 2) +
-                               (d.w ? ne8 * static_cast<uint32_t>(sizeof(FP)) : 0) + s_cpb.bytes + s_pso.bytes +
-                               s_psl.bytes + s_p.bytes + s_D.bytes + s_cf.bytes + s_cv.bytes +
-                               (fact ? s_cr.bytes : 0);
+        const uint32_t total = L.rows * jrow + (small ? as.bytes + ls.bytes + s_p.bytes + s_cv.bytes : 0u);
         if (lane == 0) {
           uint32_t* h = reinterpret_cast<uint32_t*>(st + L.hdr);
           h[kHT] = t;
           h[kHNe] = ne;
           h[kHNpt] = npt;
           h[kHNcam] = ncam;
-          h[kHDcpb] = s_cpb.delta;
-          h[kHDpso] = s_pso.delta;
-          h[kHDpsl] = s_psl.delta;
           h[kHDp] = s_p.delta;
-          h[kHDD] = s_D.delta;
-          h[kHDcf] = s_cf.delta;
-          h[kHNe8] = ne8;
-          h[kHPb] = pb;
           h[kHDcv] = s_cv.delta;
-          h[kHDcr] = s_cr.delta;
+          h[kHPb] = pb;
           mbar_arrive_expect_tx(&full[s], total);  // releases the header; completes when all bytes land
         }
         __syncwarp();
-        // copies: J rows 0..rows-1, then lcam, lpt, cpb, pso, psl, p, D, cf, camera D*p, [R f], [w]
-        const int nfixed = 9;
-        const int ncopies = L.rows + nfixed + (fact ? 1 : 0) + (d.w ? 1 : 0);
+        const int ncopies = L.rows + (small ? 4 : 0);
         for (int q = lane; q < ncopies; q += 32) {
           if (q < L.rows) {
-            bulk_g2s(st + L.J + static_cast<uint32_t>(q) * kTileEdges * sizeof(SP),
+            bulk_g2s(st + L.J + static_cast<uint32_t>(q) * pipe_jstride<SP>(),
                      d.J + static_cast<uint64_t>(q) * d.na + eb, jrow, &full[s]);
             continue;
           }
-          int c = q - L.rows;
-          if (c >= nfixed && !fact) ++c;  // skip the R f copy
-          switch (c) {
-            case 0: bulk_g2s(st + L.lcam, d.d_lcam + eb, ne8 * 2, &full[s]); break;
-            case 1: bulk_g2s(st + L.lpt, d.d_lpt + eb, ne8 * 2, &full[s]); break;
-            case 2: bulk_g2s(st + L.cpb, s_cpb.src, s_cpb.bytes, &full[s]); break;
-            case 3: bulk_g2s(st + L.pso, s_pso.src, s_pso.bytes, &full[s]); break;
-            case 4: bulk_g2s(st + L.psl, s_psl.src, s_psl.bytes, &full[s]); break;
-            case 5: bulk_g2s(st + L.p, s_p.src, s_p.bytes, &full[s]); break;
-            case 6: bulk_g2s(st + L.D, s_D.src, s_D.bytes, &full[s]); break;
-            case 7: bulk_g2s(st + L.cf, s_cf.src, s_cf.bytes, &full[s]); break;
-            case 8: bulk_g2s(st + L.camv, s_cv.src, s_cv.bytes, &full[s]); break;
-            case 9: bulk_g2s(st + L.camr, s_cr.src, s_cr.bytes, &full[s]); break;
-            default: bulk_g2s(st + L.w, d.w + eb, ne8 * static_cast<uint32_t>(sizeof(FP)), &full[s]); break;
+          switch (q - L.rows) {
+            case 0: bulk_g2s(st + L.aux, d.tile_aux + 16 * aux16, as.bytes, &full[s]); break;
+            case 1: bulk_g2s(st + L.lin, d.tile_lin + 16 * lin16, ls.bytes, &full[s]); break;
+            case 2: bulk_g2s(st + L.p, s_p.src, s_p.bytes, &full[s]); break;
+            default: bulk_g2s(st + L.camv, s_cv.src, s_cv.bytes, &full[s]); break;
           }
         }
       }
@@ -242,19 +258,28 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     const uint32_t* h = reinterpret_cast<const uint32_t*>(st + L.hdr);
     const uint32_t t = h[kHT], ne = h[kHNe], npt = h[kHNpt], pb = h[kHPb];
     const SP* sJ = reinterpret_cast<const SP*>(st + L.J);
-    const uint16_t* slc = reinterpret_cast<const uint16_t*>(st + L.lcam);
-    const uint16_t* slp = reinterpret_cast<const uint16_t*>(st + L.lpt);
-    const uint32_t* scpb = reinterpret_cast<const uint32_t*>(st + L.cpb + h[kHDcpb]);
-    const uint32_t* spso = reinterpret_cast<const uint32_t*>(st + L.pso + h[kHDpso]);
-    const uint16_t* spsl = reinterpret_cast<const uint16_t*>(st + L.psl + h[kHDpsl]);
+    constexpr int JS = pipe_jstride<SP>() / sizeof(SP);  // J row stride (elements)
+    constexpr int GS = pipe_jstride<A>() / sizeof(A);    // contribution row stride (elements)
+    A* gs = sizeof(SP) == sizeof(A) ? reinterpret_cast<A*>(pipe_smem + s * L.stage_bytes + L.J)
+                                    : reinterpret_cast<A*>(empty + kPipeMaxStages);
+    const AuxSec as = aux_sections(ne, npt);
+    const LinSec ls = lin_sections<FP>(ne, npt, h[kHNcam], d.jfact != 0, d.w != nullptr);
+    const unsigned char* aux = st + L.aux;
+    const unsigned char* lin = st + L.lin;
+    const uint16_t* slc = reinterpret_cast<const uint16_t*>(aux + as.lcam);
+    const uint16_t* slp = reinterpret_cast<const uint16_t*>(aux + as.lpt);
+    const uint16_t* spsl = reinterpret_cast<const uint16_t*>(aux + as.psl);
+    const uint16_t* spso = reinterpret_cast<const uint16_t*>(aux + as.pso);
+    const uint32_t* scpb = reinterpret_cast<const uint32_t*>(aux + as.cpb);
+    const uint8_t* scf = aux + as.cf;
+    const FP* sD = reinterpret_cast<const FP*>(lin + ls.D);
+    const FP* camr = reinterpret_cast<const FP*>(lin + ls.cr);
+    const FP* sw = reinterpret_cast<const FP*>(lin + ls.w);
     const SP* sp = reinterpret_cast<const SP*>(st + L.p + h[kHDp]);
-    const FP* sD = reinterpret_cast<const FP*>(st + L.D + h[kHDD]);
-    const uint8_t* scf = st + L.cf + h[kHDcf];
     const A* camv = reinterpret_cast<const A*>(st + L.camv + h[kHDcv]);
-    const FP* camr = reinterpret_cast<const FP*>(st + L.camr + h[kHDcr]);
 
     // ---- edge phase: thread j = edge j of the tile
-    {
+    if (!(L.dbg & 4)) {
       const uint32_t j = tid;
       const bool valid = j < ne;
       const uint32_t jj = valid ? j : 0;
@@ -266,13 +291,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
           FP U[6], R[9];
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
-            jc[k] = sJ[k * kTileEdges + jj];
-            jc[9 + k] = sJ[(3 + k) * kTileEdges + jj];
+            jc[k] = sJ[k * JS + jj];
+            jc[9 + k] = sJ[(3 + k) * JS + jj];
           }
 #pragma unroll
-          for (int k = 0; k < 6; ++k) U[k] = sJ[(6 + k) * kTileEdges + jj];
-          const FP dist = sJ[12 * kTileEdges + jj], n = sJ[13 * kTileEdges + jj];
-          const FP p0 = sJ[14 * kTileEdges + jj], p1 = sJ[15 * kTileEdges + jj];
+          for (int k = 0; k < 6; ++k) U[k] = sJ[(6 + k) * JS + jj];
+          const FP dist = sJ[12 * JS + jj], n = sJ[13 * JS + jj];
+          const FP p0 = sJ[14 * JS + jj], p1 = sJ[15 * JS + jj];
           const FP* rf = camr + 10 * lc;
 #pragma unroll
           for (int k = 0; k < 9; ++k) R[k] = rf[k];
@@ -288,11 +313,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       }
       if (!done) {
 #pragma unroll
-        for (int k = 0; k < 18; ++k) jc[k] = widen<A>(sJ[k * kTileEdges + jj]);
+        for (int k = 0; k < 18; ++k) jc[k] = widen<A>(sJ[k * JS + jj]);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) jp[k] = widen<A>(sJ[(18 + k) * kTileEdges + jj]);
+        for (int k = 0; k < 6; ++k) jp[k] = widen<A>(sJ[(18 + k) * JS + jj]);
       }
-      const A wgt = d.w ? static_cast<A>(reinterpret_cast<const FP*>(st + L.w)[jj]) : A(1);
+      const A wgt = d.w ? static_cast<A>(sw[jj]) : A(1);
       const A* cv = camv + 9 * lc;
       A u0 = A(0), u1 = A(0), s0 = A(0), s1 = A(0);
 #pragma unroll
@@ -313,29 +338,34 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       A g[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) g[k] = jc[k] * q0 + jc[9 + k] * q1;
+      // contributions over this edge's own J column (thread j alone reads column j)
+#pragma unroll
+      for (int k = 0; k < 9; ++k) gs[k * GS + j] = g[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) gs[(9 + k) * GS + j] = jp[k] * q0 + jp[3 + k] * q1;
       {
         const uint32_t prev = __shfl_up_sync(0xffffffffu, lc, 1);
         const unsigned hm = __ballot_sync(0xffffffffu, valid && (lane == 0 || lc != prev));
         const unsigned vm = __ballot_sync(0xffffffffu, valid);
-        run_reduce9_store<A, FP>(g, lane, hm, vm, hm ? scpb[warp] : 0u, d.part);
-      }
-      if (valid) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) hstage[j * 3 + k] = jp[k] * q0 + jp[3 + k] * q1;
+        __syncwarp();
+        if (!(L.dbg & 1)) chunk_runs_smem<A, FP>(gs + 32 * warp, GS, lane, hm, vm, hm ? scpb[warp] : 0u, d.part);
       }
     }
     consumer_sync();
 
-    // ---- point epilogue: warps 0..7, thread = point (same partition as k_hvp_tiles)
-    if (tid < kTileThreads) {
+    // ---- point epilogue: one half of the consumers (alternating by tile), thread
+    // = point, the same partition as k_hvp_tiles. The other half goes straight
+    // on to the next tile's edge phase, so the epilogue overlaps it.
+    const uint32_t half = i & 1;
+    if ((static_cast<uint32_t>(tid) / kTileThreads) == half && !(L.dbg & 2)) {
       FP dot = FP(0);
-      const uint32_t pi = tid;
+      const uint32_t pi = tid - half * kTileThreads;
       if (pi < npt) {
         A acc[3] = {A(0), A(0), A(0)};
-        for (uint32_t q = spso[pi] - spso[0]; q < spso[pi + 1] - spso[0]; ++q) {
+        for (uint32_t q = spso[pi]; q < spso[pi + 1]; ++q) {
           const uint32_t sl = spsl[q];
 #pragma unroll
-          for (int k = 0; k < 3; ++k) acc[k] += hstage[sl * 3 + k];
+          for (int k = 0; k < 3; ++k) acc[k] += gs[(9 + k) * GS + sl];
         }
         const uint64_t col = pcol0 + 3ull * (pb + pi);
         const bool freev = scf[3 * pi];
@@ -352,17 +382,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         }
       }
       dot = warp_sum(dot);
-      if (lane == 0) d.tile_red[8ull * t + warp] = dot;
+      if (lane == 0) d.tile_red[8ull * t + (warp & 7)] = dot;
     }
-    consumer_sync();
-    if (tid == 0) mbar_arrive(&empty[s]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp no longer reads stage s
   }
 }
 
 // Per-tile camera copies for the pipelined HVP: tcv[tile_cam_off[t] + lc] =
-// vt of the tile's local camera lc (refreshed before every HVP), tcr = R, f
-// (refreshed after every linearization, factored store only). They make each
-// tile's camera data one contiguous bulk copy.
+// vt of the tile's local camera lc, refreshed before every HVP, so each
+// tile's camera data is one contiguous bulk copy.
 template <typename FP, typename SP>
 __global__ void k_tcam_vt(Dev<FP, SP> d) {
   if (!d.st->iter_active || d.st->pcg_done) return;
@@ -371,32 +400,51 @@ __global__ void k_tcam_vt(Dev<FP, SP> d) {
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     d.tcv[i] = d.vt[9ull * d.tile_cams[i / 9] + i % 9];
 }
+// Static per-tile aux blobs (once per activation): one CTA per normal tile.
 template <typename FP, typename SP>
-__global__ void k_tcam_rf(Dev<FP, SP> d, int force) {
-  if (!force && !d.st->do_linearize) return;
-  const uint64_t n = 10ull * d.ntcams;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    d.tcr[i] = d.Rf[10ull * d.tile_cams[i / 10] + i % 10];
+__global__ void k_tile_aux(Dev<FP, SP> d) {
+  const uint32_t i = blockIdx.x;
+  const uint32_t* m = d.tile_meta + static_cast<uint64_t>(kMCount) * i;
+  const uint32_t eb = m[kMEb], ne = m[kMNe], pb = m[kMPb], npt = m[kMNpt], ch0 = m[kMCh0];
+  const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad, nch = (ne + 31) / 32;
+  const AuxSec as = aux_sections(ne, npt);
+  unsigned char* a = d.tile_aux + 16ull * m[kMAux16];
+  uint16_t* lcam = reinterpret_cast<uint16_t*>(a + as.lcam);
+  uint16_t* lpt = reinterpret_cast<uint16_t*>(a + as.lpt);
+  uint16_t* psl = reinterpret_cast<uint16_t*>(a + as.psl);
+  uint16_t* pso = reinterpret_cast<uint16_t*>(a + as.pso);
+  uint32_t* cpb = reinterpret_cast<uint32_t*>(a + as.cpb);
+  uint8_t* cf = a + as.cf;
+  const uint32_t q0 = d.pt_slot_off[pb];
+  for (uint32_t k = threadIdx.x; k < ne8; k += blockDim.x) {
+    lcam[k] = d.d_lcam[eb + k];
+    lpt[k] = d.d_lpt[eb + k];
+  }
+  for (uint32_t k = threadIdx.x; k < ne; k += blockDim.x) psl[k] = d.pt_slots[q0 + k];
+  for (uint32_t k = threadIdx.x; k <= npt; k += blockDim.x) pso[k] = static_cast<uint16_t>(d.pt_slot_off[pb + k] - q0);
+  for (uint32_t k = threadIdx.x; k < nch; k += blockDim.x) cpb[k] = d.chunk_part_base[ch0 + k];
+  for (uint32_t k = threadIdx.x; k < 3 * npt; k += blockDim.x) cf[k] = d.col_free[9ull * d.nc + 3ull * pb + k];
 }
 
-// Tile records for the pipelined HVP producer, in normal-tile list order:
-// [t, ebeg, ecnt, pbeg, npt, cam_off, ncam, chunk_base, pt_slot_off[pbeg], 0, 0, 0]
+// Per-linearization lin blobs: point D, camera R f (factored store), Huber w.
 template <typename FP, typename SP>
-__global__ void k_tile_meta(Dev<FP, SP> d, uint32_t* meta) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n_normal; i += gridDim.x * blockDim.x) {
-    const uint32_t t = d.normal_tiles[i];
-    uint32_t* m = meta + 12ull * i;
-    m[0] = t;
-    m[1] = d.tile_ebeg[t];
-    m[2] = d.tile_ecnt[t];
-    m[3] = d.tile_pbeg[t];
-    m[4] = d.tile_pbeg[t + 1] - d.tile_pbeg[t];
-    m[5] = d.tile_cam_off[t];
-    m[6] = d.tile_cam_off[t + 1] - d.tile_cam_off[t];
-    m[7] = d.tile_chunk_base[t];
-    m[8] = d.pt_slot_off[d.tile_pbeg[t]];
-    m[9] = m[10] = m[11] = 0;
+__global__ void k_tile_lin(Dev<FP, SP> d, int force) {
+  if (!force && !d.st->do_linearize) return;
+  const uint32_t i = blockIdx.x;
+  const uint32_t* m = d.tile_meta + static_cast<uint64_t>(kMCount) * i;
+  const uint32_t eb = m[kMEb], ne = m[kMNe], pb = m[kMPb], npt = m[kMNpt], cb = m[kMCb], ncam = m[kMNcam];
+  const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad;
+  const LinSec ls = lin_sections<FP>(ne, npt, ncam, d.jfact != 0, d.w != nullptr);
+  unsigned char* l = d.tile_lin + 16ull * m[kMLin16];
+  FP* D = reinterpret_cast<FP*>(l + ls.D);
+  for (uint32_t k = threadIdx.x; k < 3 * npt; k += blockDim.x) D[k] = d.D[9ull * d.nc + 3ull * pb + k];
+  if (d.jfact) {
+    FP* cr = reinterpret_cast<FP*>(l + ls.cr);
+    for (uint32_t k = threadIdx.x; k < 10 * ncam; k += blockDim.x) cr[k] = d.Rf[10ull * d.tile_cams[cb + k / 10] + k % 10];
+  }
+  if (d.w) {
+    FP* w = reinterpret_cast<FP*>(l + ls.w);
+    for (uint32_t k = threadIdx.x; k < ne8; k += blockDim.x) w[k] = d.w[eb + k];
   }
 }
 

@@ -53,6 +53,7 @@ __host__ __device__ constexpr int p9(int i, int j) { return i <= j ? i * 9 - i *
 __host__ __device__ constexpr int p3(int i, int j) { return i <= j ? i * 3 - i * (i - 1) / 2 + (j - i) : j * 3 - j * (j - 1) / 2 + (i - j); }
 
 constexpr int kLinVals = 54;  // per camera run at linearize: b (9) + upper H (45)
+constexpr int kGsStride = kTileThreads + 4;  // row stride of the HVP camera-value staging (bank spread)
 constexpr int kCamWarps = 8;  // warps per block in camera kernels
 
 // Device-resident solver state (one per handle). Scalars are FP like the
@@ -96,10 +97,11 @@ struct Dev {
   FP* Rf;           // [nc][10] factored store: R (row-major 3x3) and f per camera
   int jfact;        // 1: factored J store (analytic mode, SP == FP), DESIGN.md §2
   // pipelined HVP (hvp_pipe.cuh): tile records and per-tile camera copies
-  const uint32_t* tile_meta;  // [n_normal][12]
+  const uint32_t* tile_meta;  // [n_normal][12] (hvp_pipe.cuh TileMeta)
   uint32_t ntcams;            // tile_cam_off[ntiles]
   arith_t<SP>* tcv;           // [ntcams][9]  D*p of each tile's cameras
-  FP* tcr;                    // [ntcams][10] R, f of each tile's cameras (factored store)
+  unsigned char* tile_aux;    // static per-tile blobs (hvp_pipe.cuh AuxSec)
+  unsigned char* tile_lin;    // per-linearization per-tile blobs (LinSec)
   FP* w;            // [na] or null (default loss: w == 1)
   const uint32_t* tile_ebeg;  // padded slot begin of each tile
   const uint32_t* tile_ecnt;  // real edges of each tile
@@ -319,6 +321,49 @@ __device__ inline void run_reduce9_store(const T (&g)[9], int lane, unsigned hea
     v += __shfl_xor_sync(full, v, 1);
     if (myslot >= 0) part[static_cast<uint64_t>(slot0 + r) * 9 + myslot] = static_cast<Out>(v);
     ++r;
+  }
+}
+
+// Camera-run sums of a warp chunk from shared memory: the chunk's 32 edges
+// have written their 9 camera values to gw[k * stride + lane]; lane o of the
+// warp produces output o = 9 r + k (run r, value k) as a sequential sum over
+// the run's edges, so the 9R outputs of a chunk with R runs are plain loads
+// and adds (no shuffle trees) and their slot writes are contiguous. Fixed
+// association order (deterministic). heads/vm: ballots of run heads / valid lanes.
+template <typename A, typename FP>
+__device__ inline void chunk_runs_smem(const A* gw, int stride, int lane, unsigned heads, unsigned vm,
+                                       uint32_t slot0, FP* part) {
+  const int R = __popc(heads);
+  const int end = 32 - __clz(vm);
+  // lane q holds start(q) = the q-th head (run q spans [start(q), start(q + 1)))
+  int my_start = end;
+  {
+    unsigned hs = heads;
+    for (int k = 0; hs; ++k) {
+      const int pos = __ffs(hs) - 1;
+      hs &= hs - 1;
+      if (lane == k) my_start = pos;
+    }
+  }
+  for (int base = 0; base < 9 * R; base += 32) {  // warp-uniform passes
+    const int o = base + lane;
+    const int r = min((o * 57) >> 9, 31);  // o / 9 for o < 512
+    const int k = o - 9 * r;
+    const int start = __shfl_sync(0xffffffffu, my_start, r);
+    const int nxt = __shfl_sync(0xffffffffu, my_start, min(r + 1, 31));
+    if (o >= 9 * R) continue;
+    const int stp = r + 1 < R ? nxt : end;
+    const A* src = gw + k * stride;
+    A a0 = A(0), a1 = A(0), a2 = A(0), a3 = A(0);
+    int e = start;
+    for (; e + 4 <= stp; e += 4) {
+      a0 += src[e];
+      a1 += src[e + 1];
+      a2 += src[e + 2];
+      a3 += src[e + 3];
+    }
+    for (; e < stp; ++e) a0 += src[e];
+    part[static_cast<uint64_t>(slot0 + r) * 9 + k] = static_cast<FP>((a0 + a1) + (a2 + a3));
   }
 }
 
@@ -994,6 +1039,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d,
   __shared__ A stage[kTileEdges * 3];
   __shared__ A hacc[3];
   __shared__ FP sX[DYN ? kTilePoints * 3 : 1];
+  __shared__ __align__(16) A gsh[9 * kGsStride];
   const int tid = threadIdx.x, lane = tid & 31;
   const uint64_t pcol0 = 9ull * d.nc;
   const uint32_t t = list ? list[blockIdx.x] : blockIdx.x;
@@ -1053,7 +1099,11 @@ __global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d,
       const uint32_t prev = __shfl_up_sync(0xffffffffu, cam, 1);
       const unsigned hm = __ballot_sync(0xffffffffu, valid && (lane == 0 || cam != prev));
       const unsigned vm = __ballot_sync(0xffffffffu, valid);
-      run_reduce9_store<A, FP>(g, lane, hm, vm, hm ? d.chunk_part_base[chunk] : 0u, d.part);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) gsh[k * kGsStride + tid] = g[k];
+      __syncwarp();
+      chunk_runs_smem<A, FP>(gsh + (tid & ~31), kGsStride, lane, hm, vm, hm ? d.chunk_part_base[chunk] : 0u, d.part);
+      __syncwarp();
     }
     A h[3];
 #pragma unroll

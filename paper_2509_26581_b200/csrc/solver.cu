@@ -949,22 +949,46 @@ class Solver final : public SolverBase {
     {
       int optin = 0;
       CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g_.device));
-      pipe_ = pipe_layout<FP, SP>(d.jfact ? kJFactRows : 24, d.w != nullptr, static_cast<uint32_t>(optin));
+      pipe_ = pipe_layout<FP, SP>(d.jfact ? kJFactRows : 24, d.w != nullptr, d.jfact != 0,
+                                  static_cast<uint32_t>(optin));
       pipe_ok_ = d.J != nullptr && pipe_.stages >= 2 && d.n_normal > 0;
       if (const char* e = std::getenv("GB_HVP_PIPE")) pipe_ok_ = pipe_ok_ && std::atoi(e) != 0;
+      if (const char* e = std::getenv("GB_PIPE_DBG")) pipe_.dbg = std::atoi(e);
       d.tile_meta = nullptr;
       d.tcv = nullptr;
-      d.tcr = nullptr;
+      d.tile_aux = nullptr;
+      d.tile_lin = nullptr;
       d.ntcams = act_.tile_cam_off.empty() ? 0 : act_.tile_cam_off.back();
       if (pipe_ok_) {
         CK(cudaFuncSetAttribute(k_hvp_pipe<FP, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(pipe_.total_bytes)));
-        uint32_t* meta = static_cast<uint32_t*>(b_tmeta_.alloc(12ull * d.n_normal * sizeof(uint32_t)));
-        k_tile_meta<FP, SP><<<grid_for(d.n_normal), 256, 0, s_>>>(d, meta);
-        CK(cudaGetLastError());
-        d.tile_meta = meta;
+        // tile records with the aux / lin blob offsets (16-byte units)
+        std::vector<uint32_t> meta(static_cast<size_t>(kMCount) * d.n_normal, 0);
+        uint64_t aux16 = 0, lin16 = 0;
+        for (uint32_t i = 0; i < d.n_normal; ++i) {
+          const uint32_t t = act_.normal_tiles[i];
+          uint32_t* m = &meta[static_cast<size_t>(kMCount) * i];
+          const uint32_t ne = act_.tile_ecnt[t], npt = act_.tile_pbeg[t + 1] - act_.tile_pbeg[t];
+          const uint32_t ncam = act_.tile_cam_off[t + 1] - act_.tile_cam_off[t];
+          m[kMT] = t;
+          m[kMEb] = act_.tile_ebeg[t];
+          m[kMNe] = ne;
+          m[kMPb] = act_.tile_pbeg[t];
+          m[kMNpt] = npt;
+          m[kMCb] = act_.tile_cam_off[t];
+          m[kMNcam] = ncam;
+          m[kMCh0] = act_.tile_chunk_base[t];
+          m[kMAux16] = static_cast<uint32_t>(aux16);
+          m[kMLin16] = static_cast<uint32_t>(lin16);
+          aux16 += aux_sections(ne, npt).bytes / 16;
+          lin16 += lin_sections<FP>(ne, npt, ncam, d.jfact != 0, d.w != nullptr).bytes / 16;
+        }
+        if (aux16 > 0xffffffffull || lin16 > 0xffffffffull) throw std::invalid_argument("tile blobs exceed 64 GB");
+        d.tile_meta = to_dev(b_tmeta_, meta);
+        d.tile_aux = static_cast<unsigned char*>(b_taux_.alloc(std::max<uint64_t>(16, 16 * aux16)));
+        d.tile_lin = static_cast<unsigned char*>(b_tlin_.alloc(std::max<uint64_t>(16, 16 * lin16)));
         d.tcv = static_cast<A*>(b_tcv_.alloc(std::max<uint64_t>(1, 9ull * d.ntcams) * sizeof(A)));
-        d.tcr = d.jfact ? static_cast<FP*>(b_tcr_.alloc(std::max<uint64_t>(1, 10ull * d.ntcams) * sizeof(FP))) : nullptr;
+        pipe_aux_pending_ = true;  // built once the remaining device arrays exist (below)
       }
     }
     d.part = static_cast<FP*>(b_part_.alloc(std::max<uint64_t>(1, act_.nparts) * kLinVals * sizeof(FP)));
@@ -1010,6 +1034,11 @@ class Solver final : public SolverBase {
     CK(cudaMemsetAsync(d.xs, 0, ncols_ * sizeof(SP), s_));
     CK(cudaMemsetAsync(d.p, 0, ncols_ * sizeof(SP), s_));
     b_ptstage_.alloc(std::max<uint64_t>(1, 3 * np) * sizeof(FP));
+    if (pipe_aux_pending_) {
+      k_tile_aux<FP, SP><<<d.n_normal, 256, 0, s_>>>(d);
+      CK(cudaGetLastError());
+      pipe_aux_pending_ = false;
+    }
   }
 
   // user AoS -> internal order on the device (cameras copied as is)
@@ -1142,8 +1171,8 @@ class Solver final : public SolverBase {
       k_lin_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, force, 2);
     }
     CK(cudaGetLastError());
-    if (pipe_ok_ && dev_.tcr) {
-      k_tcam_rf<FP, SP><<<grid_for(10ull * dev_.ntcams), 256, 0, s_>>>(dev_, force);
+    if (pipe_ok_) {
+      k_tile_lin<FP, SP><<<dev_.n_normal, 128, 0, s_>>>(dev_, force);
       CK(cudaGetLastError());
     }
   }
@@ -1351,7 +1380,8 @@ class Solver final : public SolverBase {
   PipeLayout pipe_{};
   bool pipe_ok_ = false;
   uint32_t sms_ = 148;
-  DBuf b_tmeta_, b_tcv_, b_tcr_;
+  DBuf b_tmeta_, b_tcv_, b_taux_, b_tlin_;
+  bool pipe_aux_pending_ = false;
   DBuf b_J_, b_Rf_, b_w_, b_part_, b_x_, b_xn_, b_b_, b_cl_, b_D_, b_dx_, b_Hc_, b_Hp_, b_Mc_, b_Mp_, b_xs_, b_r_, b_z_, b_p_,
       b_ap_, b_tr_, b_tr2_, b_tf_, b_cr_, b_cr2_, b_cf_, b_br_, b_br2_, b_bf_;
 };
