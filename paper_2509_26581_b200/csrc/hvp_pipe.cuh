@@ -69,7 +69,7 @@ __host__ __device__ inline LinSec lin_sections(uint32_t ne, uint32_t npt, uint32
 
 // byte offsets inside one stage (all 16-byte aligned)
 struct PipeLayout {
-  uint32_t hdr, J, aux, lin, p, camv;
+  uint32_t hdr, J, aux, lin, p, z, camv;
   uint32_t stage_bytes, fixed_bytes, total_bytes;
   int stages, rows;
   int dbg;  // experiments only (GB_PIPE_DBG): 1 skip camera reduction, 2 skip epilogue, 4 skip edge math,
@@ -94,6 +94,7 @@ inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_bud
   L.aux = take(aux_sections(kTileEdges, kTilePoints).bytes);
   L.lin = take(lin_sections<FP>(kTileEdges, kTilePoints, kTileCams, fact, huber).bytes);
   L.p = take(kTilePoints * 3 * sizeof(SP) + 32);
+  L.z = take(kTilePoints * 3 * sizeof(SP) + 32);
   L.camv = take(kTileCams * 9 * sizeof(A) + 32);
   L.stage_bytes = o;
   // after the stages: 2 mbarriers per stage, then (bf16 storage only) a
@@ -159,7 +160,7 @@ __device__ inline Span span16(const void* p, uint64_t bytes) {
   return Span{reinterpret_cast<const char*>(lo), static_cast<uint32_t>(hi - lo), static_cast<uint32_t>(a - lo)};
 }
 
-enum PipeHdr : int { kHT = 0, kHNe, kHNpt, kHNcam, kHDp, kHDcv, kHPb };
+enum PipeHdr : int { kHT = 0, kHNe, kHNpt, kHNcam, kHDp, kHDcv, kHPb, kHDz };
 
 template <typename FP, typename SP>
 __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, PipeLayout L) {
@@ -180,6 +181,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
   __syncthreads();
   const uint64_t pcol0 = 9ull * d.nc;
   const uint32_t ntiles = d.n_normal;
+  // p = z + beta p pending for this HVP's points (k_pcg_dir_rest did the rest)
+  const bool dir = d.st->dir_pending != 0;
+  const FP beta = d.st->beta;
 
   if (warp == kPipeConsumers / 32) {
     // ------------------------------------------------------------ producer
@@ -211,9 +215,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         const LinSec ls = lin_sections<FP>(ne, npt, ncam, d.jfact != 0, d.w != nullptr);
         const Span s_p = span16(d.p + pcol0 + 3ull * pb, sizeof(SP) * 3ull * npt);
         const Span s_cv = span16(d.tcv + 9ull * cb, sizeof(A) * 9ull * ncam);
+        const Span s_z = span16(d.z + pcol0 + 3ull * pb, sizeof(SP) * 3ull * npt);
         const bool small = !(L.dbg & 16);  // experiments: 16 = J rows only
         const uint32_t jrow = ne8 * static_cast<uint32_t>(sizeof(SP));
-        const uint32_t total = L.rows * jrow + (small ? as.bytes + ls.bytes + s_p.bytes + s_cv.bytes : 0u);
+        const uint32_t total =
+            L.rows * jrow + (small ? as.bytes + ls.bytes + s_p.bytes + s_cv.bytes + (dir ? s_z.bytes : 0u) : 0u);
         if (lane == 0) {
           uint32_t* h = reinterpret_cast<uint32_t*>(st + L.hdr);
           h[kHT] = t;
@@ -223,10 +229,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
           h[kHDp] = s_p.delta;
           h[kHDcv] = s_cv.delta;
           h[kHPb] = pb;
+          h[kHDz] = s_z.delta;
           mbar_arrive_expect_tx(&full[s], total);  // releases the header; completes when all bytes land
         }
         __syncwarp();
-        const int ncopies = L.rows + (small ? 4 : 0);
+        const int ncopies = L.rows + (small ? (dir ? 5 : 4) : 0);
         for (int q = lane; q < ncopies; q += 32) {
           if (q < L.rows) {
             bulk_g2s(st + L.J + static_cast<uint32_t>(q) * pipe_jstride<SP>(),
@@ -237,7 +244,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
             case 0: bulk_g2s(st + L.aux, d.tile_aux + 16 * aux16, as.bytes, &full[s]); break;
             case 1: bulk_g2s(st + L.lin, d.tile_lin + 16 * lin16, ls.bytes, &full[s]); break;
             case 2: bulk_g2s(st + L.p, s_p.src, s_p.bytes, &full[s]); break;
-            default: bulk_g2s(st + L.camv, s_cv.src, s_cv.bytes, &full[s]); break;
+            case 3: bulk_g2s(st + L.camv, s_cv.src, s_cv.bytes, &full[s]); break;
+            default: bulk_g2s(st + L.z, s_z.src, s_z.bytes, &full[s]); break;
           }
         }
       }
@@ -276,6 +284,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     const FP* camr = reinterpret_cast<const FP*>(lin + ls.cr);
     const FP* sw = reinterpret_cast<const FP*>(lin + ls.w);
     const SP* sp = reinterpret_cast<const SP*>(st + L.p + h[kHDp]);
+    const SP* sz = reinterpret_cast<const SP*>(st + L.z + h[kHDz]);
     const A* camv = reinterpret_cast<const A*>(st + L.camv + h[kHDcv]);
 
     // ---- edge phase: thread j = edge j of the tile
@@ -328,7 +337,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       }
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const A v = static_cast<A>(sD[3 * lp + k]) * widen<A>(sp[3 * lp + k]);  // == vt (k_pcg_dir)
+        const SP pn = dir ? pcg_dir_value<FP, SP>(sz[3 * lp + k], sp[3 * lp + k], beta) : sp[3 * lp + k];
+        const A v = static_cast<A>(sD[3 * lp + k]) * widen<A>(pn);  // == vt (k_pcg_dir)
         s0 += jp[k] * v;
         s1 += jp[3 + k] * v;
       }
@@ -373,7 +383,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         for (int k = 0; k < 3; ++k) {
           const FP Dk = sD[3 * pi + k];
           const A damp = before ? static_cast<A>(lam_fp * Dk * Dk) : lam;
-          const SP pk = sp[3 * pi + k];
+          const SP pk = dir ? pcg_dir_value<FP, SP>(sz[3 * pi + k], sp[3 * pi + k], beta) : sp[3 * pi + k];
+          if (dir) d.p[col + k] = pk;
           const A out = freev ? damp * widen<A>(pk) + static_cast<A>(Dk) * acc[k] : A(0);
           const SP o = narrow<SP>(out);
           d.ap[col + k] = o;

@@ -69,6 +69,7 @@ struct State {
   FP rho, pap, alpha, beta, rhs_norm, scale, unscale, ref_norm;
   double pcg_relres;
   int pcg_it, pcg_done, pcg_conv, pcg_zero;
+  int dir_pending;  // p = z + beta p still to be applied to normal-tile points (fused into k_hvp_pipe)
   // step / candidate
   FP pred, chi2_new;
   int step_finite;
@@ -102,6 +103,8 @@ struct Dev {
   arith_t<SP>* tcv;           // [ntcams][9]  D*p of each tile's cameras
   unsigned char* tile_aux;    // static per-tile blobs (hvp_pipe.cuh AuxSec)
   unsigned char* tile_lin;    // per-linearization per-tile blobs (LinSec)
+  const uint32_t* cam_tc_off;  // [nc+1] camera -> its tile-camera entries (tcv rows)
+  const uint32_t* cam_tc_idx;
   FP* w;            // [na] or null (default loss: w == 1)
   const uint32_t* tile_ebeg;  // padded slot begin of each tile
   const uint32_t* tile_ecnt;  // real edges of each tile
@@ -798,6 +801,7 @@ __global__ void k_iter_begin(State<FP>* st, gb_iteration_record* recs) {
   st->lambda_solve = st->lambda;
   st->pcg_done = 0;
   st->pcg_it = 0;
+  st->dir_pending = 0;
   st->pcg_conv = 0;
   st->pcg_zero = 0;
   st->pcg_relres = 0.0;
@@ -939,6 +943,22 @@ __device__ inline void apply_block(const FP* M, const SP* r, SP* z, FP* rz, FP* 
   }
 }
 
+// z = M r for one N-column block from register values of r (already
+// narrowed to SP and widened back, exactly what apply_block re-reads)
+template <typename FP, typename SP, int N>
+__device__ inline void apply_block_reg(const FP* M, const FP (&rv)[N], SP* z, FP* rz, FP* rr) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    FP acc = FP(0);
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc += M[i <= j ? i * N - i * (i - 1) / 2 + (j - i) : j * N - j * (j - 1) / 2 + (i - j)] * rv[j];
+    const SP zi = narrow<SP>(acc);
+    z[i] = zi;
+    *rz += rv[i] * widen<FP>(zi);
+    *rr += rv[i] * rv[i];
+  }
+}
+
 // =====================================================================
 // PCG (pcg_solve, pcg.hpp:34-105) on (D H D + damp) with block Jacobi.
 // =====================================================================
@@ -971,6 +991,30 @@ __global__ void k_rhs_norm(Dev<FP, SP> d) {
 }
 
 // r = narrow(rhs * scale), x = 0, z = M r, p = z, rho = r.z, res = |r|
+// r = narrow(rhs * scale), x = 0, z = M r, p = z, vt = D p for one vertex block
+template <typename FP, typename SP, int N>
+__device__ inline void pcg_init_block(const Dev<FP, SP>& d, uint64_t col, const FP* M, FP scale, FP* rz, FP* rr) {
+  using A = arith_t<SP>;
+  FP Dv[N], rv[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    Dv[k] = d.D[col + k];
+    const FP rhs = d.st->schur ? d.rc[col + k] : -Dv[k] * d.b[col + k];
+    const SP rn = narrow<SP>(rhs * scale);
+    d.r[col + k] = rn;
+    d.xs[col + k] = narrow<SP>(FP(0));
+    rv[k] = widen<FP>(rn);
+  }
+  SP zs[N];
+  apply_block_reg<FP, SP, N>(M, rv, zs, rz, rr);
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    d.z[col + k] = zs[k];
+    d.p[col + k] = zs[k];
+    d.vt[col + k] = static_cast<A>(Dv[k]) * widen<A>(zs[k]);
+  }
+}
+
 template <typename FP, typename SP>
 __global__ void k_pcg_init(Dev<FP, SP> d) {
   if (!d.st->iter_active) return;
@@ -981,26 +1025,15 @@ __global__ void k_pcg_init(Dev<FP, SP> d) {
   for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv;
        v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const bool cam = v < d.nc;
-    const int n = cam ? 9 : 3;
     const uint64_t col = cam ? 9 * v : 9ull * d.nc + 3 * (v - d.nc);
-    for (int k = 0; k < n; ++k) {
-      const FP rhs = d.st->schur ? d.rc[col + k] : -d.D[col + k] * d.b[col + k];
-      d.r[col + k] = narrow<SP>(rhs * scale);
-      d.xs[col + k] = narrow<SP>(FP(0));
-    }
     FP lrz = FP(0), lrr = FP(0);
     if (cam)
-      apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &lrz, &lrr);
+      pcg_init_block<FP, SP, 9>(d, col, d.Mc + 45 * v, scale, &lrz, &lrr);
     else
-      apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &lrz, &lrr);
+      pcg_init_block<FP, SP, 3>(d, col, d.Mp + 6 * (v - d.nc), scale, &lrz, &lrr);
     if (counted(d, col)) {
       rz += lrz;
       rr += lrr;
-    }
-    for (int k = 0; k < n; ++k) {
-      const SP zk = d.z[col + k];
-      d.p[col + k] = zk;
-      d.vt[col + k] = static_cast<arith_t<SP>>(d.D[col + k]) * widen<arith_t<SP>>(zk);
     }
   }
   rz = block_sum(rz, scratch);
@@ -1441,21 +1474,38 @@ __global__ void k_fin(Dev<FP, SP> d, int site) {
   }
 }
 
-// x += alpha p; r -= alpha Ap; z = M r for one vertex; rr, rz partials
+// x += alpha p; r -= alpha Ap; z = M r for one N-column vertex block, all
+// loads issued before any store (the vectors are distinct arrays)
+template <typename FP, typename SP, int N>
+__device__ inline void pcg_update_block(const Dev<FP, SP>& d, uint64_t col, const FP* M, FP alpha, FP* rz, FP* rr) {
+  SP xs[N], pv[N], rs[N], aps[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    xs[k] = d.xs[col + k];
+    pv[k] = d.p[col + k];
+    rs[k] = d.r[col + k];
+    aps[k] = d.ap[col + k];
+  }
+  FP rv[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    d.xs[col + k] = narrow<SP>(widen<FP>(xs[k]) + alpha * widen<FP>(pv[k]));
+    const SP rn = narrow<SP>(widen<FP>(rs[k]) - alpha * widen<FP>(aps[k]));
+    d.r[col + k] = rn;
+    rv[k] = widen<FP>(rn);
+  }
+  apply_block_reg<FP, SP, N>(M, rv, d.z + col, rz, rr);
+}
+
 template <typename FP, typename SP>
 __device__ inline void pcg_update_vertex(const Dev<FP, SP>& d, uint64_t v, FP alpha, FP* rz, FP* rr) {
   const bool cam = v < d.nc;
-  const int n = cam ? 9 : 3;
   const uint64_t col = cam ? 9 * v : 9ull * d.nc + 3 * (v - d.nc);
-  for (int k = 0; k < n; ++k) {
-    d.xs[col + k] = narrow<SP>(widen<FP>(d.xs[col + k]) + alpha * widen<FP>(d.p[col + k]));
-    d.r[col + k] = narrow<SP>(widen<FP>(d.r[col + k]) - alpha * widen<FP>(d.ap[col + k]));
-  }
   FP lrz = FP(0), lrr = FP(0);
   if (cam)
-    apply_block<FP, SP, 9>(d.Mc + 45 * v, d.r + col, d.z + col, &lrz, &lrr);
+    pcg_update_block<FP, SP, 9>(d, col, d.Mc + 45 * v, alpha, &lrz, &lrr);
   else
-    apply_block<FP, SP, 3>(d.Mp + 6 * (v - d.nc), d.r + col, d.z + col, &lrz, &lrr);
+    pcg_update_block<FP, SP, 3>(d, col, d.Mp + 6 * (v - d.nc), alpha, &lrz, &lrr);
   if (counted(d, col)) {
     *rz += lrz;
     *rr += lrr;
@@ -1468,6 +1518,7 @@ __global__ void k_pcg_update(Dev<FP, SP> d) {
   if (!d.st->iter_active || d.st->pcg_done) return;
   __shared__ FP scratch[32];
   const FP alpha = d.st->alpha;
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.st->dir_pending = 0;  // the HVP that consumed it has run
   FP rz = FP(0), rr = FP(0);
   const uint64_t nv = d.st->schur ? static_cast<uint64_t>(d.nc) : static_cast<uint64_t>(d.nc) + d.np;
   for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv;
@@ -1491,6 +1542,13 @@ __global__ void k_pcg_update(Dev<FP, SP> d) {
       }
     }
   }
+}
+
+// p = narrow(z + beta p) (pcg.hpp:358-361), explicitly rounded so every
+// kernel that applies it (k_pcg_dir, k_pcg_dir_rest, k_hvp_pipe) agrees bitwise
+template <typename FP, typename SP>
+__device__ inline SP pcg_dir_value(SP z, SP p, FP beta) {
+  return narrow<SP>(fma_rn(beta, widen<FP>(p), widen<FP>(z)));
 }
 
 // Fused PCG step for the single-GPU path (cooperative launch): update
@@ -1541,13 +1599,12 @@ __global__ void __launch_bounds__(256) k_pcg_step(Dev<FP, SP> d) {
   const FP beta = srz / rho;
   const uint64_t n = schur ? 9ull * d.nc : d.ncols;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
-    const SP pi = narrow<SP>(widen<FP>(d.z[i]) + beta * widen<FP>(d.p[i]));
+    const SP pi = pcg_dir_value<FP, SP>(d.z[i], d.p[i], beta);
     d.p[i] = pi;
     d.vt[i] = static_cast<A>(d.D[i]) * widen<A>(pi);
   }
 }
 
-// p = narrow(z + beta p) (pcg.hpp:358-361)
 template <typename FP, typename SP>
 __global__ void k_pcg_dir(Dev<FP, SP> d) {
   if (!d.st->iter_active || d.st->pcg_done) return;
@@ -1556,10 +1613,38 @@ __global__ void k_pcg_dir(Dev<FP, SP> d) {
   const uint64_t n = d.st->schur ? 9ull * d.nc : d.ncols;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const SP pi = narrow<SP>(widen<FP>(d.z[i]) + beta * widen<FP>(d.p[i]));
+    const SP pi = pcg_dir_value<FP, SP>(d.z[i], d.p[i], beta);
     d.p[i] = pi;
     d.vt[i] = static_cast<A>(d.D[i]) * widen<A>(pi);
   }
+}
+
+// k_pcg_dir for the columns the pipelined HVP does not update itself
+// (hvp_pipe.cuh applies p = z + beta p to normal-tile points on the fly):
+// cameras, with their per-tile copies tcv (cam_tc CSR), and the points of
+// heavy tiles (column ranges). Arms dir_pending for k_hvp_pipe.
+template <typename FP, typename SP>
+__global__ void k_pcg_dir_rest(Dev<FP, SP> d, const uint64_t* rbeg, const uint64_t* rend, int nranges) {
+  if (!d.st->iter_active || d.st->pcg_done) return;
+  using A = arith_t<SP>;
+  const FP beta = d.st->beta;
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.st->dir_pending = 1;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t t0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  for (uint64_t i = t0; i < 9ull * d.nc; i += stride) {
+    const SP pi = pcg_dir_value<FP, SP>(d.z[i], d.p[i], beta);
+    d.p[i] = pi;
+    const A v = static_cast<A>(d.D[i]) * widen<A>(pi);
+    d.vt[i] = v;
+    const uint64_t c = i / 9, k = i % 9;
+    for (uint32_t q = d.cam_tc_off[c]; q < d.cam_tc_off[c + 1]; ++q) d.tcv[9ull * d.cam_tc_idx[q] + k] = v;
+  }
+  for (int r = 0; r < nranges; ++r)
+    for (uint64_t i = rbeg[r] + t0; i < rend[r]; i += stride) {
+      const SP pi = pcg_dir_value<FP, SP>(d.z[i], d.p[i], beta);
+      d.p[i] = pi;
+      d.vt[i] = static_cast<A>(d.D[i]) * widen<A>(pi);
+    }
 }
 
 // Unscale, predicted decrease, dx = D x, candidate x_new = x + dx

@@ -1035,6 +1035,44 @@ class Solver final : public SolverBase {
     CK(cudaMemsetAsync(d.p, 0, ncols_ * sizeof(SP), s_));
     b_ptstage_.alloc(std::max<uint64_t>(1, 3 * np) * sizeof(FP));
     if (pipe_aux_pending_) {
+      // camera -> tile-camera entries (stable by entry index) for k_pcg_dir_rest's tcv scatter
+      {
+        using namespace actdev;
+        const uint64_t nt = d.ntcams;
+        DBuf s_keys, s_vals, s_keys2, s_cnt;
+        uint32_t* vals = scratch<uint32_t>(s_vals, nt);
+        uint32_t* keys2 = scratch<uint32_t>(s_keys2, nt);
+        uint32_t* idx = static_cast<uint32_t*>(b_camtc_idx_.alloc(std::max<uint64_t>(1, nt) * sizeof(uint32_t)));
+        k_iota<<<grid_for(nt), 256, 0, s_>>>(nt, vals);
+        cub_sort<uint32_t>(d.tile_cams, keys2, vals, idx, nt, bits_for(nc));
+        uint32_t* cnt = scratch<uint32_t>(s_cnt, nc + 1);
+        CK(cudaMemsetAsync(cnt, 0, (nc + 1) * sizeof(uint32_t), s_));
+        k_hist<<<grid_for(nt), 256, 0, s_>>>(nt, d.tile_cams, cnt);
+        uint32_t* off = static_cast<uint32_t*>(b_camtc_off_.alloc((nc + 1) * sizeof(uint32_t)));
+        cub_scan_excl(cnt, off, nc + 1);
+        d.cam_tc_off = off;
+        d.cam_tc_idx = idx;
+        CK(cudaStreamSynchronize(s_));
+      }
+      // point columns of heavy tiles (k_pcg_dir_rest applies p = z + beta p there)
+      {
+        std::vector<uint64_t> rb, re;
+        for (uint32_t t : act_.heavy_tiles) {
+          const uint64_t c0 = 9ull * nc + 3ull * act_.tile_pbeg[t], c1 = 9ull * nc + 3ull * act_.tile_pbeg[t + 1];
+          if (!re.empty() && re.back() == c0)
+            re.back() = c1;
+          else {
+            rb.push_back(c0);
+            re.push_back(c1);
+          }
+        }
+        dir_nranges_ = static_cast<int>(rb.size());
+        dir_rbeg_ = to_dev(b_dir_rb_, rb);
+        dir_rend_ = to_dev(b_dir_re_, re);
+        uint64_t work = 9ull * nc;
+        for (size_t r = 0; r < rb.size(); ++r) work += re[r] - rb[r];
+        dir_rest_grid_ = grid_for(work);
+      }
       k_tile_aux<FP, SP><<<d.n_normal, 256, 0, s_>>>(d);
       CK(cudaGetLastError());
       pipe_aux_pending_ = false;
@@ -1129,7 +1167,9 @@ class Solver final : public SolverBase {
 
   // ------------------------------------------------------------- launches
   // one vertex per thread (memory-level parallelism beats grid-stride reuse here)
-  unsigned vert_grid() const { return std::max(1u, div_up(static_cast<uint64_t>(act_.nc) + act_.np, 256)); }
+  unsigned vert_grid() const {
+    return std::max(1u, std::min(div_up(static_cast<uint64_t>(act_.nc) + act_.np, 256), sms_ * 6u));
+  }
   unsigned col_grid() const { return std::max(1u, std::min(div_up(ncols_, 256), 148u * 8u)); }
   unsigned cam_grid() const { return std::max(1u, div_up(act_.nc, kCamWarps)); }
 
@@ -1178,11 +1218,11 @@ class Solver final : public SolverBase {
   }
 
   // HVP tile pass (dynamic mode recomputes J per edge).
-  void launch_hvp_tiles(const Dev<FP, SP>& d) {
+  void launch_hvp_tiles(const Dev<FP, SP>& d, bool tcv_ready = false) {
     if (!d.J) {
       k_hvp_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(d, nullptr);
     } else if (pipe_ok_) {  // normal tiles through the bulk-copy pipeline, heavy tiles one CTA each
-      k_tcam_vt<FP, SP><<<grid_for(9ull * d.ntcams), 256, 0, s_>>>(d);
+      if (!tcv_ready) k_tcam_vt<FP, SP><<<grid_for(9ull * d.ntcams), 256, 0, s_>>>(d);
       k_hvp_pipe<FP, SP><<<std::min<uint32_t>(d.n_normal, sms_), kPipeThreads, pipe_.total_bytes, s_>>>(d, pipe_);
       if (d.n_heavy) k_hvp_tiles<FP, SP, false, 1><<<d.n_heavy, kTileThreads, 0, s_>>>(d, d.heavy_tiles);
     } else if (hvp_minb_ == 4) {
@@ -1193,8 +1233,8 @@ class Solver final : public SolverBase {
     CK(cudaGetLastError());
   }
 
-  void launch_hvp(const Dev<FP, SP>& d) {
-    launch_hvp_tiles(d);
+  void launch_hvp(const Dev<FP, SP>& d, bool tcv_ready = false) {
+    launch_hvp_tiles(d, tcv_ready);
     if (!dist()) {
       k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 0);
     } else {
@@ -1267,8 +1307,9 @@ class Solver final : public SolverBase {
       allreduce(red_s() + kRedInitRz, 2);
       fin(2);
     }
+    const bool dir_fused = pipe_ok_ && !(!dist() && fused_pcg_);
     for (int k = 0; k < pcg_max_it; ++k) {
-      launch_hvp(dev_);
+      launch_hvp(dev_, dir_fused && k > 0);  // after k_pcg_dir_rest the per-tile camera copies are current
       if (!dist() && fused_pcg_) {
         launch_pcg_step();
         continue;
@@ -1279,7 +1320,10 @@ class Solver final : public SolverBase {
         allreduce(red_s() + kRedUpdRz, 2);
         fin(3);
       }
-      k_pcg_dir<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
+      if (dir_fused)  // normal-tile points get p = z + beta p inside the next k_hvp_pipe
+        k_pcg_dir_rest<FP, SP><<<dir_rest_grid_, 256, 0, s_>>>(dev_, dir_rbeg_, dir_rend_, dir_nranges_);
+      else
+        k_pcg_dir<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
       CK(cudaGetLastError());
     }
     k_step<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
@@ -1382,6 +1426,11 @@ class Solver final : public SolverBase {
   uint32_t sms_ = 148;
   DBuf b_tmeta_, b_tcv_, b_taux_, b_tlin_;
   bool pipe_aux_pending_ = false;
+  DBuf b_camtc_idx_, b_camtc_off_, b_dir_rb_, b_dir_re_;
+  const uint64_t* dir_rbeg_ = nullptr;
+  const uint64_t* dir_rend_ = nullptr;
+  int dir_nranges_ = 0;
+  unsigned dir_rest_grid_ = 1;
   DBuf b_J_, b_Rf_, b_w_, b_part_, b_x_, b_xn_, b_b_, b_cl_, b_D_, b_dx_, b_Hc_, b_Hp_, b_Mc_, b_Mp_, b_xs_, b_r_, b_z_, b_p_,
       b_ap_, b_tr_, b_tr2_, b_tf_, b_cr_, b_cr2_, b_cf_, b_br_, b_br2_, b_bf_;
 };
