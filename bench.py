@@ -225,6 +225,8 @@ def ours(args, shape, desc):
     # live roofline of the dominant kernel pair (HVP) on the solver stream
     ms_hvp, ms_tiles = ctypes.c_double(), ctypes.c_double()
     L.check(L.fn("time_hvp")(g._h, 20, ctypes.byref(ms_hvp), ctypes.byref(ms_tiles)))
+    kbytes, rbytes = ctypes.c_double(), ctypes.c_double()
+    L.check(L.fn("hvp_bytes")(g._h, ctypes.byref(kbytes), ctypes.byref(rbytes)))
 
     ms = ms_total / K
     if world > 1:
@@ -259,9 +261,10 @@ def ours(args, shape, desc):
         return
     sJ, sV, sA, sFP = SIZES[args.precision]
     E, N = rep.active_factors, rep.free_dims
-    hvp_bytes = E * (24 * sJ + 8) + N * (sV + sA)  # SURVEY.md §8(d) HVP algorithmic bytes
+    hvp_bytes = rbytes.value  # SURVEY.md §8(d) HVP algorithmic bytes: E (24 s_J + 8) + N (s_V + s_A)
     peak, peak_kind = measured_peak()
     achieved = hvp_bytes / (ms_hvp.value * 1e-3) / 1e9
+    kernel_gbs = kbytes.value / (ms_hvp.value * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_hvp_summary.json")
     if os.path.exists(prof):
@@ -270,7 +273,9 @@ def ours(args, shape, desc):
                 traffic = json.load(f).get("dram_bytes_per_hvp")
         except Exception:
             traffic = None
-    launches_per_it = 10 + 4 * cfg.pcg.max_iterations
+    # per LM iteration: iter_begin, precond, rhs_norm, pcg_init, tcam (first HVP), step, chi2, decide, commit,
+    # lin tiles (+heavy), lin_cams, tile_lin; per PCG iteration: hvp_pipe, hvp_cams, pcg_update, pcg_dir_rest
+    launches_per_it = 12 + 4 * cfg.pcg.max_iterations
     if world > 1:  # split camera kernels + finalize kernels
         launches_per_it += 1 + 2 * cfg.pcg.max_iterations + 5 + 2
     line = {
@@ -279,7 +284,7 @@ def ours(args, shape, desc):
         "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision], "data": "synthetic",
         "config": {"workload": desc + f" {args.precision} analytic, PCG<=10@1e-6" +
                    ("" if args.solver == "pcg" else f", {args.solver} linear solver"), "precision": args.precision,
-                   "cache": "inputs larger than L2 (J store %.2f GB)" % (E * 24 * sJ / 1e9),
+                   "cache": "inputs larger than L2 (HVP moves %.2f GB per launch, L2 126 MB)" % (kbytes.value / 1e9),
                    "parallelism": "single GPU" if world == 1 else
                    f"{world} GPUs: point-tile shards, replicated cameras, NCCL allreduce per PCG iteration"},
         "clocks": clocks.summary(),
@@ -288,10 +293,17 @@ def ours(args, shape, desc):
                 "note": "public API: build_graph + levenberg_marquardt from host arrays, incl. upload, activation, "
                         f"initial linearize and write-back, amortized over {n_it} iterations"},
         "gpu_launches": launches_per_it * K,
-        "roofline": {"kernel": "k_hvp_tiles+k_hvp_cams (HVP, one PCG iteration's dominant pair)", "bound": "hbm",
+        "roofline": {"kernel": "k_hvp_pipe (+k_tcam_vt, k_hvp_tiles for heavy tiles) + k_hvp_cams: the HVP of one "
+                               "PCG iteration", "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "algorithmic_bytes": int(hvp_bytes), "ms_per_launch": round(ms_hvp.value, 4),
-                     "ms_tiles_only": round(ms_tiles.value, 4), "peak_kind": peak_kind},
+                     "ms_tiles_only": round(ms_tiles.value, 4), "peak_kind": peak_kind,
+                     "kernel_bytes": int(kbytes.value), "kernel_gbs": round(kernel_gbs, 1),
+                     "kernel_frac": round(kernel_gbs / peak, 4),
+                     "note": "achieved/frac: SURVEY §8(d) reference-layout bytes (24 J values per edge) / time; "
+                             "kernel_*: the bytes this path actually moves (factored 16-value J store, per-tile "
+                             "blobs, partial slots; gb_hvp_bytes) / time; traffic: ncu dram bytes of one tile "
+                             "launch (profiles/ncu_hvp_summary.json)"},
         "solve": {"iterations": rep.iterations_run, "accepted": rep.accepted_steps,
                   "initial_chi2": rep.initial_chi2, "chi2_after_timed": rep.final_chi2,
                   "setup_seconds": round(rep0.setup_seconds, 3), "e2e_solve_seconds": round(e2e_s, 3),

@@ -215,6 +215,11 @@ int gb_step(gb_graph* g, int32_t n);
 int gb_end(gb_graph* g, gb_solve_report* report, gb_iteration_record* records, int32_t max_records);
 void* gb_stream(gb_graph* g);
 int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_per_hvp, double* ms_tiles_only);
+/* gb_hvp_bytes  bytes one HVP timed by gb_time_hvp moves on the configured
+ *              path (factored J store, per-tile blobs, partial slots), and the
+ *              reference-layout figure E (24 s_J + 8) + N (s_V + s_A) of
+ *              SURVEY.md §8(d) (the roofline's "algorithmic bytes"). */
+int gb_hvp_bytes(gb_graph* g, double* kernel_bytes, double* reference_bytes);
 
 /* ---- multi-GPU sharding (no reference counterpart: the reference is a
  * single-process CPU solver) -------------------------------

@@ -70,6 +70,7 @@ class SolverBase {
   virtual void end(gb_solve_report* rep, gb_iteration_record* recs, int max_recs) = 0;
   virtual void* stream() = 0;
   virtual void time_hvp(int reps, double* ms_pair, double* ms_tiles) = 0;
+  virtual void hvp_bytes(double* kernel_bytes, double* reference_bytes) = 0;
   virtual double residual_sum(int level, bool raw) = 0;
   virtual void ls_linearize(int level, double cmin, double cmax, int damping, double* chi2, int64_t* n, void* b,
                             void* diag, void* clamped, void* scaling, int32_t* finite) = 0;
@@ -360,6 +361,40 @@ class Solver final : public SolverBase {
 
   // Average device time of the HVP kernel pair (and of the tile kernel alone)
   // at the current linearization; the device State is saved and restored.
+  // Bytes one HVP (as timed by time_hvp: tile pass + camera pass) must move
+  // on the configured path, and the SURVEY.md §8(d) reference-layout figure
+  // E (24 s_J + 8) + N (s_V + s_A) for comparison.
+  void hvp_bytes(double* kernel_bytes, double* reference_bytes) override {
+    if (!have_act_) throw std::logic_error("gb_hvp_bytes before any solve");
+    const double sJ = sizeof(SP), sV = sizeof(SP), sA = sizeof(A), sF = sizeof(FP);
+    const double E = static_cast<double>(act_.n_active), ns = static_cast<double>(act_.n_slots);
+    const double N = static_cast<double>(act_.free_dims);
+    const double np3 = 3.0 * act_.np, nc9 = 9.0 * act_.nc, nparts = static_cast<double>(act_.nparts);
+    if (reference_bytes) *reference_bytes = E * (24 * sJ + 8) + N * (sV + sA);
+    double b = 0;
+    const Dev<FP, SP>& d = dev_;
+    if (pipe_ok_) {
+      double aux = 0, lin = 0;
+      for (uint32_t t : act_.normal_tiles) {
+        const uint32_t ne = act_.tile_ecnt[t], npt = act_.tile_pbeg[t + 1] - act_.tile_pbeg[t];
+        const uint32_t ncam = act_.tile_cam_off[t + 1] - act_.tile_cam_off[t];
+        aux += aux_sections(ne, npt).bytes;
+        lin += lin_sections<FP>(ne, npt, ncam, d.jfact != 0, d.w != nullptr).bytes;
+      }
+      const double rows = d.jfact ? kJFactRows : 24;
+      b += rows * sJ * ns + aux + lin;                 // J rows, static and per-linearization tile blobs
+      b += np3 * (sV + sV);                            // p in, ap out
+      b += d.ntcams * (9.0 * sA * 2 + 4.0);            // tcv gather (tile_cams, write) + tile read
+    } else {
+      b += (d.J ? 24 * sJ * ns : 0) + ns * (4 + 2);    // J, camera and point indices
+      b += np3 * (sA + sV + sF + sV + 1);              // vt, p, D in; ap out; free mask
+      b += act_.np * 4.0 + ns * 2;                     // point slot lists
+    }
+    b += nparts * 9 * sF * 2 + nparts * 4;             // camera partial slots: write, read (+ index)
+    b += nc9 * (sV + sF + sV);                         // camera p, D in; ap out
+    if (kernel_bytes) *kernel_bytes = b;
+  }
+
   void time_hvp(int reps, double* ms_pair, double* ms_tiles) override {
     if (in_solve_) throw std::logic_error("gb_time_hvp during a solve");
     if (!have_act_) throw std::logic_error("gb_time_hvp before any solve");
@@ -1627,6 +1662,10 @@ void* gb_stream(gb_graph* g) {
 
 int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_pair, double* ms_tiles) {
   return guarded([&] { g->get().time_hvp(reps < 1 ? 1 : reps, ms_pair, ms_tiles); });
+}
+
+int gb_hvp_bytes(gb_graph* g, double* kernel_bytes, double* reference_bytes) {
+  return guarded([&] { g->get().hvp_bytes(kernel_bytes, reference_bytes); });
 }
 
 int gb_nccl_unique_id(void* out128) {

@@ -25,7 +25,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__grid_size",
         "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
-        "sm__cycles_elapsed.avg.per_second"]
+        "sm__cycles_elapsed.avg.per_second", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 
 
 def launches(path, tag):
@@ -83,15 +84,16 @@ def main():
     ap.add_argument("--full")
     ap.add_argument("--full-lin")
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--hvp-label", default="hvp_pipe")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
         launches(a.launches, a.tag)
     if a.full:
-        traffic, kname = full(a.full, a.tag, "hvp_tiles")
+        traffic, kname = full(a.full, a.tag, a.hvp_label)
         with open(os.path.join(PROF, "ncu_hvp_summary.json"), "w") as f:
             json.dump({"kernel": kname, "dram_bytes_per_hvp": traffic, "source": os.path.basename(a.full),
-                       "tag": a.tag, "note": "dram__bytes_read.sum + dram__bytes_write.sum of one k_hvp_tiles launch"},
+                       "tag": a.tag, "note": "dram__bytes_read.sum + dram__bytes_write.sum of one HVP tile-kernel launch"},
                       f, indent=1)
     if a.full_lin:
         full(a.full_lin, a.tag, "lin_normal")
