@@ -30,6 +30,13 @@ constexpr int kPipeMaxStages = 4;
 
 __host__ __device__ constexpr uint32_t r16(uint64_t b) { return static_cast<uint32_t>((b + 15) / 16 * 16); }
 
+// per-camera record strides (elements) of the tile camera copies: 9 D*p values
+// (tcv) and R, f (lin blob), padded to 16-byte records for vector loads
+template <typename T>
+__host__ __device__ constexpr int cam_stride() {
+  return sizeof(T) == 8 ? 10 : 12;
+}
+
 // byte stride of one J row (and of one contribution row) in shared memory
 template <typename T>
 __host__ __device__ constexpr uint32_t pipe_jstride() {
@@ -62,7 +69,7 @@ __host__ __device__ inline LinSec lin_sections(uint32_t ne, uint32_t npt, uint32
   LinSec l;
   l.D = 0;
   l.cr = l.D + r16(sizeof(FP) * 3ull * npt);
-  l.w = l.cr + (fact ? r16(sizeof(FP) * 10ull * ncam) : 0u);
+  l.w = l.cr + (fact ? r16(sizeof(FP) * static_cast<uint64_t>(cam_stride<FP>()) * ncam) : 0u);
   l.bytes = l.w + (huber ? r16(sizeof(FP) * 1ull * ne8) : 0u);
   return l;
 }
@@ -95,7 +102,7 @@ inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_bud
   L.lin = take(lin_sections<FP>(kTileEdges, kTilePoints, kTileCams, fact, huber).bytes);
   L.p = take(kTilePoints * 3 * sizeof(SP) + 32);
   L.z = take(kTilePoints * 3 * sizeof(SP) + 32);
-  L.camv = take(kTileCams * 9 * sizeof(A) + 32);
+  L.camv = take(kTileCams * cam_stride<A>() * sizeof(A) + 32);
   L.stage_bytes = o;
   // after the stages: 2 mbarriers per stage, then (bf16 storage only) a
   // separate 12-row staging for the camera / point contributions
@@ -109,6 +116,18 @@ inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_bud
 
 // tile record, one per normal tile (list order)
 enum TileMeta : int { kMT = 0, kMEb, kMNe, kMPb, kMNpt, kMCb, kMNcam, kMCh0, kMAux16, kMLin16, kMCount = 12 };
+
+// N contiguous T from 16-byte aligned shared memory in 16-byte loads
+template <typename T, int N>
+__device__ inline void load16(const T* src, T (&out)[N]) {
+  static_assert((N * sizeof(T)) % 16 == 0, "16-byte records");
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int i = 0; i < static_cast<int>(N * sizeof(T) / 16); ++i) {
+    const uint4 v = s4[i];
+    memcpy(reinterpret_cast<char*>(out) + 16 * i, &v, 16);
+  }
+}
 
 // ---- PTX helpers: mbarrier + 1-D bulk async copy global -> shared
 __device__ inline uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -214,7 +233,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         const AuxSec as = aux_sections(ne, npt);
         const LinSec ls = lin_sections<FP>(ne, npt, ncam, d.jfact != 0, d.w != nullptr);
         const Span s_p = span16(d.p + pcol0 + 3ull * pb, sizeof(SP) * 3ull * npt);
-        const Span s_cv = span16(d.tcv + 9ull * cb, sizeof(A) * 9ull * ncam);
+        const Span s_cv = span16(d.tcv + static_cast<uint64_t>(cam_stride<A>()) * cb,
+                                 sizeof(A) * static_cast<uint64_t>(cam_stride<A>()) * ncam);
         const Span s_z = span16(d.z + pcol0 + 3ull * pb, sizeof(SP) * 3ull * npt);
         const bool small = !(L.dbg & 16);  // experiments: 16 = J rows only
         const uint32_t jrow = ne8 * static_cast<uint32_t>(sizeof(SP));
@@ -307,7 +327,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
           for (int k = 0; k < 6; ++k) U[k] = sJ[(6 + k) * JS + jj];
           const FP dist = sJ[12 * JS + jj], n = sJ[13 * JS + jj];
           const FP p0 = sJ[14 * JS + jj], p1 = sJ[15 * JS + jj];
-          const FP* rf = camr + 10 * lc;
+          FP rf[cam_stride<FP>()];
+          load16<FP, cam_stride<FP>()>(camr + cam_stride<FP>() * lc, rf);
 #pragma unroll
           for (int k = 0; k < 9; ++k) R[k] = rf[k];
 #pragma unroll
@@ -327,7 +348,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         for (int k = 0; k < 6; ++k) jp[k] = widen<A>(sJ[(18 + k) * JS + jj]);
       }
       const A wgt = d.w ? static_cast<A>(sw[jj]) : A(1);
-      const A* cv = camv + 9 * lc;
+      A cv[cam_stride<A>()];
+      load16<A, cam_stride<A>()>(camv + cam_stride<A>() * lc, cv);
       A u0 = A(0), u1 = A(0), s0 = A(0), s1 = A(0);
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
@@ -406,10 +428,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
 template <typename FP, typename SP>
 __global__ void k_tcam_vt(Dev<FP, SP> d) {
   if (!d.st->iter_active || d.st->pcg_done) return;
-  const uint64_t n = 9ull * d.ntcams;
+  constexpr int CS = cam_stride<arith_t<SP>>();
+  const uint64_t n = static_cast<uint64_t>(CS) * d.ntcams;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    d.tcv[i] = d.vt[9ull * d.tile_cams[i / 9] + i % 9];
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = i % CS;
+    d.tcv[i] = k < 9 ? d.vt[9ull * d.tile_cams[i / CS] + k] : arith_t<SP>(0);
+  }
 }
 // Static per-tile aux blobs (once per activation): one CTA per normal tile.
 template <typename FP, typename SP>
@@ -451,7 +476,9 @@ __global__ void k_tile_lin(Dev<FP, SP> d, int force) {
   for (uint32_t k = threadIdx.x; k < 3 * npt; k += blockDim.x) D[k] = d.D[9ull * d.nc + 3ull * pb + k];
   if (d.jfact) {
     FP* cr = reinterpret_cast<FP*>(l + ls.cr);
-    for (uint32_t k = threadIdx.x; k < 10 * ncam; k += blockDim.x) cr[k] = d.Rf[10ull * d.tile_cams[cb + k / 10] + k % 10];
+    constexpr int CS = cam_stride<FP>();
+    for (uint32_t k = threadIdx.x; k < CS * ncam; k += blockDim.x)
+      cr[k] = k % CS < 10 ? d.Rf[10ull * d.tile_cams[cb + k / CS] + k % CS] : FP(0);
   }
   if (d.w) {
     FP* w = reinterpret_cast<FP*>(l + ls.w);

@@ -1637,7 +1637,8 @@ __global__ void k_pcg_dir_rest(Dev<FP, SP> d, const uint64_t* rbeg, const uint64
     const A v = static_cast<A>(d.D[i]) * widen<A>(pi);
     d.vt[i] = v;
     const uint64_t c = i / 9, k = i % 9;
-    for (uint32_t q = d.cam_tc_off[c]; q < d.cam_tc_off[c + 1]; ++q) d.tcv[9ull * d.cam_tc_idx[q] + k] = v;
+    for (uint32_t q = d.cam_tc_off[c]; q < d.cam_tc_off[c + 1]; ++q)
+      d.tcv[static_cast<uint64_t>(sizeof(A) == 8 ? 10 : 12) * d.cam_tc_idx[q] + k] = v;  // hvp_pipe.cuh cam_stride
   }
   for (int r = 0; r < nranges; ++r)
     for (uint64_t i = rbeg[r] + t0; i < rend[r]; i += stride) {

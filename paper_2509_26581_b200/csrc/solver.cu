@@ -384,7 +384,7 @@ class Solver final : public SolverBase {
       const double rows = d.jfact ? kJFactRows : 24;
       b += rows * sJ * ns + aux + lin;                 // J rows, static and per-linearization tile blobs
       b += np3 * (sV + sV);                            // p in, ap out
-      b += d.ntcams * (9.0 * sA * 2 + 4.0);            // tcv gather (tile_cams, write) + tile read
+      b += d.ntcams * (cam_stride<A>() * sA * 2 + 4.0);  // tcv gather (tile_cams, write) + tile read
     } else {
       b += (d.J ? 24 * sJ * ns : 0) + ns * (4 + 2);    // J, camera and point indices
       b += np3 * (sA + sV + sF + sV + 1);              // vt, p, D in; ap out; free mask
@@ -1022,7 +1022,8 @@ class Solver final : public SolverBase {
         d.tile_meta = to_dev(b_tmeta_, meta);
         d.tile_aux = static_cast<unsigned char*>(b_taux_.alloc(std::max<uint64_t>(16, 16 * aux16)));
         d.tile_lin = static_cast<unsigned char*>(b_tlin_.alloc(std::max<uint64_t>(16, 16 * lin16)));
-        d.tcv = static_cast<A*>(b_tcv_.alloc(std::max<uint64_t>(1, 9ull * d.ntcams) * sizeof(A)));
+        d.tcv = static_cast<A*>(b_tcv_.alloc(std::max<uint64_t>(1, cam_stride<A>() * uint64_t(d.ntcams)) * sizeof(A)));
+        CK(cudaMemsetAsync(d.tcv, 0, std::max<uint64_t>(1, cam_stride<A>() * uint64_t(d.ntcams)) * sizeof(A), s_));
         pipe_aux_pending_ = true;  // built once the remaining device arrays exist (below)
       }
     }
@@ -1257,7 +1258,7 @@ class Solver final : public SolverBase {
     if (!d.J) {
       k_hvp_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(d, nullptr);
     } else if (pipe_ok_) {  // normal tiles through the bulk-copy pipeline, heavy tiles one CTA each
-      if (!tcv_ready) k_tcam_vt<FP, SP><<<grid_for(9ull * d.ntcams), 256, 0, s_>>>(d);
+      if (!tcv_ready) k_tcam_vt<FP, SP><<<grid_for(cam_stride<A>() * uint64_t(d.ntcams)), 256, 0, s_>>>(d);
       k_hvp_pipe<FP, SP><<<std::min<uint32_t>(d.n_normal, sms_), kPipeThreads, pipe_.total_bytes, s_>>>(d, pipe_);
       if (d.n_heavy) k_hvp_tiles<FP, SP, false, 1><<<d.n_heavy, kTileThreads, 0, s_>>>(d, d.heavy_tiles);
     } else if (hvp_minb_ == 4) {
