@@ -25,7 +25,7 @@
 namespace gb {
 
 constexpr int kPipeConsumers = kTileEdges;          // one consumer thread per edge of a normal tile
-constexpr int kPipeThreads = kPipeConsumers + 32;   // + one producer warp
+constexpr int kPipeThreads = kPipeConsumers + 64;   // + one producer (copy) warp + one preparer warp
 constexpr int kPipeMaxStages = 4;
 
 __host__ __device__ constexpr uint32_t r16(uint64_t b) { return static_cast<uint32_t>((b + 15) / 16 * 16); }
@@ -76,7 +76,7 @@ __host__ __device__ inline LinSec lin_sections(uint32_t ne, uint32_t npt, uint32
 
 // byte offsets inside one stage (all 16-byte aligned)
 struct PipeLayout {
-  uint32_t hdr, J, aux, lin, p, z, camv;
+  uint32_t hdr, J, aux, lin, p, z, camv, vt;
   uint32_t stage_bytes, fixed_bytes, total_bytes;
   int stages, rows;
   int dbg;  // experiments only (GB_PIPE_DBG): 1 skip camera reduction, 2 skip epilogue, 4 skip edge math,
@@ -103,10 +103,11 @@ inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_bud
   L.p = take(kTilePoints * 3 * sizeof(SP) + 32);
   L.z = take(kTilePoints * 3 * sizeof(SP) + 32);
   L.camv = take(kTileCams * cam_stride<A>() * sizeof(A) + 32);
+  L.vt = take(kTilePoints * 3 * sizeof(A));
   L.stage_bytes = o;
   // after the stages: 2 mbarriers per stage, then (bf16 storage only) a
   // separate 12-row staging for the camera / point contributions
-  L.fixed_bytes = 2 * kPipeMaxStages * 8 +
+  L.fixed_bytes = 3 * kPipeMaxStages * 8 +
                   (sizeof(SP) == sizeof(A) ? 0u : static_cast<uint32_t>(12 * pipe_jstride<A>()));
   const uint32_t avail = smem_budget > L.fixed_bytes ? smem_budget - L.fixed_bytes : 0;
   L.stages = static_cast<int>(std::min<uint32_t>(kPipeMaxStages, avail / L.stage_bytes));
@@ -189,11 +190,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
   const int S = L.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(pipe_smem + S * L.stage_bytes);
   uint64_t* empty = full + kPipeMaxStages;
+  uint64_t* ready = empty + kPipeMaxStages;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);   // producer lane 0 (arrive + expect_tx)
       mbar_init(&empty[s], kPipeConsumers / 32);  // every consumer warp, when done with the stage
+      mbar_init(&ready[s], 1);  // producer lane 0, after preparing the tile's point values
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -204,6 +207,31 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
   const bool dir = d.st->dir_pending != 0;
   const FP beta = d.st->beta;
 
+  // Preparer warp: once a tile's bytes have landed, its points are prepared in
+  // place: p <- z + beta p when the direction update is pending, and vt = D p
+  // (the HVP's gather source), so consumers gather one value per point column
+  // instead of three; then the tile is released to the consumers (ready).
+  auto prepare = [&](uint32_t ti) {
+    const int sp_ = static_cast<int>(ti % S);
+    mbar_wait(&full[sp_], (ti / S) & 1);
+    unsigned char* st = pipe_smem + sp_ * L.stage_bytes;
+    const uint32_t* h = reinterpret_cast<const uint32_t*>(st + L.hdr);
+    const uint32_t ne = h[kHNe], npt = h[kHNpt];
+    const AuxSec as = aux_sections(ne, npt);
+    const LinSec ls = lin_sections<FP>(ne, npt, h[kHNcam], d.jfact != 0, d.w != nullptr);
+    (void)as;
+    SP* pp = reinterpret_cast<SP*>(st + L.p + h[kHDp]);
+    const SP* zz = reinterpret_cast<const SP*>(st + L.z + h[kHDz]);
+    const FP* DD = reinterpret_cast<const FP*>(st + L.lin + ls.D);
+    A* vv = reinterpret_cast<A*>(st + L.vt);
+    for (uint32_t q = lane; q < 3 * npt; q += 32) {
+      const SP pn = dir ? pcg_dir_value<FP, SP>(zz[q], pp[q], beta) : pp[q];
+      pp[q] = pn;
+      vv[q] = static_cast<A>(DD[q]) * widen<A>(pn);  // == vt (k_pcg_dir)
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ready[sp_]);
+  };
   if (warp == kPipeConsumers / 32) {
     // ------------------------------------------------------------ producer
     // Tile records (tile_meta, 12 u32 each) are fetched 32 at a time, one per
@@ -272,6 +300,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     }
     return;
   }
+  if (warp == kPipeConsumers / 32 + 1) {
+    // ------------------------------------------------------------ preparer
+    for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i) prepare(i);
+    return;
+  }
 
   // -------------------------------------------------------------- consumers
   const A lam = static_cast<A>(d.st->lambda_solve);
@@ -281,7 +314,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     const uint32_t idx = blockIdx.x + i * gridDim.x;
     if (idx >= ntiles) break;
     const int s = static_cast<int>(i % S);
-    mbar_wait(&full[s], (i / S) & 1);
+    mbar_wait(&ready[s], (i / S) & 1);
     const unsigned char* st = pipe_smem + s * L.stage_bytes;
     const uint32_t* h = reinterpret_cast<const uint32_t*>(st + L.hdr);
     const uint32_t t = h[kHT], ne = h[kHNe], npt = h[kHNpt], pb = h[kHPb];
@@ -289,7 +322,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     constexpr int JS = pipe_jstride<SP>() / sizeof(SP);  // J row stride (elements)
     constexpr int GS = pipe_jstride<A>() / sizeof(A);    // contribution row stride (elements)
     A* gs = sizeof(SP) == sizeof(A) ? reinterpret_cast<A*>(pipe_smem + s * L.stage_bytes + L.J)
-                                    : reinterpret_cast<A*>(empty + kPipeMaxStages);
+                                    : reinterpret_cast<A*>(ready + kPipeMaxStages);
     const AuxSec as = aux_sections(ne, npt);
     const LinSec ls = lin_sections<FP>(ne, npt, h[kHNcam], d.jfact != 0, d.w != nullptr);
     const unsigned char* aux = st + L.aux;
@@ -304,8 +337,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     const FP* camr = reinterpret_cast<const FP*>(lin + ls.cr);
     const FP* sw = reinterpret_cast<const FP*>(lin + ls.w);
     const SP* sp = reinterpret_cast<const SP*>(st + L.p + h[kHDp]);
-    const SP* sz = reinterpret_cast<const SP*>(st + L.z + h[kHDz]);
     const A* camv = reinterpret_cast<const A*>(st + L.camv + h[kHDcv]);
+    const A* svt = reinterpret_cast<const A*>(st + L.vt);
 
     // ---- edge phase: thread j = edge j of the tile
     if (!(L.dbg & 4)) {
@@ -359,8 +392,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       }
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const SP pn = dir ? pcg_dir_value<FP, SP>(sz[3 * lp + k], sp[3 * lp + k], beta) : sp[3 * lp + k];
-        const A v = static_cast<A>(sD[3 * lp + k]) * widen<A>(pn);  // == vt (k_pcg_dir)
+        const A v = svt[3 * lp + k];
         s0 += jp[k] * v;
         s1 += jp[3 + k] * v;
       }
@@ -405,7 +437,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         for (int k = 0; k < 3; ++k) {
           const FP Dk = sD[3 * pi + k];
           const A damp = before ? static_cast<A>(lam_fp * Dk * Dk) : lam;
-          const SP pk = dir ? pcg_dir_value<FP, SP>(sz[3 * pi + k], sp[3 * pi + k], beta) : sp[3 * pi + k];
+          const SP pk = sp[3 * pi + k];  // direction update applied by the producer
           if (dir) d.p[col + k] = pk;
           const A out = freev ? damp * widen<A>(pk) + static_cast<A>(Dk) * acc[k] : A(0);
           const SP o = narrow<SP>(out);
