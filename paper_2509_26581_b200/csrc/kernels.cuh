@@ -96,6 +96,8 @@ struct Dev {
   const FP* d_obs;  // [2][na]
   SP* J;            // [24][na] full store, [16][na] factored store (jfact), or null (dynamic)
   FP* Rf;           // [nc][10] factored store: R (row-major 3x3) and f per camera
+  FP* cpre;         // [nc][kCamPre] per-camera chain record at x (snavely.cuh camera_pre)
+  FP* cpre_new;     // [nc][kCamPre] at the chi^2 evaluation point
   int jfact;        // 1: factored J store (analytic mode, SP == FP), DESIGN.md §2
   // pipelined HVP (hvp_pipe.cuh): tile records and per-tile camera copies
   const uint32_t* tile_meta;  // [n_normal][12] (hvp_pipe.cuh TileMeta)
@@ -476,6 +478,23 @@ __global__ void k_expand_J(Dev<FP, SP> d, SP* out) {
 // shared memory. Point epilogue: clamp, D = 1/sqrt(clamped), finiteness,
 // max |b|.
 // =====================================================================
+// Per-camera chain records (snavely.cuh camera_pre) of `params` into out.
+// mode 0: for a linearization (runs when it does); 1: for the candidate chi^2
+// (runs when k_chi2_tiles does); 2: unconditionally.
+template <typename FP, typename SP>
+__global__ void k_cam_pre(Dev<FP, SP> d, const FP* params, FP* out, int mode, int force) {
+  if (mode == 0 && !force && !d.st->do_linearize) return;
+  if (mode == 1 && !force && (!d.st->iter_active || !d.st->step_finite)) return;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.nc; c += gridDim.x * blockDim.x) {
+    FP cp[9], pre[kCamPre];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) cp[k] = params[9ull * c + k];
+    camera_pre<FP>(cp, pre);
+#pragma unroll
+    for (int k = 0; k < kCamPre; ++k) out[static_cast<uint64_t>(kCamPre) * c + k] = pre[k];
+  }
+}
+
 template <typename FP, typename SP, bool STORE, bool AUTO>
 __global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, const uint32_t* list, int force) {
   if (!force && !d.st->do_linearize) return;
@@ -514,7 +533,8 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, const
       snavely_residual<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res);
       snavely_jacobians_auto<FP>(cp, X, jc, jp);
     } else {
-      snavely_linearize<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res, jc, jp, fac);
+      snavely_linearize<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res, jc, jp, fac,
+                            d.cpre + static_cast<uint64_t>(kCamPre) * cam);
     }
     const FP s = res[0] * res[0] + res[1] * res[1];
     const FP w = valid ? loss_weight<FP>(loss, delta, s) : FP(0);
@@ -672,12 +692,10 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int 
     return;
   }
   if (c < d.nc && d.jfact && lane == 0) {  // factored J store: R and f per camera
-    FP cp[9], rf[10];
+    // R as the edges used it (the camera's precomputed record), f
 #pragma unroll
-    for (int k = 0; k < 9; ++k) cp[k] = d.x[9ull * c + k];
-    camera_factor<FP>(cp, rf);
-#pragma unroll
-    for (int k = 0; k < 10; ++k) d.Rf[10ull * c + k] = rf[k];
+    for (int k = 0; k < 9; ++k) d.Rf[10ull * c + k] = d.cpre[static_cast<uint64_t>(kCamPre) * c + 8 + k];
+    d.Rf[10ull * c + 9] = d.x[9ull * c + 6];
   }
   if (c < d.nc) {
     FP a0 = FP(0), a1 = FP(0);
@@ -1097,7 +1115,8 @@ __global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d,
       FP cp[9], fjc[18], fjp[6];
 #pragma unroll
       for (int k = 0; k < 9; ++k) cp[k] = d.x[9ull * cam + k];
-      snavely_jacobians<FP>(cp, &sX[3 * lp], fjc, fjp);
+      snavely_linearize<FP>(cp, &sX[3 * lp], FP(0), FP(0), nullptr, fjc, fjp, nullptr,
+                            d.cpre + static_cast<uint64_t>(kCamPre) * cam);
 #pragma unroll
       for (int k = 0; k < 18; ++k) jc[k] = static_cast<A>(fjc[k]);
 #pragma unroll
@@ -1219,7 +1238,8 @@ __global__ void k_make_vt(Dev<FP, SP> d) {
 constexpr int kLinRow = 21;  // Jc (18) + w r (2) + w (1) per staged edge
 template <typename FP>
 __host__ __device__ constexpr size_t lin_normal_smem() {
-  return sizeof(FP) * (kTilePoints * 3 + kTileCams * 9 + kTileThreads * kLinRow + kTileEdges * 9 + 32);
+  return sizeof(FP) * (kTilePoints * 3 + kTileCams * 9 + kTileThreads * kLinRow + kTileEdges * 9 + 32 +
+                       kTileCams * kCamPre);
 }
 
 template <typename FP, typename SP, bool STORE, bool AUTO>
@@ -1231,6 +1251,7 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
   FP* sJ = sC + kTileCams * 9;
   FP* pst = sJ + kTileThreads * kLinRow;
   FP* scratch = pst + kTileEdges * 9;
+  FP* sPre = scratch + 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t t = d.normal_tiles[blockIdx.x];
   const uint32_t eb = d.tile_ebeg[t], ne_t = d.tile_ecnt[t];
@@ -1239,6 +1260,9 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
   const uint64_t pcol0 = 9ull * d.nc;
   for (uint32_t i = tid; i < npt * 3; i += blockDim.x) sX[i] = d.x[pcol0 + 3ull * pb + i];
   for (uint32_t i = tid; i < ncam * 9; i += blockDim.x) sC[i] = d.x[9ull * d.tile_cams[cb + i / 9] + i % 9];
+  if (!AUTO)
+    for (uint32_t i = tid; i < ncam * kCamPre; i += blockDim.x)
+      sPre[i] = d.cpre[static_cast<uint64_t>(kCamPre) * d.tile_cams[cb + i / kCamPre] + i % kCamPre];
   __syncthreads();
   FP chi = FP(0);
   for (uint32_t c0 = 0; c0 < ne_t; c0 += kTileThreads) {
@@ -1253,7 +1277,7 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
     snavely_residual<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res);
     snavely_jacobians_auto<FP>(&sC[9 * lc], &sX[3 * lp], jc, jp);
   } else {
-    snavely_linearize<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res, jc, jp, fac);
+    snavely_linearize<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res, jc, jp, fac, &sPre[kCamPre * lc]);
   }
   const FP s = res[0] * res[0] + res[1] * res[1];
   const FP w = valid ? loss_weight<FP>(d.loss_kind, d.huber, s) : FP(0);
@@ -1712,7 +1736,8 @@ __global__ void __launch_bounds__(kTileThreads) k_chi2_tiles(Dev<FP, SP> d, cons
     for (int k = 0; k < 9; ++k) cp[k] = params[9ull * cam + k];
     const FP* X = params + pcol0 + 3ull * (pb + d.d_lpt[e]);
     FP res[2];
-    snavely_residual<FP>(cp, X, d.d_obs[e], d.d_obs[static_cast<uint64_t>(d.na) + e], res);
+    snavely_residual_pre<FP>(cp, d.cpre_new + static_cast<uint64_t>(kCamPre) * cam, X, d.d_obs[e],
+                             d.d_obs[static_cast<uint64_t>(d.na) + e], res);
     const FP s = res[0] * res[0] + res[1] * res[1];
     chi += RAW ? s : loss_value<FP>(d.loss_kind, d.huber, s);
   }

@@ -154,17 +154,73 @@ __device__ inline void camera_factor(const FP* cam, FP* rf) {
   rf[9] = cam[6];
 }
 
+// ---- per-camera precomputation ---------------------------------------------
+// Everything of the chain that depends on the camera alone (one sqrt, one
+// sincos, two reciprocals and the rotation matrix) is computed once per camera
+// per linearization / candidate evaluation (k_cam_pre) instead of once per
+// edge; the per-edge functions below read it. Record: [a s c ja js jcc s1 c2 |
+// R (9) | pad] (kCamPre values).
+constexpr int kCamPre = 18;
+
+template <typename FP>
+__device__ inline void camera_pre(const FP* cam, FP* pre) {
+  const Rodrigues<FP> Ro = rodrigues_coeffs<FP>(cam[0], cam[1], cam[2], true);
+  pre[0] = Ro.a;
+  pre[1] = Ro.s;
+  pre[2] = Ro.c;
+  pre[3] = Ro.ja;
+  pre[4] = Ro.js;
+  pre[5] = Ro.jcc;
+  pre[6] = Ro.s1;
+  pre[7] = Ro.c2;
+  rotation_matrix<FP>(Ro, cam[0], cam[1], cam[2], pre + 8);
+  pre[17] = FP(0);
+}
+
+template <typename FP>
+__device__ inline Rodrigues<FP> rodrigues_from_pre(const FP* pre) {
+  Rodrigues<FP> R;
+  R.a = pre[0];
+  R.s = pre[1];
+  R.c = pre[2];
+  R.ja = pre[3];
+  R.js = pre[4];
+  R.jcc = pre[5];
+  R.s1 = pre[6];
+  R.c2 = pre[7];
+  return R;
+}
+
+// snavely_residual with the camera's precomputed record
+template <typename FP>
+__device__ inline void snavely_residual_pre(const FP* cam, const FP* pre, const FP* X, FP o0, FP o1, FP* r) {
+  const Rodrigues<FP> R = rodrigues_from_pre(pre);
+  FP P[3];
+  rotate_translate(cam, X, R, P);
+  const FP iz = FP(1) / P[2];
+  const FP xp = -P[0] * iz, yp = -P[1] * iz;
+  const FP n = xp * xp + yp * yp;
+  const FP d = FP(1) + n * (cam[7] + n * cam[8]);
+  r[0] = cam[6] * d * xp - o0;
+  r[1] = cam[6] * d * yp - o1;
+}
+
 template <typename FP>
 __device__ inline void snavely_linearize(const FP* cam, const FP* X, FP o0, FP o1, FP* r, FP* jc, FP* jp,
-                                         FP* fac = nullptr) {
+                                         FP* fac = nullptr, const FP* pre = nullptr) {
   const FP w0 = cam[0], w1 = cam[1], w2 = cam[2];
   const FP x0 = X[0], x1 = X[1], x2 = X[2];
-  const Rodrigues<FP> Ro = rodrigues_coeffs<FP>(w0, w1, w2, true);
+  const Rodrigues<FP> Ro = pre ? rodrigues_from_pre(pre) : rodrigues_coeffs<FP>(w0, w1, w2, true);
   FP P[3];
   rotate_translate(cam, X, Ro, P);
   const FP s = Ro.js, c = Ro.jcc, s1 = Ro.s1, c2 = Ro.c2;
   FP R[9];
-  rotation_matrix<FP>(Ro, w0, w1, w2, R);
+  if (pre) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = pre[8 + k];
+  } else {
+    rotation_matrix<FP>(Ro, w0, w1, w2, R);
+  }
   // dy/dw = -s x w^T + s1 (w x x) w^T - s [x]x + c2 (w.x) w w^T + c (w x^T + (w.x) I)
   const FP cr[3] = {w1 * x2 - w2 * x1, w2 * x0 - w0 * x2, w0 * x1 - w1 * x0};
   const FP dt = w0 * x0 + w1 * x1 + w2 * x2;

@@ -432,6 +432,7 @@ class Solver final : public SolverBase {
     CK(cudaSetDevice(g_.device));
     ensure_structure(level);
     upload_params();
+    k_cam_pre<FP, SP><<<std::max(1u, div_up(act_.nc, 128)), 128, 0, s_>>>(dev_, dev_.x, dev_.cpre_new, 2, 1);
     if (raw)
       k_chi2_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, dev_.x, 1);
     else
@@ -976,6 +977,8 @@ class Solver final : public SolverBase {
     d.J = dyn ? nullptr : static_cast<SP*>(b_J_.alloc(jrows * ns * sizeof(SP)));
     if (d.J) CK(cudaMemsetAsync(d.J, 0, jrows * ns * sizeof(SP), s_));  // padding slots stay 0
     d.Rf = d.jfact ? static_cast<FP*>(b_Rf_.alloc(std::max<uint64_t>(1, 10 * nc) * sizeof(FP))) : nullptr;
+    d.cpre = static_cast<FP*>(b_cpre_.alloc(std::max<uint64_t>(1, kCamPre * nc) * sizeof(FP)));
+    d.cpre_new = static_cast<FP*>(b_cpre_new_.alloc(std::max<uint64_t>(1, kCamPre * nc) * sizeof(FP)));
     d.w = g_.loss_kind == GB_LOSS_HUBER ? static_cast<FP*>(b_w_.alloc(ns * sizeof(FP))) : nullptr;
     if (d.w) CK(cudaMemsetAsync(d.w, 0, ns * sizeof(FP), s_));
     d.loss_kind = g_.loss_kind;
@@ -1222,6 +1225,7 @@ class Solver final : public SolverBase {
 
   void enqueue_linearize(int force) {
     const size_t smem = lin_normal_smem<FP>();
+    k_cam_pre<FP, SP><<<std::max(1u, div_up(act_.nc, 128)), 128, 0, s_>>>(dev_, dev_.x, dev_.cpre, 0, force);
     const bool aut = g_.diff_mode == GB_AUTO;
     if (dev_.J && aut) {  // Auto: stored J from dual-number passes (factor_descriptor.hpp:610-624)
       if (dev_.n_normal) k_lin_normal<FP, SP, true, true><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
@@ -1376,6 +1380,7 @@ class Solver final : public SolverBase {
     k_iter_begin<FP><<<1, 1, 0, s_>>>(st_, dev_.recs);
     CK(cudaGetLastError());
     enqueue_solve(pcg_max_it);
+    k_cam_pre<FP, SP><<<std::max(1u, div_up(act_.nc, 128)), 128, 0, s_>>>(dev_, dev_.x_new, dev_.cpre_new, 1, 0);
     k_chi2_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, dev_.x_new, 0);
     CK(cudaGetLastError());
     if (dist()) {
@@ -1467,6 +1472,7 @@ class Solver final : public SolverBase {
   const uint64_t* dir_rend_ = nullptr;
   int dir_nranges_ = 0;
   unsigned dir_rest_grid_ = 1;
+  DBuf b_cpre_, b_cpre_new_;
   DBuf b_J_, b_Rf_, b_w_, b_part_, b_x_, b_xn_, b_b_, b_cl_, b_D_, b_dx_, b_Hc_, b_Hp_, b_Mc_, b_Mp_, b_xs_, b_r_, b_z_, b_p_,
       b_ap_, b_tr_, b_tr2_, b_tf_, b_cr_, b_cr2_, b_cf_, b_br_, b_br2_, b_bf_;
 };
