@@ -173,8 +173,11 @@ int gb_set_points(gb_graph* g, void* params_fp, uint64_t n, const uint8_t* fixed
  * factor_descriptor.hpp:192-210, via build_graph adapter.hpp:136-141):
  * camera/point ids, observed pixel FP[2*n], identity information, level
  * (NULL = all 0; FactorDescriptor::set_level :222-226), loss kind and Huber
- * delta (loss.hpp:15-23). Data is copied. Unknown ids -> GB_ERR_INVALID_ARGUMENT
- * (resolve_slots :549-558). */
+ * delta (loss.hpp:15-23). The arrays are referenced, not copied (like the
+ * camera / point buffers): keep them alive and unchanged until the next
+ * gb_set_observations or gb_destroy (fp32 observations are widened once into
+ * an internal copy). Unknown ids -> GB_ERR_INVALID_ARGUMENT (resolve_slots
+ * :549-558). */
 int gb_set_observations(gb_graph* g, uint64_t n, const uint32_t* camera_index,
                         const uint32_t* point_index, const void* observed_fp,
                         const uint8_t* level, int loss_kind, double huber_delta);

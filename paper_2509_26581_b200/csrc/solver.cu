@@ -49,9 +49,14 @@ struct GraphData {
   void* cams = nullptr;
   void* pts = nullptr;
   uint64_t nc = 0, np = 0, ne = 0;
-  std::vector<uint8_t> cam_fixed, pt_fixed, level;
-  std::vector<uint32_t> cam_idx, pt_idx;
-  std::vector<double> obs;
+  std::vector<uint8_t> cam_fixed, pt_fixed;
+  // Observation arrays are referenced, not copied (gb_set_observations): the
+  // caller keeps them alive and unchanged until the next set or gb_destroy.
+  const uint32_t* cam_idx = nullptr;
+  const uint32_t* pt_idx = nullptr;
+  const double* obs = nullptr;        // fp64 input as given, or obs_conv (fp32 input widened once)
+  const uint8_t* level = nullptr;     // null: all level 0
+  std::vector<double> obs_conv;
   int loss_kind = GB_LOSS_DEFAULT;
   double huber = 1.0;
   uint64_t revision = 1;
@@ -614,9 +619,9 @@ class Solver final : public SolverBase {
     in.nc = g_.nc;
     in.np = g_.np;
     in.ne = g_.ne;
-    in.cam = g_.cam_idx.data();
-    in.pt = g_.pt_idx.data();
-    in.level = g_.level.empty() ? nullptr : g_.level.data();
+    in.cam = g_.cam_idx;
+    in.pt = g_.pt_idx;
+    in.level = g_.level;
     in.cam_fixed = g_.cam_fixed.empty() ? nullptr : g_.cam_fixed.data();
     in.pt_fixed = g_.pt_fixed.empty() ? nullptr : g_.pt_fixed.data();
     in.active_level = level;
@@ -753,6 +758,13 @@ class Solver final : public SolverBase {
     h2d_bytes_ += v.size() * sizeof(T);
     return upload(b, v, s_);
   }
+  template <typename T>
+  T* to_dev(DBuf& b, const T* p, uint64_t n) {
+    h2d_bytes_ += n * sizeof(T);
+    T* d = static_cast<T*>(b.alloc(std::max<uint64_t>(1, n) * sizeof(T)));
+    if (n) CK(cudaMemcpyAsync(d, p, n * sizeof(T), cudaMemcpyHostToDevice, s_));
+    return d;
+  }
   void cub_scan_excl(const uint32_t* in, uint32_t* out, uint64_t n) {
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, static_cast<int64_t>(n), s_));
@@ -790,12 +802,12 @@ class Solver final : public SolverBase {
     DBuf s_cam, s_pt, s_lvl, s_cfix, s_pfix, s_obs, s_flag, s_pos, s_cam_a, s_pt_a, s_entry, s_key, s_key2, s_val, s_val2,
         s_rank, s_deg, s_degi, s_rb, s_k64, s_k64b, s_order, s_pkey, s_pval, s_pkey2, s_pval2, s_hc, s_hr, s_ic, s_ir,
         s_runcam, s_runcam2, s_slots, s_cnt, s_bad;
-    const uint32_t* cam = to_dev(s_cam, g_.cam_idx);
-    const uint32_t* pt = to_dev(s_pt, g_.pt_idx);
-    const uint8_t* lvl = g_.level.empty() ? nullptr : to_dev(s_lvl, g_.level);
+    const uint32_t* cam = to_dev(s_cam, g_.cam_idx, ne);
+    const uint32_t* pt = to_dev(s_pt, g_.pt_idx, ne);
+    const uint8_t* lvl = g_.level ? to_dev(s_lvl, g_.level, ne) : nullptr;
     const uint8_t* cfix = g_.cam_fixed.empty() ? nullptr : to_dev(s_cfix, g_.cam_fixed);
     const uint8_t* pfix = g_.pt_fixed.empty() ? nullptr : to_dev(s_pfix, g_.pt_fixed);
-    const double* obs = to_dev(s_obs, g_.obs);
+    const double* obs = to_dev(s_obs, g_.obs, 2 * ne);
     ptm.mark("act: h2d edges");
     uint32_t* flag = scratch<uint32_t>(s_flag, ne + 1);
     uint32_t* pos = scratch<uint32_t>(s_pos, ne + 1);
@@ -1608,18 +1620,19 @@ int gb_set_observations(gb_graph* g, uint64_t n, const uint32_t* cam, const uint
     gb::GraphData& d = g->data;
     if (n > 0xffffffffull) throw std::invalid_argument("more than 2^32 observations");
     if (loss_kind != GB_LOSS_DEFAULT && loss_kind != GB_LOSS_HUBER) throw std::invalid_argument("unknown loss kind");
+    if (n && (!cam || !pt || !observed)) throw std::invalid_argument("null observation arrays");
     d.ne = n;
-    d.cam_idx.assign(cam, cam + n);
-    d.pt_idx.assign(pt, pt + n);
-    d.obs.resize(2 * n);
+    d.cam_idx = cam;
+    d.pt_idx = pt;
     if (d.precision == GB_FP64) {
-      const double* o = static_cast<const double*>(observed);
-      std::copy(o, o + 2 * n, d.obs.begin());
+      d.obs_conv.clear();
+      d.obs = static_cast<const double*>(observed);
     } else {
       const float* o = static_cast<const float*>(observed);
-      for (uint64_t i = 0; i < 2 * n; ++i) d.obs[i] = o[i];
+      d.obs_conv.assign(o, o + 2 * n);
+      d.obs = d.obs_conv.data();
     }
-    d.level.assign(level ? level : nullptr, level ? level + n : nullptr);
+    d.level = level;
     d.loss_kind = loss_kind;
     d.huber = huber_delta;
     ++d.revision;
