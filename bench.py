@@ -288,9 +288,10 @@ def ours(args, shape, desc):
                 traffic = json.load(f).get("dram_bytes_per_hvp")
         except Exception:
             traffic = None
-    # per LM iteration: iter_begin, precond, rhs_norm, pcg_init, tcam (first HVP), step, chi2, decide, commit,
+    # per LM iteration: iter_begin, precond (cams, pts), rhs_norm, pcg_init, tcam (first HVP), step, cam_pre +
+    # chi2, decide, commit, cam_pre +
     # lin tiles (+heavy), lin_cams, tile_lin; per PCG iteration: hvp_pipe, hvp_cams, pcg_update, pcg_dir_rest
-    launches_per_it = 12 + 4 * cfg.pcg.max_iterations
+    launches_per_it = 15 + 4 * cfg.pcg.max_iterations
     if world > 1:  # split camera kernels + finalize kernels
         launches_per_it += 1 + 2 * cfg.pcg.max_iterations + 5 + 2
     line = {

@@ -924,21 +924,25 @@ __device__ inline void precond_vertex(const Dev<FP, SP>& d, const FP* H, FP* M, 
   for (int k = 0; k < NP; ++k) M[k] = out[k];
 }
 
+// Block-Jacobi build + inversion (linear_system.hpp:120-160). Cameras (9x9,
+// register-heavy) and points (3x3) are separate kernels so the point pass
+// runs at full occupancy.
 template <typename FP, typename SP>
-__global__ void k_precond(Dev<FP, SP> d) {
-  if (!d.st->iter_active) return;
-  const uint64_t nv = static_cast<uint64_t>(d.nc) + d.np;
-  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv;
+__global__ void k_precond_cams(Dev<FP, SP> d) {
+  if (!d.st->iter_active || d.st->schur) return;  // Schur: k_schur_pre_cams
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < d.nc;
        v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    if (v < d.nc) {
-      if (d.st->schur) continue;  // k_schur_pre_cams
-      const uint64_t col = 9 * v;
-      precond_vertex<FP, SP, 9>(d, d.Hc + 45 * v, d.Mc + 45 * v, col, d.col_free[col]);
-    } else {
-      const uint64_t i = v - d.nc;
-      const uint64_t col = 9ull * d.nc + 3 * i;
-      precond_vertex<FP, SP, 3>(d, d.Hp + 6 * i, d.Mp + 6 * i, col, d.col_free[col]);
-    }
+    const uint64_t col = 9 * v;
+    precond_vertex<FP, SP, 9>(d, d.Hc + 45 * v, d.Mc + 45 * v, col, d.col_free[col]);
+  }
+}
+template <typename FP, typename SP>
+__global__ void __launch_bounds__(256) k_precond_pts(Dev<FP, SP> d) {
+  if (!d.st->iter_active) return;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.np;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t col = 9ull * d.nc + 3 * i;
+    precond_vertex<FP, SP, 3>(d, d.Hp + 6 * i, d.Mp + 6 * i, col, d.col_free[col]);
   }
 }
 

@@ -162,6 +162,9 @@ class Solver final : public SolverBase {
       int sms = 0, per = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g_.device));
       sms_ = static_cast<uint32_t>(sms);
+      int o3 = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_precond_pts<FP, SP>, 256, 0));
+      pt_occ_ = static_cast<unsigned>(std::max(1, o3));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_step<FP, SP>, 256, 0));
       coop_grid_ = static_cast<unsigned>(std::max(1, sms * std::max(1, per)));
       if (const char* e = std::getenv("GB_PCG_FUSED")) fused_pcg_ = std::atoi(e) != 0;
@@ -545,7 +548,7 @@ class Solver final : public SolverBase {
   void ls_precond(double lambda, void* blocks, int32_t* fallbacks) override {
     need_ls();
     begin_solve_state(lambda, nullptr);
-    k_precond<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    launch_precond();
     CK(cudaGetLastError());
     State<FP> hs;
     std::vector<FP> mc(45ull * act_.nc), mp(6ull * act_.np);
@@ -1069,7 +1072,8 @@ class Solver final : public SolverBase {
     d.cam_red2 = static_cast<FP*>(b_cr2_.alloc(std::max<uint64_t>(1, nc) * sizeof(FP)));
     d.cam_flag = static_cast<int*>(b_cf_.alloc(std::max<uint64_t>(1, nc) * sizeof(int)));
     const uint64_t nblk =
-        std::max<uint64_t>(std::max<uint64_t>(std::max<uint64_t>(vert_grid(), col_grid()), cam_grid()), coop_grid_);
+        std::max<uint64_t>(std::max<uint64_t>(std::max<uint64_t>(vert_grid(), col_grid()), cam_grid()), coop_grid_) +
+        pt_grid();
     d.blk_red = static_cast<FP*>(b_br_.alloc(nblk * sizeof(FP)));
     d.blk_red2 = static_cast<FP*>(b_br2_.alloc(nblk * sizeof(FP)));
     d.blk_flag = static_cast<int*>(b_bf_.alloc(nblk * sizeof(int)));
@@ -1218,6 +1222,22 @@ class Solver final : public SolverBase {
 
   // ------------------------------------------------------------- launches
   // one vertex per thread (memory-level parallelism beats grid-stride reuse here)
+
+  // one full wave of the point kernels (occupancy measured once per solver)
+  unsigned pt_grid() const { return std::max(1u, std::min(div_up(act_.np, 256), sms_ * pt_occ_)); }
+  void launch_pcg_init() {
+    k_pcg_init<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+  }
+  void launch_pcg_update() {
+    k_pcg_update<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+  }
+  void launch_precond() {
+    k_precond_cams<FP, SP><<<std::max(1u, div_up(act_.nc, 64)), 64, 0, s_>>>(dev_);
+    k_precond_pts<FP, SP><<<pt_grid(), 256, 0, s_>>>(dev_);
+    CK(cudaGetLastError());
+  }
   unsigned vert_grid() const {
     return std::max(1u, std::min(div_up(static_cast<uint64_t>(act_.nc) + act_.np, 256), sms_ * 6u));
   }
@@ -1301,13 +1321,13 @@ class Solver final : public SolverBase {
   // Schur mode (kernels.cuh k_schur_*): camera blocks of S, reduced rhs, PCG
   // on the cameras, back-substitution of the points, step.
   void enqueue_solve_schur(int pcg_max_it) {
-    k_precond<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);  // point blocks = A_pp^-1
+    launch_precond();  // point blocks = A_pp^-1
     k_schur_pre_tiles<FP, SP><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_);
     k_schur_pre_cams<FP, SP><<<div_up(act_.nc, 128), 128, 0, s_>>>(dev_);
     k_schur_tiles<FP, SP, 1><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_);
     k_schur_rhs_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_);
     k_rhs_norm<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
-    k_pcg_init<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    launch_pcg_init();
     CK(cudaGetLastError());
     for (int k = 0; k < pcg_max_it; ++k) {
       k_schur_tiles<FP, SP, 0><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_);
@@ -1315,7 +1335,7 @@ class Solver final : public SolverBase {
       if (fused_pcg_) {
         launch_pcg_step();
       } else {
-        k_pcg_update<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+        launch_pcg_update();
         k_pcg_dir<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
       }
       CK(cudaGetLastError());
@@ -1345,7 +1365,7 @@ class Solver final : public SolverBase {
       enqueue_solve_schur(pcg_max_it);
       return;
     }
-    k_precond<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    launch_precond();
     CK(cudaGetLastError());
     k_rhs_norm<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
     CK(cudaGetLastError());
@@ -1353,7 +1373,7 @@ class Solver final : public SolverBase {
       allreduce(red_s() + kRedRhs, 2);
       fin(1);
     }
-    k_pcg_init<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    launch_pcg_init();
     CK(cudaGetLastError());
     if (dist()) {
       allreduce(red_s() + kRedInitRz, 2);
@@ -1366,7 +1386,7 @@ class Solver final : public SolverBase {
         launch_pcg_step();
         continue;
       }
-      k_pcg_update<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+      launch_pcg_update();
       CK(cudaGetLastError());
       if (dist()) {
         allreduce(red_s() + kRedUpdRz, 2);
@@ -1477,6 +1497,7 @@ class Solver final : public SolverBase {
   PipeLayout pipe_{};
   bool pipe_ok_ = false;
   uint32_t sms_ = 148;
+  unsigned pt_occ_ = 4;
   DBuf b_tmeta_, b_tcv_, b_taux_, b_tlin_;
   bool pipe_aux_pending_ = false;
   DBuf b_camtc_idx_, b_camtc_off_, b_dir_rb_, b_dir_re_;
