@@ -76,7 +76,7 @@ __host__ __device__ inline LinSec lin_sections(uint32_t ne, uint32_t npt, uint32
 
 // byte offsets inside one stage (all 16-byte aligned)
 struct PipeLayout {
-  uint32_t hdr, J, aux, lin, p, z, camv, vt;
+  uint32_t hdr, J, aux, lin, p, z, camv, vt, gs;
   uint32_t stage_bytes, fixed_bytes, total_bytes;
   int stages, rows;
   int dbg;  // experiments only (GB_PIPE_DBG): 1 skip camera reduction, 2 skip epilogue, 4 skip edge math,
@@ -104,11 +104,12 @@ inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_bud
   L.z = take(kTilePoints * 3 * sizeof(SP) + 32);
   L.camv = take(kTileCams * cam_stride<A>() * sizeof(A) + 32);
   L.vt = take(kTilePoints * 3 * sizeof(A));
+  // camera / point contributions: over the J rows when SP and Arith have the
+  // same width, else (bf16 storage) a 12-row area of the stage
+  L.gs = sizeof(SP) == sizeof(A) ? L.J : take(12ull * pipe_jstride<A>());
   L.stage_bytes = o;
-  // after the stages: 2 mbarriers per stage, then (bf16 storage only) a
-  // separate 12-row staging for the camera / point contributions
-  L.fixed_bytes = 3 * kPipeMaxStages * 8 +
-                  (sizeof(SP) == sizeof(A) ? 0u : static_cast<uint32_t>(12 * pipe_jstride<A>()));
+  // after the stages: 3 mbarriers per stage
+  L.fixed_bytes = 3 * kPipeMaxStages * 8;
   const uint32_t avail = smem_budget > L.fixed_bytes ? smem_budget - L.fixed_bytes : 0;
   L.stages = static_cast<int>(std::min<uint32_t>(kPipeMaxStages, avail / L.stage_bytes));
   L.total_bytes = L.stages * L.stage_bytes + L.fixed_bytes;
@@ -321,8 +322,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     const SP* sJ = reinterpret_cast<const SP*>(st + L.J);
     constexpr int JS = pipe_jstride<SP>() / sizeof(SP);  // J row stride (elements)
     constexpr int GS = pipe_jstride<A>() / sizeof(A);    // contribution row stride (elements)
-    A* gs = sizeof(SP) == sizeof(A) ? reinterpret_cast<A*>(pipe_smem + s * L.stage_bytes + L.J)
-                                    : reinterpret_cast<A*>(ready + kPipeMaxStages);
+    A* gs = reinterpret_cast<A*>(pipe_smem + s * L.stage_bytes + L.gs);  // per stage: the epilogue of
+    // this tile may still read it while the other consumer half starts the next tile
     const AuxSec as = aux_sections(ne, npt);
     const LinSec ls = lin_sections<FP>(ne, npt, h[kHNcam], d.jfact != 0, d.w != nullptr);
     const unsigned char* aux = st + L.aux;
