@@ -336,3 +336,33 @@ def test_large_problem_trace_parity(gpu, ref):
     rb = bal.levenberg_marquardt(r, cfg)
     assert [i.pcg_iterations for i in ra.iterations] == [i.pcg_iterations for i in rb.iterations]
     assert_trace_parity(ra, rb, 1e-6)
+
+
+@pytest.mark.parametrize("variant", ["before_scaling", "no_guard", "refresh_on_reject", "no_normalize",
+                                     "clamps", "tau_lambda_max", "loose_pcg"])
+def test_lm_config_variants(gpu, ref, ladybug, variant):
+    """Every LMConfig / PCGConfig / LinearSystemOptions field the reference
+    exposes (levenberg_marquardt.hpp:15-26, pcg.hpp:12-17,
+    linear_system.hpp:15-19) runs on the device with the reference's semantics:
+    the same LM trace as the compiled reference."""
+    cfg = bal_cfg(25)
+    if variant == "before_scaling":
+        cfg.damping = "before_scaling"
+    elif variant == "no_guard":
+        cfg.use_rejection_guard = False
+        cfg.pcg.max_iterations = 3
+    elif variant == "refresh_on_reject":
+        cfg.refresh_on_reject = True
+        cfg.tau = 1e-9  # tiny initial damping: early rejects
+    elif variant == "no_normalize":
+        cfg.pcg.normalize_rhs = False
+    elif variant == "clamps":
+        cfg.clamp_min, cfg.clamp_max = 1e-2, 1e6
+    elif variant == "tau_lambda_max":
+        cfg.tau, cfg.lambda_max = 10.0, 1e4
+    elif variant == "loose_pcg":
+        cfg.pcg.tolerance, cfg.pcg.rejection_ratio = 1e-2, 2.0
+    g, r, ra, rb = run_pair(ladybug, ref, cfg=cfg)
+    assert_trace_parity(ra, rb, 1e-6)
+    assert [i.pcg_iterations for i in ra.iterations] == [i.pcg_iterations for i in rb.iterations]
+    assert [i.low_quality_step for i in ra.iterations] == [i.low_quality_step for i in rb.iterations]
