@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);   // producer lane 0 (arrive + expect_tx)
       mbar_init(&empty[s], kPipeConsumers / 32);  // every consumer warp, when done with the stage
-      mbar_init(&ready[s], 1);  // producer lane 0, after preparing the tile's point values
+      mbar_init(&ready[s], 32);  // every preparer lane, after preparing the tile's point values
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -230,8 +230,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       pp[q] = pn;
       vv[q] = static_cast<A>(DD[q]) * widen<A>(pn);  // == vt (k_pcg_dir)
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&ready[sp_]);
+    mbar_arrive(&ready[sp_]);  // every lane releases its own writes
   };
   if (warp == kPipeConsumers / 32) {
     // ------------------------------------------------------------ producer
@@ -345,7 +344,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     if (!(L.dbg & 4)) {
       const uint32_t j = tid;
       const bool valid = j < ne;
-      const uint32_t jj = valid ? j : 0;
+      const uint32_t jj = valid ? j : 0;  // indices of an invalid lane: edge 0's (its J column is its own)
       const uint32_t lc = slc[jj], lp = slp[jj];
       A jc[18], jp[6];
       bool done = false;
@@ -354,13 +353,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
           FP U[6], R[9];
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
-            jc[k] = sJ[k * JS + jj];
-            jc[9 + k] = sJ[(3 + k) * JS + jj];
+            jc[k] = sJ[k * JS + j];
+            jc[9 + k] = sJ[(3 + k) * JS + j];
           }
 #pragma unroll
-          for (int k = 0; k < 6; ++k) U[k] = sJ[(6 + k) * JS + jj];
-          const FP dist = sJ[12 * JS + jj], n = sJ[13 * JS + jj];
-          const FP p0 = sJ[14 * JS + jj], p1 = sJ[15 * JS + jj];
+          for (int k = 0; k < 6; ++k) U[k] = sJ[(6 + k) * JS + j];
+          const FP dist = sJ[12 * JS + j], n = sJ[13 * JS + j];
+          const FP p0 = sJ[14 * JS + j], p1 = sJ[15 * JS + j];
           FP rf[cam_stride<FP>()];
           load16<FP, cam_stride<FP>()>(camr + cam_stride<FP>() * lc, rf);
 #pragma unroll
@@ -377,9 +376,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       }
       if (!done) {
 #pragma unroll
-        for (int k = 0; k < 18; ++k) jc[k] = widen<A>(sJ[k * JS + jj]);
+        for (int k = 0; k < 18; ++k) jc[k] = widen<A>(sJ[k * JS + j]);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) jp[k] = widen<A>(sJ[(18 + k) * JS + jj]);
+        for (int k = 0; k < 6; ++k) jp[k] = widen<A>(sJ[(18 + k) * JS + j]);
       }
       const A wgt = d.w ? static_cast<A>(sw[jj]) : A(1);
       A cv[cam_stride<A>()];
