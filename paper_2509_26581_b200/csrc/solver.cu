@@ -13,7 +13,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -89,6 +91,51 @@ class SolverBase {
 };
 
 // ------------------------------------------------------------- device memory
+// Process-wide cache of freed device blocks (>= 1 MiB), per device, so that a
+// graph built after another one (bench e2e, repeated solves, tests) reuses its
+// memory instead of paying cudaMalloc's page mapping again. Blocks are reused
+// when they are at most 2x the request; the cache holds at most 1/3 of the
+// device's memory and is flushed before an allocation is retried on OOM.
+class BlockCache {
+ public:
+  static BlockCache& get() {
+    static BlockCache c;
+    return c;
+  }
+  void* take(int dev, size_t bytes) {
+    std::lock_guard<std::mutex> lk(m_);
+    auto& f = free_[dev];
+    auto it = f.lower_bound(bytes);
+    if (it == f.end() || it->first > 2 * bytes) return nullptr;
+    void* p = it->second;
+    held_[dev] -= it->first;
+    f.erase(it);
+    return p;
+  }
+  // returns false when the caller should cudaFree the block itself
+  bool give(int dev, void* p, size_t bytes) {
+    if (bytes < (1u << 20)) return false;
+    size_t total = 0, fr = 0;
+    if (cudaMemGetInfo(&fr, &total) != cudaSuccess) return false;
+    std::lock_guard<std::mutex> lk(m_);
+    if (held_[dev] + bytes > total / 3) return false;
+    free_[dev].emplace(bytes, p);
+    held_[dev] += bytes;
+    return true;
+  }
+  void flush(int dev) {
+    std::lock_guard<std::mutex> lk(m_);
+    for (auto& kv : free_[dev]) cudaFree(kv.second);
+    free_[dev].clear();
+    held_[dev] = 0;
+  }
+
+ private:
+  std::mutex m_;
+  std::map<int, std::multimap<size_t, void*>> free_;
+  std::map<int, size_t> held_;
+};
+
 class DBuf {
  public:
   static constexpr size_t kSlack = 64;
@@ -97,14 +144,33 @@ class DBuf {
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_) {
+      // stream work that may still use the block completes first (cudaFree's own semantics)
+      cudaDeviceSynchronize();
+      if (!BlockCache::get().give(dev_, p_, cap_)) cudaFree(p_);
+    }
     p_ = nullptr;
-    bytes_ = 0;
+    bytes_ = cap_ = 0;
   }
   void* alloc(size_t bytes) {
     if (bytes <= bytes_ && p_) return p_;
     release();
-    CK(cudaMalloc(&p_, bytes + kSlack));  // slack: 16-byte-widened bulk copies may read past the end
+    CK(cudaGetDevice(&dev_));
+    const size_t want = bytes + kSlack;  // slack: 16-byte-widened bulk copies may read past the end
+    void* c = BlockCache::get().take(dev_, want);
+    if (c) {
+      p_ = c;
+      cap_ = want;  // conservative: the block is at least this large
+    } else {
+      cudaError_t e = cudaMalloc(&p_, want);
+      if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        BlockCache::get().flush(dev_);
+        e = cudaMalloc(&p_, want);
+      }
+      CK(e);
+      cap_ = want;
+    }
     bytes_ = bytes;
     return p_;
   }
@@ -115,7 +181,8 @@ class DBuf {
 
  private:
   void* p_ = nullptr;
-  size_t bytes_ = 0;
+  size_t bytes_ = 0, cap_ = 0;
+  int dev_ = 0;
 };
 
 template <typename T>
