@@ -113,6 +113,7 @@ EXPORTED = [
     "gb_ls_jacobians", "gb_incidence", "gb_synthetic_bal", "gb_begin", "gb_step", "gb_end", "gb_stream",
     "gb_time_hvp", "gb_hvp_bytes", "gb_nccl_unique_id", "gb_set_distributed", "gb_shard_plan", "gb_activation_selfcheck",
     "gb_set_linear_solver",
+    "gbg_last_error", "gbg_circle_solve", "gbg_vi_solve",  # generic path, include/gb_generic.h
 ]
 
 

@@ -35,7 +35,8 @@ def tiny_problem(t):
 # ----------------------------------------------------------- C ABI surface
 def test_abi_exports_every_declared_symbol():
     header = open(os.path.join(ROOT, "include", "gb_bal.h")).read()
-    declared = set(re.findall(r"\b(gb_[a-z_0-9]+)\s*\(", header))
+    header += open(os.path.join(ROOT, "include", "gb_generic.h")).read()
+    declared = set(re.findall(r"\b(gbg?_[a-z_0-9]+)\s*\(", header))
     assert declared == set(_abi.EXPORTED)
     lib = ctypes.CDLL(_abi.LIB_PATH)
     for name in declared:
