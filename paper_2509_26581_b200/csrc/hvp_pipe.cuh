@@ -404,15 +404,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       for (int k = 0; k < 9; ++k) g[k] = jc[k] * q0 + jc[9 + k] * q1;
       // contributions over this edge's own J column (thread j alone reads column j)
 #pragma unroll
-      for (int k = 0; k < 9; ++k) gs[k * GS + j] = g[k];
-#pragma unroll
       for (int k = 0; k < 3; ++k) gs[(9 + k) * GS + j] = jp[k] * q0 + jp[3 + k] * q1;
       {
         const uint32_t prev = __shfl_up_sync(0xffffffffu, lc, 1);
         const unsigned hm = __ballot_sync(0xffffffffu, valid && (lane == 0 || lc != prev));
         const unsigned vm = __ballot_sync(0xffffffffu, valid);
-        __syncwarp();
-        if (!(L.dbg & 1)) chunk_runs_smem<A, FP>(gs + 32 * warp, GS, lane, hm, vm, hm ? scpb[warp] : 0u, d.part);
+        if (!(L.dbg & 1))
+          camera_runs<A, FP>(g, valid, lane, hm, vm, hm ? scpb[warp] : 0u, gs + 32 * warp, GS, d.part);
       }
     }
     consumer_sync();

@@ -266,69 +266,6 @@ __device__ inline void seg_reduce(T (&v)[K], int lane, int run_end) {
   }
 }
 
-// Camera-run sums of 9 values over a 32-edge warp chunk whose runs are
-// contiguous lane ranges (edges sorted by camera inside a tile), written to
-// the run's partial slot. Per run: lanes outside it contribute 0, then a
-// 5-stage transpose reduction (xor 16/8/4/2/1 exchanging 5/3/2/1/1 values,
-// i.e. 12 shuffles instead of seg_reduce's 45) leaves value k of the run
-// total in the two lanes 2m, 2m+1 of a fixed m(k). Fixed association order,
-// so results are deterministic. heads/vm: ballots of run heads / valid lanes.
-__device__ inline int rr9_slot(int lane) {
-  const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
-  const int q = b2 ? (b1 ? -1 : 2) : b1;                 // position in the stage-2 list
-  const int p = q < 0 ? -1 : (b3 ? (q == 2 ? -1 : 3 + q) : q);  // position in the stage-1 list
-  if (p < 0) return -1;
-  return b4 ? (p < 4 ? 5 + p : -1) : p;
-}
-
-template <typename T, typename Out>
-__device__ inline void run_reduce9_store(const T (&g)[9], int lane, unsigned heads, unsigned vm, uint32_t slot0,
-                                         Out* part) {
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-  const int myslot = (lane & 1) ? -1 : rr9_slot(lane);
-  const unsigned full = 0xffffffffu;
-  uint32_t r = 0;
-  while (heads) {
-    const int start = __ffs(heads) - 1;
-    heads &= heads - 1;
-    const int stop = heads ? __ffs(heads) - 1 : 32 - __clz(vm);
-    const bool in = lane >= start && lane < stop;
-    T a[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) a[k] = in ? g[k] : T(0);
-    T k1[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const T hi = i < 4 ? a[5 + i] : T(0);
-      k1[i] = b4 ? hi : a[i];
-      const T snd = b4 ? a[i] : hi;
-      k1[i] += __shfl_xor_sync(full, snd, 16);
-    }
-    T k2[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const T hi = i < 2 ? k1[3 + i] : T(0);
-      k2[i] = b3 ? hi : k1[i];
-      const T snd = b3 ? k1[i] : hi;
-      k2[i] += __shfl_xor_sync(full, snd, 8);
-    }
-    T k3[2];
-    {
-      k3[0] = b2 ? k2[2] : k2[0];
-      k3[1] = b2 ? T(0) : k2[1];
-      const T s0 = b2 ? k2[0] : k2[2];
-      const T s1 = b2 ? k2[1] : T(0);
-      k3[0] += __shfl_xor_sync(full, s0, 4);
-      k3[1] += __shfl_xor_sync(full, s1, 4);
-    }
-    T v = b1 ? k3[1] : k3[0];
-    v += __shfl_xor_sync(full, b1 ? k3[0] : k3[1], 2);
-    v += __shfl_xor_sync(full, v, 1);
-    if (myslot >= 0) part[static_cast<uint64_t>(slot0 + r) * 9 + myslot] = static_cast<Out>(v);
-    ++r;
-  }
-}
-
 // Camera-run sums of a warp chunk from shared memory: the chunk's 32 edges
 // have written their 9 camera values to gw[k * stride + lane]; lane o of the
 // warp produces output o = 9 r + k (run r, value k) as a sequential sum over
@@ -370,6 +307,64 @@ __device__ inline void chunk_runs_smem(const A* gw, int stride, int lane, unsign
     for (; e < stp; ++e) a0 += src[e];
     part[static_cast<uint64_t>(slot0 + r) * 9 + k] = static_cast<FP>((a0 + a1) + (a2 + a3));
   }
+}
+
+// Camera-run sums of one warp chunk (both HVP tile kernels). The common case
+// of a single run (one camera for all valid lanes) reduces in registers: lanes
+// outside contribute 0 and a 5-stage transpose reduction (xor 16/8/4/2/1
+// exchanging 5/3/2/1/1 values: 12 shuffles, no shared memory) leaves value k
+// of the total in the two lanes 2m, 2m+1 of a fixed m(k). Several runs go
+// through shared memory (chunk_runs_smem). Fixed association orders either
+// way (deterministic), identical in k_hvp_tiles and k_hvp_pipe.
+__device__ inline int rr9_slot(int lane) {
+  const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
+  const int q = b2 ? (b1 ? -1 : 2) : b1;                         // position in the stage-2 list
+  const int p = q < 0 ? -1 : (b3 ? (q == 2 ? -1 : 3 + q) : q);  // position in the stage-1 list
+  if (p < 0) return -1;
+  return b4 ? (p < 4 ? 5 + p : -1) : p;
+}
+
+template <typename A, typename FP>
+__device__ inline void camera_runs(const A (&g)[9], bool valid, int lane, unsigned hm, unsigned vm, uint32_t slot0,
+                                   A* gw, int stride, FP* part) {
+  if (!hm) return;
+  if (__popc(hm) == 1) {
+    const unsigned full = 0xffffffffu;
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+    A a[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) a[k] = valid ? g[k] : A(0);
+    A k1[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const A hi = i < 4 ? a[5 + i] : A(0);
+      k1[i] = b4 ? hi : a[i];
+      k1[i] += __shfl_xor_sync(full, b4 ? a[i] : hi, 16);
+    }
+    A k2[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const A hi = i < 2 ? k1[3 + i] : A(0);
+      k2[i] = b3 ? hi : k1[i];
+      k2[i] += __shfl_xor_sync(full, b3 ? k1[i] : hi, 8);
+    }
+    A k3[2];
+    k3[0] = b2 ? k2[2] : k2[0];
+    k3[1] = b2 ? A(0) : k2[1];
+    k3[0] += __shfl_xor_sync(full, b2 ? k2[0] : k2[2], 4);
+    k3[1] += __shfl_xor_sync(full, b2 ? k2[1] : A(0), 4);
+    A v = b1 ? k3[1] : k3[0];
+    v += __shfl_xor_sync(full, b1 ? k3[0] : k3[1], 2);
+    v += __shfl_xor_sync(full, v, 1);
+    const int slot = (lane & 1) ? -1 : rr9_slot(lane);
+    if (slot >= 0) part[static_cast<uint64_t>(slot0) * 9 + slot] = static_cast<FP>(v);
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) gw[k * stride + lane] = g[k];
+  __syncwarp();
+  chunk_runs_smem<A, FP>(gw, stride, lane, hm, vm, slot0, part);
+  __syncwarp();
 }
 
 struct RunInfo {
@@ -1155,11 +1150,8 @@ __global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d,
       const uint32_t prev = __shfl_up_sync(0xffffffffu, cam, 1);
       const unsigned hm = __ballot_sync(0xffffffffu, valid && (lane == 0 || cam != prev));
       const unsigned vm = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-      for (int k = 0; k < 9; ++k) gsh[k * kGsStride + tid] = g[k];
-      __syncwarp();
-      chunk_runs_smem<A, FP>(gsh + (tid & ~31), kGsStride, lane, hm, vm, hm ? d.chunk_part_base[chunk] : 0u, d.part);
-      __syncwarp();
+      camera_runs<A, FP>(g, valid, lane, hm, vm, hm ? d.chunk_part_base[chunk] : 0u, gsh + (tid & ~31), kGsStride,
+                         d.part);
     }
     A h[3];
 #pragma unroll
