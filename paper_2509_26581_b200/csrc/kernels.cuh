@@ -1231,7 +1231,17 @@ __global__ void k_make_vt(Dev<FP, SP> d) {
 // 32-edge chunk run by run with one lane per output value (54 values over
 // 32 lanes), i.e. plain FMAs over shared memory instead of shuffle trees.
 // Dynamic shared memory: see lin_normal_smem().
-constexpr int kLinRow = 21;  // Jc (18) + w r (2) + w (1) per staged edge
+constexpr int kLinRow = 22;  // Jc (18) + w r (2) + w (1) + pad per staged edge (16-byte rows)
+template <typename FP>
+struct Pair;
+template <>
+struct Pair<double> {
+  using type = double2;
+};
+template <>
+struct Pair<float> {
+  using type = float2;
+};
 template <typename FP>
 __host__ __device__ constexpr size_t lin_normal_smem() {
   return sizeof(FP) * (kTilePoints * 3 + kTileCams * 9 + kTileThreads * kLinRow + kTileEdges * 9 + 32 +
@@ -1289,10 +1299,16 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
   const FP wr0 = valid ? w * res[0] : FP(0), wr1 = valid ? w * res[1] : FP(0);
   FP* row = sJ + tid * kLinRow;
 #pragma unroll
-  for (int k = 0; k < 18; ++k) row[k] = valid ? jc[k] : FP(0);
+  // row layout: 10 pairs (Jc0[k], Jc1[k]) k < 9, (w r0, w r1), then w: a
+  // reduction lane reads both rows' operands of one column with one 2-wide load
+  for (int k = 0; k < 9; ++k) {
+    row[2 * k] = valid ? jc[k] : FP(0);
+    row[2 * k + 1] = valid ? jc[9 + k] : FP(0);
+  }
   row[18] = wr0;
   row[19] = wr1;
   row[20] = w;
+  row[21] = FP(0);
   if (valid) {
     FP* pv = pst + j * 9;
     pv[0] = jp[0] * wr0 + jp[3] * wr1;
@@ -1315,10 +1331,10 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
   // value v < 9: b_v = sum Jc0v wr0 + Jc1v wr1; v >= 9: H(i,j) = sum w (Jc0i Jc0j + Jc1i Jc1j)
   const bool has1 = lane + 32 < kLinVals;
   const bool isb = lane < 9;
-  // value v0: m * (row[i0] row[k0] + row[i0 + 9] row[k1]) with m = 1 (b) or w (H)
+  // value v0: m * (P[i0].0 P[k0].0 + P[i0].1 P[k0].1) over the row's pairs P,
+  // with m = 1 (b: k0 = the (w r0, w r1) pair) or w (H)
   const int i0 = isb ? lane : p9row(lane - 9);
-  const int k0 = isb ? 18 : p9col(lane - 9);
-  const int k1 = isb ? 19 : 9 + p9col(lane - 9);
+  const int k0 = isb ? 9 : p9col(lane - 9);
   const int i1 = has1 ? p9row(lane + 32 - 9) : 0;
   const int j1 = has1 ? p9col(lane + 32 - 9) : 0;
   const uint32_t slot0 = d.chunk_part_base[d.tile_chunk_base[t] + c0 / 32 + warp];
@@ -1331,9 +1347,15 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
     FP acc0 = FP(0), acc1 = FP(0);
     for (int q = start; q < stop; ++q) {
       const FP* rr = sJ + (32 * warp + q) * kLinRow;
+      using P2 = typename Pair<FP>::type;
+      const P2* pr = reinterpret_cast<const P2*>(rr);
       const FP m0 = isb ? FP(1) : rr[20];
-      acc0 += m0 * (rr[i0] * rr[k0] + rr[9 + i0] * rr[k1]);
-      if (has1) acc1 += rr[20] * (rr[i1] * rr[j1] + rr[9 + i1] * rr[9 + j1]);
+      const P2 a = pr[i0], b = pr[k0];
+      acc0 += m0 * (a.x * b.x + a.y * b.y);
+      if (has1) {
+        const P2 c = pr[i1], e = pr[j1];
+        acc1 += rr[20] * (c.x * e.x + c.y * e.y);
+      }
     }
     FP* dst = d.part + static_cast<uint64_t>(slot0 + run) * kLinVals;
     dst[lane] = acc0;
