@@ -340,6 +340,105 @@ __global__ void __launch_bounds__(kBlock) k_back(Sets<FP> S, FSetDev<FP, F> f, i
   for (int k = 0; k < D; ++k) acc[col + k] = g[k];
 }
 
+// Warp-per-vertex variants for vertices with many incident factors (poses
+// seen by ~100 stereo factors): lanes stride over the vertex's items and the
+// partial sums meet in a fixed-order butterfly (deterministic).
+template <typename FP>
+__device__ inline FP warp_allsum(FP v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename FP, typename F, int D>
+__global__ void __launch_bounds__(kBlock) k_back_w(Sets<FP> S, FSetDev<FP, F> f, int set, FP* acc) {
+  const VSetDev<FP>& vs = S.s[set];
+  const uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= vs.n || vs.col[v] < 0) return;  // warp-uniform
+  FP g[D];
+  for (int k = 0; k < D; ++k) g[k] = FP(0);
+  for (uint32_t q = f.csr_off[set][v] + lane; q < f.csr_off[set][v + 1]; q += 32) {
+    const uint32_t it = f.csr_item[set][q];
+    const uint32_t a = it / F::K;
+    const int s = static_cast<int>(it % F::K);
+    const FP* blk = f.J + static_cast<uint64_t>(F::R * F::SUMD) * a + F::R * F::pre(s);
+    const FP* qa = f.q + static_cast<uint64_t>(F::R) * a;
+    for (int c = 0; c < D; ++c) {
+      FP t = FP(0);
+      for (int row = 0; row < F::R; ++row) t += blk[row * D + c] * qa[row];
+      g[c] += t;
+    }
+  }
+  const int64_t col = vs.col[v];
+  for (int k = 0; k < D; ++k) {
+    const FP t = warp_allsum(g[k]);
+    if (lane == 0) acc[col + k] += t;
+  }
+}
+
+template <typename FP, typename F, int D>
+__global__ void __launch_bounds__(kBlock) k_acc_w(Sets<FP> S, FSetDev<FP, F> f, int set, FP* b, FP* H) {
+  const VSetDev<FP>& vs = S.s[set];
+  const uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= vs.n || vs.col[v] < 0) return;  // warp-uniform
+  FP bb[D], hh[D * D];
+  for (int k = 0; k < D; ++k) bb[k] = FP(0);
+  for (int k = 0; k < D * D; ++k) hh[k] = FP(0);
+  for (uint32_t q = f.csr_off[set][v] + lane; q < f.csr_off[set][v + 1]; q += 32) {
+    const uint32_t it = f.csr_item[set][q];
+    const uint32_t a = it / F::K;
+    const int s = static_cast<int>(it % F::K);
+    const FP* blk = f.J + static_cast<uint64_t>(F::R * F::SUMD) * a + F::R * F::pre(s);
+    const FP* wr = f.wr + static_cast<uint64_t>(F::R) * a;
+    const FP w = f.w[a];
+    for (int c = 0; c < D; ++c) {
+      FP gg = FP(0);
+      for (int row = 0; row < F::R; ++row) gg += blk[row * D + c] * wr[row];
+      bb[c] += gg;
+    }
+    for (int c1 = 0; c1 < D; ++c1)
+      for (int c2 = 0; c2 < D; ++c2) {
+        FP h = FP(0);
+        for (int row = 0; row < F::R; ++row) h += blk[row * D + c1] * blk[row * D + c2];
+        hh[c1 * D + c2] += w * h;
+      }
+  }
+  const int64_t col = vs.col[v];
+  FP* Hv = H + vs.hoff + static_cast<int64_t>(D * D) * v;
+  for (int k = 0; k < D; ++k) {
+    const FP t = warp_allsum(bb[k]);
+    if (lane == 0) b[col + k] += t;
+  }
+  for (int k = 0; k < D * D; ++k) {
+    const FP t = warp_allsum(hh[k]);
+    if (lane == 0) Hv[k] += t;
+  }
+}
+
+// HVP forward with one warp per factor and one lane per residual row (wide
+// factors such as the 15-row IMU preintegration)
+template <typename FP, typename F>
+__global__ void __launch_bounds__(kBlock) k_fwd_w(Sets<FP> S, FSetDev<FP, F> f, const FP* vt) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int row = threadIdx.x & 31;
+  if (i >= f.n || row >= F::R) return;
+  const FP* Ji = f.J + static_cast<uint64_t>(F::R * F::SUMD) * i;
+  FP u = FP(0);
+#pragma unroll
+  for (int s = 0; s < F::K; ++s) {
+    const VSetDev<FP>& vs = S.s[F::vs(s)];
+    const int64_t col = vs.col[f.idx[F::K * i + s]];
+    if (col < 0) continue;
+    const int d = F::dim(s);
+    const FP* blk = Ji + F::R * F::pre(s);
+    FP a = FP(0);
+    for (int c = 0; c < d; ++c) a += blk[row * d + c] * vt[col + c];
+    u += a;
+  }
+  f.q[static_cast<uint64_t>(F::R) * i + row] = f.w[i] * u;
+}
+
 // ------------------------------------------------------------ vector kernels
 template <typename FP>
 __global__ void k_scale(uint64_t n, const FP* b, const FP* diag, double cmin, double cmax, FP* clamped, FP* D,
@@ -570,6 +669,7 @@ struct FSetHost {
   DVec<typename F::Const> cst;
   DVec<FP> J, wr, w, q;
   DVec<uint32_t> off[kMaxSets], item[kMaxSets];
+  uint64_t items[kMaxSets] = {0, 0, 0};
 
   void upload(const std::vector<typename F::Obs>& o, const std::vector<typename F::Const>& c) {
     n = static_cast<uint32_t>(o.size());
@@ -604,6 +704,7 @@ struct FSetHost {
           if (F::vs(s) == st) it[cur[hidx[F::K * a + s]]++] = F::K * a + s;
       off[st].up(o);
       item[st].up(it);
+      items[st] = it.size();
     }
   }
   FSetDev<FP, F> dev() const {
@@ -639,20 +740,30 @@ struct FactorOps {
     GCK(cudaGetLastError());
     return sum_parts(part, nblk(f.n));
   }
+  // many incident items per vertex: one warp per vertex
+  static bool wide(const std::vector<VSetHost<FP>*>& sets, const FSetHost<FP, F>& f, int st) {
+    return sets[st]->n && f.items[st] >= 16ull * sets[st]->n;
+  }
   static void acc(const Sets<FP>& S, const std::vector<VSetHost<FP>*>& sets, const FSetHost<FP, F>& f, FP* b,
                   FP* H) {
     for (int st = 0; st < static_cast<int>(sets.size()); ++st) {
       if (!f.off[st].p || !f.n) continue;
       by_dim(sets[st]->dim, [&](auto Dc) {
         constexpr int D = decltype(Dc)::value;
-        k_acc<FP, F, D><<<nblk(sets[st]->n), kBlock>>>(S, f.dev(), st, b, H);
+        if (D <= 6 && wide(sets, f, st))
+          k_acc_w<FP, F, D><<<nblk(32ull * sets[st]->n), kBlock>>>(S, f.dev(), st, b, H);
+        else
+          k_acc<FP, F, D><<<nblk(sets[st]->n), kBlock>>>(S, f.dev(), st, b, H);
       });
       GCK(cudaGetLastError());
     }
   }
   static void fwd(const Sets<FP>& S, const FSetHost<FP, F>& f, const FP* vt) {
     if (!f.n) return;
-    k_fwd<FP, F><<<nblk(f.n), kBlock>>>(S, f.dev(), vt);
+    if (F::R >= 8)
+      k_fwd_w<FP, F><<<nblk(32ull * f.n), kBlock>>>(S, f.dev(), vt);
+    else
+      k_fwd<FP, F><<<nblk(f.n), kBlock>>>(S, f.dev(), vt);
     GCK(cudaGetLastError());
   }
   static void back(const Sets<FP>& S, const std::vector<VSetHost<FP>*>& sets, const FSetHost<FP, F>& f, FP* acc) {
@@ -660,7 +771,10 @@ struct FactorOps {
       if (!f.off[st].p || !f.n) continue;
       by_dim(sets[st]->dim, [&](auto Dc) {
         constexpr int D = decltype(Dc)::value;
-        k_back<FP, F, D><<<nblk(sets[st]->n), kBlock>>>(S, f.dev(), st, acc);
+        if (wide(sets, f, st))
+          k_back_w<FP, F, D><<<nblk(32ull * sets[st]->n), kBlock>>>(S, f.dev(), st, acc);
+        else
+          k_back<FP, F, D><<<nblk(sets[st]->n), kBlock>>>(S, f.dev(), st, acc);
       });
       GCK(cudaGetLastError());
     }
