@@ -149,7 +149,7 @@ def reference_arm(args, shape, desc):
     # bounded sample: 1 warm-up LM iteration + up to 5 timed ones of the full
     # workload (each is ~seconds on the host at Final scale)
     timed = max(1, min(args.steps, 5))
-    r = refbind.build_graph(problem, args.precision, "analytic", workers=cores)
+    r = refbind.build_graph(problem, args.precision, args.mode, workers=cores)
     t0 = time.perf_counter()
     rep = bal.levenberg_marquardt(r, lm_config(1 + timed, bal))
     wall = time.perf_counter() - t0
@@ -162,7 +162,7 @@ def reference_arm(args, shape, desc):
         "impl": "reference", "metric": "LM iteration ms (synthetic BAL BA)", "value": round(ms, 3),
         "unit": "ms/LM-iteration", "n_gpus": world, "steps": len(its), "warmup": 1, "ms_per_step": round(ms, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision],
-        "data": "synthetic", "config": {"workload": desc + f" {args.precision} analytic, PCG<=10@1e-6",
+        "data": "synthetic", "config": {"workload": desc + f" {args.precision} {args.mode}, PCG<=10@1e-6",
                                         "precision": args.precision, "host_cores": cores},
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms/LM-iteration", "cores": cores, "kind": "reference",
                          "sample": sample},
@@ -194,7 +194,7 @@ def ours(args, shape, desc):
         obj = [bal.nccl_unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    g = bal.build_graph(problem, args.precision, "analytic", device=local)
+    g = bal.build_graph(problem, args.precision, args.mode, device=local)
     if args.solver != "pcg":
         g.set_linear_solver(args.solver)
     if world > 1:
@@ -254,7 +254,7 @@ def ours(args, shape, desc):
         torch.distributed.broadcast_object_list(obj, src=0)
         torch.distributed.barrier()
     t0 = time.perf_counter()
-    g2 = bal.build_graph(problem_h, args.precision, "analytic", device=local)
+    g2 = bal.build_graph(problem_h, args.precision, args.mode, device=local)
     if args.solver != "pcg":
         g2.set_linear_solver(args.solver)
     if world > 1:
@@ -300,7 +300,7 @@ def ours(args, shape, desc):
         "metric": "LM iteration ms (synthetic BAL BA)", "value": round(ms, 4), "unit": "ms/LM-iteration",
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(ms, 4), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision], "data": "synthetic",
-        "config": {"workload": desc + f" {args.precision} analytic, PCG<=10@1e-6" +
+        "config": {"workload": desc + f" {args.precision} {args.mode}, PCG<=10@1e-6" +
                    ("" if args.solver == "pcg" else f", {args.solver} linear solver"), "precision": args.precision,
                    "cache": "inputs larger than L2 (HVP moves %.2f GB per launch, L2 126 MB)" % (kbytes.value / 1e9),
                    "parallelism": "single GPU" if world == 1 else
@@ -344,7 +344,7 @@ def cpu_baseline(args, problem):
             return {"value": None, "unit": "ms/LM-iteration", "cores": 0, "kind": "reference",
                     "sample": "oracle/_ref not built"}
         cores = os.cpu_count() or 1
-        r = refbind.build_graph(problem, args.precision, "analytic", workers=cores)
+        r = refbind.build_graph(problem, args.precision, args.mode, workers=cores)
         rep = bal.levenberg_marquardt(r, lm_config(2, bal))
         its = rep.iterations[1:] if len(rep.iterations) > 1 else rep.iterations
         ms = 1e3 * statistics.mean(i.wall_seconds for i in its)
@@ -364,6 +364,8 @@ def main():
     ap.add_argument("--workload", default="final", choices=sorted(WORKLOADS))
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32", "fp32-bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="analytic", choices=["analytic", "auto", "dynamic"],
+                    help="DifferentiationMode (dynamic = implicit low-memory HVP)")
     ap.add_argument("--solver", default="pcg", choices=["pcg", "schur"],
                     help="pcg = the reference algorithm (headline); schur = Schur-complement mode")
     args = ap.parse_args()
