@@ -27,7 +27,7 @@
 
 namespace {
 
-std::string g_err;
+thread_local std::string g_err;
 
 template <typename F>
 int guarded(F&& f) {

@@ -1137,7 +1137,7 @@ void lm_solve(Model<FP, Fs...>& m, const gb_lm_config& cfg, gb_solve_report* rep
 
 // ====================================================================== C ABI
 namespace {
-std::string g_gerr;
+thread_local std::string g_gerr;  // per calling thread, like gb_last_error
 template <typename Fn>
 int gguard(Fn&& f) {
   try {

@@ -99,6 +99,7 @@ struct Dev {
   FP* cpre;         // [nc][kCamPre] per-camera chain record at x (snavely.cuh camera_pre)
   FP* cpre_new;     // [nc][kCamPre] at the chi^2 evaluation point
   int jfact;        // 1: factored J store (analytic mode, SP == FP), DESIGN.md §2
+  int want_dx;      // k_step also stores dx (the LinearSystem::solve_step surface only)
   // pipelined HVP (hvp_pipe.cuh): tile records and per-tile camera copies
   const uint32_t* tile_meta;  // [n_normal][12] (hvp_pipe.cuh TileMeta)
   uint32_t ntcams;            // tile_cam_off[ntiles]
@@ -1711,7 +1712,7 @@ __global__ void k_step(Dev<FP, SP> d) {
     const FP damp = before ? lam * Di * Di : lam;
     if (counted(d, i)) pred += xsi * (damp * xsi + rhs);
     const FP dxi = Di * xsi;
-    d.dx[i] = dxi;
+    if (d.want_dx) d.dx[i] = dxi;
     if (!is_finite(dxi)) fin = 0;
     const FP xi = d.x[i];
     d.x_new[i] = d.col_free[i] ? xi + dxi : xi;

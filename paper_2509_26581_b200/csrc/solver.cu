@@ -646,7 +646,9 @@ class Solver final : public SolverBase {
                      int32_t* finite) override {
     need_ls();
     begin_solve_state(lambda, &pcg);
+    dev_.want_dx = 1;  // this surface returns dx; the LM loop's k_step skips the store
     enqueue_solve(pcg.max_iterations);
+    dev_.want_dx = 0;
     State<FP> hs;
     CK(cudaMemcpyAsync(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost, s_));
     std::vector<FP> h(ncols_);
