@@ -366,3 +366,47 @@ def test_lm_config_variants(gpu, ref, ladybug, variant):
     assert_trace_parity(ra, rb, 1e-6)
     assert [i.pcg_iterations for i in ra.iterations] == [i.pcg_iterations for i in rb.iterations]
     assert [i.low_quality_step for i in ra.iterations] == [i.low_quality_step for i in rb.iterations]
+
+
+def _exact_problem(problem):
+    """The problem's observations replaced by exact projections of its own
+    initial parameters (zero residual start, test_lm_optimizer.cpp:115-126)."""
+    from oracle import restatement as R
+
+    q = problem.copy()
+    cams = q.cameras[q.camera_index]
+    pts = q.points[q.point_index]
+    # binary64 Snavely predictions (snavely.hpp:48-61): residual against obs = 0
+    q.observations[:] = R.residual(cams, pts, np.zeros((len(cams), 2)), R.Prec("fp64"))
+    return q
+
+
+@pytest.mark.parametrize("case", ["gradient_small", "damping_overflow", "no_free_parameters", "max_iterations"])
+def test_terminations(gpu, ref, case):
+    """Every Termination the reference's loop can report (levenberg_marquardt.hpp:28-35)
+    is reached on the device with the reference's trace."""
+    p = bal.synthetic_bal(*TINY, seed=21)
+    cfg = bal_cfg(30)
+    fixed = None
+    if case == "gradient_small":
+        # zero-residual start; the tolerance sits above the last-ulp residuals
+        # (device sincos / FMA vs libm) that an exactly-zero threshold would see
+        p = _exact_problem(p)
+        cfg.gradient_tolerance = 1e-6
+    elif case == "damping_overflow":
+        cfg.lambda_max, cfg.tau = 1e-3, 1.0  # the first reject already overflows
+        cfg.max_iterations = 30
+    elif case == "no_free_parameters":
+        fixed = (np.ones(TINY[0], bool), np.ones(TINY[1], bool))
+    else:
+        cfg.max_iterations, cfg.tolerance = 3, 0.0
+    g, r = pair(p, ref, fixed=fixed)
+    ra, rb = bal.levenberg_marquardt(g, cfg), bal.levenberg_marquardt(r, cfg)
+    assert ra.termination == rb.termination
+    if case != "damping_overflow":
+        assert ra.termination == case
+    if case == "gradient_small":  # chi^2 ~0: last-ulp residuals, compare absolutely
+        assert len(ra.iterations) == len(rb.iterations) == 1
+        assert ra.final_chi2 < 1e-18 and rb.final_chi2 < 1e-18
+    else:
+        assert_trace_parity(ra, rb, 1e-6)
