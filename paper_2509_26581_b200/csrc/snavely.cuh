@@ -329,24 +329,40 @@ __device__ inline void dsincos(Dual<T> a, Dual<T>* sn, Dual<T>* cs) {
   *cs = {c, -s * a.d};
 }
 
+// Rodrigues coefficients a, s, c of rotate_angle_axis (snavely.hpp:18-35) on duals
 template <typename FP>
-__device__ inline void snavely_project_dual(const Dual<FP>* camera, const Dual<FP>* X, Dual<FP>* predicted) {
+__device__ inline void dual_rot_coeffs(const Dual<FP>* omega, Dual<FP>* a, Dual<FP>* s, Dual<FP>* c) {
   using D = Dual<FP>;
-  const D* omega = camera;
   const D theta2 = omega[0] * omega[0] + omega[1] * omega[1] + omega[2] * omega[2];
-  D a, s, c;
   if (theta2.v < taylor_threshold<FP>::value) {
     const D u = theta2;
-    a = FP(1) - u * FP(0.5) + u * u * (FP(1) / FP(24));
-    s = FP(1) - u * (FP(1) / FP(6)) + u * u * (FP(1) / FP(120));
-    c = FP(0.5) - u * (FP(1) / FP(24)) + u * u * (FP(1) / FP(720));
+    *a = FP(1) - u * FP(0.5) + u * u * (FP(1) / FP(24));
+    *s = FP(1) - u * (FP(1) / FP(6)) + u * u * (FP(1) / FP(120));
+    *c = FP(0.5) - u * (FP(1) / FP(24)) + u * u * (FP(1) / FP(720));
   } else {
     const D theta = dsqrt(theta2);
     D sn, cs;
     dsincos(theta, &sn, &cs);
-    a = cs;
-    s = sn / theta;
-    c = (FP(1) - a) / theta2;
+    *a = cs;
+    *s = sn / theta;
+    *c = (FP(1) - *a) / theta2;
+  }
+}
+
+// rot (optional): the coefficients of a pass whose rotation is not seeded
+// (their derivative parts are 0), computed once per edge
+template <typename FP>
+__device__ inline void snavely_project_dual(const Dual<FP>* camera, const Dual<FP>* X, Dual<FP>* predicted,
+                                            const Dual<FP>* rot = nullptr) {
+  using D = Dual<FP>;
+  const D* omega = camera;
+  D a, s, c;
+  if (rot) {
+    a = rot[0];
+    s = rot[1];
+    c = rot[2];
+  } else {
+    dual_rot_coeffs<FP>(omega, &a, &s, &c);
   }
   const D wx = omega[1] * X[2] - omega[2] * X[1];
   const D wy = omega[2] * X[0] - omega[0] * X[2];
@@ -369,6 +385,15 @@ __device__ inline void snavely_project_dual(const Dual<FP>* camera, const Dual<F
 // jc (2x9) and jp (2x3) by 12 dual passes
 template <typename FP>
 __device__ inline void snavely_jacobians_auto(const FP* cam, const FP* X, FP* jc, FP* jp) {
+  // passes 3..11 seed t, f, k1, k2 or X: the rotation coefficients are those
+  // of an unseeded omega, computed once (sqrt/sincos/divisions not repeated)
+  Dual<FP> rot[3];
+  {
+    Dual<FP> w0[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) w0[i] = {cam[i], FP(0)};
+    dual_rot_coeffs<FP>(w0, &rot[0], &rot[1], &rot[2]);
+  }
 #pragma unroll 1
   for (int k = 0; k < 12; ++k) {
     Dual<FP> c[9], x[3], pred[2];
@@ -376,7 +401,7 @@ __device__ inline void snavely_jacobians_auto(const FP* cam, const FP* X, FP* jc
     for (int i = 0; i < 9; ++i) c[i] = {cam[i], i == k ? FP(1) : FP(0)};
 #pragma unroll
     for (int i = 0; i < 3; ++i) x[i] = {X[i], 9 + i == k ? FP(1) : FP(0)};
-    snavely_project_dual<FP>(c, x, pred);
+    snavely_project_dual<FP>(c, x, pred, k < 3 ? nullptr : rot);
     if (k < 9) {
       jc[k] = pred[0].d;
       jc[9 + k] = pred[1].d;
