@@ -115,9 +115,13 @@ class BlockCache {
   // returns false when the caller should cudaFree the block itself
   bool give(int dev, void* p, size_t bytes) {
     if (bytes < (1u << 20)) return false;
-    size_t total = 0, fr = 0;
-    if (cudaMemGetInfo(&fr, &total) != cudaSuccess) return false;
     std::lock_guard<std::mutex> lk(m_);
+    size_t& total = total_[dev];
+    if (!total) {  // device memory size, queried once
+      size_t fr = 0;
+      if (cudaMemGetInfo(&fr, &total) != cudaSuccess) total = 0;
+      if (!total) return false;
+    }
     if (held_[dev] + bytes > total / 3) return false;
     free_[dev].emplace(bytes, p);
     held_[dev] += bytes;
@@ -134,6 +138,7 @@ class BlockCache {
   std::mutex m_;
   std::map<int, std::multimap<size_t, void*>> free_;
   std::map<int, size_t> held_;
+  std::map<int, size_t> total_;
 };
 
 class DBuf {
