@@ -46,17 +46,16 @@ __host__ __device__ constexpr uint32_t pipe_jstride() {
 // Section offsets inside a tile's aux blob (static) and lin blob (per
 // linearization); identical on the host (sizes) and the device (reads).
 struct AuxSec {
-  uint32_t lcam, lpt, psl, pso, cpb, cf, bytes;
+  uint32_t lcam, lpt, psl, pso, cf, bytes;
 };
 __host__ __device__ inline AuxSec aux_sections(uint32_t ne, uint32_t npt) {
-  const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad, nch = (ne + 31) / 32;
+  const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad;
   AuxSec a;
   a.lcam = 0;
   a.lpt = a.lcam + r16(2ull * ne8);
   a.psl = a.lpt + r16(2ull * ne8);
   a.pso = a.psl + r16(2ull * ne);
-  a.cpb = a.pso + r16(2ull * (npt + 1));
-  a.cf = a.cpb + r16(4ull * nch);
+  a.cf = a.pso + r16(2ull * (npt + 1));
   a.bytes = a.cf + r16(3ull * npt);
   return a;
 }
@@ -76,7 +75,7 @@ __host__ __device__ inline LinSec lin_sections(uint32_t ne, uint32_t npt, uint32
 
 // byte offsets inside one stage (all 16-byte aligned)
 struct PipeLayout {
-  uint32_t hdr, J, aux, lin, p, z, camv, vt, gs;
+  uint32_t hdr, J, aux, lin, p, z, camv, vt, gs, runs;
   uint32_t stage_bytes, fixed_bytes, total_bytes;
   int stages, rows;
   int dbg;  // experiments only (GB_PIPE_DBG): 1 skip camera reduction, 2 skip epilogue, 4 skip edge math,
@@ -94,7 +93,7 @@ inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_bud
     return r;
   };
   L.rows = rows;
-  L.hdr = take(16 * 4);
+  L.hdr = take(32 * 4);
   // J rows at a padded stride (bank spread); rows 0..11 are reused for the
   // edges' camera (9) and point (3) contributions when sizeof(SP) == sizeof(A)
   L.J = take(static_cast<uint64_t>(rows) * pipe_jstride<SP>());
@@ -104,6 +103,7 @@ inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_bud
   L.z = take(kTilePoints * 3 * sizeof(SP) + 32);
   L.camv = take(kTileCams * cam_stride<A>() * sizeof(A) + 32);
   L.vt = take(kTilePoints * 3 * sizeof(A));
+  L.runs = take(4 * kTileEdges + 32);  // the tile's camera-run slot spans (at most one run per edge)
   // camera / point contributions: over the J rows when SP and Arith have the
   // same width, else (bf16 storage) a 12-row area of the stage
   L.gs = sizeof(SP) == sizeof(A) ? L.J : take(12ull * pipe_jstride<A>());
@@ -117,7 +117,8 @@ inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_bud
 }
 
 // tile record, one per normal tile (list order)
-enum TileMeta : int { kMT = 0, kMEb, kMNe, kMPb, kMNpt, kMCb, kMNcam, kMCh0, kMAux16, kMLin16, kMCount = 12 };
+// kMSlot0 / kMNruns: the tile's camera-run slots [slot0, slot0 + nruns) (filled on the device by k_tile_aux)
+enum TileMeta : int { kMT = 0, kMEb, kMNe, kMPb, kMNpt, kMCb, kMNcam, kMCh0, kMAux16, kMLin16, kMSlot0, kMNruns, kMCount };
 
 // N contiguous T from 16-byte aligned shared memory in 16-byte loads
 template <typename T, int N>
@@ -181,7 +182,19 @@ __device__ inline Span span16(const void* p, uint64_t bytes) {
   return Span{reinterpret_cast<const char*>(lo), static_cast<uint32_t>(hi - lo), static_cast<uint32_t>(a - lo)};
 }
 
-enum PipeHdr : int { kHT = 0, kHNe, kHNpt, kHNcam, kHDp, kHDcv, kHPb, kHDz };
+enum PipeHdr : int { kHT = 0, kHNe, kHNpt, kHNcam, kHDp, kHDcv, kHPb, kHDz, kHLpt, kHPsl, kHPso, kHDr, kHCf, kHCr, kHW, kHNr, kHSlot0 };
+
+// stage index + parity of a ring of S stages (no integer division per tile)
+struct RingPos {
+  int s = 0;
+  unsigned ph = 0;
+  __device__ void next(int S) {
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
 
 template <typename FP, typename SP>
 __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, PipeLayout L) {
@@ -212,23 +225,37 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
   // place: p <- z + beta p when the direction update is pending, and vt = D p
   // (the HVP's gather source), so consumers gather one value per point column
   // instead of three; then the tile is released to the consumers (ready).
-  auto prepare = [&](uint32_t ti) {
-    const int sp_ = static_cast<int>(ti % S);
-    mbar_wait(&full[sp_], (ti / S) & 1);
+  auto prepare = [&](const RingPos& rp) {
+    const int sp_ = rp.s;
+    mbar_wait(&full[sp_], rp.ph);
     unsigned char* st = pipe_smem + sp_ * L.stage_bytes;
     const uint32_t* h = reinterpret_cast<const uint32_t*>(st + L.hdr);
-    const uint32_t ne = h[kHNe], npt = h[kHNpt];
-    const AuxSec as = aux_sections(ne, npt);
-    const LinSec ls = lin_sections<FP>(ne, npt, h[kHNcam], d.jfact != 0, d.w != nullptr);
-    (void)as;
+    const uint32_t npt = h[kHNpt];
     SP* pp = reinterpret_cast<SP*>(st + L.p + h[kHDp]);
     const SP* zz = reinterpret_cast<const SP*>(st + L.z + h[kHDz]);
-    const FP* DD = reinterpret_cast<const FP*>(st + L.lin + ls.D);
+    const FP* DD = reinterpret_cast<const FP*>(st + L.lin);  // lin section D at offset 0
     A* vv = reinterpret_cast<A*>(st + L.vt);
-    for (uint32_t q = lane; q < 3 * npt; q += 32) {
-      const SP pn = dir ? pcg_dir_value<FP, SP>(zz[q], pp[q], beta) : pp[q];
-      pp[q] = pn;
-      vv[q] = static_cast<A>(DD[q]) * widen<A>(pn);  // == vt (k_pcg_dir)
+    const uint32_t n3 = 3 * npt;
+    constexpr int U = 4;  // values per lane per pass, loads batched ahead of the stores
+    for (uint32_t q0 = lane; q0 < n3; q0 += 32 * U) {
+      SP pv[U], zv[U];
+      FP dv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t q = min(q0 + 32 * u, n3 - 1);
+        pv[u] = pp[q];
+        zv[u] = dir ? zz[q] : pv[u];
+        dv[u] = DD[q];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t q = q0 + 32 * u;
+        if (q < n3) {
+          const SP pn = dir ? pcg_dir_value<FP, SP>(zv[u], pv[u], beta) : pv[u];
+          pp[q] = pn;
+          vv[q] = static_cast<A>(dv[u]) * widen<A>(pn);  // == vt (k_pcg_dir)
+        }
+      }
     }
     mbar_arrive(&ready[sp_]);  // every lane releases its own writes
   };
@@ -238,6 +265,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     // lane, so the producer pays one dependent round trip per 32 tiles; every
     // other byte moves by bulk copy.
     uint32_t i = 0;
+    RingPos rp;
     for (uint32_t base = blockIdx.x; base < ntiles; base += 32u * gridDim.x) {
       const uint32_t my = base + lane * gridDim.x;
       uint4 m0 = make_uint4(0, 0, 0, 0), m1 = m0, m2 = m0;
@@ -248,14 +276,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         m2 = r[2];
       }
       const uint32_t nb = min(32u, (ntiles - base + gridDim.x - 1) / gridDim.x);
-      for (uint32_t k = 0; k < nb; ++k, ++i) {
+      for (uint32_t k = 0; k < nb; ++k, ++i, rp.next(S)) {
         const uint32_t t = __shfl_sync(0xffffffffu, m0.x, k), eb = __shfl_sync(0xffffffffu, m0.y, k);
         const uint32_t ne = __shfl_sync(0xffffffffu, m0.z, k), pb = __shfl_sync(0xffffffffu, m0.w, k);
         const uint32_t npt = __shfl_sync(0xffffffffu, m1.x, k), cb = __shfl_sync(0xffffffffu, m1.y, k);
         const uint32_t ncam = __shfl_sync(0xffffffffu, m1.z, k);
         const uint64_t aux16 = __shfl_sync(0xffffffffu, m2.x, k), lin16 = __shfl_sync(0xffffffffu, m2.y, k);
-        const int s = static_cast<int>(i % S);
-        if (i >= static_cast<uint32_t>(S)) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+        const uint32_t slot0 = __shfl_sync(0xffffffffu, m2.z, k), nruns = __shfl_sync(0xffffffffu, m2.w, k);
+        const int s = rp.s;
+        if (i >= static_cast<uint32_t>(S)) mbar_wait(&empty[s], rp.ph ^ 1u);
         unsigned char* st = pipe_smem + s * L.stage_bytes;
         const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad;
         const AuxSec as = aux_sections(ne, npt);
@@ -264,10 +293,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         const Span s_cv = span16(d.tcv + static_cast<uint64_t>(cam_stride<A>()) * cb,
                                  sizeof(A) * static_cast<uint64_t>(cam_stride<A>()) * ncam);
         const Span s_z = span16(d.z + pcol0 + 3ull * pb, sizeof(SP) * 3ull * npt);
+        const Span s_r = span16(d.slot_span + slot0, 4ull * nruns);
         const bool small = !(L.dbg & 16);  // experiments: 16 = J rows only
         const uint32_t jrow = ne8 * static_cast<uint32_t>(sizeof(SP));
         const uint32_t total =
-            L.rows * jrow + (small ? as.bytes + ls.bytes + s_p.bytes + s_cv.bytes + (dir ? s_z.bytes : 0u) : 0u);
+            L.rows * jrow +
+            (small ? as.bytes + ls.bytes + s_p.bytes + s_cv.bytes + s_r.bytes + (dir ? s_z.bytes : 0u) : 0u);
         if (lane == 0) {
           uint32_t* h = reinterpret_cast<uint32_t*>(st + L.hdr);
           h[kHT] = t;
@@ -278,10 +309,19 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
           h[kHDcv] = s_cv.delta;
           h[kHPb] = pb;
           h[kHDz] = s_z.delta;
+          h[kHLpt] = as.lpt;
+          h[kHPsl] = as.psl;
+          h[kHPso] = as.pso;
+          h[kHDr] = s_r.delta;
+          h[kHNr] = nruns;
+          h[kHSlot0] = slot0;
+          h[kHCf] = as.cf;
+          h[kHCr] = ls.cr;
+          h[kHW] = ls.w;
           mbar_arrive_expect_tx(&full[s], total);  // releases the header; completes when all bytes land
         }
         __syncwarp();
-        const int ncopies = L.rows + (small ? (dir ? 5 : 4) : 0);
+        const int ncopies = L.rows + (small ? (dir ? 6 : 5) : 0);
         for (int q = lane; q < ncopies; q += 32) {
           if (q < L.rows) {
             bulk_g2s(st + L.J + static_cast<uint32_t>(q) * pipe_jstride<SP>(),
@@ -293,6 +333,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
             case 1: bulk_g2s(st + L.lin, d.tile_lin + 16 * lin16, ls.bytes, &full[s]); break;
             case 2: bulk_g2s(st + L.p, s_p.src, s_p.bytes, &full[s]); break;
             case 3: bulk_g2s(st + L.camv, s_cv.src, s_cv.bytes, &full[s]); break;
+            case 4: bulk_g2s(st + L.runs, s_r.src, s_r.bytes, &full[s]); break;
             default: bulk_g2s(st + L.z, s_z.src, s_z.bytes, &full[s]); break;
           }
         }
@@ -302,7 +343,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
   }
   if (warp == kPipeConsumers / 32 + 1) {
     // ------------------------------------------------------------ preparer
-    for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i) prepare(i);
+    RingPos rp;
+    for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i, rp.next(S)) prepare(rp);
     return;
   }
 
@@ -310,11 +352,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
   const A lam = static_cast<A>(d.st->lambda_solve);
   const int before = d.st->before_scaling;
   const FP lam_fp = static_cast<FP>(d.st->lambda_solve);
-  for (uint32_t i = 0;; ++i) {
+  RingPos rp;
+  for (uint32_t i = 0;; ++i, rp.next(S)) {
     const uint32_t idx = blockIdx.x + i * gridDim.x;
     if (idx >= ntiles) break;
-    const int s = static_cast<int>(i % S);
-    mbar_wait(&ready[s], (i / S) & 1);
+    const int s = rp.s;
+    mbar_wait(&ready[s], rp.ph);
     const unsigned char* st = pipe_smem + s * L.stage_bytes;
     const uint32_t* h = reinterpret_cast<const uint32_t*>(st + L.hdr);
     const uint32_t t = h[kHT], ne = h[kHNe], npt = h[kHNpt], pb = h[kHPb];
@@ -323,19 +366,17 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     constexpr int GS = pipe_jstride<A>() / sizeof(A);    // contribution row stride (elements)
     A* gs = reinterpret_cast<A*>(pipe_smem + s * L.stage_bytes + L.gs);  // per stage: the epilogue of
     // this tile may still read it while the other consumer half starts the next tile
-    const AuxSec as = aux_sections(ne, npt);
-    const LinSec ls = lin_sections<FP>(ne, npt, h[kHNcam], d.jfact != 0, d.w != nullptr);
+    // section offsets of the aux / lin blobs, computed by the producer
     const unsigned char* aux = st + L.aux;
     const unsigned char* lin = st + L.lin;
-    const uint16_t* slc = reinterpret_cast<const uint16_t*>(aux + as.lcam);
-    const uint16_t* slp = reinterpret_cast<const uint16_t*>(aux + as.lpt);
-    const uint16_t* spsl = reinterpret_cast<const uint16_t*>(aux + as.psl);
-    const uint16_t* spso = reinterpret_cast<const uint16_t*>(aux + as.pso);
-    const uint32_t* scpb = reinterpret_cast<const uint32_t*>(aux + as.cpb);
-    const uint8_t* scf = aux + as.cf;
-    const FP* sD = reinterpret_cast<const FP*>(lin + ls.D);
-    const FP* camr = reinterpret_cast<const FP*>(lin + ls.cr);
-    const FP* sw = reinterpret_cast<const FP*>(lin + ls.w);
+    const uint16_t* slc = reinterpret_cast<const uint16_t*>(aux);
+    const uint16_t* slp = reinterpret_cast<const uint16_t*>(aux + h[kHLpt]);
+    const uint16_t* spsl = reinterpret_cast<const uint16_t*>(aux + h[kHPsl]);
+    const uint16_t* spso = reinterpret_cast<const uint16_t*>(aux + h[kHPso]);
+    const uint8_t* scf = aux + h[kHCf];
+    const FP* sD = reinterpret_cast<const FP*>(lin);
+    const FP* camr = reinterpret_cast<const FP*>(lin + h[kHCr]);
+    const FP* sw = reinterpret_cast<const FP*>(lin + h[kHW]);
     const SP* sp = reinterpret_cast<const SP*>(st + L.p + h[kHDp]);
     const A* camv = reinterpret_cast<const A*>(st + L.camv + h[kHDcv]);
     const A* svt = reinterpret_cast<const A*>(st + L.vt);
@@ -405,13 +446,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       // contributions over this edge's own J column (thread j alone reads column j)
 #pragma unroll
       for (int k = 0; k < 3; ++k) gs[(9 + k) * GS + j] = jp[k] * q0 + jp[3 + k] * q1;
-      {
-        const uint32_t prev = __shfl_up_sync(0xffffffffu, lc, 1);
-        const unsigned hm = __ballot_sync(0xffffffffu, valid && (lane == 0 || lc != prev));
-        const unsigned vm = __ballot_sync(0xffffffffu, valid);
-        if (!(L.dbg & 1))
-          camera_runs<A, FP>(g, valid, lane, hm, vm, hm ? scpb[warp] : 0u, gs + 32 * warp, GS, d.part);
-      }
+      // camera contributions too: reduced per camera run after the sync
+#pragma unroll
+      for (int k = 0; k < 9; ++k) gs[k * GS + j] = g[k];
     }
     consumer_sync();
 
@@ -419,7 +456,19 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
     // = point, the same partition as k_hvp_tiles. The other half goes straight
     // on to the next tile's edge phase, so the epilogue overlaps it.
     const uint32_t half = i & 1;
-    if ((static_cast<uint32_t>(tid) / kTileThreads) == half && !(L.dbg & 2)) {
+    if ((static_cast<uint32_t>(tid) / kTileThreads) != half) {
+      // ---- camera runs: the other half, one thread per (run, value), the
+      // association order of chunk_runs_smem (identical to k_hvp_tiles)
+      const uint32_t nr = h[kHNr];
+      const uint32_t* spans = reinterpret_cast<const uint32_t*>(st + L.runs + h[kHDr]);
+      const uint32_t slot0 = h[kHSlot0];
+      for (uint32_t o = tid - (1 - half) * kTileThreads; o < 9 * nr && !(L.dbg & 1); o += kTileThreads) {
+        const uint32_t r = o / 9, k = o - 9 * r;
+        const uint32_t sp2 = spans[r];
+        const A* src = gs + k * GS;
+        run_sum_store<A, FP>(src, sp2 & 0xffffu, sp2 >> 16, d.part + static_cast<uint64_t>(slot0 + r) * 9 + k);
+      }
+    } else if (!(L.dbg & 2)) {
       FP dot = FP(0);
       const uint32_t pi = tid - half * kTileThreads;
       if (pi < npt) {
@@ -479,7 +528,6 @@ __global__ void k_tile_aux(Dev<FP, SP> d) {
   uint16_t* lpt = reinterpret_cast<uint16_t*>(a + as.lpt);
   uint16_t* psl = reinterpret_cast<uint16_t*>(a + as.psl);
   uint16_t* pso = reinterpret_cast<uint16_t*>(a + as.pso);
-  uint32_t* cpb = reinterpret_cast<uint32_t*>(a + as.cpb);
   uint8_t* cf = a + as.cf;
   const uint32_t q0 = d.pt_slot_off[pb];
   for (uint32_t k = threadIdx.x; k < ne8; k += blockDim.x) {
@@ -488,7 +536,29 @@ __global__ void k_tile_aux(Dev<FP, SP> d) {
   }
   for (uint32_t k = threadIdx.x; k < ne; k += blockDim.x) psl[k] = d.pt_slots[q0 + k];
   for (uint32_t k = threadIdx.x; k <= npt; k += blockDim.x) pso[k] = static_cast<uint16_t>(d.pt_slot_off[pb + k] - q0);
-  for (uint32_t k = threadIdx.x; k < nch; k += blockDim.x) cpb[k] = d.chunk_part_base[ch0 + k];
+  // camera-run slot spans: run r of chunk q (slot chunk_part_base[ch0 + q] + r)
+  // covers tile edges [lo, hi), cut at chunk ends like the HVP tile kernels'
+  if (threadIdx.x < 32) {
+    const uint32_t lane = threadIdx.x;
+    for (uint32_t q = 0; q < nch; ++q) {
+      const uint32_t e = 32 * q + lane;
+      const bool valid = e < ne;
+      const uint32_t cam = valid ? d.d_lcam[eb + e] : 0u;
+      const uint32_t prev = __shfl_up_sync(0xffffffffu, cam, 1);
+      const unsigned heads = __ballot_sync(0xffffffffu, valid && (lane == 0 || cam != prev));
+      if ((heads >> lane) & 1u) {
+        const unsigned later = lane == 31 ? 0u : heads & (0xffffffffu << (lane + 1));
+        const uint32_t hi = later ? 32 * q + __ffs(later) - 1 : min(32 * q + 32, ne);
+        const uint32_t slot = d.chunk_part_base[ch0 + q] + __popc(heads & ((1u << lane) - 1u));
+        d.slot_span[slot] = e | (hi << 16);
+      }
+    }
+    if (lane == 0) {
+      uint32_t* mw = const_cast<uint32_t*>(m);
+      mw[kMSlot0] = d.chunk_part_base[ch0];
+      mw[kMNruns] = d.chunk_part_base[ch0 + nch] - d.chunk_part_base[ch0];
+    }
+  }
   for (uint32_t k = threadIdx.x; k < 3 * npt; k += blockDim.x) cf[k] = d.col_free[9ull * d.nc + 3ull * pb + k];
 }
 

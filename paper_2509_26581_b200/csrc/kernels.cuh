@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <utility>
 
 #include "activate.hpp"
 #include "common.cuh"
@@ -105,6 +106,7 @@ struct Dev {
   uint32_t ntcams;            // tile_cam_off[ntiles]
   arith_t<SP>* tcv;           // [ntcams][9]  D*p of each tile's cameras
   unsigned char* tile_aux;    // static per-tile blobs (hvp_pipe.cuh AuxSec)
+  uint32_t* slot_span;        // [nparts] tile-relative edge range [lo, hi) of each camera-run slot (lo | hi << 16)
   unsigned char* tile_lin;    // per-linearization per-tile blobs (LinSec)
   const uint32_t* cam_tc_off;  // [nc+1] camera -> its tile-camera entries (tcv rows)
   const uint32_t* cam_tc_idx;
@@ -267,6 +269,23 @@ __device__ inline void seg_reduce(T (&v)[K], int lane, int run_end) {
   }
 }
 
+// Sum of src[lo, hi) in a fixed association order (4 interleaved partial
+// sums), stored to *dst. Every camera-run reduction of the HVP goes through it,
+// so the tile kernels and the pipelined kernel produce identical bits.
+template <typename A, typename FP>
+__device__ __forceinline__ void run_sum_store(const A* src, uint32_t lo, uint32_t hi, FP* dst) {
+  A a0 = A(0), a1 = A(0), a2 = A(0), a3 = A(0);
+  uint32_t e = lo;
+  for (; e + 4 <= hi; e += 4) {
+    a0 += src[e];
+    a1 += src[e + 1];
+    a2 += src[e + 2];
+    a3 += src[e + 3];
+  }
+  for (; e < hi; ++e) a0 += src[e];
+  *dst = static_cast<FP>((a0 + a1) + (a2 + a3));
+}
+
 // Camera-run sums of a warp chunk from shared memory: the chunk's 32 edges
 // have written their 9 camera values to gw[k * stride + lane]; lane o of the
 // warp produces output o = 9 r + k (run r, value k) as a sequential sum over
@@ -296,71 +315,17 @@ __device__ inline void chunk_runs_smem(const A* gw, int stride, int lane, unsign
     const int nxt = __shfl_sync(0xffffffffu, my_start, min(r + 1, 31));
     if (o >= 9 * R) continue;
     const int stp = r + 1 < R ? nxt : end;
-    const A* src = gw + k * stride;
-    A a0 = A(0), a1 = A(0), a2 = A(0), a3 = A(0);
-    int e = start;
-    for (; e + 4 <= stp; e += 4) {
-      a0 += src[e];
-      a1 += src[e + 1];
-      a2 += src[e + 2];
-      a3 += src[e + 3];
-    }
-    for (; e < stp; ++e) a0 += src[e];
-    part[static_cast<uint64_t>(slot0 + r) * 9 + k] = static_cast<FP>((a0 + a1) + (a2 + a3));
+    run_sum_store<A, FP>(gw + k * stride, start, stp, part + static_cast<uint64_t>(slot0 + r) * 9 + k);
   }
 }
 
-// Camera-run sums of one warp chunk (both HVP tile kernels). The common case
-// of a single run (one camera for all valid lanes) reduces in registers: lanes
-// outside contribute 0 and a 5-stage transpose reduction (xor 16/8/4/2/1
-// exchanging 5/3/2/1/1 values: 12 shuffles, no shared memory) leaves value k
-// of the total in the two lanes 2m, 2m+1 of a fixed m(k). Several runs go
-// through shared memory (chunk_runs_smem). Fixed association orders either
-// way (deterministic), identical in k_hvp_tiles and k_hvp_pipe.
-__device__ inline int rr9_slot(int lane) {
-  const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
-  const int q = b2 ? (b1 ? -1 : 2) : b1;                         // position in the stage-2 list
-  const int p = q < 0 ? -1 : (b3 ? (q == 2 ? -1 : 3 + q) : q);  // position in the stage-1 list
-  if (p < 0) return -1;
-  return b4 ? (p < 4 ? 5 + p : -1) : p;
-}
-
+// Camera-run sums of one warp chunk (k_hvp_tiles): the chunk's edges stage
+// their 9 camera values in shared memory and chunk_runs_smem sums each run in
+// run_sum_store order, the order k_hvp_pipe uses tile-wide (identical bits).
 template <typename A, typename FP>
-__device__ inline void camera_runs(const A (&g)[9], bool valid, int lane, unsigned hm, unsigned vm, uint32_t slot0,
-                                   A* gw, int stride, FP* part) {
+__device__ inline void camera_runs(const A (&g)[9], int lane, unsigned hm, unsigned vm, uint32_t slot0, A* gw,
+                                   int stride, FP* part) {
   if (!hm) return;
-  if (__popc(hm) == 1) {
-    const unsigned full = 0xffffffffu;
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-    A a[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) a[k] = valid ? g[k] : A(0);
-    A k1[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const A hi = i < 4 ? a[5 + i] : A(0);
-      k1[i] = b4 ? hi : a[i];
-      k1[i] += __shfl_xor_sync(full, b4 ? a[i] : hi, 16);
-    }
-    A k2[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const A hi = i < 2 ? k1[3 + i] : A(0);
-      k2[i] = b3 ? hi : k1[i];
-      k2[i] += __shfl_xor_sync(full, b3 ? k1[i] : hi, 8);
-    }
-    A k3[2];
-    k3[0] = b2 ? k2[2] : k2[0];
-    k3[1] = b2 ? A(0) : k2[1];
-    k3[0] += __shfl_xor_sync(full, b2 ? k2[0] : k2[2], 4);
-    k3[1] += __shfl_xor_sync(full, b2 ? k2[1] : A(0), 4);
-    A v = b1 ? k3[1] : k3[0];
-    v += __shfl_xor_sync(full, b1 ? k3[0] : k3[1], 2);
-    v += __shfl_xor_sync(full, v, 1);
-    const int slot = (lane & 1) ? -1 : rr9_slot(lane);
-    if (slot >= 0) part[static_cast<uint64_t>(slot0) * 9 + slot] = static_cast<FP>(v);
-    return;
-  }
 #pragma unroll
   for (int k = 0; k < 9; ++k) gw[k * stride + lane] = g[k];
   __syncwarp();
@@ -1151,8 +1116,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d,
       const uint32_t prev = __shfl_up_sync(0xffffffffu, cam, 1);
       const unsigned hm = __ballot_sync(0xffffffffu, valid && (lane == 0 || cam != prev));
       const unsigned vm = __ballot_sync(0xffffffffu, valid);
-      camera_runs<A, FP>(g, valid, lane, hm, vm, hm ? d.chunk_part_base[chunk] : 0u, gsh + (tid & ~31), kGsStride,
-                         d.part);
+      camera_runs<A, FP>(g, lane, hm, vm, hm ? d.chunk_part_base[chunk] : 0u, gsh + (tid & ~31), kGsStride, d.part);
     }
     A h[3];
 #pragma unroll
@@ -1233,6 +1197,67 @@ __global__ void k_make_vt(Dev<FP, SP> d) {
 // 32 lanes), i.e. plain FMAs over shared memory instead of shuffle trees.
 // Dynamic shared memory: see lin_normal_smem().
 constexpr int kLinRow = 22;  // Jc (18) + w r (2) + w (1) + pad per staged edge (16-byte rows)
+constexpr int kLinShflRuns = 3;  // chunks with at most this many camera runs reduce in registers
+
+// One edge's contribution to camera value V of its run: V < 9 is b_V = Jc0V w r0
+// + Jc1V w r1, V in [9, 54) is H(i, j) = w (Jc0i Jc0j + Jc1i Jc1j) (packed upper).
+template <typename FP, int V>
+__device__ __forceinline__ FP lin_cam_value(const FP* jc, FP wr0, FP wr1, FP w) {
+  if constexpr (V < 9) {
+    return jc[V] * wr0 + jc[9 + V] * wr1;
+  } else if constexpr (V >= kLinVals) {
+    return FP(0);
+  } else {
+    constexpr int i = p9row(V - 9), k = p9col(V - 9);
+    return w * (jc[i] * jc[k] + jc[9 + i] * jc[9 + k]);
+  }
+}
+
+// first butterfly step (xor 16): values I and I + 32 generated in pairs
+template <typename FP, int... I>
+__device__ __forceinline__ void lin_shfl_first(FP* v, bool hi, const FP* jc, FP wr0, FP wr1, FP w,
+                                               std::integer_sequence<int, I...>) {
+  ((v[I] = [&] {
+     const FP a = lin_cam_value<FP, I>(jc, wr0, wr1, w);
+     const FP b = lin_cam_value<FP, I + 32>(jc, wr0, wr1, w);
+     return (hi ? b : a) + __shfl_xor_sync(0xffffffffu, hi ? a : b, 16);
+   }()),
+   ...);
+}
+
+template <typename FP, int O>
+__device__ __forceinline__ void lin_shfl_step(FP* v, int lane) {
+  const bool hi = lane & O;
+#pragma unroll
+  for (int i = 0; i < 2 * O; ++i) {
+    const FP keep = hi ? v[i + 2 * O] : v[i], send = hi ? v[i] : v[i + 2 * O];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+  }
+}
+
+// Sum of the 54 camera values over the lanes with `in` set, written to dst[0,
+// 54). Lanes outside zero their inputs (so their values are exactly +0, even
+// where a Jacobian entry is not finite); then a transposing butterfly (each xor step halves the values a lane holds,
+// 62 fp64 shuffles per warp) instead of shared-memory staging; lane l ends
+// with values 2l and 2l+1.
+template <typename FP>
+__device__ __forceinline__ void lin_cam_shfl(bool in, const FP* jc_in, FP wr0, FP wr1, FP w, int lane, FP* dst) {
+  FP jc[18];
+#pragma unroll
+  for (int k = 0; k < 18; ++k) jc[k] = in ? jc_in[k] : FP(0);
+  if (!in) wr0 = wr1 = w = FP(0);
+  FP v[32];
+  lin_shfl_first<FP>(v, (lane & 16) != 0, jc, wr0, wr1, w, std::make_integer_sequence<int, 32>{});
+  lin_shfl_step<FP, 8>(v, lane);
+  lin_shfl_step<FP, 4>(v, lane);
+  lin_shfl_step<FP, 2>(v, lane);
+  lin_shfl_step<FP, 1>(v, lane);
+  if (2 * lane < kLinVals) {
+    dst[2 * lane] = v[0];
+    dst[2 * lane + 1] = v[1];
+  }
+}
+
 template <typename FP>
 struct Pair;
 template <>
@@ -1250,7 +1275,7 @@ __host__ __device__ constexpr size_t lin_normal_smem() {
 }
 
 template <typename FP, typename SP, bool STORE, bool AUTO>
-__global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int force) {
+__global__ void __launch_bounds__(kTileThreads, 2) k_lin_normal(Dev<FP, SP> d, int force) {
   if (!force && !d.st->do_linearize) return;
   extern __shared__ __align__(16) unsigned char lin_smem[];
   FP* sX = reinterpret_cast<FP*>(lin_smem);
@@ -1298,18 +1323,6 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
   }
   if (d.w && valid) d.w[e] = w;
   const FP wr0 = valid ? w * res[0] : FP(0), wr1 = valid ? w * res[1] : FP(0);
-  FP* row = sJ + tid * kLinRow;
-#pragma unroll
-  // row layout: 10 pairs (Jc0[k], Jc1[k]) k < 9, (w r0, w r1), then w: a
-  // reduction lane reads both rows' operands of one column with one 2-wide load
-  for (int k = 0; k < 9; ++k) {
-    row[2 * k] = valid ? jc[k] : FP(0);
-    row[2 * k + 1] = valid ? jc[9 + k] : FP(0);
-  }
-  row[18] = wr0;
-  row[19] = wr1;
-  row[20] = w;
-  row[21] = FP(0);
   if (valid) {
     FP* pv = pst + j * 9;
     pv[0] = jp[0] * wr0 + jp[3] * wr1;
@@ -1327,6 +1340,34 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
   const uint32_t prev = __shfl_up_sync(full, lc, 1);
   const unsigned hm = __ballot_sync(full, valid && (lane == 0 || lc != prev));
   const unsigned vm = __ballot_sync(full, valid);
+  const uint32_t slot0 = d.chunk_part_base[d.tile_chunk_base[t] + c0 / 32 + warp];
+  if (__popc(hm) <= kLinShflRuns) {
+    // few runs (the common case: a tile's edges are camera-sorted): one
+    // register butterfly per run
+    unsigned heads = hm;
+    uint32_t run = 0;
+    while (heads) {
+      const int start = __ffs(heads) - 1;
+      heads &= heads - 1;
+      const int stop = heads ? __ffs(heads) - 1 : 32 - __clz(vm);
+      lin_cam_shfl<FP>(lane >= start && lane < stop, jc, wr0, wr1, w, lane,
+                       d.part + static_cast<uint64_t>(slot0 + run) * kLinVals);
+      ++run;
+    }
+    continue;
+  }
+  FP* row = sJ + tid * kLinRow;
+#pragma unroll
+  // row layout: 10 pairs (Jc0[k], Jc1[k]) k < 9, (w r0, w r1), then w: a
+  // reduction lane reads both rows' operands of one column with one 2-wide load
+  for (int k = 0; k < 9; ++k) {
+    row[2 * k] = valid ? jc[k] : FP(0);
+    row[2 * k + 1] = valid ? jc[9 + k] : FP(0);
+  }
+  row[18] = wr0;
+  row[19] = wr1;
+  row[20] = w;
+  row[21] = FP(0);
   __syncwarp();
   // camera side: lane owns values v0 = lane and v1 = lane + 32 (< 54);
   // value v < 9: b_v = sum Jc0v wr0 + Jc1v wr1; v >= 9: H(i,j) = sum w (Jc0i Jc0j + Jc1i Jc1j)
@@ -1338,7 +1379,6 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
   const int k0 = isb ? 9 : p9col(lane - 9);
   const int i1 = has1 ? p9row(lane + 32 - 9) : 0;
   const int j1 = has1 ? p9col(lane + 32 - 9) : 0;
-  const uint32_t slot0 = d.chunk_part_base[d.tile_chunk_base[t] + c0 / 32 + warp];
   unsigned heads = hm;
   uint32_t run = 0;
   while (heads) {
@@ -1363,8 +1403,9 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_normal(Dev<FP, SP> d, int 
     if (has1) dst[32 + lane] = acc1;
     ++run;
   }
-  __syncthreads();
+  __syncwarp();  // this warp's staged rows are rewritten next pass
   }
+  __syncthreads();  // pst complete
 
   // point epilogue (same as the generic kernel)
   FP gmax = FP(0);

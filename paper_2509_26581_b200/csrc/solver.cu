@@ -465,6 +465,7 @@ class Solver final : public SolverBase {
       b += rows * sJ * ns + aux + lin;                 // J rows, static and per-linearization tile blobs
       b += np3 * (sV + sV);                            // p in, ap out
       b += d.ntcams * (cam_stride<A>() * sA * 2 + 4.0);  // tcv gather (tile_cams, write) + tile read
+      b += 4.0 * nparts;                               // camera-run slot spans
     } else {
       b += (d.J ? 24 * sJ * ns : 0) + ns * (4 + 2);    // J, camera and point indices
       b += np3 * (sA + sV + sF + sV + 1);              // vt, p, D in; ap out; free mask
@@ -1084,6 +1085,7 @@ class Solver final : public SolverBase {
       d.tile_meta = nullptr;
       d.tcv = nullptr;
       d.tile_aux = nullptr;
+      d.slot_span = nullptr;
       d.tile_lin = nullptr;
       d.ntcams = act_.tile_cam_off.empty() ? 0 : act_.tile_cam_off.back();
       if (pipe_ok_) {
@@ -1113,6 +1115,7 @@ class Solver final : public SolverBase {
         if (aux16 > 0xffffffffull || lin16 > 0xffffffffull) throw std::invalid_argument("tile blobs exceed 64 GB");
         d.tile_meta = to_dev(b_tmeta_, meta);
         d.tile_aux = static_cast<unsigned char*>(b_taux_.alloc(std::max<uint64_t>(16, 16 * aux16)));
+        d.slot_span = static_cast<uint32_t*>(b_sspan_.alloc(std::max<uint64_t>(4, 4ull * act_.nparts)));
         d.tile_lin = static_cast<unsigned char*>(b_tlin_.alloc(std::max<uint64_t>(16, 16 * lin16)));
         d.tcv = static_cast<A*>(b_tcv_.alloc(std::max<uint64_t>(1, cam_stride<A>() * uint64_t(d.ntcams)) * sizeof(A)));
         CK(cudaMemsetAsync(d.tcv, 0, std::max<uint64_t>(1, cam_stride<A>() * uint64_t(d.ntcams)) * sizeof(A), s_));
@@ -1572,7 +1575,7 @@ class Solver final : public SolverBase {
   bool pipe_ok_ = false;
   uint32_t sms_ = 148;
   unsigned pt_occ_ = 4;
-  DBuf b_tmeta_, b_tcv_, b_taux_, b_tlin_;
+  DBuf b_tmeta_, b_tcv_, b_taux_, b_tlin_, b_sspan_;
   bool pipe_aux_pending_ = false;
   DBuf b_camtc_idx_, b_camtc_off_, b_dir_rb_, b_dir_re_;
   const uint64_t* dir_rbeg_ = nullptr;
