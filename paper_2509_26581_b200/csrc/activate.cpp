@@ -213,7 +213,8 @@ void activate(const ActivationInput& in, Activation& out) {
 
   // device edge order: active edges sorted by camera (stable in a), then
   // stably bucketed by tile -> inside a tile: (camera, a). Tiles start on
-  // kEdgePad boundaries; the padding slots are dummies.
+  // kJBlock boundaries (one J store block per normal tile); the padding slots
+  // are dummies.
   std::vector<uint32_t> order;
   {
     std::vector<uint32_t> all(na);
@@ -231,7 +232,7 @@ void activate(const ActivationInput& in, Activation& out) {
   for (uint32_t t = 0; t < out.ntiles; ++t) {
     out.tile_ecnt[t] = real_beg[t + 1] - real_beg[t];
     out.tile_ebeg[t] = static_cast<uint32_t>(slot);
-    slot += (out.tile_ecnt[t] + kEdgePad - 1) / kEdgePad * kEdgePad;
+    slot += (out.tile_ecnt[t] + kJBlock - 1) / kJBlock * kJBlock;
   }
   if (slot > 0xffffffffull) throw std::invalid_argument("more than 2^32 padded edge slots");
   out.tile_ebeg[out.ntiles] = static_cast<uint32_t>(slot);

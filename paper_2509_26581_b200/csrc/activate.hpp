@@ -19,6 +19,7 @@ constexpr int kTileThreads = 256;  // CTA size of every tile kernel
 constexpr int kTileEdges = 512;    // max edges of a normal tile (SMEM staging of the point side)
 constexpr int kTilePoints = 256;   // max points of a tile
 constexpr int kEdgePad = 8;        // tile edge ranges start on 8-edge boundaries (16-byte aligned rows)
+constexpr int kJBlock = kTileEdges;  // tile slot ranges are padded to whole 512-slot blocks (J store blocks)
 constexpr int kTileCams = 64;      // max distinct cameras of a normal tile (SMEM camera staging)
 constexpr uint32_t kNoKey = 0xffffffffu;
 
@@ -54,7 +55,7 @@ struct Activation {
   std::vector<uint32_t> tile_ebeg, tile_pbeg, tile_chunk_base;  // size ntiles+1; tile_ebeg padded
   std::vector<uint32_t> tile_ecnt;                              // real edges of each tile
   std::vector<uint32_t> normal_tiles, heavy_tiles;              // tile ids by kind
-  uint64_t n_slots = 0;                                         // padded device edge slots (multiple of kEdgePad)
+  uint64_t n_slots = 0;                                         // padded device edge slots (multiple of kJBlock)
   // device edge order d (tile-major, camera then factor index inside a tile),
   // padded: slots [tile_ebeg[t] + tile_ecnt[t], tile_ebeg[t+1]) are dummies
   std::vector<uint32_t> d_a;    // d -> active factor a (kNoKey for padding)

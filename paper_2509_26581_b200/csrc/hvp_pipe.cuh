@@ -40,7 +40,7 @@ __host__ __device__ constexpr int cam_stride() {
 // byte stride of one J row (and of one contribution row) in shared memory
 template <typename T>
 __host__ __device__ constexpr uint32_t pipe_jstride() {
-  return static_cast<uint32_t>(kTileEdges * sizeof(T) + 16);
+  return static_cast<uint32_t>(jstore_stride<T>() * sizeof(T));  // == the J store block's row stride
 }
 
 // Section offsets inside a tile's aux blob (static) and lin blob (per
@@ -286,7 +286,6 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         const int s = rp.s;
         if (i >= static_cast<uint32_t>(S)) mbar_wait(&empty[s], rp.ph ^ 1u);
         unsigned char* st = pipe_smem + s * L.stage_bytes;
-        const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad;
         const AuxSec as = aux_sections(ne, npt);
         const LinSec ls = lin_sections<FP>(ne, npt, ncam, d.jfact != 0, d.w != nullptr);
         const Span s_p = span16(d.p + pcol0 + 3ull * pb, sizeof(SP) * 3ull * npt);
@@ -295,9 +294,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         const Span s_z = span16(d.z + pcol0 + 3ull * pb, sizeof(SP) * 3ull * npt);
         const Span s_r = span16(d.slot_span + slot0, 4ull * nruns);
         const bool small = !(L.dbg & 16);  // experiments: 16 = J rows only
-        const uint32_t jrow = ne8 * static_cast<uint32_t>(sizeof(SP));
+        const uint32_t jblock = static_cast<uint32_t>(L.rows) * pipe_jstride<SP>();
         const uint32_t total =
-            L.rows * jrow +
+            jblock +
             (small ? as.bytes + ls.bytes + s_p.bytes + s_cv.bytes + s_r.bytes + (dir ? s_z.bytes : 0u) : 0u);
         if (lane == 0) {
           uint32_t* h = reinterpret_cast<uint32_t*>(st + L.hdr);
@@ -321,19 +320,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
           mbar_arrive_expect_tx(&full[s], total);  // releases the header; completes when all bytes land
         }
         __syncwarp();
-        const int ncopies = L.rows + (small ? (dir ? 6 : 5) : 0);
+        const int ncopies = 1 + (small ? (dir ? 6 : 5) : 0);
         for (int q = lane; q < ncopies; q += 32) {
-          if (q < L.rows) {
-            bulk_g2s(st + L.J + static_cast<uint32_t>(q) * pipe_jstride<SP>(),
-                     d.J + static_cast<uint64_t>(q) * d.na + eb, jrow, &full[s]);
-            continue;
-          }
-          switch (q - L.rows) {
-            case 0: bulk_g2s(st + L.aux, d.tile_aux + 16 * aux16, as.bytes, &full[s]); break;
-            case 1: bulk_g2s(st + L.lin, d.tile_lin + 16 * lin16, ls.bytes, &full[s]); break;
-            case 2: bulk_g2s(st + L.p, s_p.src, s_p.bytes, &full[s]); break;
-            case 3: bulk_g2s(st + L.camv, s_cv.src, s_cv.bytes, &full[s]); break;
-            case 4: bulk_g2s(st + L.runs, s_r.src, s_r.bytes, &full[s]); break;
+          switch (q) {
+            case 0: bulk_g2s(st + L.J, d.J + jidx<SP>(eb, 0, L.rows), jblock, &full[s]); break;  // the tile's J block
+            case 1: bulk_g2s(st + L.aux, d.tile_aux + 16 * aux16, as.bytes, &full[s]); break;
+            case 2: bulk_g2s(st + L.lin, d.tile_lin + 16 * lin16, ls.bytes, &full[s]); break;
+            case 3: bulk_g2s(st + L.p, s_p.src, s_p.bytes, &full[s]); break;
+            case 4: bulk_g2s(st + L.camv, s_cv.src, s_cv.bytes, &full[s]); break;
+            case 5: bulk_g2s(st + L.runs, s_r.src, s_r.bytes, &full[s]); break;
             default: bulk_g2s(st + L.z, s_z.src, s_z.bytes, &full[s]); break;
           }
         }

@@ -360,22 +360,42 @@ __device__ inline RunInfo run_info(uint32_t cam, bool valid, uint32_t chunk_slot
 // operator is exactly J; it moves 16 instead of 24 values per edge.
 constexpr int kJFactRows = 16;
 
+// J store layout: blocks of kJBlock slots (a normal tile is exactly one block,
+// so the pipelined HVP moves it with ONE bulk copy); inside a block, row k of
+// the tile's J at a padded row stride (16 bytes of padding spread the shared-
+// memory banks of the HVP's contribution rows that overlay it).
+template <typename SP>
+__host__ __device__ constexpr int jstore_stride() {
+  return static_cast<int>((kJBlock * sizeof(SP) + 16) / sizeof(SP));
+}
+template <typename SP>
+__host__ __device__ inline uint64_t jidx(uint32_t e, int k, int rows) {
+  static_assert(kJBlock == 512, "block index by shift");
+  return static_cast<uint64_t>(e >> 9) * (static_cast<uint64_t>(rows) * jstore_stride<SP>()) +
+         static_cast<uint64_t>(k) * jstore_stride<SP>() + (e & 511u);
+}
+// elements of the J store for ns slots (a multiple of kJBlock)
+template <typename SP>
+__host__ __device__ inline uint64_t jstore_elems(uint64_t ns, int rows) {
+  return (ns + kJBlock - 1) / kJBlock * static_cast<uint64_t>(rows) * jstore_stride<SP>();
+}
+
 template <typename FP, typename SP>
 __device__ inline void store_J(const Dev<FP, SP>& d, uint32_t e, const FP* jc, const FP* jp, const FP* fac) {
-  const uint64_t na = d.na;
   if (d.jfact) {
+    constexpr int R = kJFactRows;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      d.J[k * na + e] = narrow<SP>(jc[k]);
-      d.J[(3 + k) * na + e] = narrow<SP>(jc[9 + k]);
+      d.J[jidx<SP>(e, k, R)] = narrow<SP>(jc[k]);
+      d.J[jidx<SP>(e, 3 + k, R)] = narrow<SP>(jc[9 + k]);
     }
 #pragma unroll
-    for (int k = 0; k < 10; ++k) d.J[(6 + k) * na + e] = narrow<SP>(fac[k]);
+    for (int k = 0; k < 10; ++k) d.J[jidx<SP>(e, 6 + k, R)] = narrow<SP>(fac[k]);
   } else {
 #pragma unroll
-    for (int k = 0; k < 18; ++k) d.J[k * na + e] = narrow<SP>(jc[k]);
+    for (int k = 0; k < 18; ++k) d.J[jidx<SP>(e, k, 24)] = narrow<SP>(jc[k]);
 #pragma unroll
-    for (int k = 0; k < 6; ++k) d.J[(18 + k) * na + e] = narrow<SP>(jp[k]);
+    for (int k = 0; k < 6; ++k) d.J[jidx<SP>(e, 18 + k, 24)] = narrow<SP>(jp[k]);
   }
 }
 
@@ -383,18 +403,19 @@ template <typename FP, typename SP>
 __device__ inline void load_J(const Dev<FP, SP>& d, uint32_t e, uint32_t cam, arith_t<SP>* jc, arith_t<SP>* jp) {
   using A = arith_t<SP>;
   const SP* J = d.J;
-  const uint64_t na = d.na;
   if constexpr (std::is_same<SP, FP>::value) {
     if (d.jfact) {
+      constexpr int RR = kJFactRows;
       FP U[6], R[9];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        jc[k] = J[k * na + e];
-        jc[9 + k] = J[(3 + k) * na + e];
+        jc[k] = J[jidx<SP>(e, k, RR)];
+        jc[9 + k] = J[jidx<SP>(e, 3 + k, RR)];
       }
 #pragma unroll
-      for (int k = 0; k < 6; ++k) U[k] = J[(6 + k) * na + e];
-      const FP dist = J[12 * na + e], n = J[13 * na + e], p0 = J[14 * na + e], p1 = J[15 * na + e];
+      for (int k = 0; k < 6; ++k) U[k] = J[jidx<SP>(e, 6 + k, RR)];
+      const FP dist = J[jidx<SP>(e, 12, RR)], n = J[jidx<SP>(e, 13, RR)];
+      const FP p0 = J[jidx<SP>(e, 14, RR)], p1 = J[jidx<SP>(e, 15, RR)];
       const FP* rf = d.Rf + 10ull * cam;
 #pragma unroll
       for (int k = 0; k < 9; ++k) R[k] = rf[k];
@@ -409,9 +430,9 @@ __device__ inline void load_J(const Dev<FP, SP>& d, uint32_t e, uint32_t cam, ar
     }
   }
 #pragma unroll
-  for (int k = 0; k < 18; ++k) jc[k] = widen<A>(J[k * na + e]);
+  for (int k = 0; k < 18; ++k) jc[k] = widen<A>(J[jidx<SP>(e, k, 24)]);
 #pragma unroll
-  for (int k = 0; k < 6; ++k) jp[k] = widen<A>(J[(18 + k) * na + e]);
+  for (int k = 0; k < 6; ++k) jp[k] = widen<A>(J[jidx<SP>(e, 18 + k, 24)]);
 }
 
 // Full 24-value rows from either store (LinearSystem accessor surface).

@@ -462,12 +462,12 @@ class Solver final : public SolverBase {
         lin += lin_sections<FP>(ne, npt, ncam, d.jfact != 0, d.w != nullptr).bytes;
       }
       const double rows = d.jfact ? kJFactRows : 24;
-      b += rows * sJ * ns + aux + lin;                 // J rows, static and per-linearization tile blobs
+      b += jstore_elems<SP>(act_.n_slots, static_cast<int>(rows)) * sJ + aux + lin;  // J blocks, tile blobs
       b += np3 * (sV + sV);                            // p in, ap out
       b += d.ntcams * (cam_stride<A>() * sA * 2 + 4.0);  // tcv gather (tile_cams, write) + tile read
       b += 4.0 * nparts;                               // camera-run slot spans
     } else {
-      b += (d.J ? 24 * sJ * ns : 0) + ns * (4 + 2);    // J, camera and point indices
+      b += (d.J ? jstore_elems<SP>(act_.n_slots, 24) * sJ : 0) + ns * (4 + 2);  // J, camera and point indices
       b += np3 * (sA + sV + sF + sV + 1);              // vt, p, D in; ap out; free mask
       b += act_.np * 4.0 + ns * 2;                     // point slot lists
     }
@@ -946,7 +946,7 @@ class Solver final : public SolverBase {
     for (uint32_t t = 0; t < T; ++t) {
       act_.tile_ecnt[t] = real_beg[t + 1] - real_beg[t];
       act_.tile_ebeg[t] = static_cast<uint32_t>(slot);
-      slot += (act_.tile_ecnt[t] + kEdgePad - 1) / kEdgePad * kEdgePad;
+      slot += (act_.tile_ecnt[t] + kJBlock - 1) / kJBlock * kJBlock;
       act_.tile_chunk_base[t + 1] = act_.tile_chunk_base[t] + (act_.tile_ecnt[t] + 31) / 32;
     }
     if (slot > 0xffffffffull) throw std::invalid_argument("more than 2^32 padded edge slots");
@@ -1064,8 +1064,9 @@ class Solver final : public SolverBase {
     d.jfact = (!dyn && g_.diff_mode == GB_ANALYTIC && std::is_same<SP, FP>::value) ? 1 : 0;
     if (const char* e = std::getenv("GB_JFACT")) d.jfact = d.jfact && std::atoi(e) != 0;
     const uint64_t jrows = d.jfact ? kJFactRows : 24;
-    d.J = dyn ? nullptr : static_cast<SP*>(b_J_.alloc(jrows * ns * sizeof(SP)));
-    if (d.J) CK(cudaMemsetAsync(d.J, 0, jrows * ns * sizeof(SP), s_));  // padding slots stay 0
+    const uint64_t jbytes = jstore_elems<SP>(ns, static_cast<int>(jrows)) * sizeof(SP);
+    d.J = dyn ? nullptr : static_cast<SP*>(b_J_.alloc(jbytes));
+    if (d.J) CK(cudaMemsetAsync(d.J, 0, jbytes, s_));  // padding slots stay 0
     d.Rf = d.jfact ? static_cast<FP*>(b_Rf_.alloc(std::max<uint64_t>(1, 10 * nc) * sizeof(FP))) : nullptr;
     d.cpre = static_cast<FP*>(b_cpre_.alloc(std::max<uint64_t>(1, kCamPre * nc) * sizeof(FP)));
     d.cpre_new = static_cast<FP*>(b_cpre_new_.alloc(std::max<uint64_t>(1, kCamPre * nc) * sizeof(FP)));
