@@ -224,6 +224,15 @@ int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_per_hvp, double* ms_tiles_
  *              SURVEY.md §8(d) (the roofline's "algorithmic bytes"). */
 int gb_hvp_bytes(gb_graph* g, double* kernel_bytes, double* reference_bytes);
 
+/* gb_host_alloc / gb_host_free  page-locked host memory for the caller's
+ *              camera / point arrays (bal::BalGraph owns its AoS arrays,
+ *              adapter.hpp:82-90), so the solve's upload and in-place write-
+ *              back run at full host-link rate. Freed blocks are cached for the
+ *              next graph. gb_host_alloc returns NULL when no device is usable
+ *              (the caller then uses ordinary memory). */
+void* gb_host_alloc(uint64_t bytes);
+void gb_host_free(void* p);
+
 /* ---- multi-GPU sharding (no reference counterpart: the reference is a
  * single-process CPU solver) -------------------------------
  * One process (or host thread) per shard. Every rank registers the FULL

@@ -269,6 +269,36 @@ def device_backend() -> Backend:
     return Backend(_abi.lib(), "gb_")
 
 
+class _PinnedBlock:
+    """A gb_host_alloc block exposed to numpy; freed (returned to the
+    library's cache) when the last array viewing it goes away."""
+
+    def __init__(self, backend: "Backend", nbytes: int):
+        self._free = backend.fn("host_free")
+        self.ptr = backend.fn("host_alloc")(max(1, nbytes))
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (self.ptr or 0, False),
+                                    "version": 3}
+
+    def __del__(self):
+        if self.ptr:
+            self._free(self.ptr)
+            self.ptr = None
+
+
+def _owned_array(src, dtype, backend: "Backend") -> np.ndarray:
+    """A contiguous copy of src owned by the graph: page-locked memory from the
+    device library when available (full-rate upload and write-back), else an
+    ordinary numpy copy."""
+    a = np.ascontiguousarray(src, dtype=dtype)
+    if backend.prefix == "gb_" and a.nbytes:
+        blk = _PinnedBlock(backend, a.nbytes)
+        if blk.ptr:
+            out = np.asarray(blk).view(a.dtype).reshape(a.shape)
+            np.copyto(out, a)
+            return out
+    return a.copy()
+
+
 class BalGraph:
     """bal::BalGraph (adapter.hpp:82-100): owns the camera and point arrays
     (AoS, graph precision) that the solver refines IN PLACE."""
@@ -285,8 +315,8 @@ class BalGraph:
         self.backend = backend or device_backend()
         self.FP, self.SP, self.A = dtypes(precision)
         self.num_observations = problem.num_observations
-        self.cameras = np.ascontiguousarray(problem.cameras, dtype=self.FP).copy()
-        self.points = np.ascontiguousarray(problem.points, dtype=self.FP).copy()
+        self.cameras = _owned_array(problem.cameras, self.FP, self.backend)
+        self.points = _owned_array(problem.points, self.FP, self.backend)
         self._cam_idx = np.ascontiguousarray(problem.camera_index, dtype=np.uint32)
         self._pt_idx = np.ascontiguousarray(problem.point_index, dtype=np.uint32)
         self._obs = np.ascontiguousarray(problem.observations, dtype=self.FP)

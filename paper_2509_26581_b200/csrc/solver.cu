@@ -141,6 +141,60 @@ class BlockCache {
   std::map<int, size_t> total_;
 };
 
+// Page-locked host blocks for graph-owned parameter arrays (gb_host_alloc):
+// uploads and write-backs from them run at full PCIe/C2C rate. Freed blocks
+// are kept for the next graph (reuse when at most 2x the request, at most
+// 8 GiB held), like the device BlockCache above.
+class HostCache {
+ public:
+  static HostCache& get() {
+    static HostCache c;
+    return c;
+  }
+  void* alloc(size_t bytes) {
+    if (!bytes) bytes = 1;
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      auto it = free_.lower_bound(bytes);
+      if (it != free_.end() && it->first <= 2 * bytes) {
+        void* p = it->second;
+        held_ -= it->first;
+        size_[p] = it->first;
+        free_.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(m_);
+    size_[p] = bytes;
+    return p;
+  }
+  void release(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(m_);
+    auto it = size_.find(p);
+    if (it == size_.end()) return;
+    const size_t bytes = it->second;
+    size_.erase(it);
+    if (held_ + bytes > (size_t(8) << 30)) {
+      cudaFreeHost(p);
+      return;
+    }
+    free_.emplace(bytes, p);
+    held_ += bytes;
+  }
+
+ private:
+  std::mutex m_;
+  std::multimap<size_t, void*> free_;
+  std::map<void*, size_t> size_;
+  size_t held_ = 0;
+};
+
 class DBuf {
  public:
   static constexpr size_t kSlack = 64;
@@ -1786,6 +1840,10 @@ int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_pair, double* ms_tiles) {
 int gb_hvp_bytes(gb_graph* g, double* kernel_bytes, double* reference_bytes) {
   return guarded([&] { g->get().hvp_bytes(kernel_bytes, reference_bytes); });
 }
+
+void* gb_host_alloc(uint64_t bytes) { return gb::HostCache::get().alloc(static_cast<size_t>(bytes)); }
+
+void gb_host_free(void* p) { gb::HostCache::get().release(p); }
 
 int gb_nccl_unique_id(void* out128) {
   return guarded([&] { gb::nccl_unique_id(out128); });
