@@ -1810,7 +1810,8 @@ __global__ void __launch_bounds__(kTileThreads) k_chi2_tiles(Dev<FP, SP> d, cons
   const uint32_t eb = d.tile_ebeg[t], ee = eb + d.tile_ecnt[t], pb = d.tile_pbeg[t];
   const uint64_t pcol0 = 9ull * d.nc;
   FP chi = FP(0);
-  for (uint32_t e = eb + threadIdx.x; e < ee; e += blockDim.x) {
+#pragma unroll 2
+  for (uint32_t e = eb + threadIdx.x; e < ee; e += blockDim.x) {  // unrolled: both edges' loads in flight
     const uint32_t cam = d.d_cam[e];
     FP cp[9];
 #pragma unroll
