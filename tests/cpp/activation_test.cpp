@@ -27,6 +27,8 @@ static void check(const gb::Activation& a, uint64_t np_local, bool sharded) {
   uint64_t real = 0;
   for (uint32_t t = 0; t < a.ntiles; ++t) {
     REQUIRE(a.tile_ebeg[t] % gb::kEdgePad == 0);
+    REQUIRE(a.tile_ebeg[t] % gb::kJBlock == 0);  // one J store block per normal tile
+    REQUIRE(a.tile_ebeg[t + 1] - a.tile_ebeg[t] == (a.tile_ecnt[t] + gb::kJBlock - 1) / gb::kJBlock * gb::kJBlock);
     REQUIRE(a.tile_ebeg[t] + a.tile_ecnt[t] <= a.tile_ebeg[t + 1]);
     real += a.tile_ecnt[t];
     const uint32_t npt = a.tile_pbeg[t + 1] - a.tile_pbeg[t];

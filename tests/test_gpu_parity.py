@@ -256,6 +256,25 @@ def test_deterministic(gpu, ladybug):
     assert outs[0][2] == outs[1][2]
 
 
+def test_page_locked_graph_arrays(gpu, ladybug):
+    """bal::BalGraph's own arrays (adapter.hpp:82-90) live in gb_host_alloc
+    memory; an array kept past its graph stays valid (the block is not handed
+    to the next graph while any view of it is alive)."""
+    g = bal.build_graph(ladybug, "fp64")
+    owner = g.cameras
+    while owner is not None and not isinstance(owner, bal._PinnedBlock):
+        owner = getattr(owner, "base", None)
+    assert owner is not None and owner.ptr
+    bal.levenberg_marquardt(g, bal_cfg(3))
+    kept = g.cameras
+    snap = kept.copy()
+    del g
+    g2 = bal.build_graph(ladybug, "fp64")
+    bal.levenberg_marquardt(g2, bal_cfg(5))
+    assert np.array_equal(kept.view(np.uint64), snap.view(np.uint64))
+    assert not np.shares_memory(kept, g2.cameras)
+
+
 def test_non_finite_initial_chi2_raises(gpu):
     p = bal.synthetic_bal(*TINY, seed=3)
     p.points[0] = [0.0, 0.0, 0.0]
