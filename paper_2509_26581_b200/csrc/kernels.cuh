@@ -148,8 +148,6 @@ struct Dev {
   FP* tile_red2;  // [ntiles]
   int* tile_flag; // [ntiles]
   FP* cam_red;    // [nc]
-  FP* cam_red2;   // [nc]
-  int* cam_flag;  // [nc]
   FP* blk_red;    // [nblk]
   FP* blk_red2;   // [nblk]
   int* blk_flag;  // [nblk]
@@ -642,6 +640,31 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, const
 // phase 0: fused (world == 1); phase 1: per-rank camera sums and tile
 // scalars into red/redmax; phase 2: camera b/H/D from the allreduced sums and
 // the finalize.
+// Sum of camera c's 54-value linearize partials in slot-list order (lane v:
+// value v in a0, value 32 + v in a1); eight slots' loads in flight at a time.
+template <typename FP, typename SP>
+__device__ inline void lin_cam_sum(const Dev<FP, SP>& d, uint32_t c, int lane, FP& a0, FP& a1) {
+  constexpr int B = 8;
+  const uint32_t beg = d.cam_part_off[c], end = d.cam_part_off[c + 1];
+  for (uint32_t q0 = beg; q0 < end; q0 += B) {
+    const uint32_t mine = q0 + (lane & (B - 1)) < end ? d.cam_part_idx[q0 + (lane & (B - 1))] : 0u;
+    FP v0[B], v1[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const FP* src = d.part + static_cast<uint64_t>(__shfl_sync(0xffffffffu, mine, u)) * kLinVals;
+      const bool ok = q0 + u < end;
+      v0[u] = ok ? src[lane] : FP(0);
+      v1[u] = ok && lane < kLinVals - 32 ? src[32 + lane] : FP(0);
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (q0 + u < end) {
+        a0 += v0[u];
+        a1 += v1[u];
+      }
+  }
+}
+
 template <typename FP, typename SP>
 __global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int force, int phase) {
   if (!force && !d.st->do_linearize) return;
@@ -651,11 +674,7 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int 
   if (phase == 1) {
     if (c < d.nc) {
       FP a0 = FP(0), a1 = FP(0);
-      for (uint32_t q = d.cam_part_off[c]; q < d.cam_part_off[c + 1]; ++q) {
-        const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * kLinVals;
-        a0 += src[lane];
-        if (lane < kLinVals - 32) a1 += src[32 + lane];
-      }
+      lin_cam_sum(d, c, lane, a0, a1);
       d.red[54ull * c + lane] = a0;
       if (lane < kLinVals - 32) d.red[54ull * c + 32 + lane] = a1;
     }
@@ -679,14 +698,12 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int 
     for (int k = 0; k < 9; ++k) d.Rf[10ull * c + k] = d.cpre[static_cast<uint64_t>(kCamPre) * c + 8 + k];
     d.Rf[10ull * c + 9] = d.x[9ull * c + 6];
   }
+  FP gm_t = FP(0);  // per thread: its warp's camera (uniform over the warp)
+  int fin_t = 1;
   if (c < d.nc) {
     FP a0 = FP(0), a1 = FP(0);
     if (phase == 0) {
-      for (uint32_t q = d.cam_part_off[c]; q < d.cam_part_off[c + 1]; ++q) {
-        const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * kLinVals;
-        a0 += src[lane];
-        if (lane < kLinVals - 32) a1 += src[32 + lane];
-      }
+      lin_cam_sum(d, c, lane, a0, a1);
     } else {
       a0 = d.red[54ull * c + lane];
       if (lane < kLinVals - 32) a1 = d.red[54ull * c + 32 + lane];
@@ -713,24 +730,39 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_lin_cams(Dev<FP, SP> d, int 
         gm = fabs(a0);
       }
     }
-    gm = warp_max(gm);
-    fin = __all_sync(0xffffffffu, fin);
-    if (lane == 0) {
-      d.cam_red2[c] = gm;
-      d.cam_flag[c] = fin;
+    gm_t = gm;
+    fin_t = fin;
+  }
+  // this block's cameras (max |b|, finiteness) and, when fused, its fixed slice
+  // of the tiles' chi^2 / max |b| / flag partials: the last block then folds
+  // one partial per block instead of every tile's (fixed order, deterministic)
+  FP chi_t = FP(0);
+  if (phase == 0) {
+    const uint32_t per = (d.ntiles + gridDim.x - 1) / gridDim.x;
+    const uint32_t lo = min(d.ntiles, per * blockIdx.x), hi = min(d.ntiles, lo + per);
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      chi_t += __ldcg(d.tile_red + i);
+      gm_t = fmax(gm_t, __ldcg(d.tile_red2 + i));
+      fin_t &= __ldcg(d.tile_flag + i) ? 1 : 0;
     }
   }
+  const FP bchi = block_sum(chi_t, scratch);
+  const FP bmax = block_max(gm_t, scratch);
+  const int bfin = __syncthreads_and(fin_t);
+  if (threadIdx.x == 0) {
+    d.blk_red[blockIdx.x] = bchi;
+    d.blk_red2[blockIdx.x] = bmax;
+    d.blk_flag[blockIdx.x] = bfin;
+  }
   if (last_block(&d.st->cnt[0])) {
-    const FP m2 = reduce_partials_max(d.cam_red2, d.nc, scratch);
-    const int fc = reduce_flags_and(d.cam_flag, d.nc);
+    const FP m = reduce_partials_max(d.blk_red2, gridDim.x, scratch);
+    const int f = reduce_flags_and(d.blk_flag, gridDim.x);
     if (phase == 0) {
-      const FP chi = reduce_partials(d.tile_red, d.ntiles, scratch);
-      const FP m1 = reduce_partials_max(d.tile_red2, d.ntiles, scratch);
-      const int f = reduce_flags_and(d.tile_flag, d.ntiles) & fc;
-      if (threadIdx.x == 0) fin_lin(d.st, chi, f != 0, fmax(m1, m2));
+      const FP chi = reduce_partials(d.blk_red, gridDim.x, scratch);
+      if (threadIdx.x == 0) fin_lin(d.st, chi, f != 0, m);
     } else if (threadIdx.x == 0) {
       const FP* rs = d.red + red_scalars(d);
-      fin_lin(d.st, rs[kRedLinChi], fc != 0 && rs[kRedLinFail] == FP(0), fmax(d.redmax[kRedMaxLin], m2));
+      fin_lin(d.st, rs[kRedLinChi], f != 0 && rs[kRedLinFail] == FP(0), fmax(d.redmax[kRedMaxLin], m));
     }
   }
 }
@@ -1806,27 +1838,29 @@ template <typename FP, typename SP, bool RAW>
 __global__ void __launch_bounds__(kTileThreads) k_chi2_tiles(Dev<FP, SP> d, const FP* params, int force) {
   if (!force && (!d.st->iter_active || !d.st->step_finite)) return;
   __shared__ FP scratch[32];
-  const uint32_t t = blockIdx.x;
-  const uint32_t eb = d.tile_ebeg[t], ee = eb + d.tile_ecnt[t], pb = d.tile_pbeg[t];
   const uint64_t pcol0 = 9ull * d.nc;
+  // grid-stride over tiles (a fixed tile set and order per block), one
+  // partial per block, so the last block folds gridDim.x values, not ntiles
   FP chi = FP(0);
-#pragma unroll 2
-  for (uint32_t e = eb + threadIdx.x; e < ee; e += blockDim.x) {  // unrolled: both edges' loads in flight
-    const uint32_t cam = d.d_cam[e];
-    FP cp[9];
+  for (uint32_t t = blockIdx.x; t < d.ntiles; t += gridDim.x) {
+    const uint32_t eb = d.tile_ebeg[t], ee = eb + d.tile_ecnt[t], pb = d.tile_pbeg[t];
+    for (uint32_t e = eb + threadIdx.x; e < ee; e += blockDim.x) {
+      const uint32_t cam = d.d_cam[e];
+      FP cp[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) cp[k] = params[9ull * cam + k];
-    const FP* X = params + pcol0 + 3ull * (pb + d.d_lpt[e]);
-    FP res[2];
-    snavely_residual_pre<FP>(cp, d.cpre_new + static_cast<uint64_t>(kCamPre) * cam, X, d.d_obs[e],
-                             d.d_obs[static_cast<uint64_t>(d.na) + e], res);
-    const FP s = res[0] * res[0] + res[1] * res[1];
-    chi += RAW ? s : loss_value<FP>(d.loss_kind, d.huber, s);
+      for (int k = 0; k < 9; ++k) cp[k] = params[9ull * cam + k];
+      const FP* X = params + pcol0 + 3ull * (pb + d.d_lpt[e]);
+      FP res[2];
+      snavely_residual_pre<FP>(cp, d.cpre_new + static_cast<uint64_t>(kCamPre) * cam, X, d.d_obs[e],
+                               d.d_obs[static_cast<uint64_t>(d.na) + e], res);
+      const FP s = res[0] * res[0] + res[1] * res[1];
+      chi += RAW ? s : loss_value<FP>(d.loss_kind, d.huber, s);
+    }
   }
   chi = block_sum(chi, scratch);
-  if (threadIdx.x == 0) d.tile_red[t] = chi;
+  if (threadIdx.x == 0) d.blk_red[blockIdx.x] = chi;
   if (last_block(&d.st->cnt[7])) {
-    const FP s = reduce_partials(d.tile_red, d.ntiles, scratch);
+    const FP s = reduce_partials(d.blk_red, gridDim.x, scratch);
     if (threadIdx.x == 0) {
       if (!d.dist || force)
         d.st->chi2_new = s;

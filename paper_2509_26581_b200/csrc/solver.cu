@@ -291,6 +291,8 @@ class Solver final : public SolverBase {
       int o3 = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_precond_pts<FP, SP>, 256, 0));
       pt_occ_ = static_cast<unsigned>(std::max(1, o3));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_chi2_tiles<FP, SP, false>, kTileThreads, 0));
+      chi2_occ_ = static_cast<unsigned>(std::max(1, o3));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_step<FP, SP>, 256, 0));
       coop_grid_ = static_cast<unsigned>(std::max(1, sms * std::max(1, per)));
       if (const char* e = std::getenv("GB_PCG_FUSED")) fused_pcg_ = std::atoi(e) != 0;
@@ -569,9 +571,9 @@ class Solver final : public SolverBase {
     upload_params();
     k_cam_pre<FP, SP><<<std::max(1u, div_up(act_.nc, 128)), 128, 0, s_>>>(dev_, dev_.x, dev_.cpre_new, 2, 1);
     if (raw)
-      k_chi2_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, dev_.x, 1);
+      k_chi2_tiles<FP, SP, true><<<chi2_grid(), kTileThreads, 0, s_>>>(dev_, dev_.x, 1);
     else
-      k_chi2_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, dev_.x, 1);
+      k_chi2_tiles<FP, SP, false><<<chi2_grid(), kTileThreads, 0, s_>>>(dev_, dev_.x, 1);
     CK(cudaGetLastError());
     if (dist()) allreduce(&st_->chi2_new, 1);
     State<FP> hs;
@@ -1201,10 +1203,10 @@ class Solver final : public SolverBase {
     d.tile_red2 = static_cast<FP*>(b_tr2_.alloc(act_.ntiles * sizeof(FP)));
     d.tile_flag = static_cast<int*>(b_tf_.alloc(act_.ntiles * sizeof(int)));
     d.cam_red = static_cast<FP*>(b_cr_.alloc(std::max<uint64_t>(1, nc) * sizeof(FP)));
-    d.cam_red2 = static_cast<FP*>(b_cr2_.alloc(std::max<uint64_t>(1, nc) * sizeof(FP)));
-    d.cam_flag = static_cast<int*>(b_cf_.alloc(std::max<uint64_t>(1, nc) * sizeof(int)));
     const uint64_t nblk =
-        std::max<uint64_t>(std::max<uint64_t>(std::max<uint64_t>(vert_grid(), col_grid()), cam_grid()), coop_grid_) +
+        std::max<uint64_t>(std::max<uint64_t>(std::max<uint64_t>(std::max<uint64_t>(vert_grid(), col_grid()), cam_grid()),
+                                              coop_grid_),
+                           chi2_grid()) +
         pt_grid();
     d.blk_red = static_cast<FP*>(b_br_.alloc(nblk * sizeof(FP)));
     d.blk_red2 = static_cast<FP*>(b_br2_.alloc(nblk * sizeof(FP)));
@@ -1356,6 +1358,7 @@ class Solver final : public SolverBase {
   // one vertex per thread (memory-level parallelism beats grid-stride reuse here)
 
   // one full wave of the point kernels (occupancy measured once per solver)
+  unsigned chi2_grid() const { return std::max(1u, std::min(act_.ntiles, sms_ * chi2_occ_)); }
   unsigned pt_grid() const { return std::max(1u, std::min(div_up(act_.np, 256), sms_ * pt_occ_)); }
   void launch_pcg_init() {
     k_pcg_init<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
@@ -1545,7 +1548,7 @@ class Solver final : public SolverBase {
     CK(cudaGetLastError());
     enqueue_solve(pcg_max_it);
     k_cam_pre<FP, SP><<<std::max(1u, div_up(act_.nc, 128)), 128, 0, s_>>>(dev_, dev_.x_new, dev_.cpre_new, 1, 0);
-    k_chi2_tiles<FP, SP, false><<<act_.ntiles, kTileThreads, 0, s_>>>(dev_, dev_.x_new, 0);
+    k_chi2_tiles<FP, SP, false><<<chi2_grid(), kTileThreads, 0, s_>>>(dev_, dev_.x_new, 0);
     CK(cudaGetLastError());
     if (dist()) {
       allreduce(red_s() + kRedChi, 1);
@@ -1630,6 +1633,7 @@ class Solver final : public SolverBase {
   bool pipe_ok_ = false;
   uint32_t sms_ = 148;
   unsigned pt_occ_ = 4;
+  unsigned chi2_occ_ = 4;
   DBuf b_tmeta_, b_tcv_, b_taux_, b_tlin_, b_sspan_;
   bool pipe_aux_pending_ = false;
   DBuf b_camtc_idx_, b_camtc_off_, b_dir_rb_, b_dir_re_;
@@ -1639,7 +1643,7 @@ class Solver final : public SolverBase {
   unsigned dir_rest_grid_ = 1;
   DBuf b_cpre_, b_cpre_new_;
   DBuf b_J_, b_Rf_, b_w_, b_part_, b_x_, b_xn_, b_b_, b_cl_, b_D_, b_dx_, b_Hc_, b_Hp_, b_Mc_, b_Mp_, b_xs_, b_r_, b_z_, b_p_,
-      b_ap_, b_tr_, b_tr2_, b_tf_, b_cr_, b_cr2_, b_cf_, b_br_, b_br2_, b_bf_;
+      b_ap_, b_tr_, b_tr2_, b_tf_, b_cr_, b_br_, b_br2_, b_bf_;
 };
 
 std::unique_ptr<SolverBase> make_solver(GraphData& g) {
