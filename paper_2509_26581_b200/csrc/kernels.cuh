@@ -1249,8 +1249,6 @@ __global__ void k_make_vt(Dev<FP, SP> d) {
 // 32-edge chunk run by run with one lane per output value (54 values over
 // 32 lanes), i.e. plain FMAs over shared memory instead of shuffle trees.
 // Dynamic shared memory: see lin_normal_smem().
-constexpr int kLinRow = 22;  // Jc (18) + w r (2) + w (1) + pad per staged edge (16-byte rows)
-constexpr int kLinShflRuns = 3;  // chunks with at most this many camera runs reduce in registers
 
 // One edge's contribution to camera value V of its run: V < 9 is b_V = Jc0V w r0
 // + Jc1V w r1, V in [9, 54) is H(i, j) = w (Jc0i Jc0j + Jc1i Jc1j) (packed upper).
@@ -1311,30 +1309,21 @@ __device__ __forceinline__ void lin_cam_shfl(bool in, const FP* jc_in, FP wr0, F
   }
 }
 
-template <typename FP>
-struct Pair;
-template <>
-struct Pair<double> {
-  using type = double2;
-};
-template <>
-struct Pair<float> {
-  using type = float2;
-};
+// 128-thread CTAs (four passes over a 512-edge tile), four per SM: while one
+// CTA waits at a barrier or on its prologue gathers, three others compute.
+constexpr int kLinThreads = 128;
 template <typename FP>
 __host__ __device__ constexpr size_t lin_normal_smem() {
-  return sizeof(FP) * (kTilePoints * 3 + kTileCams * 9 + kTileThreads * kLinRow + kTileEdges * 9 + 32 +
-                       kTileCams * kCamPre);
+  return sizeof(FP) * (kTilePoints * 3 + kTileCams * 9 + kTileEdges * 9 + 32 + kTileCams * kCamPre);
 }
 
 template <typename FP, typename SP, bool STORE, bool AUTO>
-__global__ void __launch_bounds__(kTileThreads, 2) k_lin_normal(Dev<FP, SP> d, int force) {
+__global__ void __launch_bounds__(kLinThreads, 4) k_lin_normal(Dev<FP, SP> d, int force) {
   if (!force && !d.st->do_linearize) return;
   extern __shared__ __align__(16) unsigned char lin_smem[];
   FP* sX = reinterpret_cast<FP*>(lin_smem);
   FP* sC = sX + kTilePoints * 3;
-  FP* sJ = sC + kTileCams * 9;
-  FP* pst = sJ + kTileThreads * kLinRow;
+  FP* pst = sC + kTileCams * 9;
   FP* scratch = pst + kTileEdges * 9;
   FP* sPre = scratch + 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1350,7 +1339,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_lin_normal(Dev<FP, SP> d, i
       sPre[i] = d.cpre[static_cast<uint64_t>(kCamPre) * d.tile_cams[cb + i / kCamPre] + i % kCamPre];
   __syncthreads();
   FP chi = FP(0);
-  for (uint32_t c0 = 0; c0 < ne_t; c0 += kTileThreads) {
+  for (uint32_t c0 = 0; c0 < ne_t; c0 += kLinThreads) {
   const uint32_t j = c0 + tid;
   const bool valid = j < ne_t;
   const uint32_t e = eb + (valid ? j : 0);
@@ -1393,10 +1382,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_lin_normal(Dev<FP, SP> d, i
   const uint32_t prev = __shfl_up_sync(full, lc, 1);
   const unsigned hm = __ballot_sync(full, valid && (lane == 0 || lc != prev));
   const unsigned vm = __ballot_sync(full, valid);
-  const uint32_t slot0 = d.chunk_part_base[d.tile_chunk_base[t] + c0 / 32 + warp];
-  if (__popc(hm) <= kLinShflRuns) {
-    // few runs (the common case: a tile's edges are camera-sorted): one
-    // register butterfly per run
+  const uint32_t slot0 = hm ? d.chunk_part_base[d.tile_chunk_base[t] + c0 / 32 + warp] : 0u;
+  {
+    // one register butterfly per camera run of the chunk (a tile's edges are
+    // camera-sorted, so a chunk has ~1.5 runs on average)
     unsigned heads = hm;
     uint32_t run = 0;
     while (heads) {
@@ -1407,56 +1396,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_lin_normal(Dev<FP, SP> d, i
                        d.part + static_cast<uint64_t>(slot0 + run) * kLinVals);
       ++run;
     }
-    continue;
   }
-  FP* row = sJ + tid * kLinRow;
-#pragma unroll
-  // row layout: 10 pairs (Jc0[k], Jc1[k]) k < 9, (w r0, w r1), then w: a
-  // reduction lane reads both rows' operands of one column with one 2-wide load
-  for (int k = 0; k < 9; ++k) {
-    row[2 * k] = valid ? jc[k] : FP(0);
-    row[2 * k + 1] = valid ? jc[9 + k] : FP(0);
-  }
-  row[18] = wr0;
-  row[19] = wr1;
-  row[20] = w;
-  row[21] = FP(0);
-  __syncwarp();
-  // camera side: lane owns values v0 = lane and v1 = lane + 32 (< 54);
-  // value v < 9: b_v = sum Jc0v wr0 + Jc1v wr1; v >= 9: H(i,j) = sum w (Jc0i Jc0j + Jc1i Jc1j)
-  const bool has1 = lane + 32 < kLinVals;
-  const bool isb = lane < 9;
-  // value v0: m * (P[i0].0 P[k0].0 + P[i0].1 P[k0].1) over the row's pairs P,
-  // with m = 1 (b: k0 = the (w r0, w r1) pair) or w (H)
-  const int i0 = isb ? lane : p9row(lane - 9);
-  const int k0 = isb ? 9 : p9col(lane - 9);
-  const int i1 = has1 ? p9row(lane + 32 - 9) : 0;
-  const int j1 = has1 ? p9col(lane + 32 - 9) : 0;
-  unsigned heads = hm;
-  uint32_t run = 0;
-  while (heads) {
-    const int start = __ffs(heads) - 1;
-    heads &= heads - 1;
-    const int stop = heads ? __ffs(heads) - 1 : 32 - __clz(vm);
-    FP acc0 = FP(0), acc1 = FP(0);
-    for (int q = start; q < stop; ++q) {
-      const FP* rr = sJ + (32 * warp + q) * kLinRow;
-      using P2 = typename Pair<FP>::type;
-      const P2* pr = reinterpret_cast<const P2*>(rr);
-      const FP m0 = isb ? FP(1) : rr[20];
-      const P2 a = pr[i0], b = pr[k0];
-      acc0 += m0 * (a.x * b.x + a.y * b.y);
-      if (has1) {
-        const P2 c = pr[i1], e = pr[j1];
-        acc1 += rr[20] * (c.x * e.x + c.y * e.y);
-      }
-    }
-    FP* dst = d.part + static_cast<uint64_t>(slot0 + run) * kLinVals;
-    dst[lane] = acc0;
-    if (has1) dst[32 + lane] = acc1;
-    ++run;
-  }
-  __syncwarp();  // this warp's staged rows are rewritten next pass
   }
   __syncthreads();  // pst complete
 

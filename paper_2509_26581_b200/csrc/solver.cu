@@ -1395,15 +1395,15 @@ class Solver final : public SolverBase {
     k_cam_pre<FP, SP><<<std::max(1u, div_up(act_.nc, 128)), 128, 0, s_>>>(dev_, dev_.x, dev_.cpre, 0, force);
     const bool aut = g_.diff_mode == GB_AUTO;
     if (dev_.J && aut) {  // Auto: stored J from dual-number passes (factor_descriptor.hpp:610-624)
-      if (dev_.n_normal) k_lin_normal<FP, SP, true, true><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
+      if (dev_.n_normal) k_lin_normal<FP, SP, true, true><<<dev_.n_normal, kLinThreads, smem, s_>>>(dev_, force);
       if (dev_.n_heavy)
         k_lin_tiles<FP, SP, true, true><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
     } else if (dev_.J) {
-      if (dev_.n_normal) k_lin_normal<FP, SP, true, false><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
+      if (dev_.n_normal) k_lin_normal<FP, SP, true, false><<<dev_.n_normal, kLinThreads, smem, s_>>>(dev_, force);
       if (dev_.n_heavy)
         k_lin_tiles<FP, SP, true, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
     } else {
-      if (dev_.n_normal) k_lin_normal<FP, SP, false, false><<<dev_.n_normal, kTileThreads, smem, s_>>>(dev_, force);
+      if (dev_.n_normal) k_lin_normal<FP, SP, false, false><<<dev_.n_normal, kLinThreads, smem, s_>>>(dev_, force);
       if (dev_.n_heavy)
         k_lin_tiles<FP, SP, false, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
     }
