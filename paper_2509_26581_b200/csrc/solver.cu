@@ -304,6 +304,8 @@ class Solver final : public SolverBase {
     CK(cudaFuncSetAttribute(k_lin_normal<FP, SP, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(lin_normal_smem<FP>())));
     CK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s_up_, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev_up_, cudaEventDisableTiming));
     st_ = static_cast<State<FP>*>(st_buf_.alloc(sizeof(State<FP>)));
     CK(cudaMemsetAsync(st_, 0, sizeof(State<FP>), s_));
   }
@@ -312,6 +314,8 @@ class Solver final : public SolverBase {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (flag_host_) cudaFreeHost(flag_host_);
     cudaStreamDestroy(s_);
+    cudaEventDestroy(ev_up_);
+    cudaStreamDestroy(s_up_);
   }
 
   // current activation (the last level used; level 0 if never activated)
@@ -941,7 +945,13 @@ class Solver final : public SolverBase {
     const uint8_t* lvl = g_.level ? to_dev(s_lvl, g_.level, ne) : nullptr;
     const uint8_t* cfix = g_.cam_fixed.empty() ? nullptr : to_dev(s_cfix, g_.cam_fixed);
     const uint8_t* pfix = g_.pt_fixed.empty() ? nullptr : to_dev(s_pfix, g_.pt_fixed);
-    const double* obs = to_dev(s_obs, g_.obs, 2 * ne);
+    // observations are first needed by k_place: their upload (2/3 of the
+    // input bytes) runs on a side stream under compaction, point ordering and
+    // the host tile pass
+    double* obs = static_cast<double*>(s_obs.alloc(std::max<uint64_t>(1, 2 * ne) * sizeof(double)));
+    if (ne) CK(cudaMemcpyAsync(obs, g_.obs, 2 * ne * sizeof(double), cudaMemcpyHostToDevice, s_up_));
+    CK(cudaEventRecord(ev_up_, s_up_));
+    h2d_bytes_ += 2 * ne * sizeof(double);
     ptm.mark("act: h2d edges");
     uint32_t* flag = scratch<uint32_t>(s_flag, ne + 1);
     uint32_t* pos = scratch<uint32_t>(s_pos, ne + 1);
@@ -1039,6 +1049,7 @@ class Solver final : public SolverBase {
     uint32_t* pval = scratch<uint32_t>(s_pval, na);
     uint32_t* hc = scratch<uint32_t>(s_hc, na);
     uint32_t* hr = scratch<uint32_t>(s_hr, na);
+    CK(cudaStreamWaitEvent(s_, ev_up_, 0));  // observations uploaded
     k_place<FP><<<grid_for(na), 256, 0, s_>>>(na, k64b, order, cam_a, pt_a, entry_a, rank, rb, d.tile_ebeg,
                                                d.tile_pbeg, obs, ns, d_a, d_cam, d_lpt, d_obs, pkey, pval, hc, hr);
     CK(cudaGetLastError());
@@ -1594,6 +1605,8 @@ class Solver final : public SolverBase {
 
   GraphData& g_;
   cudaStream_t s_ = nullptr;
+  cudaStream_t s_up_ = nullptr;  // side stream: the observation upload overlaps activation (device activation)
+  cudaEvent_t ev_up_ = nullptr;
   // phase state of the current solve
   gb_lm_config cfg_{};
   gb_solve_report rep_{};
