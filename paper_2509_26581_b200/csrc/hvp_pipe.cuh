@@ -103,7 +103,7 @@ inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_bud
   L.z = take(kTilePoints * 3 * sizeof(SP) + 32);
   L.camv = take(kTileCams * cam_stride<A>() * sizeof(A) + 32);
   L.vt = take(kTilePoints * 3 * sizeof(A));
-  L.runs = take(4 * kTileEdges + 32);  // the tile's camera-run slot spans (at most one run per edge)
+  L.runs = take(8 * kTileEdges + 32);  // the tile's camera-run spans + storage slots (at most one run per edge)
   // camera / point contributions: over the J rows when SP and Arith have the
   // same width, else (bf16 storage) a 12-row area of the stage
   L.gs = sizeof(SP) == sizeof(A) ? L.J : take(12ull * pipe_jstride<A>());
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
         const Span s_cv = span16(d.tcv + static_cast<uint64_t>(cam_stride<A>()) * cb,
                                  sizeof(A) * static_cast<uint64_t>(cam_stride<A>()) * ncam);
         const Span s_z = span16(d.z + pcol0 + 3ull * pb, sizeof(SP) * 3ull * npt);
-        const Span s_r = span16(d.slot_span + slot0, 4ull * nruns);
+        const Span s_r = span16(d.slot_span + slot0, 8ull * nruns);
         const bool small = !(L.dbg & 16);  // experiments: 16 = J rows only
         const uint32_t jblock = static_cast<uint32_t>(L.rows) * pipe_jstride<SP>();
         const uint32_t total =
@@ -455,13 +455,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       // ---- camera runs: the other half, one thread per (run, value), the
       // association order of chunk_runs_smem (identical to k_hvp_tiles)
       const uint32_t nr = h[kHNr];
-      const uint32_t* spans = reinterpret_cast<const uint32_t*>(st + L.runs + h[kHDr]);
+      const uint2* spans = reinterpret_cast<const uint2*>(st + L.runs + h[kHDr]);
       const uint32_t slot0 = h[kHSlot0];
       for (uint32_t o = tid - (1 - half) * kTileThreads; o < 9 * nr && !(L.dbg & 1); o += kTileThreads) {
         const uint32_t r = o / 9, k = o - 9 * r;
-        const uint32_t sp2 = spans[r];
+        const uint2 sp2 = spans[r];
         const A* src = gs + k * GS;
-        run_sum_store<A, FP>(src, sp2 & 0xffffu, sp2 >> 16, d.part + static_cast<uint64_t>(slot0 + r) * 9 + k);
+        run_sum_store<A, FP>(src, sp2.x & 0xffffu, sp2.x >> 16, d.part + static_cast<uint64_t>(sp2.y) * 9 + k);
       }
     } else if (!(L.dbg & 2)) {
       FP dot = FP(0);
@@ -545,7 +545,7 @@ __global__ void k_tile_aux(Dev<FP, SP> d) {
         const unsigned later = lane == 31 ? 0u : heads & (0xffffffffu << (lane + 1));
         const uint32_t hi = later ? 32 * q + __ffs(later) - 1 : min(32 * q + 32, ne);
         const uint32_t slot = d.chunk_part_base[ch0 + q] + __popc(heads & ((1u << lane) - 1u));
-        d.slot_span[slot] = e | (hi << 16);
+        d.slot_span[slot] = make_uint2(e | (hi << 16), d.run_slot[slot]);
       }
     }
     if (lane == 0) {

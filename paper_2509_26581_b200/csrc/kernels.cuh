@@ -106,7 +106,9 @@ struct Dev {
   uint32_t ntcams;            // tile_cam_off[ntiles]
   arith_t<SP>* tcv;           // [ntcams][9]  D*p of each tile's cameras
   unsigned char* tile_aux;    // static per-tile blobs (hvp_pipe.cuh AuxSec)
-  uint32_t* slot_span;        // [nparts] tile-relative edge range [lo, hi) of each camera-run slot (lo | hi << 16)
+  uint2* slot_span;           // [nparts] per run: tile-relative edge range [lo, hi) (lo | hi << 16), storage slot
+  const uint32_t* run_slot;   // [nparts] run (chunk_part_base + r) -> storage slot: camera-major, so each
+                              // camera's partials are contiguous for the camera kernels (position in cam_part_idx)
   unsigned char* tile_lin;    // per-linearization per-tile blobs (LinSec)
   const uint32_t* cam_tc_off;  // [nc+1] camera -> its tile-camera entries (tcv rows)
   const uint32_t* cam_tc_idx;
@@ -267,6 +269,12 @@ __device__ inline void seg_reduce(T (&v)[K], int lane, int run_end) {
   }
 }
 
+// run_slot[cam_part_idx[q]] = q: partial-slot storage in camera-list order
+static __global__ void k_run_slots(uint32_t n, const uint32_t* cam_part_idx, uint32_t* run_slot) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
+    run_slot[cam_part_idx[q]] = q;
+}
+
 // Sum of src[lo, hi) in a fixed association order (4 interleaved partial
 // sums), stored to *dst. Every camera-run reduction of the HVP goes through it,
 // so the tile kernels and the pipelined kernel produce identical bits.
@@ -292,7 +300,7 @@ __device__ __forceinline__ void run_sum_store(const A* src, uint32_t lo, uint32_
 // association order (deterministic). heads/vm: ballots of run heads / valid lanes.
 template <typename A, typename FP>
 __device__ inline void chunk_runs_smem(const A* gw, int stride, int lane, unsigned heads, unsigned vm,
-                                       uint32_t slot0, FP* part) {
+                                       uint32_t slot0, FP* part, const uint32_t* run_slot) {
   const int R = __popc(heads);
   const int end = 32 - __clz(vm);
   // lane q holds start(q) = the q-th head (run q spans [start(q), start(q + 1)))
@@ -313,7 +321,7 @@ __device__ inline void chunk_runs_smem(const A* gw, int stride, int lane, unsign
     const int nxt = __shfl_sync(0xffffffffu, my_start, min(r + 1, 31));
     if (o >= 9 * R) continue;
     const int stp = r + 1 < R ? nxt : end;
-    run_sum_store<A, FP>(gw + k * stride, start, stp, part + static_cast<uint64_t>(slot0 + r) * 9 + k);
+    run_sum_store<A, FP>(gw + k * stride, start, stp, part + static_cast<uint64_t>(run_slot[slot0 + r]) * 9 + k);
   }
 }
 
@@ -322,12 +330,12 @@ __device__ inline void chunk_runs_smem(const A* gw, int stride, int lane, unsign
 // run_sum_store order, the order k_hvp_pipe uses tile-wide (identical bits).
 template <typename A, typename FP>
 __device__ inline void camera_runs(const A (&g)[9], int lane, unsigned hm, unsigned vm, uint32_t slot0, A* gw,
-                                   int stride, FP* part) {
+                                   int stride, FP* part, const uint32_t* run_slot) {
   if (!hm) return;
 #pragma unroll
   for (int k = 0; k < 9; ++k) gw[k * stride + lane] = g[k];
   __syncwarp();
-  chunk_runs_smem<A, FP>(gw, stride, lane, hm, vm, slot0, part);
+  chunk_runs_smem<A, FP>(gw, stride, lane, hm, vm, slot0, part, run_slot);
   __syncwarp();
 }
 
@@ -553,7 +561,7 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, const
       }
       seg_reduce<FP, 9>(v, lane, ri.run_end);
       if (ri.head) {
-        FP* dst = d.part + static_cast<uint64_t>(ri.slot) * kLinVals + 9 * g;
+        FP* dst = d.part + static_cast<uint64_t>(d.run_slot[ri.slot]) * kLinVals + 9 * g;
 #pragma unroll
         for (int k = 0; k < 9; ++k) dst[k] = v[k];
       }
@@ -647,7 +655,7 @@ __device__ inline void lin_cam_sum(const Dev<FP, SP>& d, uint32_t c, int lane, F
   constexpr int B = 8;
   const uint32_t beg = d.cam_part_off[c], end = d.cam_part_off[c + 1];
   for (uint32_t q0 = beg; q0 < end; q0 += B) {
-    const uint32_t mine = q0 + (lane & (B - 1)) < end ? d.cam_part_idx[q0 + (lane & (B - 1))] : 0u;
+    const uint32_t mine = q0 + (lane & (B - 1)) < end ? q0 + (lane & (B - 1)) : 0u;  // storage slot = position
     FP v0[B], v1[B];
 #pragma unroll
     for (int u = 0; u < B; ++u) {
@@ -1169,7 +1177,8 @@ __global__ void __launch_bounds__(kTileThreads, MINB) k_hvp_tiles(Dev<FP, SP> d,
       const uint32_t prev = __shfl_up_sync(0xffffffffu, cam, 1);
       const unsigned hm = __ballot_sync(0xffffffffu, valid && (lane == 0 || cam != prev));
       const unsigned vm = __ballot_sync(0xffffffffu, valid);
-      camera_runs<A, FP>(g, lane, hm, vm, hm ? d.chunk_part_base[chunk] : 0u, gsh + (tid & ~31), kGsStride, d.part);
+      camera_runs<A, FP>(g, lane, hm, vm, hm ? d.chunk_part_base[chunk] : 0u, gsh + (tid & ~31), kGsStride, d.part,
+                         d.run_slot);
     }
     A h[3];
 #pragma unroll
@@ -1393,7 +1402,7 @@ __global__ void __launch_bounds__(kLinThreads, 4) k_lin_normal(Dev<FP, SP> d, in
       heads &= heads - 1;
       const int stop = heads ? __ffs(heads) - 1 : 32 - __clz(vm);
       lin_cam_shfl<FP>(lane >= start && lane < stop, jc, wr0, wr1, w, lane,
-                       d.part + static_cast<uint64_t>(slot0 + run) * kLinVals);
+                       d.part + static_cast<uint64_t>(d.run_slot[slot0 + run]) * kLinVals);
       ++run;
     }
   }
@@ -1461,7 +1470,7 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams(Dev<FP, SP> d, int 
     for (int k = 0; k < 9; ++k) acc[k] = FP(0);
     if (phase != 2) {
       for (uint32_t q = d.cam_part_off[c] + lane; q < d.cam_part_off[c + 1]; q += 32) {
-        const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * 9;
+        const FP* src = d.part + static_cast<uint64_t>(q) * 9;  // camera-major storage
 #pragma unroll
         for (int k = 0; k < 9; ++k) acc[k] += src[k];
       }
@@ -1714,8 +1723,16 @@ __global__ void k_pcg_dir_rest(Dev<FP, SP> d, const uint64_t* rbeg, const uint64
     const A v = static_cast<A>(d.D[i]) * widen<A>(pi);
     d.vt[i] = v;
     const uint64_t c = i / 9, k = i % 9;
-    for (uint32_t q = d.cam_tc_off[c]; q < d.cam_tc_off[c + 1]; ++q)
-      d.tcv[static_cast<uint64_t>(sizeof(A) == 8 ? 10 : 12) * d.cam_tc_idx[q] + k] = v;  // hvp_pipe.cuh cam_stride
+    constexpr uint64_t CS = sizeof(A) == 8 ? 10 : 12;  // hvp_pipe.cuh cam_stride
+    const uint32_t q1 = d.cam_tc_off[c + 1];
+    for (uint32_t q = d.cam_tc_off[c]; q < q1; q += 8) {  // the camera's tile copies, 8 index loads in flight
+      uint32_t tc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tc[u] = q + u < q1 ? d.cam_tc_idx[q + u] : 0u;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q + u < q1) d.tcv[CS * tc[u] + k] = v;
+    }
   }
   for (int r = 0; r < nranges; ++r)
     for (uint64_t i = rbeg[r] + t0; i < rend[r]; i += stride) {
@@ -1876,7 +1893,7 @@ __global__ void __launch_bounds__(kTileThreads) k_schur_pre_tiles(Dev<FP, SP> d)
       }
       seg_reduce<FP, 9>(v, lane, ri.run_end);
       if (ri.head) {
-        FP* dst = d.part + static_cast<uint64_t>(ri.slot) * kLinVals + 9 * g;
+        FP* dst = d.part + static_cast<uint64_t>(d.run_slot[ri.slot]) * kLinVals + 9 * g;
 #pragma unroll
         for (int k = 0; k < 9; ++k) dst[k] = v[k];
       }
@@ -1910,7 +1927,7 @@ __global__ void k_schur_pre_cams(Dev<FP, SP> d) {
       if (i == j) B[q] += d.st->before_scaling ? lam * Dv[i] * Dv[i] : lam;
     }
   for (uint32_t s2 = d.cam_part_off[c]; s2 < d.cam_part_off[c + 1]; ++s2) {
-    const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[s2]) * kLinVals;
+    const FP* src = d.part + static_cast<uint64_t>(s2) * kLinVals;  // camera-major storage
 #pragma unroll
     for (int k = 0; k < 45; ++k) B[k] -= src[k];
   }
@@ -2070,7 +2087,7 @@ __global__ void __launch_bounds__(kTileThreads) k_schur_tiles(Dev<FP, SP> d) {
     const RunInfo ri = run_info(cam, valid, d.chunk_part_base[chunk]);
     seg_reduce<A, 9>(g, lane, ri.run_end);
     if (ri.head) {
-      FP* dst = d.part + static_cast<uint64_t>(ri.slot) * 9;
+      FP* dst = d.part + static_cast<uint64_t>(d.run_slot[ri.slot]) * 9;
 #pragma unroll
       for (int k = 0; k < 9; ++k) dst[k] = static_cast<FP>(g[k]);
     }
@@ -2089,7 +2106,7 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_schur_rhs_cams(Dev<FP, SP> d
 #pragma unroll
   for (int k = 0; k < 9; ++k) acc[k] = FP(0);
   for (uint32_t q = d.cam_part_off[c] + lane; q < d.cam_part_off[c + 1]; q += 32) {
-    const FP* src = d.part + static_cast<uint64_t>(d.cam_part_idx[q]) * 9;
+    const FP* src = d.part + static_cast<uint64_t>(q) * 9;  // camera-major storage
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc[k] += src[k];
   }

@@ -525,7 +525,7 @@ class Solver final : public SolverBase {
       b += jstore_elems<SP>(act_.n_slots, static_cast<int>(rows)) * sJ + aux + lin;  // J blocks, tile blobs
       b += np3 * (sV + sV);                            // p in, ap out
       b += d.ntcams * (cam_stride<A>() * sA * 2 + 4.0);  // tcv gather (tile_cams, write) + tile read
-      b += 4.0 * nparts;                               // camera-run slot spans
+      b += 8.0 * nparts;                               // camera-run spans + storage slots
     } else {
       b += (d.J ? jstore_elems<SP>(act_.n_slots, 24) * sJ : 0) + ns * (4 + 2);  // J, camera and point indices
       b += np3 * (sA + sV + sF + sV + 1);              // vt, p, D in; ap out; free mask
@@ -1183,7 +1183,7 @@ class Solver final : public SolverBase {
         if (aux16 > 0xffffffffull || lin16 > 0xffffffffull) throw std::invalid_argument("tile blobs exceed 64 GB");
         d.tile_meta = to_dev(b_tmeta_, meta);
         d.tile_aux = static_cast<unsigned char*>(b_taux_.alloc(std::max<uint64_t>(16, 16 * aux16)));
-        d.slot_span = static_cast<uint32_t*>(b_sspan_.alloc(std::max<uint64_t>(4, 4ull * act_.nparts)));
+        d.slot_span = static_cast<uint2*>(b_sspan_.alloc(std::max<uint64_t>(8, 8ull * act_.nparts)));
         d.tile_lin = static_cast<unsigned char*>(b_tlin_.alloc(std::max<uint64_t>(16, 16 * lin16)));
         d.tcv = static_cast<A*>(b_tcv_.alloc(std::max<uint64_t>(1, cam_stride<A>() * uint64_t(d.ntcams)) * sizeof(A)));
         CK(cudaMemsetAsync(d.tcv, 0, std::max<uint64_t>(1, cam_stride<A>() * uint64_t(d.ntcams)) * sizeof(A), s_));
@@ -1191,6 +1191,12 @@ class Solver final : public SolverBase {
       }
     }
     d.part = static_cast<FP*>(b_part_.alloc(std::max<uint64_t>(1, act_.nparts) * kLinVals * sizeof(FP)));
+    {  // camera-major storage of the partial slots: run -> its position in the camera lists
+      uint32_t* rs = static_cast<uint32_t*>(b_runslot_.alloc(std::max<uint64_t>(1, act_.nparts) * sizeof(uint32_t)));
+      if (act_.nparts) k_run_slots<<<grid_for(act_.nparts), 256, 0, s_>>>(act_.nparts, d.cam_part_idx, rs);
+      CK(cudaGetLastError());
+      d.run_slot = rs;
+    }
     d.x = static_cast<FP*>(b_x_.alloc(ncols_ * sizeof(FP)));
     d.x_new = static_cast<FP*>(b_xn_.alloc(ncols_ * sizeof(FP)));
     d.b = static_cast<FP*>(b_b_.alloc(ncols_ * sizeof(FP)));
@@ -1647,7 +1653,7 @@ class Solver final : public SolverBase {
   uint32_t sms_ = 148;
   unsigned pt_occ_ = 4;
   unsigned chi2_occ_ = 4;
-  DBuf b_tmeta_, b_tcv_, b_taux_, b_tlin_, b_sspan_;
+  DBuf b_tmeta_, b_tcv_, b_taux_, b_tlin_, b_sspan_, b_runslot_;
   bool pipe_aux_pending_ = false;
   DBuf b_camtc_idx_, b_camtc_off_, b_dir_rb_, b_dir_re_;
   const uint64_t* dir_rbeg_ = nullptr;
