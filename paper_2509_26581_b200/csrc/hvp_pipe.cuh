@@ -182,7 +182,7 @@ __device__ inline Span span16(const void* p, uint64_t bytes) {
   return Span{reinterpret_cast<const char*>(lo), static_cast<uint32_t>(hi - lo), static_cast<uint32_t>(a - lo)};
 }
 
-enum PipeHdr : int { kHT = 0, kHNe, kHNpt, kHNcam, kHDp, kHDcv, kHPb, kHDz, kHLpt, kHPsl, kHPso, kHDr, kHCf, kHCr, kHW, kHNr, kHSlot0 };
+enum PipeHdr : int { kHT = 0, kHNe, kHNpt, kHNcam, kHDp, kHDcv, kHPb, kHDz, kHLpt, kHPsl, kHPso, kHDr, kHCf, kHCr, kHW, kHNr };
 
 // stage index + parity of a ring of S stages (no integer division per tile)
 struct RingPos {
@@ -313,7 +313,6 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
           h[kHPso] = as.pso;
           h[kHDr] = s_r.delta;
           h[kHNr] = nruns;
-          h[kHSlot0] = slot0;
           h[kHCf] = as.cf;
           h[kHCr] = ls.cr;
           h[kHW] = ls.w;
@@ -456,7 +455,6 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       // association order of chunk_runs_smem (identical to k_hvp_tiles)
       const uint32_t nr = h[kHNr];
       const uint2* spans = reinterpret_cast<const uint2*>(st + L.runs + h[kHDr]);
-      const uint32_t slot0 = h[kHSlot0];
       for (uint32_t o = tid - (1 - half) * kTileThreads; o < 9 * nr && !(L.dbg & 1); o += kTileThreads) {
         const uint32_t r = o / 9, k = o - 9 * r;
         const uint2 sp2 = spans[r];
