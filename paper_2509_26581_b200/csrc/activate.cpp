@@ -59,10 +59,16 @@ void build_incidence(uint64_t nvert, const std::vector<uint32_t>& vert_of_a, con
 
 void greedy_tiles(const std::vector<uint32_t>& deg_int, std::vector<uint32_t>& tile_pbeg,
                   std::vector<uint32_t>& tile_ebeg, std::vector<uint32_t>& tile_of_pt) {
-  const uint64_t np = deg_int.size();
+  tile_of_pt.resize(deg_int.size());
+  greedy_tiles(deg_int.data(), deg_int.size(), tile_pbeg, tile_ebeg, tile_of_pt.data());
+}
+
+void greedy_tiles(const uint32_t* deg_int, uint64_t np, std::vector<uint32_t>& tile_pbeg,
+                  std::vector<uint32_t>& tile_ebeg, uint32_t* tile_of_pt) {
   tile_pbeg.assign(1, 0);
   tile_ebeg.assign(1, 0);
-  tile_of_pt.resize(np);
+  tile_pbeg.reserve(np / 64 + 2);
+  tile_ebeg.reserve(np / 64 + 2);
   uint64_t te = 0, tp = 0, ecount = 0;
   for (uint64_t i = 0; i < np; ++i) {
     const uint64_t d = deg_int[i];
@@ -72,7 +78,7 @@ void greedy_tiles(const std::vector<uint32_t>& deg_int, std::vector<uint32_t>& t
       tile_ebeg.push_back(static_cast<uint32_t>(ecount));
       te = tp = 0;
     }
-    tile_of_pt[i] = static_cast<uint32_t>(tile_pbeg.size() - 1);
+    if (tile_of_pt) tile_of_pt[i] = static_cast<uint32_t>(tile_pbeg.size() - 1);
     te += d;
     tp += 1;
     ecount += d;

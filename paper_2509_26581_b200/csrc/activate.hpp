@@ -85,6 +85,9 @@ void shard(const Activation& full, int world, int rank, Activation& out);
 // building blocks shared with the device activation (activate_dev.cuh)
 void greedy_tiles(const std::vector<uint32_t>& deg_int, std::vector<uint32_t>& tile_pbeg,
                   std::vector<uint32_t>& tile_ebeg, std::vector<uint32_t>& tile_of_pt);
+// the same over a raw degree array; tile_of_pt may be null
+void greedy_tiles(const uint32_t* deg_int, uint64_t np, std::vector<uint32_t>& tile_pbeg,
+                  std::vector<uint32_t>& tile_ebeg, uint32_t* tile_of_pt);
 void classify_tiles(Activation& out);
 // FactorDescriptor::build_incidence for one slot (factor_descriptor.hpp:710-753)
 void build_incidence_host(uint64_t nvert, const std::vector<uint32_t>& vert_of_a, const uint8_t* fixed, Incidence& inc);

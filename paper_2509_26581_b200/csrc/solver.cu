@@ -995,13 +995,23 @@ class Solver final : public SolverBase {
     CK(cudaMemsetAsync(degi + np, 0, sizeof(uint32_t), s_));
     k_rank<<<grid_for(np), 256, 0, s_>>>(np, pt_order, deg, rank, degi);
     CK(cudaGetLastError());
-    std::vector<uint32_t> hdeg(np);
-    if (np) CK(cudaMemcpyAsync(hdeg.data(), degi, np * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
+    // degrees to page-locked host memory (the host greedy pass reads them)
+    struct HostBlock {
+      void* p;
+      ~HostBlock() { HostCache::get().release(p); }
+    } hb{HostCache::get().alloc(std::max<uint64_t>(1, np) * sizeof(uint32_t))};
+    std::vector<uint32_t> hdeg_fallback;
+    uint32_t* hdeg = static_cast<uint32_t*>(hb.p);
+    if (!hdeg) {
+      hdeg_fallback.resize(np);
+      hdeg = hdeg_fallback.data();
+    }
+    if (np) CK(cudaMemcpyAsync(hdeg, degi, np * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
     CK(cudaStreamSynchronize(s_));
     // tiles: the host greedy over degrees (activate.cpp greedy_tiles)
     ptm.mark("act: compact + point order");
-    std::vector<uint32_t> real_beg, tile_of_pt;
-    greedy_tiles(hdeg, act_.tile_pbeg, real_beg, tile_of_pt);
+    std::vector<uint32_t> real_beg;
+    greedy_tiles(hdeg, np, act_.tile_pbeg, real_beg, nullptr);
     ptm.mark("act: host greedy tiles");
     act_.ntiles = static_cast<uint32_t>(act_.tile_pbeg.size() - 1);
     const uint32_t T = act_.ntiles;
