@@ -102,12 +102,14 @@ class BlockCache {
     static BlockCache c;
     return c;
   }
-  void* take(int dev, size_t bytes) {
+  // a cached block of at least `bytes` (at most 2x); *cap = its true size
+  void* take(int dev, size_t bytes, size_t* cap) {
     std::lock_guard<std::mutex> lk(m_);
     auto& f = free_[dev];
     auto it = f.lower_bound(bytes);
     if (it == f.end() || it->first > 2 * bytes) return nullptr;
     void* p = it->second;
+    *cap = it->first;
     held_[dev] -= it->first;
     f.erase(it);
     return p;
@@ -212,14 +214,18 @@ class DBuf {
     bytes_ = cap_ = 0;
   }
   void* alloc(size_t bytes) {
-    if (bytes <= bytes_ && p_) return p_;
+    if (p_ && bytes + kSlack <= cap_) {  // the block already holds it
+      bytes_ = bytes;
+      return p_;
+    }
     release();
     CK(cudaGetDevice(&dev_));
     const size_t want = bytes + kSlack;  // slack: 16-byte-widened bulk copies may read past the end
-    void* c = BlockCache::get().take(dev_, want);
+    size_t got = 0;
+    void* c = BlockCache::get().take(dev_, want, &got);
     if (c) {
       p_ = c;
-      cap_ = want;  // conservative: the block is at least this large
+      cap_ = got;  // the block's true size (it goes back to the cache as such)
     } else {
       cudaError_t e = cudaMalloc(&p_, want);
       if (e == cudaErrorMemoryAllocation) {
@@ -237,6 +243,7 @@ class DBuf {
   T* as() const {
     return static_cast<T*>(p_);
   }
+  size_t capacity() const { return cap_; }
 
  private:
   void* p_ = nullptr;
@@ -903,21 +910,28 @@ class Solver final : public SolverBase {
     if (n) CK(cudaMemcpyAsync(d, p, n * sizeof(T), cudaMemcpyHostToDevice, s_));
     return d;
   }
+  // CUB temp storage: sized for the largest request seen so far with 2x
+  // headroom, so activation's growing requests do not re-allocate (a
+  // re-allocation synchronizes the device, stalling the overlapped uploads)
+  void* cub_temp(size_t bytes) {
+    if (b_cub_.as<void>() && bytes + DBuf::kSlack <= b_cub_.capacity()) return b_cub_.as<void>();
+    return b_cub_.alloc(std::max<size_t>(bytes, 2 * b_cub_.capacity()) + (size_t(4) << 20));
+  }
   void cub_scan_excl(const uint32_t* in, uint32_t* out, uint64_t n) {
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, static_cast<int64_t>(n), s_));
-    CK(cub::DeviceScan::ExclusiveSum(b_cub_.alloc(tmp), tmp, in, out, static_cast<int64_t>(n), s_));
+    CK(cub::DeviceScan::ExclusiveSum(cub_temp(tmp), tmp, in, out, static_cast<int64_t>(n), s_));
   }
   void cub_scan_incl(const uint32_t* in, uint32_t* out, uint64_t n) {
     size_t tmp = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out, static_cast<int64_t>(n), s_));
-    CK(cub::DeviceScan::InclusiveSum(b_cub_.alloc(tmp), tmp, in, out, static_cast<int64_t>(n), s_));
+    CK(cub::DeviceScan::InclusiveSum(cub_temp(tmp), tmp, in, out, static_cast<int64_t>(n), s_));
   }
   template <typename K>
   void cub_sort(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, int end_bit) {
     size_t tmp = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, static_cast<int64_t>(n), 0, end_bit, s_));
-    CK(cub::DeviceRadixSort::SortPairs(b_cub_.alloc(tmp), tmp, kin, kout, vin, vout, static_cast<int64_t>(n), 0,
+    CK(cub::DeviceRadixSort::SortPairs(cub_temp(tmp), tmp, kin, kout, vin, vout, static_cast<int64_t>(n), 0,
                                        end_bit, s_));
   }
   unsigned grid_for(uint64_t n) const {
@@ -953,6 +967,20 @@ class Solver final : public SolverBase {
     CK(cudaEventRecord(ev_up_, s_up_));
     h2d_bytes_ += 2 * ne * sizeof(double);
     ptm.mark("act: h2d edges");
+    {  // CUB temp storage for the largest sort / scan of this activation, sized up
+       // front: growing it later would synchronize the device mid-activation
+      size_t t1 = 0, t2 = 0, t3 = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, static_cast<const uint64_t*>(nullptr),
+                                         static_cast<uint64_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                         static_cast<uint32_t*>(nullptr), static_cast<int64_t>(ne), 0, 64, s_));
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, t2, static_cast<const uint32_t*>(nullptr),
+                                         static_cast<uint32_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                         static_cast<uint32_t*>(nullptr), static_cast<int64_t>(std::max(ne, np)), 0, 32,
+                                         s_));
+      CK(cub::DeviceScan::InclusiveSum(nullptr, t3, static_cast<const uint32_t*>(nullptr),
+                                       static_cast<uint32_t*>(nullptr), static_cast<int64_t>(ne + np + 1), s_));
+      cub_temp(std::max(t1, std::max(t2, t3)));
+    }
     uint32_t* flag = scratch<uint32_t>(s_flag, ne + 1);
     uint32_t* pos = scratch<uint32_t>(s_pos, ne + 1);
     int* bad = scratch<int>(s_bad, 1);
@@ -967,6 +995,7 @@ class Solver final : public SolverBase {
     CK(cudaMemcpyAsync(&na32, pos + ne, sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
     CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s_));
     CK(cudaStreamSynchronize(s_));
+    ptm.mark("act:  flags + count");
     if (hbad) {  // reproduce the exact diagnostic (resolve_slots, factor_descriptor.hpp:549-558)
       Activation tmp;
       activate(activation_input(level), tmp);
@@ -977,6 +1006,7 @@ class Solver final : public SolverBase {
     uint32_t* pt_a = scratch<uint32_t>(s_pt_a, na);
     uint32_t* entry_a = scratch<uint32_t>(s_entry, na);
     k_compact<<<grid_for(ne), 256, 0, s_>>>(ne, flag, pos, cam, pt, cam_a, pt_a, entry_a);
+    ptm.mark("act:  compact");
     // internal point order: stable sort by smallest active camera
     uint32_t* key = scratch<uint32_t>(s_key, np);
     uint32_t* key2 = scratch<uint32_t>(s_key2, np);
@@ -987,9 +1017,11 @@ class Solver final : public SolverBase {
     k_iota<<<grid_for(np), 256, 0, s_>>>(np, val);
     k_point_stats<<<grid_for(na), 256, 0, s_>>>(na, cam_a, pt_a, key, deg);
     CK(cudaGetLastError());
+    ptm.mark("act:  point stats");
     uint32_t* pt_order = static_cast<uint32_t*>(b_pt_order_.alloc(std::max<uint64_t>(1, np) * sizeof(uint32_t)));
     cub_sort<uint32_t>(key, key2, val, pt_order, np, bits_for(nc + 1));
     pt_order_dev_ = pt_order;
+    ptm.mark("act:  point sort");
     uint32_t* rank = scratch<uint32_t>(s_rank, np);
     uint32_t* degi = scratch<uint32_t>(s_degi, np + 1);
     CK(cudaMemsetAsync(degi + np, 0, sizeof(uint32_t), s_));
