@@ -232,6 +232,9 @@ int gb_hvp_bytes(gb_graph* g, double* kernel_bytes, double* reference_bytes);
  *              (the caller then uses ordinary memory). */
 void* gb_host_alloc(uint64_t bytes);
 void gb_host_free(void* p);
+/* gb_host_copy  memcpy split over host threads (fills those arrays from the
+ *              caller's problem at full host-memory bandwidth). */
+void gb_host_copy(void* dst, const void* src, uint64_t bytes);
 
 /* ---- multi-GPU sharding (no reference counterpart: the reference is a
  * single-process CPU solver) -------------------------------

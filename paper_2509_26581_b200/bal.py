@@ -294,7 +294,7 @@ def _owned_array(src, dtype, backend: "Backend") -> np.ndarray:
         blk = _PinnedBlock(backend, a.nbytes)
         if blk.ptr:
             out = np.asarray(blk).view(a.dtype).reshape(a.shape)
-            np.copyto(out, a)
+            backend.fn("host_copy")(out.ctypes.data, a.ctypes.data, a.nbytes)
             return out
     return a.copy()
 

@@ -16,6 +16,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -1909,6 +1910,25 @@ int gb_hvp_bytes(gb_graph* g, double* kernel_bytes, double* reference_bytes) {
 void* gb_host_alloc(uint64_t bytes) { return gb::HostCache::get().alloc(static_cast<size_t>(bytes)); }
 
 void gb_host_free(void* p) { gb::HostCache::get().release(p); }
+
+void gb_host_copy(void* dst, const void* src, uint64_t bytes) {
+  // large copies split over host threads (one thread moves ~10-15 GB/s)
+  const uint64_t chunk = uint64_t(8) << 20;
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const unsigned nt = static_cast<unsigned>(std::min<uint64_t>(hw, (bytes + chunk - 1) / chunk));
+  if (nt <= 1) {
+    if (bytes) std::memcpy(dst, src, bytes);
+    return;
+  }
+  const uint64_t per = (bytes + nt - 1) / nt;
+  std::vector<std::thread> th;
+  for (unsigned i = 0; i < nt; ++i) {
+    const uint64_t lo = i * per, hi = std::min(bytes, lo + per);
+    if (lo >= hi) break;
+    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo); });
+  }
+  for (auto& t : th) t.join();
+}
 
 int gb_nccl_unique_id(void* out128) {
   return guarded([&] { gb::nccl_unique_id(out128); });
