@@ -228,6 +228,8 @@ class DBuf {
       p_ = c;
       cap_ = got;  // the block's true size (it goes back to the cache as such)
     } else {
+      if (std::getenv("GB_TIMING") && want >= (1u << 20))
+        std::fprintf(stderr, "[gb]   cudaMalloc %.1f MB (cache miss)\n", want / 1048576.0);
       cudaError_t e = cudaMalloc(&p_, want);
       if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
