@@ -242,10 +242,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_hvp_pipe(Dev<FP, SP> d, Pip
       FP dv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint32_t q = min(q0 + 32 * u, n3 - 1);
-        pv[u] = pp[q];
-        zv[u] = dir ? zz[q] : pv[u];
-        dv[u] = DD[q];
+        const uint32_t q = q0 + 32 * u;
+        if (q < n3) {  // lanes past the end read nothing (no cross-lane overlap with the stores)
+          pv[u] = pp[q];
+          zv[u] = dir ? zz[q] : pv[u];
+          dv[u] = DD[q];
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
