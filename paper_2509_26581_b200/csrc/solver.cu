@@ -777,6 +777,7 @@ class Solver final : public SolverBase {
   }
 
   void ensure_structure(int level) {
+    pts_staged_ = false;  // set again only by a device activation run below
     if (have_act_ && act_rev_ == g_.revision && act_level_ == level) return;
     if (!g_.cams || !g_.pts) throw std::logic_error("cameras and points must be set before solving");
     host_plan_ = false;
@@ -967,6 +968,11 @@ class Solver final : public SolverBase {
     // the host tile pass
     double* obs = static_cast<double*>(s_obs.alloc(std::max<uint64_t>(1, 2 * ne) * sizeof(double)));
     if (ne) CK(cudaMemcpyAsync(obs, g_.obs, 2 * ne * sizeof(double), cudaMemcpyHostToDevice, s_up_));
+    {  // the point parameters too (upload_params then only gathers them into the internal order)
+      FP* stage = static_cast<FP*>(b_ptstage_.alloc(std::max<uint64_t>(1, 3 * np) * sizeof(FP)));
+      if (np) CK(cudaMemcpyAsync(stage, g_.pts, 3 * np * sizeof(FP), cudaMemcpyHostToDevice, s_up_));
+      pts_staged_ = true;
+    }
     CK(cudaEventRecord(ev_up_, s_up_));
     h2d_bytes_ += 2 * ne * sizeof(double);
     ptm.mark("act: h2d edges");
@@ -1343,11 +1349,13 @@ class Solver final : public SolverBase {
       CK(cudaMemcpyAsync(dev_.x + 9 * nc, loc.data(), loc.size() * sizeof(FP), cudaMemcpyHostToDevice, s_));
       CK(cudaStreamSynchronize(s_));
     } else {
-      CK(cudaMemcpyAsync(stage, g_.pts, 3 * np * sizeof(FP), cudaMemcpyHostToDevice, s_));
+      if (!pts_staged_)  // else already uploaded under the device activation (s_ waited on ev_up_)
+        CK(cudaMemcpyAsync(stage, g_.pts, 3 * np * sizeof(FP), cudaMemcpyHostToDevice, s_));
       actdev::k_gather_points<FP><<<grid_for(3 * np), 256, 0, s_>>>(static_cast<uint32_t>(np), pt_order_dev_, stage,
                                                                     dev_.x + 9 * nc);
       CK(cudaGetLastError());
     }
+    pts_staged_ = false;
     h2d_bytes_ += ncols_ * sizeof(FP);
   }
 
@@ -1658,6 +1666,7 @@ class Solver final : public SolverBase {
   cudaStream_t s_ = nullptr;
   cudaStream_t s_up_ = nullptr;  // side stream: the observation upload overlaps activation (device activation)
   cudaEvent_t ev_up_ = nullptr;
+  bool pts_staged_ = false;      // the point parameters are already in b_ptstage_ (this begin's activation)
   // phase state of the current solve
   gb_lm_config cfg_{};
   gb_solve_report rep_{};
