@@ -443,4 +443,28 @@ void ref_update_damping(double* lambda, double* nu, int accepted, double gain) {
 // bfloat16 RNE narrowing (bfloat16.hpp:25-33).
 std::uint16_t ref_bf16_round(float f) { return gopt::bfloat16::round_from(f); }
 
+// bal::parse_bal_file (src/bal_problem.cpp:81-119): reads a BAL text file with
+// the reference's own tokenizer. Call once with NULL outputs to get the shape,
+// then again with arrays of that size.
+int ref_parse_bal_file(const char* path, std::uint64_t* shape3, std::uint32_t* cam, std::uint32_t* pt,
+                       double* obs, double* cams, double* pts) {
+  return guarded([&] {
+    const gopt::bal::BALProblem p = gopt::bal::parse_bal_file(path);
+    shape3[0] = p.num_cameras();
+    shape3[1] = p.num_points();
+    shape3[2] = p.num_observations();
+    if (!cam) return;
+    for (std::size_t i = 0; i < p.observations.size(); ++i) {
+      cam[i] = p.observations[i].camera_index;
+      pt[i] = p.observations[i].point_index;
+      obs[2 * i] = p.observations[i].x;
+      obs[2 * i + 1] = p.observations[i].y;
+    }
+    for (std::size_t c = 0; c < p.cameras.size(); ++c)
+      for (int k = 0; k < 9; ++k) cams[9 * c + k] = p.cameras[c][k];
+    for (std::size_t q = 0; q < p.points.size(); ++q)
+      for (int k = 0; k < 3; ++k) pts[3 * q + k] = p.points[q][k];
+  });
+}
+
 }  // extern "C"
