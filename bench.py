@@ -8,17 +8,37 @@ and tests/acceptance.cpp:69-80's BAL configuration).
 
 A step is one LM iteration (levenberg_marquardt.hpp:149-220: block-Jacobi
 build, <=10 PCG iterations with matrix-free HVP, step, candidate chi^2,
-accept/reject, re-linearization on accept). Inputs are device-resident before
-the timed region; the J store (5.57 GB) is far larger than L2, so no flush is
-needed. Prints ONE JSON line on rank 0.
+accept/reject, re-linearization on accept), the span one
+IterationRecord.wall_seconds covers (:150,209).
 
---impl reference times the unmodified reference CPU solver (oracle/_ref,
-compiled from /root/reference with the Eigen-subset shim) on this box's host
-cores on the same workload.
+Timed window. The timed solve runs exactly W+K LM iterations: its
+relative-decrease and gradient tolerances are 0, so it cannot stop inside the
+window (with the reference's 1e-6 the synthetic Final problem converges after
+21 iterations; tolerance 0 keeps iterating, every step still accepted with 10
+PCG iterations — the window's accept/reject mix and PCG counts are in the
+line). W warm-up iterations run first, then K are timed with CUDA events on
+the solver stream. Inputs are device-resident; the J store (3.7 GB) is far
+larger than L2, so no flush is needed. The reference arm times the SAME
+window (iterations W+1..W+K of the same tolerance-0 solve).
+
+e2e: the reference configuration (50 LM iterations, tolerance 1e-6, i.e. run
+to convergence) through the public API from pinned host arrays: graph build,
+upload, activation, initial linearize, every iteration, write-back; ms per
+iteration = wall time / iterations.
+
+--gpus N > 1 without a torchrun environment re-launches this script under
+torch.distributed.run with N ranks (one per GPU; the point tiles are sharded,
+cameras replicated, NCCL allreduce per reduction site). Prints ONE JSON line
+on rank 0.
+
+Both arms read the problem from paper_2509_26581_b200/gb_gen_bal (a host-only
+executable), so the reference arm never loads the product library.
 """
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,14 +57,83 @@ WORKLOADS = {
     "ladybug": (49, 7776, 31843, "synthetic Ladybug-49-shaped BA (49 cams, 7,776 pts, 31,843 obs)"),
 }
 DTYPE = {"fp64": "f64", "fp32": "f32", "fp32-bf16": "f32/bf16-storage"}
-SIZES = {"fp64": (8, 8, 8, 8), "fp32": (4, 4, 4, 4), "fp32-bf16": (2, 2, 4, 4)}  # s_J, s_V, s_A, s_FP
+METRIC = "LM iteration ms (synthetic BAL BA)"
+UNIT = "ms/LM-iteration"
+GEN = os.path.join(ROOT, "paper_2509_26581_b200", "gb_gen_bal")
+# sources of the HVP tile kernel: the committed ncu DRAM traffic is only
+# reported while they are unchanged since the capture
+HVP_SOURCES = ["hvp_pipe.cuh", "kernels.cuh", "common.cuh", "snavely.cuh"]
 
 
-def lm_config(max_iterations, bal):
-    c = bal.LMConfig(max_iterations=max_iterations)
+# ------------------------------------------------------------------ inputs
+def load_problem(nc, np_, ne, seed=42):
+    """The synthetic problem from the standalone writer (binary layout in
+    csrc/gen_bal.cpp), as a bal.BALProblem."""
+    from paper_2509_26581_b200.bal import BALProblem
+
+    if not os.path.exists(GEN):
+        raise SystemExit(f"{GEN} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    raw = subprocess.run([GEN, str(nc), str(np_), str(ne), "--seed", str(seed)], check=True,
+                         stdout=subprocess.PIPE).stdout
+    if raw[:8] != b"GBBAL01\0":
+        raise SystemExit("gb_gen_bal: bad output")
+    nc_, np2, ne_ = np.frombuffer(raw, np.uint64, 3, 8)
+    assert (nc_, np2, ne_) == (nc, np_, ne)
+    off = 32
+
+    def take(dtype, n):
+        nonlocal off
+        a = np.frombuffer(raw, dtype, n, off).copy()
+        off += a.nbytes
+        return a
+
+    cam = take(np.uint32, ne)
+    pt = take(np.uint32, ne)
+    obs = take(np.float64, 2 * ne).reshape(ne, 2)
+    cams = take(np.float64, 9 * nc).reshape(nc, 9)
+    pts = take(np.float64, 3 * np_).reshape(np_, 3)
+    return BALProblem(cams, pts, cam, pt, obs)
+
+
+def timed_config(bal, n):
+    """W+K iterations, never terminating early (tolerances 0)."""
+    c = bal.LMConfig(max_iterations=n, tolerance=0.0, gradient_tolerance=0.0)
     c.pcg.max_iterations = 10
     c.pcg.tolerance = 1e-6
     return c
+
+
+def reference_config(bal):
+    """tests/acceptance.cpp:69-80: 50 LM iterations, PCG 10 @ 1e-6, tolerance 1e-6."""
+    c = bal.LMConfig(max_iterations=50)
+    c.pcg.max_iterations = 10
+    c.pcg.tolerance = 1e-6
+    return c
+
+
+def host_info():
+    """Host CPU model, usable cores and the cgroup CPU quota."""
+    info = {"os_cpu_count": os.cpu_count()}
+    try:
+        info["affinity_cores"] = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    for path in ("/sys/fs/cgroup/cpu.max", "/sys/fs/cgroup/cpu/cpu.cfs_quota_us"):
+        try:
+            with open(path) as f:
+                info["cgroup_cpu_quota"] = f"{path}: {f.read().strip()}"
+            break
+        except Exception:
+            pass
+    return info
 
 
 def measured_peak():
@@ -54,6 +143,28 @@ def measured_peak():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def hvp_source_sha():
+    h = hashlib.sha256()
+    for f in HVP_SOURCES:
+        with open(os.path.join(ROOT, "paper_2509_26581_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def committed_traffic():
+    """ncu DRAM bytes of one HVP tile launch (profiles/ncu_hvp_summary.json),
+    or None with the reason when the kernel sources changed since."""
+    prof = os.path.join(ROOT, "profiles", "ncu_hvp_summary.json")
+    try:
+        with open(prof) as f:
+            s = json.load(f)
+    except Exception:
+        return None, "no committed ncu capture"
+    if s.get("kernel_source_sha") != hvp_source_sha():
+        return None, f"stale: capture {s.get('tag')} predates the current HVP kernel sources"
+    return s.get("dram_bytes_per_hvp"), f"ncu --set full capture {s.get('tag')} ({s.get('source')}) of these sources"
 
 
 class ClockSampler:
@@ -129,71 +240,141 @@ class ClockSampler:
                 "samples": len(self.sm), "source": self.source}
 
 
-def dist_setup():
+# ------------------------------------------------------------- launching
+def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
 
 
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_command(argv, nproc, port):
+    """torch.distributed.run command that re-runs this script with nproc ranks."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def resolve_world(args, env, visible_gpus):
+    """What to do for --gpus N: 'run' in this process, or 'spawn' N ranks.
+    Raises SystemExit on an inconsistent request (never silently runs fewer
+    ranks than asked for)."""
+    if "WORLD_SIZE" in env:
+        world = int(env["WORLD_SIZE"])
+        if world != args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per requested GPU")
+        return "run"
+    if args.gpus <= 1 or args.impl == "reference":
+        return "run"  # the reference arm is a host-core run on rank 0 alone
+    if visible_gpus < args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} requested but only {visible_gpus} CUDA device(s) visible")
+    return "spawn"
+
+
+# ------------------------------------------------------------- reference arm
 def reference_arm(args, shape, desc):
-    """The reference CPU solver (oracle/_ref) on this box's host cores."""
-    world, rank, _ = dist_setup()
+    """The reference CPU solver (oracle/_ref, the unmodified reference compiled
+    from its sources) on this box's host cores, same problem, same window."""
+    world, rank, _ = dist_env()
     if rank != 0:
         return
     from oracle import refbind
     from paper_2509_26581_b200 import bal
 
     cores = os.cpu_count() or 1
-    problem = bal.synthetic_bal(*shape, seed=42)
-    # bounded sample: 1 warm-up LM iteration + up to 5 timed ones of the full
-    # workload (each is ~seconds on the host at Final scale)
-    timed = max(1, min(args.steps, 5))
+    problem = load_problem(*shape)
+    W, K = args.warmup, args.steps
     r = refbind.build_graph(problem, args.precision, args.mode, workers=cores)
     t0 = time.perf_counter()
-    rep = bal.levenberg_marquardt(r, lm_config(1 + timed, bal))
+    rep = bal.levenberg_marquardt(r, timed_config(bal, W + K))
     wall = time.perf_counter() - t0
-    its = rep.iterations[1:] if len(rep.iterations) > 1 else rep.iterations
-    ms = 1e3 * statistics.mean(i.wall_seconds for i in its)
-    sample = (f"{len(its)} LM iteration(s) (after 1 warm-up) of the reference solver on the full workload, "
-              f"workers={cores}; per-iteration IterationRecord.wall_seconds (levenberg_marquardt.hpp:150,209); "
-              f"reference solve incl. activation {rep.total_seconds:.1f} s for {len(rep.iterations)} iterations")
+    if len(rep.iterations) < W + K:
+        raise SystemExit(f"reference solve terminated after {len(rep.iterations)} < W+K iterations "
+                         f"({rep.termination})")
+    window = rep.iterations[W:W + K]
+    ms = 1e3 * statistics.mean(i.wall_seconds for i in window)
+    sample = (f"LM iterations {W + 1}..{W + K} (after {W} warm-up iterations) of the reference solver on the full "
+              f"workload, tolerance 0 (the same window as the device arm), workers={cores}; per-iteration "
+              f"IterationRecord.wall_seconds (levenberg_marquardt.hpp:150,209)")
     line = {
-        "impl": "reference", "metric": "LM iteration ms (synthetic BAL BA)", "value": round(ms, 3),
-        "unit": "ms/LM-iteration", "n_gpus": world, "steps": len(its), "warmup": 1, "ms_per_step": round(ms, 3),
-        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision],
-        "data": "synthetic", "config": {"workload": desc + f" {args.precision} {args.mode}, PCG<=10@1e-6",
-                                        "precision": args.precision, "host_cores": cores},
-        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/LM-iteration", "cores": cores, "kind": "reference",
-                         "sample": sample},
-        "e2e": {"value": round(ms, 3), "unit": "ms/LM-iteration", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": DTYPE[args.precision], "data": "synthetic (paper_2509_26581_b200/gb_gen_bal)",
+        "config": {"workload": desc + f" {args.precision} {args.mode}, PCG<=10@1e-6",
+                   "precision": args.precision, "host_cores": cores},
+        "cpu_baseline": {"value": round(ms, 3), "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample,
+                         "host": host_info()},
+        "e2e": {"value": round(ms, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "window": window_summary(window),
         "solve_seconds": round(rep.total_seconds, 3), "wall_seconds": round(wall, 3),
     }
     print(json.dumps(line), flush=True)
 
 
+def window_summary(recs):
+    return {"accepted": sum(1 for i in recs if i.accepted), "rejected": sum(1 for i in recs if not i.accepted),
+            "pcg_iterations": [i.pcg_iterations for i in recs],
+            "chi2_first": recs[0].chi2_before if recs else None, "chi2_last": recs[-1].chi2_after if recs else None}
+
+
+def cpu_baseline(args, problem):
+    """The reference solver (oracle/_ref) on the host cores: a bounded sample
+    of the same workload (1 timed LM iteration after 1 warm-up, ~20 s)."""
+    try:
+        from oracle import refbind
+        from paper_2509_26581_b200 import bal
+
+        if not refbind.available():
+            return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref not built"}
+        cores = os.cpu_count() or 1
+        r = refbind.build_graph(problem, args.precision, args.mode, workers=cores)
+        rep = bal.levenberg_marquardt(r, timed_config(bal, 2))
+        its = rep.iterations[1:]
+        ms = 1e3 * statistics.mean(i.wall_seconds for i in its)
+        return {"value": round(ms, 2), "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"LM iteration 2 (after 1 warm-up), full workload, workers={cores} "
+                          f"(reference solve incl. activation {rep.total_seconds:.1f} s)",
+                "host": host_info()}
+    except Exception as e:  # the baseline is reported, never the thing measured
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+
+# ------------------------------------------------------------- device arm
 def ours(args, shape, desc):
     import ctypes
 
     import torch
 
-    world, rank, local = dist_setup()
+    world, rank, local = dist_env()
     from paper_2509_26581_b200 import _abi, bal
 
+    if not torch.cuda.is_available():
+        raise SystemExit("no CUDA device: the device arm has no CPU fallback")
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    problem = bal.synthetic_bal(*shape, seed=42)
+    problem = load_problem(*shape)
     W, K = args.warmup, args.steps
-    cfg = lm_config(W + K, bal)
+    cfg = timed_config(bal, W + K)
 
-    uid = None
-    if world > 1:  # NCCL communicator of the solver library (point-tile shards, replicated cameras)
+    def shared_uid():
+        if world == 1:
+            return None
         obj = [bal.nccl_unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+        return obj[0]
+
+    uid = shared_uid()
     g = bal.build_graph(problem, args.precision, args.mode, device=local)
     if args.solver != "pcg":
         g.set_linear_solver(args.solver)
@@ -203,6 +384,8 @@ def ours(args, shape, desc):
     c = cfg.to_c()
     rep0 = _abi.gb_solve_report()
     L.check(L.fn("begin")(g._h, ctypes.byref(c), ctypes.byref(rep0)))
+    kernels = ctypes.c_int32()
+    L.check(L.fn("iteration_kernels")(g._h, ctypes.byref(kernels)))
     stream = torch.cuda.ExternalStream(L.fn("stream")(g._h), device=local)
     L.check(L.fn("step")(g._h, W))
     torch.cuda.synchronize()
@@ -216,12 +399,17 @@ def ours(args, shape, desc):
         ev1.record(stream)
         ev1.synchronize()
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     ms_total = ev0.elapsed_time(ev1)
     rep = _abi.gb_solve_report()
     recs = (_abi.gb_iteration_record * (W + K))()
     L.check(L.fn("end")(g._h, ctypes.byref(rep), recs, W + K))
     if rep.iterations_run < W + K:
-        raise SystemExit(f"solve terminated after {rep.iterations_run} < W+K iterations: timed steps would be no-ops")
+        raise SystemExit(f"solve terminated after {rep.iterations_run} < W+K iterations "
+                         f"({_abi.TERMINATION_NAMES[rep.termination]}): timed steps would be no-ops")
+    report = bal._report(rep, recs)
+    window = report.iterations[W:W + K]
     # live roofline of the dominant kernel pair (HVP) on the solver stream
     ms_hvp, ms_tiles = ctypes.c_double(), ctypes.c_double()
     L.check(L.fn("time_hvp")(g._h, 20, ctypes.byref(ms_hvp), ctypes.byref(ms_tiles)))
@@ -229,18 +417,20 @@ def ours(args, shape, desc):
     L.check(L.fn("hvp_bytes")(g._h, ctypes.byref(kbytes), ctypes.byref(rbytes)))
 
     ms = ms_total / K
+    setup_s = [rep0.setup_seconds]
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
+        allsetup = [None] * world
+        torch.distributed.all_gather_object(allsetup, rep0.setup_seconds)
+        setup_s = allsetup
 
-    # the timed graph is done: its device memory returns to the solver's block cache
-    del stream, g
-    # e2e through the public API: host arrays -> graph -> solve -> host arrays.
-    # The problem's arrays live in pinned host memory (the e2e contract), so
-    # the upload inside the timed region runs at PCIe/C2C speed.
+    del stream, g  # the timed graph's device memory returns to the solver's block cache
+
+    # e2e through the public API: pinned host arrays -> graph -> solve -> host arrays
     def pinned(a):
-        t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=torch.cuda.is_available())
+        t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
         t.numpy()[...] = a
         return t
 
@@ -248,9 +438,13 @@ def ours(args, shape, desc):
             pinned(problem.point_index.astype(np.int32)), pinned(problem.observations)]
     problem_h = bal.BALProblem(pins[0].numpy(), pins[1].numpy(), pins[2].numpy().view(np.uint32),
                                pins[3].numpy().view(np.uint32), pins[4].numpy())
+    ecfg = reference_config(bal)
     torch.cuda.synchronize()
 
-    def e2e_once(uid):
+    def e2e_once():
+        uid = shared_uid()
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
         g2 = bal.build_graph(problem_h, args.precision, args.mode, device=local)
         if args.solver != "pcg":
@@ -258,118 +452,75 @@ def ours(args, shape, desc):
         if world > 1:
             g2.set_distributed(world, rank, "nccl", uid)
         t_built = time.perf_counter()
-        rep2 = bal.levenberg_marquardt(g2, cfg)
+        rep2 = bal.levenberg_marquardt(g2, ecfg)
         e2e_s = time.perf_counter() - t0
         parts = {"build_graph_s": round(t_built - t0, 4), "solve_call_s": round(e2e_s - (t_built - t0), 4),
                  "solver_total_s": round(rep2.total_seconds, 4), "solver_setup_s": round(rep2.setup_seconds, 4),
-                 "iterations_s": round(sum(i.wall_seconds for i in rep2.iterations), 4)}
+                 "iterations_s": round(sum(i.wall_seconds for i in rep2.iterations), 4),
+                 "iterations": len(rep2.iterations), "termination": rep2.termination}
         del g2
         return e2e_s, rep2, parts
 
-    # best of two end-to-end solves (guards the number against sporadic host
-    # hiccups; both are reported)
-    runs = []
-    for rep_i in range(2):
-        uid = None
-        if world > 1:
-            o = [bal.nccl_unique_id() if rank == 0 else None]
-            torch.distributed.broadcast_object_list(o, src=0)
-            torch.distributed.barrier()
-            uid = o[0]
-        runs.append(e2e_once(uid))
-    e2e_s, rep2, e2e_parts = min(runs, key=lambda r: r[0])
-    e2e_parts = {"best": e2e_parts, "runs": [r[2] for r in runs]}
+    runs = [e2e_once() for _ in range(2)]
+    e2e_s = statistics.mean(r[0] for r in runs)
+    rep2 = runs[-1][1]
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     n_it = max(1, len(rep2.iterations))
     e2e_ms = 1e3 * e2e_s / n_it
-    h2d = (rep2.h2d_bytes + problem.observations.size * 0) / n_it
+    h2d = rep2.h2d_bytes / n_it
     d2h = rep2.d2h_bytes / n_it
 
     if rank != 0:
         return
-    sJ, sV, sA, sFP = SIZES[args.precision]
-    E, N = rep.active_factors, rep.free_dims
     hvp_bytes = rbytes.value  # SURVEY.md §8(d) HVP algorithmic bytes: E (24 s_J + 8) + N (s_V + s_A)
     peak, peak_kind = measured_peak()
     achieved = hvp_bytes / (ms_hvp.value * 1e-3) / 1e9
     kernel_gbs = kbytes.value / (ms_hvp.value * 1e-3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_hvp_summary.json")
-    if os.path.exists(prof):
-        try:
-            with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_hvp")
-        except Exception:
-            traffic = None
-    # per LM iteration: iter_begin, precond (cams, pts), rhs_norm, pcg_init, tcam (first HVP), step, cam_pre +
-    # chi2, decide, commit, cam_pre +
-    # lin tiles (+heavy), lin_cams, tile_lin; per PCG iteration: hvp_pipe, hvp_cams, pcg_update, pcg_dir_rest
-    launches_per_it = 15 + 4 * cfg.pcg.max_iterations
-    if world > 1:  # split camera kernels + finalize kernels
-        launches_per_it += 1 + 2 * cfg.pcg.max_iterations + 5 + 2
+    traffic, traffic_note = committed_traffic()
     line = {
-        "metric": "LM iteration ms (synthetic BAL BA)", "value": round(ms, 4), "unit": "ms/LM-iteration",
+        "metric": METRIC, "value": round(ms, 4), "unit": UNIT,
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(ms, 4), "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision], "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision],
+        "data": "synthetic (paper_2509_26581_b200/gb_gen_bal, seed 42)",
         "config": {"workload": desc + f" {args.precision} {args.mode}, PCG<=10@1e-6" +
                    ("" if args.solver == "pcg" else f", {args.solver} linear solver"), "precision": args.precision,
+                   "timed_window": f"LM iterations {W + 1}..{W + K} of a tolerance-0 solve (no early termination)",
                    "cache": "inputs larger than L2 (HVP moves %.2f GB per launch, L2 126 MB)" % (kbytes.value / 1e9),
                    "parallelism": "single GPU" if world == 1 else
-                   f"{world} GPUs: point-tile shards, replicated cameras, NCCL allreduce per PCG iteration"},
+                   f"{world} GPUs: point-tile shards, replicated cameras, NCCL allreduce per reduction site"},
         "clocks": clocks.summary(),
-        "e2e": {"value": round(e2e_ms, 3), "unit": "ms/LM-iteration", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h),
-                "parts": e2e_parts,
-                "note": "public API: build_graph + levenberg_marquardt from pinned host arrays, incl. upload, "
-                        f"activation, initial linearize and write-back, amortized over {n_it} iterations"},
-        "gpu_launches": launches_per_it * K,
+        "e2e": {"value": round(e2e_ms, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "solve_seconds": round(e2e_s, 4),
+                "runs": [r[2] for r in runs],
+                "note": "public API: build_graph + levenberg_marquardt (reference config: 50 LM iterations, "
+                        "tolerance 1e-6) from pinned host arrays, incl. upload, activation, initial linearize and "
+                        f"write-back; mean of 2 solves, amortized over their {n_it} iterations"},
+        "gpu_launches": int(kernels.value) * K,
+        "gpu_launches_note": f"{kernels.value} kernel nodes in the captured per-iteration CUDA graph x {K} replays",
         "roofline": {"kernel": "k_hvp_pipe (+k_tcam_vt, k_hvp_tiles for heavy tiles) + k_hvp_cams: the HVP of one "
                                "PCG iteration", "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic, "algorithmic_bytes": int(hvp_bytes), "ms_per_launch": round(ms_hvp.value, 4),
-                     "ms_tiles_only": round(ms_tiles.value, 4), "peak_kind": peak_kind,
-                     "kernel_bytes": int(kbytes.value), "kernel_gbs": round(kernel_gbs, 1),
+                     "traffic": traffic, "traffic_note": traffic_note, "algorithmic_bytes": int(hvp_bytes),
+                     "ms_per_launch": round(ms_hvp.value, 4), "ms_tiles_only": round(ms_tiles.value, 4),
+                     "peak_kind": peak_kind, "kernel_bytes": int(kbytes.value), "kernel_gbs": round(kernel_gbs, 1),
                      "kernel_frac": round(kernel_gbs / peak, 4),
                      "note": "achieved/frac: SURVEY §8(d) reference-layout bytes (24 J values per edge) / time; "
                              "kernel_*: the bytes this path actually moves (factored 16-value J store, per-tile "
-                             "blobs, partial slots; gb_hvp_bytes) / time; traffic: ncu dram bytes of one tile "
-                             "launch (profiles/ncu_hvp_summary.json)"},
-        "solve": {"iterations": rep.iterations_run, "accepted": rep.accepted_steps,
-                  "initial_chi2": rep.initial_chi2, "chi2_after_timed": rep.final_chi2,
-                  "setup_seconds": round(rep0.setup_seconds, 3), "e2e_solve_seconds": round(e2e_s, 3),
-                  "iteration_ms": [round(1e3 * recs[i].wall_seconds, 3) for i in range(W + K)]},
+                             "blobs, partial slots; gb_hvp_bytes) / time"},
+        "window": window_summary(window),
+        "solve": {"iterations": rep.iterations_run, "initial_chi2": rep.initial_chi2,
+                  "chi2_after_timed": rep.final_chi2, "setup_seconds_per_rank": [round(s, 4) for s in setup_s],
+                  "iteration_ms": [round(1e3 * i.wall_seconds, 3) for i in report.iterations]},
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, problem)
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(args, problem):
-    """The reference solver (oracle/_ref) on the host cores: a bounded sample
-    of the same workload (1 timed LM iteration after 1 warm-up)."""
-    try:
-        from oracle import refbind
-        from paper_2509_26581_b200 import bal
-
-        if not refbind.available():
-            return {"value": None, "unit": "ms/LM-iteration", "cores": 0, "kind": "reference",
-                    "sample": "oracle/_ref not built"}
-        cores = os.cpu_count() or 1
-        r = refbind.build_graph(problem, args.precision, args.mode, workers=cores)
-        rep = bal.levenberg_marquardt(r, lm_config(2, bal))
-        its = rep.iterations[1:] if len(rep.iterations) > 1 else rep.iterations
-        ms = 1e3 * statistics.mean(i.wall_seconds for i in its)
-        return {"value": round(ms, 2), "unit": "ms/LM-iteration", "cores": cores, "kind": "reference",
-                "sample": f"{len(its)} LM iteration after 1 warm-up, full workload, workers={cores} "
-                          f"(reference solve incl. activation {rep.total_seconds:.1f} s)"}
-    except Exception as e:  # the baseline is reported, never the thing measured
-        return {"value": None, "unit": "ms/LM-iteration", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
-
-
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -382,9 +533,24 @@ def main():
                     help="DifferentiationMode (dynamic = implicit low-memory HVP)")
     ap.add_argument("--solver", default="pcg", choices=["pcg", "schur"],
                     help="pcg = the reference algorithm (headline); schur = Schur-complement mode")
-    args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "ours":
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
         args.warmup = 3
+    return args
+
+
+def main():
+    args = parse_args()
+    visible = 0
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import torch
+
+        visible = torch.cuda.device_count()
+    what = resolve_world(args, os.environ, visible)
+    if what == "spawn":
+        env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"),
+                   NCCL_DEBUG_SUBSYS=os.environ.get("NCCL_DEBUG_SUBSYS", "INIT"))
+        sys.exit(subprocess.call(launch_command(sys.argv[1:], args.gpus, free_port()), env=env))
     nc, np_, ne, desc = WORKLOADS[args.workload]
     if args.impl == "reference":
         reference_arm(args, (nc, np_, ne), desc)

@@ -223,6 +223,10 @@ int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_per_hvp, double* ms_tiles_
  *              reference-layout figure E (24 s_J + 8) + N (s_V + s_A) of
  *              SURVEY.md §8(d) (the roofline's "algorithmic bytes"). */
 int gb_hvp_bytes(gb_graph* g, double* kernel_bytes, double* reference_bytes);
+/* gb_iteration_kernels  number of kernel launches one LM iteration replays
+ *              (kernel nodes of the captured per-iteration CUDA graph, between
+ *              gb_begin and gb_end; 0 when the iteration is not captured). */
+int gb_iteration_kernels(gb_graph* g, int32_t* kernels);
 
 /* gb_host_alloc / gb_host_free  page-locked host memory for the caller's
  *              camera / point arrays (bal::BalGraph owns its AoS arrays,

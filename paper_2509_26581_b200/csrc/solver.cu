@@ -79,6 +79,7 @@ class SolverBase {
   virtual void* stream() = 0;
   virtual void time_hvp(int reps, double* ms_pair, double* ms_tiles) = 0;
   virtual void hvp_bytes(double* kernel_bytes, double* reference_bytes) = 0;
+  virtual int iteration_kernels() const = 0;  // kernel nodes of one captured LM iteration (0: not captured)
   virtual double residual_sum(int level, bool raw) = 0;
   virtual void ls_linearize(int level, double cmin, double cmax, int damping, double* chi2, int64_t* n, void* b,
                             void* diag, void* clamped, void* scaling, int32_t* finite) = 0;
@@ -545,6 +546,8 @@ class Solver final : public SolverBase {
     b += nc9 * (sV + sF + sV);                         // camera p, D in; ap out
     if (kernel_bytes) *kernel_bytes = b;
   }
+
+  int iteration_kernels() const override { return graph_exec_ ? graph_kernels_ : 0; }
 
   void time_hvp(int reps, double* ms_pair, double* ms_tiles) override {
     if (in_solve_) throw std::logic_error("gb_time_hvp during a solve");
@@ -1639,6 +1642,17 @@ class Solver final : public SolverBase {
     CK(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
     enqueue_iteration(pcg_max_it);
     CK(cudaStreamEndCapture(s_, &graph));
+    // kernel nodes of one LM iteration (gb_iteration_kernels: bench.py's gpu_launches)
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+    graph_kernels_ = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      CK(cudaGraphNodeGetType(nd, &t));
+      graph_kernels_ += t == cudaGraphNodeTypeKernel;
+    }
     CK(cudaGraphInstantiate(&graph_exec_, graph, 0));
     CK(cudaGraphDestroy(graph));
     graph_pcg_it_ = pcg_max_it;
@@ -1690,6 +1704,7 @@ class Solver final : public SolverBase {
   size_t h2d_bytes_ = 0, d2h_bytes_ = 0;
   cudaGraphExec_t graph_exec_ = nullptr;
   int graph_pcg_it_ = -1;
+  int graph_kernels_ = 0;
   gb_iteration_record* graph_recs_ = nullptr;
   DBuf st_buf_, rec_buf_, dbg_buf_;
   DBuf b_rc_, b_xp_;
@@ -1912,6 +1927,10 @@ void* gb_stream(gb_graph* g) {
 
 int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_pair, double* ms_tiles) {
   return guarded([&] { g->get().time_hvp(reps < 1 ? 1 : reps, ms_pair, ms_tiles); });
+}
+
+int gb_iteration_kernels(gb_graph* g, int32_t* kernels) {
+  return guarded([&] { *kernels = g->get().iteration_kernels(); });
 }
 
 int gb_hvp_bytes(gb_graph* g, double* kernel_bytes, double* reference_bytes) {

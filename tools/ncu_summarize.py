@@ -91,9 +91,14 @@ def main():
         launches(a.launches, a.tag)
     if a.full:
         traffic, kname = full(a.full, a.tag, a.hvp_label)
+        import sys
+
+        sys.path.insert(0, ROOT)
+        from bench import hvp_source_sha
+
         with open(os.path.join(PROF, "ncu_hvp_summary.json"), "w") as f:
             json.dump({"kernel": kname, "dram_bytes_per_hvp": traffic, "source": os.path.basename(a.full),
-                       "tag": a.tag, "note": "dram__bytes_read.sum + dram__bytes_write.sum of one HVP tile-kernel launch"},
+                       "tag": a.tag, "kernel_source_sha": hvp_source_sha(), "note": "dram__bytes_read.sum + dram__bytes_write.sum of one HVP tile-kernel launch"},
                       f, indent=1)
     if a.full_lin:
         full(a.full_lin, a.tag, "lin_normal")
