@@ -251,12 +251,20 @@ void gb_host_copy(void* dst, const void* src, uint64_t bytes);
  *           rank 0, shared with the other ranks out of band.
  *   kind 1: in-process loopback (ranks are host threads on one GPU; for
  *           testing the sharded path on a single device); id = uint64 key.
+ *   kind 2: shared memory (one process per rank on one host, any devices,
+ *           also several ranks on the same GPU; host-synchronous collectives
+ *           through a POSIX shm segment); id = uint64 key, equal on all ranks.
  * gb_shard_plan (host only) reports each rank's [tile0,tile1), [point0,point1)
  * (internal order), edge count and (optionally) the owner rank of every point
  * for `world` ranks. world == 1 with kind 0 runs the collective code path on
  * a single rank. */
 int gb_nccl_unique_id(void* out128);
 int gb_set_distributed(gb_graph* g, int world, int rank, int kind, const void* id);
+/* Test hook (host only, no GPU): the kind-2 shared-memory collectives on host
+ * buffers: allreduce (sum, or max) of data[n] in rank order, then a broadcast
+ * of bcast[nb] (may be NULL) from rank world-1. Blocks until all ranks call. */
+int gb_shm_allreduce_selftest(int world, int rank, uint64_t key, double* data, uint64_t n, int max, double* bcast,
+                              uint64_t nb);
 int gb_shard_plan(uint64_t num_cameras, uint64_t num_points, uint64_t n, const uint32_t* camera_index,
                   const uint32_t* point_index, int world, uint32_t* tiles_out, uint32_t* points_out,
                   uint64_t* edges_out, uint32_t* point_owner);

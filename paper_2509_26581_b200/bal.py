@@ -373,9 +373,14 @@ class BalGraph:
     def set_distributed(self, world: int, rank: int, kind: str = "nccl", uid: bytes = b""):
         """Shard this graph over `world` ranks (this handle is `rank`). kind
         'nccl': uid = nccl_unique_id() from rank 0; kind 'loopback': ranks are
-        host threads of this process on one GPU, uid = an 8-byte group key."""
+        host threads of this process on one GPU, uid = an 8-byte group key;
+        kind 'shm': one process per rank on this host (shared-memory
+        collectives, any devices), uid = an 8-byte key equal on all ranks."""
+        kinds = {"nccl": 0, "loopback": 1, "shm": 2}
+        if kind not in kinds:
+            raise ValueError(f"unknown reducer kind: {kind}")
         buf = ctypes.create_string_buffer(bytes(uid).ljust(128, b"\0"), 128)
-        self.backend.check(self.backend.fn("set_distributed")(self._h, world, rank, 0 if kind == "nccl" else 1, buf))
+        self.backend.check(self.backend.fn("set_distributed")(self._h, world, rank, kinds[kind], buf))
         self._bind()
 
     # -- objective

@@ -299,21 +299,25 @@ void activate(const ActivationInput& in, Activation& out) {
 
 namespace gb {
 
-void shard_range(const Activation& full, int world, int rank, uint32_t* tile0, uint32_t* tile1, uint32_t* point0,
-                 uint32_t* point1) {
-  const uint64_t total = full.n_slots;
+void shard_bounds(const uint32_t* tile_ebeg, const uint32_t* tile_pbeg, uint32_t ntiles, int world, int rank,
+                  uint32_t* tile0, uint32_t* tile1, uint32_t* point0, uint32_t* point1) {
+  const uint64_t total = tile_ebeg[ntiles];
   auto bound = [&](int r) -> uint32_t {
     if (r <= 0) return 0;
-    if (r >= world) return full.ntiles;
+    if (r >= world) return ntiles;
     const uint64_t target = total * static_cast<uint64_t>(r) / static_cast<uint64_t>(world);
     // first tile whose slot begin reaches the target
-    return static_cast<uint32_t>(std::lower_bound(full.tile_ebeg.begin(), full.tile_ebeg.end() - 1, target) -
-                                 full.tile_ebeg.begin());
+    return static_cast<uint32_t>(std::lower_bound(tile_ebeg, tile_ebeg + ntiles, target) - tile_ebeg);
   };
   *tile0 = bound(rank);
   *tile1 = std::max(*tile0, bound(rank + 1));
-  *point0 = full.tile_pbeg[*tile0];
-  *point1 = full.tile_pbeg[*tile1];
+  *point0 = tile_pbeg[*tile0];
+  *point1 = tile_pbeg[*tile1];
+}
+
+void shard_range(const Activation& full, int world, int rank, uint32_t* tile0, uint32_t* tile1, uint32_t* point0,
+                 uint32_t* point1) {
+  shard_bounds(full.tile_ebeg.data(), full.tile_pbeg.data(), full.ntiles, world, rank, tile0, tile1, point0, point1);
 }
 
 void shard(const Activation& full, int world, int rank, Activation& out) {

@@ -81,6 +81,10 @@ void activate(const ActivationInput& in, Activation& out);
 void shard_range(const Activation& full, int world, int rank, uint32_t* tile0, uint32_t* tile1, uint32_t* point0,
                  uint32_t* point1);
 void shard(const Activation& full, int world, int rank, Activation& out);
+// the same balance over raw tile arrays (tile_ebeg / tile_pbeg: ntiles + 1
+// entries), shared by the host shard() and the per-rank device activation
+void shard_bounds(const uint32_t* tile_ebeg, const uint32_t* tile_pbeg, uint32_t ntiles, int world, int rank,
+                  uint32_t* tile0, uint32_t* tile1, uint32_t* point0, uint32_t* point1);
 
 // building blocks shared with the device activation (activate_dev.cuh)
 void greedy_tiles(const std::vector<uint32_t>& deg_int, std::vector<uint32_t>& tile_pbeg,

@@ -79,12 +79,20 @@ __device__ inline uint32_t tile_of_rank(const uint32_t* tile_pbeg, uint32_t ntil
   return lo;
 }
 
+// key (tile, camera) of every active edge; edges whose point lies outside this
+// rank's internal range [p0, p1) get the sentinel tile ntiles (sorted last)
 __global__ void k_edge_keys(uint64_t na, const uint32_t* cam_a, const uint32_t* pt_a, const uint32_t* pt_rank,
-                            const uint32_t* tile_pbeg, uint32_t ntiles, uint64_t* key, uint32_t* val) {
+                            const uint32_t* tile_pbeg, uint32_t ntiles, uint32_t p0, uint32_t p1, uint64_t* key,
+                            uint32_t* val) {
   for (uint64_t a = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; a < na;
        a += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t t = tile_of_rank(tile_pbeg, ntiles, pt_rank[pt_a[a]]);
-    key[a] = (static_cast<uint64_t>(t) << 32) | cam_a[a];
+    const uint32_t r = pt_rank[pt_a[a]];
+    if (r < p0 || r >= p1) {
+      key[a] = (static_cast<uint64_t>(ntiles) << 32) | 0xffffffffull;
+    } else {
+      const uint32_t t = tile_of_rank(tile_pbeg, ntiles, r - p0);
+      key[a] = (static_cast<uint64_t>(t) << 32) | cam_a[a];
+    }
     val[a] = static_cast<uint32_t>(a);
   }
 }
@@ -92,7 +100,7 @@ __global__ void k_edge_keys(uint64_t na, const uint32_t* cam_a, const uint32_t* 
 // place edge k of the sorted order into its padded slot; emit head flags
 template <typename FP>
 __global__ void k_place(uint64_t na, const uint64_t* skey, const uint32_t* order, const uint32_t* cam_a,
-                        const uint32_t* pt_a, const uint32_t* entry_a, const uint32_t* pt_rank,
+                        const uint32_t* pt_a, const uint32_t* entry_a, const uint32_t* pt_rank, uint32_t p0,
                         const uint32_t* real_beg, const uint32_t* tile_ebeg, const uint32_t* tile_pbeg,
                         const double* obs, uint64_t ns, uint32_t* d_a, uint32_t* d_cam, uint16_t* d_lpt, FP* d_obs,
                         uint32_t* pkey, uint32_t* pval, uint32_t* head_cam, uint32_t* head_run) {
@@ -103,7 +111,7 @@ __global__ void k_place(uint64_t na, const uint64_t* skey, const uint32_t* order
     const uint32_t cam = static_cast<uint32_t>(skey[k]);
     const uint32_t j = static_cast<uint32_t>(k - real_beg[t]);
     const uint64_t d = tile_ebeg[t] + j;
-    const uint32_t r = pt_rank[pt_a[a]];
+    const uint32_t r = pt_rank[pt_a[a]] - p0;  // rank-local internal point
     d_a[d] = a;
     d_cam[d] = cam_a[a];
     d_lpt[d] = static_cast<uint16_t>(r - tile_pbeg[t]);

@@ -10,6 +10,10 @@
 //                    eager launches, host rendezvous per collective). Lets the
 //                    sharded path be tested on a single device; results are
 //                    reduced in rank order like a deterministic allreduce.
+//   ShmReducer       one PROCESS per rank on one host (any GPUs, also all on
+//                    the same device): POSIX shared memory, host barriers,
+//                    rank-order sums. Lets the sharded path run as real
+//                    separate processes where NCCL cannot (one GPU).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -30,8 +34,13 @@ class Reducer {
   virtual void broadcast(void* buf, size_t bytes, int root, cudaStream_t s) = 0;
 };
 
-// kind 0: NCCL, id = 128-byte ncclUniqueId; kind 1: loopback, id = uint64 group key
+// kind 0: NCCL, id = 128-byte ncclUniqueId; kind 1: loopback, id = uint64 group
+// key; kind 2: shared memory, id = uint64 segment key
 std::unique_ptr<Reducer> make_reducer(int kind, int world, int rank, const void* id);
+// the shared-memory collectives on host buffers (CPU test hook): sum/max
+// allreduce of data[n], then a broadcast of bcast[nb] from rank world-1
+void shm_allreduce_selftest(int world, int rank, uint64_t key, double* data, uint64_t n, int max, double* bcast,
+                            uint64_t nb);
 // ncclGetUniqueId through the runtime-loaded NCCL (128 bytes)
 void nccl_unique_id(void* out128);
 

@@ -121,9 +121,9 @@ class BlockCache {
     if (bytes < (1u << 20)) return false;
     std::lock_guard<std::mutex> lk(m_);
     size_t& total = total_[dev];
-    if (!total) {  // device memory size, queried once
-      size_t fr = 0;
-      if (cudaMemGetInfo(&fr, &total) != cudaSuccess) total = 0;
+    if (!total) {  // the memory size of `dev` (not of the current device), queried once
+      cudaDeviceProp prop;
+      if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) total = prop.totalGlobalMem;
       if (!total) return false;
     }
     if (held_[dev] + bytes > total / 3) return false;
@@ -208,9 +208,15 @@ class DBuf {
   ~DBuf() { release(); }
   void release() {
     if (p_) {
-      // stream work that may still use the block completes first (cudaFree's own semantics)
+      // stream work that may still use the block completes first (cudaFree's own
+      // semantics), on the block's own device (another graph may have made a
+      // different device current on this thread)
+      int cur = -1;
+      cudaGetDevice(&cur);
+      if (cur != dev_) cudaSetDevice(dev_);
       cudaDeviceSynchronize();
       if (!BlockCache::get().give(dev_, p_, cap_)) cudaFree(p_);
+      if (cur != dev_ && cur >= 0) cudaSetDevice(cur);
     }
     p_ = nullptr;
     bytes_ = cap_ = 0;
@@ -321,6 +327,7 @@ class Solver final : public SolverBase {
     CK(cudaMemsetAsync(st_, 0, sizeof(State<FP>), s_));
   }
   ~Solver() override {
+    cudaSetDevice(g_.device);  // this handle's streams, events and blocks live there
     for (auto& e : ev_) cudaEventDestroy(e);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (flag_host_) cudaFreeHost(flag_host_);
@@ -339,11 +346,15 @@ class Solver final : public SolverBase {
   // device activation == host activation, array by array (empty string = ok)
   std::string selfcheck(int level) override {
     CK(cudaSetDevice(g_.device));
-    if (g_.reducer) throw std::logic_error("selfcheck applies to the single-GPU (device-activated) path");
     have_act_ = false;
     ensure_structure(level);
+    // host reference: the full activation, sliced to this rank when sharded
     Activation h;
-    activate(activation_input(level), h);
+    {
+      Activation full;
+      activate(activation_input(level), full);
+      shard(full, g_.world(), g_.rank(), h);
+    }
     std::string err;
     auto cmp = [&](const char* name, const auto* dptr, const auto& hv) {
       using T = typename std::decay_t<decltype(hv)>::value_type;
@@ -784,25 +795,7 @@ class Solver final : public SolverBase {
     if (have_act_ && act_rev_ == g_.revision && act_level_ == level) return;
     if (!g_.cams || !g_.pts) throw std::logic_error("cameras and points must be set before solving");
     host_plan_ = false;
-    if (g_.reducer) {  // sharded: host activation + slicing (tested on CPU and by the loopback suite)
-      const ActivationInput in = activation_input(level);
-      Activation full;
-      activate(in, full);
-      full_np_ = full.np;
-      full_pt_order_ = full.pt_order;
-      shard_p0_.assign(g_.world() + 1, 0);
-      for (int r = 0; r < g_.world(); ++r) {
-        uint32_t t0, t1, p0, p1;
-        shard_range(full, g_.world(), r, &t0, &t1, &p0, &p1);
-        shard_p0_[r] = p0;
-        shard_p0_[r + 1] = p1;
-      }
-      shard(full, g_.world(), g_.rank(), act_);
-      host_plan_ = true;
-      upload_structure_host();
-    } else {
-      device_structure(level);
-    }
+    device_structure(level);  // sharded: this rank's point-tile range only
     have_act_ = true;
     act_rev_ = g_.revision;
     act_level_ = level;
@@ -821,6 +814,7 @@ class Solver final : public SolverBase {
   // reference column map and incidence CSRs.
   void ensure_host_plan() {
     if (host_plan_) return;
+    need_single();
     activate(activation_input(act_level_), act_);
     host_plan_ = true;
     build_ref_map();
@@ -1052,28 +1046,62 @@ class Solver final : public SolverBase {
     }
     if (np) CK(cudaMemcpyAsync(hdeg, degi, np * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
     CK(cudaStreamSynchronize(s_));
-    // tiles: the host greedy over degrees (activate.cpp greedy_tiles)
+    // tiles: the host greedy over degrees (activate.cpp greedy_tiles), over ALL
+    // points: the tile plan, and with it every rank's shard, is global
     ptm.mark("act: compact + point order");
-    std::vector<uint32_t> real_beg;
-    greedy_tiles(hdeg, np, act_.tile_pbeg, real_beg, nullptr);
+    std::vector<uint32_t> gpbeg, greal;
+    greedy_tiles(hdeg, np, gpbeg, greal, nullptr);
     ptm.mark("act: host greedy tiles");
-    act_.ntiles = static_cast<uint32_t>(act_.tile_pbeg.size() - 1);
-    const uint32_t T = act_.ntiles;
+    const uint32_t GT = static_cast<uint32_t>(gpbeg.size() - 1);
+    std::vector<uint32_t> gebeg(GT + 1, 0);
+    {
+      uint64_t slot = 0;
+      for (uint32_t t = 0; t < GT; ++t) {
+        gebeg[t] = static_cast<uint32_t>(slot);
+        slot += (greal[t + 1] - greal[t] + kJBlock - 1) / kJBlock * kJBlock;
+        if (slot > 0xffffffffull) throw std::invalid_argument("more than 2^32 padded edge slots");
+      }
+      gebeg[GT] = static_cast<uint32_t>(slot);
+    }
+    // this rank's contiguous tile range [t0, t1) / internal points [p0, p1)
+    // (shard_bounds: the same balance as the host shard(); world 1: everything)
+    uint32_t t0 = 0, t1 = GT, p0 = 0, p1 = static_cast<uint32_t>(np);
+    if (g_.reducer) {
+      const int W = g_.world();
+      shard_p0_.assign(W + 1, 0);
+      for (int r = 0; r < W; ++r) {
+        uint32_t a0, a1, q0, q1;
+        shard_bounds(gebeg.data(), gpbeg.data(), GT, W, r, &a0, &a1, &q0, &q1);
+        shard_p0_[r] = q0;
+        shard_p0_[r + 1] = q1;
+      }
+      shard_bounds(gebeg.data(), gpbeg.data(), GT, W, g_.rank(), &t0, &t1, &p0, &p1);
+      full_np_ = np;  // the write-back scatters every rank's points through the global order
+      full_pt_order_.resize(np);
+      if (np) CK(cudaMemcpyAsync(full_pt_order_.data(), pt_order, np * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
+    }
+    const uint32_t T = t1 - t0;
+    const uint64_t npl = p1 - p0;
+    act_.np = npl;
+    act_.ntiles = T;
+    act_.tile_pbeg.resize(T + 1);
     act_.tile_ecnt.resize(T);
     act_.tile_ebeg.assign(T + 1, 0);
     act_.tile_chunk_base.assign(T + 1, 0);
-    uint64_t slot = 0;
+    std::vector<uint32_t> real_beg(T + 1);
+    for (uint32_t t = 0; t <= T; ++t) {
+      act_.tile_pbeg[t] = gpbeg[t0 + t] - p0;
+      act_.tile_ebeg[t] = gebeg[t0 + t] - gebeg[t0];
+      real_beg[t] = greal[t0 + t] - greal[t0];
+    }
     for (uint32_t t = 0; t < T; ++t) {
       act_.tile_ecnt[t] = real_beg[t + 1] - real_beg[t];
-      act_.tile_ebeg[t] = static_cast<uint32_t>(slot);
-      slot += (act_.tile_ecnt[t] + kJBlock - 1) / kJBlock * kJBlock;
       act_.tile_chunk_base[t + 1] = act_.tile_chunk_base[t] + (act_.tile_ecnt[t] + 31) / 32;
     }
-    if (slot > 0xffffffffull) throw std::invalid_argument("more than 2^32 padded edge slots");
-    act_.tile_ebeg[T] = static_cast<uint32_t>(slot);
-    act_.n_slots = slot;
+    act_.n_slots = act_.tile_ebeg[T];
     act_.nchunks = act_.tile_chunk_base[T];
-    const uint64_t ns = slot;
+    const uint64_t ns = act_.n_slots;
+    const uint64_t nal = real_beg[T];  // this rank's active edges
     dev_ = Dev<FP, SP>{};
     set_counts();
     Dev<FP, SP>& d = dev_;
@@ -1087,8 +1115,9 @@ class Solver final : public SolverBase {
     uint64_t* k64b = scratch<uint64_t>(s_k64b, na);
     uint32_t* vals = scratch<uint32_t>(s_val2, na);
     uint32_t* order = scratch<uint32_t>(s_order, na);
-    k_edge_keys<<<grid_for(na), 256, 0, s_>>>(na, cam_a, pt_a, rank, d.tile_pbeg, T, k64, vals);
+    k_edge_keys<<<grid_for(na), 256, 0, s_>>>(na, cam_a, pt_a, rank, d.tile_pbeg, T, p0, p1, k64, vals);
     CK(cudaGetLastError());
+    // other ranks' edges carry the sentinel tile T: the first nal sorted keys are this rank's
     cub_sort<uint64_t>(k64, k64b, vals, order, na, 32 + bits_for(T));
     // padded slot arrays
     uint32_t* d_a = static_cast<uint32_t*>(b_da_.alloc(std::max<uint64_t>(1, ns) * sizeof(uint32_t)));
@@ -1104,17 +1133,17 @@ class Solver final : public SolverBase {
     uint32_t* hc = scratch<uint32_t>(s_hc, na);
     uint32_t* hr = scratch<uint32_t>(s_hr, na);
     CK(cudaStreamWaitEvent(s_, ev_up_, 0));  // observations uploaded
-    k_place<FP><<<grid_for(na), 256, 0, s_>>>(na, k64b, order, cam_a, pt_a, entry_a, rank, rb, d.tile_ebeg,
-                                               d.tile_pbeg, obs, ns, d_a, d_cam, d_lpt, d_obs, pkey, pval, hc, hr);
+    k_place<FP><<<grid_for(nal), 256, 0, s_>>>(nal, k64b, order, cam_a, pt_a, entry_a, rank, p0, rb, d.tile_ebeg,
+                                                d.tile_pbeg, obs, ns, d_a, d_cam, d_lpt, d_obs, pkey, pval, hc, hr);
     CK(cudaGetLastError());
     uint32_t* ic = scratch<uint32_t>(s_ic, na);
     uint32_t* ir = scratch<uint32_t>(s_ir, na);
-    cub_scan_incl(hc, ic, na);
-    cub_scan_incl(hr, ir, na);
+    cub_scan_incl(hc, ic, nal);
+    cub_scan_incl(hr, ir, nal);
     uint32_t* tile_cam_off = static_cast<uint32_t*>(b_tile_cam_off_.alloc((T + 1) * sizeof(uint32_t)));
     uint32_t* chunk_part_base =
         static_cast<uint32_t*>(b_chunk_part_.alloc((act_.nchunks + 1) * sizeof(uint32_t)));
-    k_tile_offsets<<<grid_for(T + 1), 256, 0, s_>>>(T, na, rb, d.tile_ecnt, d.tile_chunk_base, ic, ir, tile_cam_off,
+    k_tile_offsets<<<grid_for(T + 1), 256, 0, s_>>>(T, nal, rb, d.tile_ecnt, d.tile_chunk_base, ic, ir, tile_cam_off,
                                                      chunk_part_base);
     CK(cudaGetLastError());
     act_.tile_cam_off.resize(T + 1);
@@ -1128,18 +1157,18 @@ class Solver final : public SolverBase {
     const uint32_t ncams_total = act_.tile_cam_off[T];
     uint32_t* tile_cams = static_cast<uint32_t*>(b_tile_cams_.alloc(std::max<uint32_t>(1, ncams_total) * sizeof(uint32_t)));
     uint32_t* run_cam = scratch<uint32_t>(s_runcam, nparts);
-    k_runs<<<grid_for(na), 256, 0, s_>>>(na, k64b, rb, d.tile_ebeg, tile_cam_off, hc, ic, hr, ir, d_lcam, tile_cams,
+    k_runs<<<grid_for(nal), 256, 0, s_>>>(nal, k64b, rb, d.tile_ebeg, tile_cam_off, hc, ic, hr, ir, d_lcam, tile_cams,
                                           run_cam);
     k_pad<<<grid_for(T), 256, 0, s_>>>(T, d.tile_ebeg, d.tile_ecnt, d_cam, d_lcam);
     CK(cudaGetLastError());
     // per-point slot lists: stable sort of (point rank, slot) + degree scan
     uint32_t* pkey2 = scratch<uint32_t>(s_pkey2, na);
     uint32_t* pval2 = scratch<uint32_t>(s_pval2, na);
-    cub_sort<uint32_t>(pkey, pkey2, pval, pval2, na, bits_for(np));
-    uint16_t* pt_slots = static_cast<uint16_t*>(b_pt_slots_.alloc(std::max<uint64_t>(1, na) * sizeof(uint16_t)));
-    k_u32_to_u16<<<grid_for(na), 256, 0, s_>>>(na, pval2, pt_slots);
-    uint32_t* pt_slot_off = static_cast<uint32_t*>(b_pt_slot_off_.alloc((np + 1) * sizeof(uint32_t)));
-    cub_scan_excl(degi, pt_slot_off, np + 1);
+    cub_sort<uint32_t>(pkey, pkey2, pval, pval2, nal, bits_for(npl));
+    uint16_t* pt_slots = static_cast<uint16_t*>(b_pt_slots_.alloc(std::max<uint64_t>(1, nal) * sizeof(uint16_t)));
+    k_u32_to_u16<<<grid_for(nal), 256, 0, s_>>>(nal, pval2, pt_slots);
+    uint32_t* pt_slot_off = static_cast<uint32_t*>(b_pt_slot_off_.alloc((npl + 1) * sizeof(uint32_t)));
+    cub_scan_excl(degi + p0, pt_slot_off, npl + 1);  // degi[p1] is never summed (exclusive)
     // camera -> partial-slot CSR
     uint32_t* slots = scratch<uint32_t>(s_slots, nparts);
     uint32_t* runcam2 = scratch<uint32_t>(s_runcam2, nparts);
@@ -1153,8 +1182,9 @@ class Solver final : public SolverBase {
     cub_scan_excl(cnt, cam_part_off, nc + 1);
     // columns: free mask in internal order
     uint8_t* col_free = static_cast<uint8_t*>(b_col_free_.alloc(std::max<uint64_t>(1, ncols_)));
-    k_col_free<<<grid_for(ncols_), 256, 0, s_>>>(static_cast<uint32_t>(nc), static_cast<uint32_t>(np), cfix, pfix,
-                                                 pt_order, col_free);
+    pt_order_dev_ = pt_order + p0;  // this rank's internal points -> point ids
+    k_col_free<<<grid_for(ncols_), 256, 0, s_>>>(static_cast<uint32_t>(nc), static_cast<uint32_t>(npl), cfix, pfix,
+                                                 pt_order_dev_, col_free);
     CK(cudaGetLastError());
     classify_tiles(act_);
     d.normal_tiles = to_dev(b_normal_, act_.normal_tiles);
@@ -1344,22 +1374,18 @@ class Solver final : public SolverBase {
     const uint64_t nc = act_.nc, np = act_.np;
     FP* stage = b_ptstage_.as<FP>();
     CK(cudaMemcpyAsync(dev_.x, g_.cams, 9 * nc * sizeof(FP), cudaMemcpyHostToDevice, s_));
-    if (dist()) {  // the shard's own points only
-      std::vector<FP> loc(3 * np);
-      const FP* up = static_cast<const FP*>(g_.pts);
-      for (uint64_t i = 0; i < np; ++i)
-        for (int k = 0; k < 3; ++k) loc[3 * i + k] = up[3ull * act_.pt_order[i] + k];
-      CK(cudaMemcpyAsync(dev_.x + 9 * nc, loc.data(), loc.size() * sizeof(FP), cudaMemcpyHostToDevice, s_));
-      CK(cudaStreamSynchronize(s_));
-    } else {
-      if (!pts_staged_)  // else already uploaded under the device activation (s_ waited on ev_up_)
-        CK(cudaMemcpyAsync(stage, g_.pts, 3 * np * sizeof(FP), cudaMemcpyHostToDevice, s_));
-      actdev::k_gather_points<FP><<<grid_for(3 * np), 256, 0, s_>>>(static_cast<uint32_t>(np), pt_order_dev_, stage,
-                                                                    dev_.x + 9 * nc);
-      CK(cudaGetLastError());
+    // every user point is staged (a shard gathers its own internal range:
+    // pt_order_dev_ points at it)
+    const uint64_t np_all = g_.np;
+    if (!pts_staged_) {  // else already uploaded under the device activation (s_ waited on ev_up_)
+      stage = static_cast<FP*>(b_ptstage_.alloc(std::max<uint64_t>(1, 3 * np_all) * sizeof(FP)));
+      if (np_all) CK(cudaMemcpyAsync(stage, g_.pts, 3 * np_all * sizeof(FP), cudaMemcpyHostToDevice, s_));
     }
+    actdev::k_gather_points<FP><<<grid_for(3 * np), 256, 0, s_>>>(static_cast<uint32_t>(np), pt_order_dev_, stage,
+                                                                  dev_.x + 9 * nc);
+    CK(cudaGetLastError());
     pts_staged_ = false;
-    h2d_bytes_ += ncols_ * sizeof(FP);
+    h2d_bytes_ += (9 * nc + 3 * np_all) * sizeof(FP);
   }
 
   void download_params() {
@@ -1962,6 +1988,11 @@ void gb_host_copy(void* dst, const void* src, uint64_t bytes) {
 
 int gb_nccl_unique_id(void* out128) {
   return guarded([&] { gb::nccl_unique_id(out128); });
+}
+
+int gb_shm_allreduce_selftest(int world, int rank, uint64_t key, double* data, uint64_t n, int max, double* bcast,
+                              uint64_t nb) {
+  return guarded([&] { gb::shm_allreduce_selftest(world, rank, key, data, n, max, bcast, nb); });
 }
 
 int gb_set_distributed(gb_graph* g, int world, int rank, int kind, const void* id) {

@@ -109,3 +109,48 @@ def test_shard_plan_partitions():
         assert np.bincount(owner, minlength=world).sum() == p.num_points
         if world > 1:  # balanced by edge count
             assert edges.max() <= 1.2 * edges.mean() + 600
+
+
+# ---------------------------------------------------------------------------
+# The product's shared-memory reducer (kind 2) between real processes: sums
+# in rank order (every rank gets identical bits), max, multi-slot messages,
+# broadcast. The same collectives carry the sharded GPU solve in
+# tests/test_gpu_sharded.py::test_shm_processes_match_single_gpu.
+def shm_worker(rank, world, key, n, outq):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from paper_2509_26581_b200 import _abi
+
+    L = _abi.lib()
+    rng = np.random.default_rng(100 + rank)
+    data = rng.standard_normal(n)
+    mx = data.copy()
+    bc = np.full(5000, float(rank))
+    rc1 = L.gb_shm_allreduce_selftest(world, rank, key, data.ctypes.data, n, 0, bc.ctypes.data, bc.size)
+    rc2 = L.gb_shm_allreduce_selftest(world, rank, key + 1, mx.ctypes.data, n, 1, None, 0)
+    outq.put((rank, rc1, rc2, data, mx, bc))
+
+
+@pytest.mark.parametrize("world,n", [(3, 1000), (2, 1_500_000)])
+def test_shm_reducer_processes(world, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    key = 0x5EED0000 + world * 7 + os.getpid() % 1000 * 16
+    procs = [ctx.Process(target=shm_worker, args=(r, world, key, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in range(world)), key=lambda t: t[0])
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    ins = [np.random.default_rng(100 + r).standard_normal(n) for r in range(world)]
+    want = ins[0].copy()
+    for x in ins[1:]:
+        want = want + x  # rank order
+    want_max = np.maximum.reduce(ins)
+    for rank, rc1, rc2, data, mx, bc in res:
+        assert rc1 == 0 and rc2 == 0
+        assert np.array_equal(data.view(np.uint64), want.view(np.uint64))
+        assert np.array_equal(mx, want_max)
+        assert np.all(bc == world - 1)
