@@ -312,6 +312,16 @@ int gb_incidence(gb_graph* g, int descriptor, uint64_t* nseg, uint64_t* nitems,
                  uint64_t* vertex_of_segment, uint64_t* offsets, uint32_t* items_factor,
                  uint16_t* items_slot);
 
+/* ---- report wire format -------------------------------------------------
+ * Replaces gopt::to_json(const SolveReport&).dump() and gopt::to_csv
+ * (include/gopt/report.hpp:32-71; used by src/experiment.cpp:84,90): the
+ * same bytes for a report + its n IterationRecords. Writes at most cap bytes
+ * (NUL-terminated) into buf (may be NULL); *needed = full length + 1. */
+int gb_report_json(const gb_solve_report* report, const gb_iteration_record* records, int32_t n, char* buf,
+                   uint64_t cap, uint64_t* needed);
+int gb_report_csv(const gb_solve_report* report, const gb_iteration_record* records, int32_t n, char* buf,
+                  uint64_t cap, uint64_t* needed);
+
 /* ---- synthetic BAL-shaped problems (bench / test input) -------------------
  * Deterministic generator with the semantics of tests/synthetic_bal.hpp:16-113
  * (camera ring, point cloud, pixel noise, perturbed initial estimate), sized

@@ -47,6 +47,11 @@
 
 #include "gb_bal.h"
 
+#if __has_include("json.hpp")
+#include "gopt/report.hpp"
+#define GB_REF_REPORT 1
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -466,5 +471,58 @@ int ref_parse_bal_file(const char* path, std::uint64_t* shape3, std::uint32_t* c
       for (int k = 0; k < 3; ++k) pts[3 * q + k] = p.points[q][k];
   });
 }
+
+#ifdef GB_REF_REPORT
+// gopt::to_json(report).dump() / gopt::to_csv(report) (report.hpp:32-71) of a
+// SolveReport rebuilt from the C structs
+static gopt::SolveReport from_c(const gb_solve_report* r, const gb_iteration_record* recs, int n) {
+  gopt::SolveReport s;
+  for (int i = 0; i < n; ++i) {
+    gopt::IterationRecord x;
+    x.iteration = recs[i].iteration;
+    x.chi2_before = recs[i].chi2_before;
+    x.chi2_after = recs[i].chi2_after;
+    x.lambda = recs[i].lambda;
+    x.pcg_iterations = recs[i].pcg_iterations;
+    x.pcg_converged = recs[i].pcg_converged != 0;
+    x.pcg_relative_residual = recs[i].pcg_relative_residual;
+    x.low_quality_step = recs[i].low_quality_step != 0;
+    x.precond_fallback_blocks = recs[i].precond_fallback_blocks;
+    x.accepted = recs[i].accepted != 0;
+    x.wall_seconds = recs[i].wall_seconds;
+    s.iterations.push_back(x);
+  }
+  s.initial_chi2 = r->initial_chi2;
+  s.final_chi2 = r->final_chi2;
+  s.accepted_steps = r->accepted_steps;
+  s.termination = static_cast<gopt::Termination>(r->termination);
+  s.total_seconds = r->total_seconds;
+  s.free_dims = r->free_dims;
+  s.residual_dims = r->residual_dims;
+  s.active_factors = r->active_factors;
+  s.memory.jacobian_bytes = r->memory.jacobian_bytes;
+  s.memory.preconditioner_bytes = r->memory.preconditioner_bytes;
+  s.memory.workspace_bytes = r->memory.workspace_bytes;
+  s.memory.graph_bytes = r->memory.graph_bytes;
+  return s;
+}
+static int emit(const std::string& s, char* buf, std::uint64_t cap, std::uint64_t* needed) {
+  if (needed) *needed = s.size() + 1;
+  if (buf && cap) {
+    const std::size_t n = std::min<std::uint64_t>(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+  return GB_OK;
+}
+int ref_report_json(const gb_solve_report* r, const gb_iteration_record* recs, std::int32_t n, char* buf,
+                    std::uint64_t cap, std::uint64_t* needed) {
+  return emit(gopt::to_json(from_c(r, recs, n)).dump(), buf, cap, needed);
+}
+int ref_report_csv(const gb_solve_report* r, const gb_iteration_record* recs, std::int32_t n, char* buf,
+                   std::uint64_t cap, std::uint64_t* needed) {
+  return emit(gopt::to_csv(from_c(r, recs, n)), buf, cap, needed);
+}
+#endif
 
 }  // extern "C"

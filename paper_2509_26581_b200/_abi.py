@@ -112,7 +112,7 @@ EXPORTED = [
     "gb_total_error", "gb_ls_linearize", "gb_ls_hvp", "gb_ls_preconditioner", "gb_ls_solve_step",
     "gb_ls_jacobians", "gb_incidence", "gb_synthetic_bal", "gb_begin", "gb_step", "gb_end", "gb_stream",
     "gb_time_hvp", "gb_hvp_bytes", "gb_iteration_kernels", "gb_host_alloc", "gb_host_free", "gb_host_copy", "gb_nccl_unique_id", "gb_set_distributed", "gb_shm_allreduce_selftest", "gb_shard_plan", "gb_activation_selfcheck",
-    "gb_set_linear_solver",
+    "gb_set_linear_solver", "gb_report_json", "gb_report_csv",
     "gbg_last_error", "gbg_circle_solve", "gbg_vi_solve",  # generic path, include/gb_generic.h
 ]
 
@@ -163,6 +163,8 @@ def declare(lib: ctypes.CDLL, prefix: str = "gb_") -> ctypes.CDLL:
         f("activation_selfcheck", c_int, vp, c_int)
         f("set_linear_solver", c_int, vp, c_int)
         f("set_distributed", c_int, vp, c_int, c_int, c_int, vp)
+        f("report_json", c_int, POINTER(gb_solve_report), vp, c_int32, vp, c_uint64, POINTER(c_uint64))
+        f("report_csv", c_int, POINTER(gb_solve_report), vp, c_int32, vp, c_uint64, POINTER(c_uint64))
         f("shm_allreduce_selftest", c_int, c_int, c_int, c_uint64, vp, c_uint64, c_int, vp, c_uint64)
         f("shard_plan", c_int, c_uint64, c_uint64, c_uint64, vp, vp, c_int, vp, vp, vp, vp)
     else:

@@ -1,4 +1,5 @@
-"""BASELINE.json configs at their full published shapes (GPU).
+"""BASELINE.json configs at their full published shapes (GPU). The runs to
+convergence against the reference are in tests/test_gpu_convergence.py.
 
 configs[1] Dubrovnik-356 fp64 vs fp32, configs[2] Venice-1778 mixed precision
 with the implicit (dynamic, low-memory) HVP, configs[3] Final-13682 sharded.
@@ -80,33 +81,12 @@ def dubrovnik():
     return bal.synthetic_bal(*DUBROVNIK, seed=42)
 
 
-def test_dubrovnik_fp64_trace(gpu, ref, dubrovnik):
-    g, r, ra, rb = solve_pair(dubrovnik, ref, "fp64", "analytic", 4)
-    check_trace(ra, rb, 1e-6, pcg_exact=True)
-    # refined parameters agree too (the in-place write-back contract)
-    assert np.allclose(g.cameras, r.cameras, rtol=1e-6, atol=1e-9)
-
-
 def test_dubrovnik_fp32_vs_reference_and_fp64(gpu, ref, dubrovnik):
     g, r, ra, rb = solve_pair(dubrovnik, ref, "fp32", "analytic", 4)
     check_low_precision(dubrovnik, g, r, ra, rb)
     g64 = bal.build_graph(dubrovnik, "fp64")
     r64 = bal.levenberg_marquardt(g64, cfg(4))
     assert abs(ra.final_chi2 - r64.final_chi2) <= 1e-3 * r64.final_chi2
-
-
-def test_venice_mixed_dynamic(gpu, ref):
-    p = bal.synthetic_bal(*VENICE, seed=42)
-    g, r, ra, rb = solve_pair(p, ref, "fp32-bf16", "dynamic", 2)
-    check_low_precision(p, g, r, ra, rb)
-    assert ra.memory["jacobian_bytes"] == 0 == rb.memory["jacobian_bytes"]  # low-memory mode stores no J
-
-
-def test_final_fp64_first_iteration(gpu, ref):
-    """Final-13682 at full size: one LM iteration against the reference."""
-    p = bal.synthetic_bal(*FINAL, seed=42)
-    g, r, ra, rb = solve_pair(p, ref, "fp64", "analytic", 1)
-    check_trace(ra, rb, 1e-6, pcg_exact=True)
 
 
 def test_final_sharded_two_ranks_match_single(gpu):
