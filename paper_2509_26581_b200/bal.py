@@ -156,6 +156,44 @@ class SolveReport:
             it["lambda"] = it.pop("lambda_")
         return d
 
+    def to_c(self):
+        """(gb_solve_report, gb_iteration_record[n]) of this report."""
+        r = _abi.gb_solve_report()
+        r.initial_chi2, r.final_chi2 = self.initial_chi2, self.final_chi2
+        r.accepted_steps = self.accepted_steps
+        r.termination = _abi.TERMINATION_NAMES.index(self.termination)
+        r.total_seconds = self.total_seconds
+        r.free_dims, r.residual_dims, r.active_factors = self.free_dims, self.residual_dims, self.active_factors
+        for k in ("jacobian_bytes", "preconditioner_bytes", "workspace_bytes", "graph_bytes"):
+            setattr(r.memory, k, int(self.memory[k]))
+        n = len(self.iterations)
+        r.iterations_run = n
+        recs = (_abi.gb_iteration_record * max(1, n))()
+        for c, it in zip(recs, self.iterations):
+            c.iteration, c.chi2_before, c.chi2_after, c.lambda_ = it.iteration, it.chi2_before, it.chi2_after, it.lambda_
+            c.pcg_iterations, c.pcg_converged = it.pcg_iterations, int(it.pcg_converged)
+            c.pcg_relative_residual, c.low_quality_step = it.pcg_relative_residual, int(it.low_quality_step)
+            c.precond_fallback_blocks, c.accepted, c.wall_seconds = (it.precond_fallback_blocks, int(it.accepted),
+                                                                     it.wall_seconds)
+        return r, recs
+
+    def _wire(self, name: str) -> str:
+        r, recs = self.to_c()
+        fn = getattr(_abi.lib(), "gb_report_" + name)
+        need = ctypes.c_uint64()
+        Backend(_abi.lib(), "gb_").check(fn(ctypes.byref(r), recs, len(self.iterations), None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(need.value)
+        Backend(_abi.lib(), "gb_").check(fn(ctypes.byref(r), recs, len(self.iterations), buf, need.value, None))
+        return buf.value.decode()
+
+    def to_json(self) -> str:
+        """gopt::to_json(report).dump() (report.hpp:32-47), byte for byte."""
+        return self._wire("json")
+
+    def to_csv(self) -> str:
+        """gopt::to_csv(report) (report.hpp:51-71), byte for byte."""
+        return self._wire("csv")
+
 
 # ---------------------------------------------------------------- BAL problem
 @dataclass

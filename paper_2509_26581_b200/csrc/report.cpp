@@ -4,7 +4,7 @@
 // JSON: the reference builds an nlohmann::json object and callers dump() it
 // (src/experiment.cpp:84). nlohmann's default object type is an ordered
 // std::map, so dump() writes keys in ascending byte order, compactly, with
-// doubles in nlohmann's to_chars form: shortest round-trip digits, plain
+// doubles in nlohmann's to_chars form: Grisu2 round-trip digits, plain
 // notation for decimal exponents in (-4, 15], scientific otherwise
 // ("1e-05", "1.5e+20"), a trailing ".0" on integral values, null for
 // non-finite values. This writer reproduces that byte for byte without the
@@ -14,12 +14,11 @@
 // CSV: report.hpp:51-71 (std::to_string for the '#' header values, %.17g /
 // %.6f for the rows).
 
-#include <charconv>
+#include <cstdint>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
-#include <system_error>
 
 #include "gb_bal.h"
 
@@ -37,34 +36,134 @@ const char* term_name(int t) {
   return "?";  // levenberg_marquardt.hpp:46
 }
 
-// nlohmann::detail::to_chars formatting of a finite double
+// ---- shortest-digit generation: Grisu2 (Loitsch, "Printing floating-point
+// numbers quickly and accurately with integers", PLDI 2010), the variant
+// nlohmann/json's to_chars uses: boundaries m-/m+ of the double, one cached
+// power of ten that brings the exponent into [-60, -32], digit generation
+// between the (conservatively narrowed) boundaries, then the round-towards-v
+// correction. Grisu2 is not always the shortest representation (it is always
+// a correct round trip), so the digits differ from Ryu / std::to_chars on
+// ~1% of values; reproducing nlohmann's bytes needs this exact algorithm.
+struct DiyFp {
+  uint64_t f;
+  int e;
+};
+DiyFp dsub(DiyFp x, DiyFp y) { return {x.f - y.f, x.e}; }
+DiyFp dmul(DiyFp x, DiyFp y) {  // upper 64 bits of the 128-bit product, rounded half up
+  const unsigned __int128 p = static_cast<unsigned __int128>(x.f) * y.f;
+  const uint64_t h = static_cast<uint64_t>(p >> 64), l = static_cast<uint64_t>(p);
+  return {h + (l >> 63), x.e + y.e + 64};
+}
+DiyFp dnorm(DiyFp x) {
+  while ((x.f >> 63) == 0) {
+    x.f <<= 1;
+    --x.e;
+  }
+  return x;
+}
+DiyFp dnorm_to(DiyFp x, int e) { return {x.f << (x.e - e), e}; }
+
+struct CachedPow {
+  uint64_t f;
+  int e, k;
+};
+constexpr CachedPow kPow10[] = {
+#include "pow10_table.inc"
+};
+
+// digits of v into buf (no sign), *len digits, value = digits * 10^*dexp
+void grisu2(double v, char* buf, int* len, int* dexp) {
+  uint64_t bits;
+  std::memcpy(&bits, &v, 8);
+  const uint64_t E = bits >> 52, F = bits & ((uint64_t(1) << 52) - 1);
+  const DiyFp w = E == 0 ? DiyFp{F, 1 - 1075} : DiyFp{F + (uint64_t(1) << 52), static_cast<int>(E) - 1075};
+  const bool lower_closer = F == 0 && E > 1;
+  const DiyFp mp{2 * w.f + 1, w.e - 1};
+  const DiyFp mm = lower_closer ? DiyFp{4 * w.f - 1, w.e - 2} : DiyFp{2 * w.f - 1, w.e - 1};
+  const DiyFp wp = dnorm(mp);
+  const DiyFp wm = dnorm_to(mm, wp.e);
+  const DiyFp vn = dnorm(w);
+  // cached power c = 10^-k with alpha <= e(c * w+) + 64 <= gamma
+  const int f = -60 - wp.e - 1;
+  const int k = (f * 78913) / (1 << 18) + (f > 0);
+  const CachedPow c = kPow10[(300 + k + 7) / 8];
+  const DiyFp cm{c.f, c.e};
+  const DiyFp W = dmul(vn, cm), Wm = dmul(wm, cm), Wp = dmul(wp, cm);
+  const DiyFp Mm{Wm.f + 1, Wm.e}, Mp{Wp.f - 1, Wp.e};
+  *dexp = -c.k;
+  // digit generation
+  uint64_t delta = dsub(Mp, Mm).f, dist = dsub(Mp, W).f;
+  const DiyFp one{uint64_t(1) << -Mp.e, Mp.e};
+  uint32_t p1 = static_cast<uint32_t>(Mp.f >> -one.e);
+  uint64_t p2 = Mp.f & (one.f - 1);
+  auto round = [&](uint64_t rest, uint64_t ten_k) {
+    while (rest < dist && delta - rest >= ten_k && (rest + ten_k < dist || dist - rest > rest + ten_k - dist)) {
+      --buf[*len - 1];
+      rest += ten_k;
+    }
+  };
+  uint32_t pow10;
+  int n;
+  if (p1 >= 1000000000) pow10 = 1000000000, n = 10;
+  else if (p1 >= 100000000) pow10 = 100000000, n = 9;
+  else if (p1 >= 10000000) pow10 = 10000000, n = 8;
+  else if (p1 >= 1000000) pow10 = 1000000, n = 7;
+  else if (p1 >= 100000) pow10 = 100000, n = 6;
+  else if (p1 >= 10000) pow10 = 10000, n = 5;
+  else if (p1 >= 1000) pow10 = 1000, n = 4;
+  else if (p1 >= 100) pow10 = 100, n = 3;
+  else if (p1 >= 10) pow10 = 10, n = 2;
+  else pow10 = 1, n = 1;
+  *len = 0;
+  while (n > 0) {
+    const uint32_t d = p1 / pow10, r = p1 % pow10;
+    buf[(*len)++] = static_cast<char>('0' + d);
+    p1 = r;
+    --n;
+    const uint64_t rest = (static_cast<uint64_t>(p1) << -one.e) + p2;
+    if (rest <= delta) {
+      *dexp += n;
+      round(rest, static_cast<uint64_t>(pow10) << -one.e);
+      return;
+    }
+    pow10 /= 10;
+  }
+  int m = 0;
+  for (;;) {
+    p2 *= 10;
+    const uint64_t d = p2 >> -one.e, r = p2 & (one.f - 1);
+    buf[(*len)++] = static_cast<char>('0' + d);
+    p2 = r;
+    ++m;
+    delta *= 10;
+    dist *= 10;
+    if (p2 <= delta) break;
+  }
+  *dexp -= m;
+  round(p2, one.f);
+}
+
+// nlohmann::detail::to_chars of a double: sign, "0.0", Grisu2 digits, then
+// plain notation for decimal-point positions in (-4, 15], else scientific
 void put_double(std::string& out, double v) {
   if (!std::isfinite(v)) {
     out += "null";
     return;
   }
+  if (std::signbit(v)) {
+    out += '-';
+    v = -v;
+  }
   if (v == 0) {
-    out += std::signbit(v) ? "-0.0" : "0.0";
+    out += "0.0";
     return;
   }
-  // shortest round-trip digits and decimal exponent from the scientific form
-  char sci[64];
-  const auto r = std::to_chars(sci, sci + sizeof(sci), v, std::chars_format::scientific);
-  std::string s(sci, r.ptr);
-  std::string sign;
-  if (s[0] == '-') {
-    sign = "-";
-    s.erase(0, 1);
-  }
-  const size_t epos = s.find('e');
-  const int e10 = std::atoi(s.c_str() + epos + 1);
-  std::string digits;
-  for (size_t i = 0; i < epos; ++i)
-    if (s[i] != '.') digits += s[i];
-  const int k = static_cast<int>(digits.size());
-  const int n = e10 + 1;  // position of the decimal point relative to the digits
+  char dig[32];
+  int k = 0, dexp = 0;
+  grisu2(v, dig, &k, &dexp);
+  const std::string digits(dig, dig + k);
+  const int n = k + dexp;  // position of the decimal point relative to the digits
   constexpr int kMinExp = -4, kMaxExp = 15;
-  out += sign;
   if (k <= n && n <= kMaxExp) {  // integral: digits, zeros, ".0"
     out += digits;
     out.append(static_cast<size_t>(n - k), '0');

@@ -11,10 +11,15 @@ from paper_2509_26581_b200 import bal
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+NLOHMANN = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty"
+
+
 def build_client(tmp_path):
     exe = str(tmp_path / "facade_bal")
+    json_inc = ["-I", NLOHMANN] if os.path.isdir(NLOHMANN) else []
     subprocess.check_call(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include", "gopt_b200"), "-I",
-                           os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "cpp", "facade_bal.cpp"),
+                           os.path.join(ROOT, "include")] + json_inc +
+                          [os.path.join(ROOT, "tests", "cpp", "facade_bal.cpp"),
                            "-L", os.path.join(ROOT, "paper_2509_26581_b200"), "-lgb_bal", "-o", exe])
     return exe
 
@@ -42,3 +47,6 @@ def test_facade_solve_matches(gpu, ref, tmp_path):
     assert abs(float(fp64["mse1"]) - r.mse()) <= 1e-6 * r.mse()
     for name in ("fp32", "fp32-bf16"):
         assert abs(float(rows[name]["final_chi2"]) - rr.final_chi2) <= 1e-4 * rr.final_chi2
+    # to_csv: 2 header comments + column line + one row per iteration
+    rep = dict(kv.split("=") for kv in re.search(r"^fp64-report (.*)$", out.stdout, re.M).group(1).split())
+    assert int(rep["csv_lines"]) == 3 + int(fp64["iterations"]) and int(rep["json_bytes"]) > 100
