@@ -9,11 +9,14 @@
 // block-Jacobi PCG with a matrix-free HVP (pcg.hpp:34-105,
 // linear_system.hpp:104-115) and the LM loop (levenberg_marquardt.hpp:115-224).
 //
-// Unlike the BAL path (every decision on the device inside a CUDA graph),
-// this engine keeps the LM/PCG scalar decisions on the host: every reduction
-// is a fixed-order block reduction on the device whose per-block partials the
-// host sums in order (deterministic). The reference's own engine runs the same
-// model traits in oracle/ref_generic.cpp; tests/test_gpu_generic.py compares.
+// Like the BAL path, every LM / PCG decision runs on the device: the scalars
+// live in a device GState, each reduction is a fixed-order block reduction
+// whose per-block partials a one-block decision kernel folds in order
+// (deterministic), every kernel is gated by the state's flags, and one LM
+// iteration (pcg.max_iterations unrolled PCG steps) is captured once into a
+// CUDA graph and replayed; the host only polls a termination flag one
+// iteration behind. The reference's own engine runs the same model traits in
+// oracle/ref_generic.cpp; tests/test_gpu_generic.py compares.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -185,7 +188,8 @@ __device__ inline void gather_params(const Sets<FP>& S, const FSetDev<FP, F>& f,
 
 // linearize one factor type: residual, loss, Auto Jacobian columns, chi partials
 template <typename FP, typename F>
-__global__ void __launch_bounds__(kBlock) k_lin(Sets<FP> S, FSetDev<FP, F> f, LossCfg loss, FP* part) {
+__global__ void __launch_bounds__(kBlock) k_lin(const int* on, Sets<FP> S, FSetDev<FP, F> f, LossCfg loss, FP* part) {
+  if (on && !*on) return;  // device-side gate (LM / PCG state)
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   FP chi = FP(0);
   if (i < f.n) {
@@ -229,7 +233,8 @@ __global__ void __launch_bounds__(kBlock) k_lin(Sets<FP> S, FSetDev<FP, F> f, Lo
 
 // chi^2 of one factor type at x (cand = 0) or x_new (cand = 1)
 template <typename FP, typename F>
-__global__ void __launch_bounds__(kBlock) k_chi(Sets<FP> S, FSetDev<FP, F> f, LossCfg loss, int cand, FP* part) {
+__global__ void __launch_bounds__(kBlock) k_chi(const int* on, Sets<FP> S, FSetDev<FP, F> f, LossCfg loss, int cand, FP* part) {
+  if (on && !*on) return;  // device-side gate (LM / PCG state)
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   FP chi = FP(0);
   if (i < f.n) {
@@ -259,7 +264,8 @@ __device__ inline int slot_prefix(int s) {
 // b, diag and the dense H block of every free vertex of set `set` from factor
 // type F (accumulate_gradient_and_diagonal + the unscaled precond blocks)
 template <typename FP, typename F, int D>
-__global__ void __launch_bounds__(kBlock) k_acc(Sets<FP> S, FSetDev<FP, F> f, int set, FP* b, FP* H) {
+__global__ void __launch_bounds__(kBlock) k_acc(const int* on, Sets<FP> S, FSetDev<FP, F> f, int set, FP* b, FP* H) {
+  if (on && !*on) return;  // device-side gate (LM / PCG state)
   const VSetDev<FP>& vs = S.s[set];
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= vs.n || vs.col[v] < 0) return;
@@ -293,7 +299,8 @@ __global__ void __launch_bounds__(kBlock) k_acc(Sets<FP> S, FSetDev<FP, F> f, in
 
 // HVP forward of one factor type: q = w J (D p) at the free slot columns
 template <typename FP, typename F>
-__global__ void __launch_bounds__(kBlock) k_fwd(Sets<FP> S, FSetDev<FP, F> f, const FP* vt) {
+__global__ void __launch_bounds__(kBlock) k_fwd(const int* on, Sets<FP> S, FSetDev<FP, F> f, const FP* vt) {
+  if (on && !*on) return;  // device-side gate (LM / PCG state)
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= f.n) return;
   FP u[F::R];
@@ -318,7 +325,8 @@ __global__ void __launch_bounds__(kBlock) k_fwd(Sets<FP> S, FSetDev<FP, F> f, co
 
 // HVP scatter (as a per-vertex gather over the CSR): acc += J_s^T q
 template <typename FP, typename F, int D>
-__global__ void __launch_bounds__(kBlock) k_back(Sets<FP> S, FSetDev<FP, F> f, int set, FP* acc) {
+__global__ void __launch_bounds__(kBlock) k_back(const int* on, Sets<FP> S, FSetDev<FP, F> f, int set, FP* acc) {
+  if (on && !*on) return;  // device-side gate (LM / PCG state)
   const VSetDev<FP>& vs = S.s[set];
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= vs.n || vs.col[v] < 0) return;
@@ -350,7 +358,8 @@ __device__ inline FP warp_allsum(FP v) {
 }
 
 template <typename FP, typename F, int D>
-__global__ void __launch_bounds__(kBlock) k_back_w(Sets<FP> S, FSetDev<FP, F> f, int set, FP* acc) {
+__global__ void __launch_bounds__(kBlock) k_back_w(const int* on, Sets<FP> S, FSetDev<FP, F> f, int set, FP* acc) {
+  if (on && !*on) return;  // device-side gate (LM / PCG state)
   const VSetDev<FP>& vs = S.s[set];
   const uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -377,7 +386,8 @@ __global__ void __launch_bounds__(kBlock) k_back_w(Sets<FP> S, FSetDev<FP, F> f,
 }
 
 template <typename FP, typename F, int D>
-__global__ void __launch_bounds__(kBlock) k_acc_w(Sets<FP> S, FSetDev<FP, F> f, int set, FP* b, FP* H) {
+__global__ void __launch_bounds__(kBlock) k_acc_w(const int* on, Sets<FP> S, FSetDev<FP, F> f, int set, FP* b, FP* H) {
+  if (on && !*on) return;  // device-side gate (LM / PCG state)
   const VSetDev<FP>& vs = S.s[set];
   const uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -419,7 +429,8 @@ __global__ void __launch_bounds__(kBlock) k_acc_w(Sets<FP> S, FSetDev<FP, F> f, 
 // HVP forward with one warp per factor and one lane per residual row (wide
 // factors such as the 15-row IMU preintegration)
 template <typename FP, typename F>
-__global__ void __launch_bounds__(kBlock) k_fwd_w(Sets<FP> S, FSetDev<FP, F> f, const FP* vt) {
+__global__ void __launch_bounds__(kBlock) k_fwd_w(const int* on, Sets<FP> S, FSetDev<FP, F> f, const FP* vt) {
+  if (on && !*on) return;  // device-side gate (LM / PCG state)
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int row = threadIdx.x & 31;
   if (i >= f.n || row >= F::R) return;
@@ -439,10 +450,67 @@ __global__ void __launch_bounds__(kBlock) k_fwd_w(Sets<FP> S, FSetDev<FP, F> f, 
   f.q[static_cast<uint64_t>(F::R) * i + row] = f.w[i] * u;
 }
 
-// ------------------------------------------------------------ vector kernels
+// ------------------------------------------------------------ device state
+// Every LM / PCG scalar lives here; the decisions are one-block kernels, so an
+// LM iteration is a fixed kernel sequence (captured once into a CUDA graph,
+// like the BAL path) and the host never waits on a reduction.
 template <typename FP>
-__global__ void k_scale(uint64_t n, const FP* b, const FP* diag, double cmin, double cmax, FP* clamped, FP* D,
-                        FP* part_max, int* bad) {
+struct GState {
+  FP chi2, lambda, nu, gmax, rhs_norm, scale, ref_norm, unscale, rho, alpha, pred;
+  double relres, final_chi2;
+  int it, terminated, termination, accepted_steps;
+  // gates: iteration running, PCG running, step finite (candidate evaluated),
+  // accepted (commit), linearize now
+  int iter_active, pcg_active, step_ok, accepted, do_lin;
+  int finite, pcg_it, pcg_conv, fallbacks, bad, badx;
+};
+
+// LM configuration as the device reads it
+struct GCfg {
+  int max_it, pcg_max_it, normalize_rhs, use_guard, refresh_on_reject, before;
+  double tol, grad_tol, lambda_max, tau, pcg_tol, pcg_ratio, cmin, cmax;
+};
+
+// up to 4 partial-sum segments folded in order
+template <typename FP>
+struct Segs {
+  const FP* p[4];
+  unsigned n[4];
+  int count;
+};
+
+// fixed-order fold of per-block partials inside ONE block (deterministic):
+// strided per-thread sums, then a shared-memory tree; result on every thread
+template <typename FP>
+__device__ FP block_fold(const FP* p, unsigned n, bool mx) {
+  __shared__ FP sh[kBlock];
+  FP acc = FP(0);
+  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) acc = mx ? ::fmax(acc, p[i]) : acc + p[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = kBlock / 2; o > 0; o >>= 1) {
+    if (static_cast<int>(threadIdx.x) < o)
+      sh[threadIdx.x] = mx ? ::fmax(sh[threadIdx.x], sh[threadIdx.x + o]) : sh[threadIdx.x] + sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  const FP r = sh[0];
+  __syncthreads();
+  return r;
+}
+template <typename FP>
+__device__ FP fold_segs(const Segs<FP>& s) {
+  FP t = FP(0);
+  for (int k = 0; k < s.count; ++k) t += block_fold(s.p[k], s.n[k], false);
+  return t;
+}
+
+// ------------------------------------------------------------ vector kernels
+#define GGATE \
+  if (on && !*on) return
+template <typename FP>
+__global__ void k_scale(const int* on, uint64_t n, const FP* b, const FP* diag, double cmin, double cmax, FP* clamped,
+                        FP* D, FP* part_max, int* bad) {
+  GGATE;
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   FP gm = FP(0);
   if (i < n) {
@@ -466,7 +534,8 @@ __global__ void k_scale(uint64_t n, const FP* b, const FP* diag, double cmin, do
 }
 
 template <typename FP>
-__global__ void k_dot(uint64_t n, const FP* a, const FP* b, FP* part) {
+__global__ void k_dot(const int* on, uint64_t n, const FP* a, const FP* b, FP* part) {
+  GGATE;
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   FP v = i < n ? a[i] * b[i] : FP(0);
   v = block_sum(v);
@@ -474,34 +543,55 @@ __global__ void k_dot(uint64_t n, const FP* a, const FP* b, FP* part) {
 }
 
 template <typename FP>
-__global__ void k_axpy_vt(uint64_t n, const FP* D, const FP* p, FP* vt) {  // vt = D p
+__global__ void k_axpy_vt(const int* on, uint64_t n, const FP* D, const FP* p, FP* vt) {  // vt = D p
+  GGATE;
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i < n) vt[i] = D[i] * p[i];
 }
 
 template <typename FP>
-__global__ void k_hvp_fin(uint64_t n, const FP* D, const FP* p, const FP* acc, double lam, int before, FP* ap) {
+__global__ void k_hvp_fin(const int* on, uint64_t n, const FP* D, const FP* p, const FP* acc, const GState<FP>* st,
+                          int before, FP* ap) {
+  GGATE;
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
-  const FP damp = before ? FP(lam) * D[i] * D[i] : FP(lam);
+  const FP lam = st->lambda;
+  const FP damp = before ? lam * D[i] * D[i] : lam;
   ap[i] = damp * p[i] + D[i] * acc[i];
+}
+
+template <typename T>
+__global__ void k_fill(const int* on, uint64_t n, T* y, T v) {
+  GGATE;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    y[i] = v;
+}
+template <typename T>
+__global__ void k_copy(const int* on, uint64_t n, T* y, const T* x) {
+  GGATE;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    y[i] = x[i];
 }
 
 // block-Jacobi of one vertex set: B = D H D + damping (linear_system.hpp:120-160),
 // Cholesky inverse or the clamped diagonal fallback
 template <typename FP, int D>
-__global__ void k_precond(Sets<FP> S, int set, const FP* H, const FP* Dv, double lam, int before, double cmin,
-                          double cmax, FP* M, int* fallbacks) {
+__global__ void k_precond(const int* on, Sets<FP> S, int set, const FP* H, const FP* Dv, const GState<FP>* st,
+                          int before, double cmin, double cmax, FP* M, int* fallbacks) {
+  GGATE;
   const VSetDev<FP>& vs = S.s[set];
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= vs.n || vs.col[v] < 0) return;
+  const FP lam = st->lambda;
   const int64_t col = vs.col[v];
   const FP* Hv = H + vs.hoff + static_cast<int64_t>(D * D) * v;
   FP B[D * D], L[D * D];
   for (int i = 0; i < D; ++i)
     for (int j = 0; j < D; ++j) {
       B[i * D + j] = Dv[col + i] * Hv[i * D + j] * Dv[col + j];
-      if (i == j) B[i * D + j] += before ? FP(lam) * Dv[col + i] * Dv[col + i] : FP(lam);
+      if (i == j) B[i * D + j] += before ? lam * Dv[col + i] * Dv[col + i] : lam;
     }
   bool ok = true;
   for (int j = 0; j < D && ok; ++j) {  // L L^T = B
@@ -548,12 +638,13 @@ __global__ void k_precond(Sets<FP> S, int set, const FP* H, const FP* Dv, double
   }
 }
 
-// z = M r for one vertex set; r.z and r.r partials per block
+// z = M r for one vertex set; r.z partials per block
 template <typename FP, int D>
-__global__ void k_apply(Sets<FP> S, int set, const FP* M, const FP* r, FP* z, FP* part_rz, FP* part_rr) {
+__global__ void k_apply(const int* on, Sets<FP> S, int set, const FP* M, const FP* r, FP* z, FP* part_rz) {
+  GGATE;
   const VSetDev<FP>& vs = S.s[set];
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  FP rz = FP(0), rr = FP(0);
+  FP rz = FP(0);
   if (v < vs.n && vs.col[v] >= 0) {
     const int64_t col = vs.col[v];
     const FP* Mv = M + vs.hoff + static_cast<int64_t>(D * D) * v;
@@ -562,35 +653,292 @@ __global__ void k_apply(Sets<FP> S, int set, const FP* M, const FP* r, FP* z, FP
       for (int j = 0; j < D; ++j) t += Mv[i * D + j] * r[col + j];
       z[col + i] = t;
       rz += r[col + i] * t;
-      rr += r[col + i] * r[col + i];
     }
   }
   rz = block_sum(rz);
-  rr = block_sum(rr);
-  if (threadIdx.x == 0) {
-    part_rz[blockIdx.x] = rz;
-    part_rr[blockIdx.x] = rr;
-  }
+  if (threadIdx.x == 0) part_rz[blockIdx.x] = rz;
 }
 
+// r = scale * rhs (pcg.hpp:49-54: multiply by the reciprocal)
 template <typename FP>
-__global__ void k_lincomb(uint64_t n, FP* y, FP a, const FP* x, FP b) {  // y = a y + b x
+__global__ void k_init_r(const int* on, uint64_t n, const GState<FP>* st, const FP* rhs, FP* r) {
+  GGATE;
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) y[i] = a * y[i] + b * x[i];
+  if (i < n) r[i] = st->scale * rhs[i] + FP(0) * rhs[i];
+}
+// x += alpha p; r -= alpha ap (pcg.hpp:78-80)
+template <typename FP>
+__global__ void k_update_xr(const int* on, uint64_t n, const GState<FP>* st, const FP* p, const FP* ap, FP* x, FP* r) {
+  GGATE;
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const FP a = st->alpha;
+  x[i] = FP(1) * x[i] + a * p[i];
+  r[i] = FP(1) * r[i] + (-a) * ap[i];
+}
+// p = beta p + z
+template <typename FP>
+__global__ void k_dir(const int* on, uint64_t n, const FP* beta, const FP* z, FP* p) {
+  GGATE;
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) p[i] = *beta * p[i] + FP(1) * z[i];
+}
+// x *= unscale (x_scaled = x_pcg * ||rhs||)
+template <typename FP>
+__global__ void k_unscale(const int* on, uint64_t n, const GState<FP>* st, FP* x) {
+  GGATE;
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) x[i] = st->unscale * x[i] + FP(0) * x[i];
 }
 
-// x_new = x + D (x_pcg * unscale) at the free columns of one set
+// x_new = x + D x_scaled at the free columns of one set
 template <typename FP, int D>
-__global__ void k_apply_step(Sets<FP> S, int set, const FP* Dv, const FP* xs, FP unscale) {
+__global__ void k_apply_step(const int* on, Sets<FP> S, int set, const FP* Dv, const FP* xs) {
+  GGATE;
   const VSetDev<FP>& vs = S.s[set];
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= vs.n) return;
   const int64_t col = vs.col[v];
   for (int k = 0; k < D; ++k) {
     const FP cur = vs.x[static_cast<uint64_t>(D) * v + k];
-    vs.xn[static_cast<uint64_t>(D) * v + k] = col < 0 ? cur : cur + Dv[col + k] * (xs[col + k] * unscale);
+    vs.xn[static_cast<uint64_t>(D) * v + k] = col < 0 ? cur : cur + Dv[col + k] * (xs[col + k] * FP(1));
   }
 }
+
+template <typename FP>
+__global__ void k_diag(const int* on, Sets<FP> S, int set, int dim, const FP* H, FP* diag) {
+  GGATE;
+  const VSetDev<FP>& vs = S.s[set];
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= vs.n || vs.col[v] < 0) return;
+  const FP* Hv = H + vs.hoff + static_cast<int64_t>(dim) * dim * v;
+  for (int k = 0; k < dim; ++k) diag[vs.col[v] + k] = Hv[k * dim + k];
+}
+template <typename FP>
+__global__ void k_damp_max(uint64_t n, const FP* D, const FP* cl, FP* part) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  FP m = i < n ? D[i] * D[i] * cl[i] : FP(0);
+  __shared__ FP sh[32];
+  for (int o = 16; o > 0; o >>= 1) m = ::fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    FP r = FP(0);
+    for (int k = 0; k < (int)(blockDim.x + 31) / 32; ++k) r = ::fmax(r, sh[k]);
+    part[blockIdx.x] = r;
+  }
+}
+template <typename FP>
+__global__ void k_rhs(const int* on, uint64_t n, const FP* D, const FP* b, FP* rhs) {
+  GGATE;
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) rhs[i] = -D[i] * b[i];
+}
+template <typename FP>
+__global__ void k_pred(const int* on, uint64_t n, const FP* D, const FP* x, const FP* rhs, const GState<FP>* st,
+                       int before, FP* part, int* bad) {
+  GGATE;
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  FP v = FP(0);
+  if (i < n) {
+    const FP lam = st->lambda;
+    const FP damp = before ? lam * D[i] * D[i] : lam;
+    v = x[i] * (damp * x[i] + rhs[i]);
+    if (!isfinite(D[i] * x[i])) atomicOr(bad, 1);
+  }
+  v = block_sum(v);
+  if (threadIdx.x == 0) part[blockIdx.x] = v;
+}
+
+// ------------------------------------------------------- decision kernels
+// (one block each; every thread takes part in the folds, thread 0 decides)
+
+// levenberg_marquardt.hpp:149-169: record start, the non-finite and gradient checks
+template <typename FP>
+__global__ void k_g_iter_begin(GState<FP>* st, gb_iteration_record* recs, GCfg c) {
+  if (threadIdx.x != 0) return;
+  st->accepted = 0;
+  st->step_ok = 0;
+  st->do_lin = 0;
+  st->pcg_active = 0;
+  if (st->terminated || st->it >= c.max_it) {
+    st->iter_active = 0;
+    return;
+  }
+  const int it = ++st->it;
+  gb_iteration_record& r = recs[it - 1];
+  r = gb_iteration_record{};
+  r.iteration = it;
+  r.chi2_before = static_cast<double>(st->chi2);
+  r.lambda = static_cast<double>(st->lambda);
+  if (!st->finite || st->gmax < FP(c.grad_tol)) {
+    r.chi2_after = r.chi2_before;
+    st->termination = !st->finite ? GB_TERM_NON_FINITE_LINEARIZATION : GB_TERM_GRADIENT_SMALL;
+    st->terminated = 1;
+    st->iter_active = 0;
+    return;
+  }
+  st->iter_active = 1;
+  st->fallbacks = 0;
+  st->badx = 0;
+  st->pcg_it = 0;
+  st->pcg_conv = 0;
+  st->relres = 0.0;
+  st->unscale = FP(1);
+}
+
+// pcg.hpp:43-57: rhs norm, scaling
+template <typename FP>
+__global__ void k_g_pcg_begin(GState<FP>* st, const FP* part, unsigned n, GCfg c) {
+  if (!st->iter_active) return;
+  const FP nrm = ::sqrt(block_fold(part, n, false));
+  if (threadIdx.x != 0) return;
+  st->rhs_norm = nrm;
+  if (!(nrm > FP(0))) {
+    st->pcg_conv = isfinite(nrm) ? 1 : 0;
+    st->pcg_active = 0;
+    st->unscale = FP(1);
+    return;
+  }
+  st->scale = c.normalize_rhs ? FP(1) / nrm : FP(1);
+  st->ref_norm = c.normalize_rhs ? FP(1) : nrm;
+  st->unscale = c.normalize_rhs ? nrm : FP(1);
+  st->pcg_active = 1;
+}
+
+// rho = r.z (sets in order), res = |r| (pcg.hpp:58-64)
+template <typename FP>
+__global__ void k_g_rho(GState<FP>* st, Segs<FP> rz, const FP* part_rr, unsigned n) {
+  if (!st->pcg_active) return;
+  const FP rho = fold_segs(rz);
+  const FP rr = block_fold(part_rr, n, false);
+  if (threadIdx.x != 0) return;
+  st->rho = rho;
+  st->relres = static_cast<double>(::sqrt(rr) / st->ref_norm);
+}
+
+// pcg.hpp:70-77: pAp, breakdown check, alpha
+template <typename FP>
+__global__ void k_g_pap(GState<FP>* st, const FP* part, unsigned n) {
+  if (!st->pcg_active) return;
+  const FP pap = block_fold(part, n, false);
+  if (threadIdx.x != 0) return;
+  if (!(pap > FP(0)) || !isfinite(pap)) {
+    st->pcg_conv = 0;
+    st->pcg_active = 0;
+    return;
+  }
+  st->alpha = st->rho / pap;
+}
+
+// pcg.hpp:81-88: iteration count, residual, convergence
+template <typename FP>
+__global__ void k_g_res(GState<FP>* st, const FP* part, unsigned n, GCfg c) {
+  if (!st->pcg_active) return;
+  const FP res = ::sqrt(block_fold(part, n, false));
+  if (threadIdx.x != 0) return;
+  ++st->pcg_it;
+  st->relres = static_cast<double>(res / st->ref_norm);
+  if (!isfinite(st->relres)) {
+    st->pcg_conv = 0;
+    st->pcg_active = 0;
+  } else if (res <= FP(c.pcg_tol) * st->ref_norm) {
+    st->pcg_conv = 1;
+    st->pcg_active = 0;
+  } else if (st->pcg_it >= c.pcg_max_it) {
+    st->pcg_active = 0;  // max_iterations: the trailing direction update changes no output
+  }
+}
+
+// pcg.hpp:89-93: rho' = r.z, beta (then p = z + beta p)
+template <typename FP>
+__global__ void k_g_beta(GState<FP>* st, Segs<FP> rz, FP* beta_out) {
+  if (!st->pcg_active) return;
+  const FP rho_next = fold_segs(rz);
+  if (threadIdx.x != 0) return;
+  *beta_out = rho_next / st->rho;
+  st->rho = rho_next;
+}
+
+// linear_system.hpp:198-206 pred + finiteness, levenberg_marquardt.hpp:170-178 guard
+template <typename FP>
+__global__ void k_g_step(GState<FP>* st, gb_iteration_record* recs, const FP* part, unsigned n, GCfg c) {
+  if (!st->iter_active) return;
+  const FP pred = block_fold(part, n, false);
+  if (threadIdx.x != 0) return;
+  st->pred = pred;
+  gb_iteration_record& r = recs[st->it - 1];
+  r.pcg_iterations = st->pcg_it;
+  r.pcg_converged = st->pcg_conv;
+  r.pcg_relative_residual = st->relres;
+  r.precond_fallback_blocks = st->fallbacks;
+  if (c.use_guard && !st->pcg_conv && st->relres > c.pcg_ratio * c.pcg_tol) {
+    r.low_quality_step = 1;
+    st->lambda *= st->nu;
+  }
+  st->step_ok = st->badx ? 0 : 1;
+}
+
+// levenberg_marquardt.hpp:179-219: candidate chi^2, accept / reject, Nielsen,
+// termination (the re-linearization itself follows, gated on do_lin)
+template <typename FP>
+__global__ void k_g_decide(GState<FP>* st, gb_iteration_record* recs, Segs<FP> chi, GCfg c) {
+  if (!st->iter_active) return;
+  const FP s = fold_segs(chi);
+  if (threadIdx.x != 0) return;
+  const FP chi2_new = st->step_ok ? s : FP(NAN);
+  gb_iteration_record& r = recs[st->it - 1];
+  r.chi2_after = static_cast<double>(chi2_new);
+  const bool acc = isfinite(chi2_new) && chi2_new < st->chi2;
+  r.accepted = acc ? 1 : 0;
+  st->accepted = acc ? 1 : 0;
+  FP rel = FP(0);
+  if (acc) {
+    ++st->accepted_steps;
+    const FP gain = st->pred > FP(0) ? (st->chi2 - chi2_new) / st->pred : FP(INFINITY);
+    const FP g = FP(2) * gain - FP(1);
+    st->lambda *= ::fmax(FP(1) / FP(3), FP(1) - g * g * g);
+    st->nu = FP(2);
+    rel = (st->chi2 - chi2_new) / st->chi2;
+    st->do_lin = 1;
+  } else {
+    st->lambda *= st->nu;
+    st->nu *= FP(2);
+    st->do_lin = c.refresh_on_reject ? 1 : 0;
+  }
+  if (acc && static_cast<double>(rel) < c.tol) {
+    st->termination = GB_TERM_TOLERANCE_REACHED;
+    st->terminated = 1;
+  } else if (static_cast<double>(st->lambda) > c.lambda_max) {
+    st->termination = GB_TERM_DAMPING_OVERFLOW;
+    st->terminated = 1;
+  }
+}
+
+// linear_system.hpp:67-82 end: chi^2 (kept only on accept), finiteness, max|b|
+template <typename FP>
+__global__ void k_g_lin_end(GState<FP>* st, Segs<FP> chi, const FP* part_max, unsigned n) {
+  if (!st->do_lin) return;
+  const FP s = fold_segs(chi);
+  const FP gm = block_fold(part_max, n, true);
+  if (threadIdx.x != 0) return;
+  st->gmax = gm;
+  st->finite = (isfinite(s) && !st->bad) ? 1 : 0;
+  if (st->accepted) {
+    st->chi2 = s;
+    st->final_chi2 = static_cast<double>(s);
+  }
+}
+
+// lambda0 = tau max(D^2 clamped) (linear_system.hpp:94-99), nu = 2
+template <typename FP>
+__global__ void k_g_init_damping(GState<FP>* st, const FP* part, unsigned n, GCfg c) {
+  const FP m = block_fold(part, n, true);
+  if (threadIdx.x != 0) return;
+  st->lambda = FP(c.tau) * m;
+  st->nu = FP(2);
+}
+#undef GGATE
 
 // ===================================================================== host
 #define GCK(x)                                                                                          \
@@ -620,23 +968,9 @@ struct DVec {
     if (!h.empty()) GCK(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
     return p;
   }
-  T* zero() {
-    GCK(cudaMemset(p, 0, std::max<size_t>(1, n) * sizeof(T)));
-    return p;
-  }
 };
 
 inline unsigned nblk(uint64_t n) { return static_cast<unsigned>(std::max<uint64_t>(1, (n + kBlock - 1) / kBlock)); }
-
-// fixed-order sum of per-block partials (deterministic)
-template <typename FP>
-FP sum_parts(const FP* dpart, unsigned n) {
-  std::vector<FP> h(n);
-  GCK(cudaMemcpy(h.data(), dpart, n * sizeof(FP), cudaMemcpyDeviceToHost));
-  FP s = FP(0);
-  for (FP v : h) s += v;
-  return s;
-}
 
 template <typename Fn>
 void by_dim(int dim, Fn&& fn) {
@@ -661,6 +995,7 @@ struct VSetHost {
 
 template <typename FP, typename F>
 struct FSetHost {
+  using Factor = F;
   static constexpr int kR = F::R;
   uint32_t n = 0;
   std::vector<uint32_t> hidx;
@@ -670,6 +1005,7 @@ struct FSetHost {
   DVec<FP> J, wr, w, q;
   DVec<uint32_t> off[kMaxSets], item[kMaxSets];
   uint64_t items[kMaxSets] = {0, 0, 0};
+  uint64_t part_off = 0;  // this type's slice of the chi^2 partials
 
   void upload(const std::vector<typename F::Obs>& o, const std::vector<typename F::Const>& c) {
     n = static_cast<uint32_t>(o.size());
@@ -725,132 +1061,61 @@ struct FSetHost {
   }
 };
 
-// per factor type: linearize, accumulate, chi^2, HVP passes
+// per factor type: linearize, accumulate, chi^2, HVP passes (all gated)
 template <typename FP, typename F>
 struct FactorOps {
-  static FP lin(const Sets<FP>& S, const FSetHost<FP, F>& f, LossCfg l, FP* part) {
-    if (!f.n) return FP(0);
-    k_lin<FP, F><<<nblk(f.n), kBlock>>>(S, f.dev(), l, part);
+  static void lin(cudaStream_t s, const int* on, const Sets<FP>& S, const FSetHost<FP, F>& f, LossCfg l, FP* part) {
+    if (!f.n) return;
+    k_lin<FP, F><<<nblk(f.n), kBlock, 0, s>>>(on, S, f.dev(), l, part + f.part_off);
     GCK(cudaGetLastError());
-    return sum_parts(part, nblk(f.n));
   }
-  static FP chi(const Sets<FP>& S, const FSetHost<FP, F>& f, LossCfg l, int cand, FP* part) {
-    if (!f.n) return FP(0);
-    k_chi<FP, F><<<nblk(f.n), kBlock>>>(S, f.dev(), l, cand, part);
+  static void chi(cudaStream_t s, const int* on, const Sets<FP>& S, const FSetHost<FP, F>& f, LossCfg l, int cand,
+                  FP* part) {
+    if (!f.n) return;
+    k_chi<FP, F><<<nblk(f.n), kBlock, 0, s>>>(on, S, f.dev(), l, cand, part + f.part_off);
     GCK(cudaGetLastError());
-    return sum_parts(part, nblk(f.n));
   }
   // many incident items per vertex: one warp per vertex
   static bool wide(const std::vector<VSetHost<FP>*>& sets, const FSetHost<FP, F>& f, int st) {
     return sets[st]->n && f.items[st] >= 16ull * sets[st]->n;
   }
-  static void acc(const Sets<FP>& S, const std::vector<VSetHost<FP>*>& sets, const FSetHost<FP, F>& f, FP* b,
-                  FP* H) {
+  static void acc(cudaStream_t s, const int* on, const Sets<FP>& S, const std::vector<VSetHost<FP>*>& sets,
+                  const FSetHost<FP, F>& f, FP* b, FP* H) {
     for (int st = 0; st < static_cast<int>(sets.size()); ++st) {
       if (!f.off[st].p || !f.n) continue;
       by_dim(sets[st]->dim, [&](auto Dc) {
         constexpr int D = decltype(Dc)::value;
         if (D <= 6 && wide(sets, f, st))
-          k_acc_w<FP, F, D><<<nblk(32ull * sets[st]->n), kBlock>>>(S, f.dev(), st, b, H);
+          k_acc_w<FP, F, D><<<nblk(32ull * sets[st]->n), kBlock, 0, s>>>(on, S, f.dev(), st, b, H);
         else
-          k_acc<FP, F, D><<<nblk(sets[st]->n), kBlock>>>(S, f.dev(), st, b, H);
+          k_acc<FP, F, D><<<nblk(sets[st]->n), kBlock, 0, s>>>(on, S, f.dev(), st, b, H);
       });
       GCK(cudaGetLastError());
     }
   }
-  static void fwd(const Sets<FP>& S, const FSetHost<FP, F>& f, const FP* vt) {
+  static void fwd(cudaStream_t s, const int* on, const Sets<FP>& S, const FSetHost<FP, F>& f, const FP* vt) {
     if (!f.n) return;
     if (F::R >= 8)
-      k_fwd_w<FP, F><<<nblk(32ull * f.n), kBlock>>>(S, f.dev(), vt);
+      k_fwd_w<FP, F><<<nblk(32ull * f.n), kBlock, 0, s>>>(on, S, f.dev(), vt);
     else
-      k_fwd<FP, F><<<nblk(f.n), kBlock>>>(S, f.dev(), vt);
+      k_fwd<FP, F><<<nblk(f.n), kBlock, 0, s>>>(on, S, f.dev(), vt);
     GCK(cudaGetLastError());
   }
-  static void back(const Sets<FP>& S, const std::vector<VSetHost<FP>*>& sets, const FSetHost<FP, F>& f, FP* acc) {
+  static void back(cudaStream_t s, const int* on, const Sets<FP>& S, const std::vector<VSetHost<FP>*>& sets,
+                   const FSetHost<FP, F>& f, FP* acc) {
     for (int st = 0; st < static_cast<int>(sets.size()); ++st) {
       if (!f.off[st].p || !f.n) continue;
       by_dim(sets[st]->dim, [&](auto Dc) {
         constexpr int D = decltype(Dc)::value;
         if (wide(sets, f, st))
-          k_back_w<FP, F, D><<<nblk(32ull * sets[st]->n), kBlock>>>(S, f.dev(), st, acc);
+          k_back_w<FP, F, D><<<nblk(32ull * sets[st]->n), kBlock, 0, s>>>(on, S, f.dev(), st, acc);
         else
-          k_back<FP, F, D><<<nblk(sets[st]->n), kBlock>>>(S, f.dev(), st, acc);
+          k_back<FP, F, D><<<nblk(sets[st]->n), kBlock, 0, s>>>(on, S, f.dev(), st, acc);
       });
       GCK(cudaGetLastError());
     }
   }
 };
-
-template <typename FP, typename F>
-FP ops_lin(const Sets<FP>& S, const FSetHost<FP, F>& f, LossCfg l, FP* part) {
-  return FactorOps<FP, F>::lin(S, f, l, part);
-}
-template <typename FP, typename F>
-FP ops_chi(const Sets<FP>& S, const FSetHost<FP, F>& f, LossCfg l, int cand, FP* part) {
-  return FactorOps<FP, F>::chi(S, f, l, cand, part);
-}
-template <typename FP, typename F>
-void ops_acc(const Sets<FP>& S, const std::vector<VSetHost<FP>*>& sets, const FSetHost<FP, F>& f, FP* b, FP* H) {
-  FactorOps<FP, F>::acc(S, sets, f, b, H);
-}
-template <typename FP, typename F>
-void ops_fwd(const Sets<FP>& S, const FSetHost<FP, F>& f, const FP* vt) {
-  FactorOps<FP, F>::fwd(S, f, vt);
-}
-template <typename FP, typename F>
-void ops_back(const Sets<FP>& S, const std::vector<VSetHost<FP>*>& sets, const FSetHost<FP, F>& f, FP* acc) {
-  FactorOps<FP, F>::back(S, sets, f, acc);
-}
-
-template <typename FP>
-__global__ void k_diag(Sets<FP> S, int set, int dim, const FP* H, FP* diag) {
-  const VSetDev<FP>& vs = S.s[set];
-  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= vs.n || vs.col[v] < 0) return;
-  const FP* Hv = H + vs.hoff + static_cast<int64_t>(dim) * dim * v;
-  for (int k = 0; k < dim; ++k) diag[vs.col[v] + k] = Hv[k * dim + k];
-}
-template <typename FP>
-__global__ void k_damp_max(uint64_t n, const FP* D, const FP* cl, FP* part) {
-  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  FP m = i < n ? D[i] * D[i] * cl[i] : FP(0);
-  __shared__ FP sh[32];
-  for (int o = 16; o > 0; o >>= 1) m = ::fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    FP r = FP(0);
-    for (int k = 0; k < (int)(blockDim.x + 31) / 32; ++k) r = ::fmax(r, sh[k]);
-    part[blockIdx.x] = r;
-  }
-}
-template <typename FP>
-__global__ void k_rhs(uint64_t n, const FP* D, const FP* b, FP* rhs) {
-  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) rhs[i] = -D[i] * b[i];
-}
-template <typename FP>
-__global__ void k_pred(uint64_t n, const FP* D, const FP* x, const FP* rhs, double lam, int before, FP* part,
-                       int* bad) {
-  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  FP v = FP(0);
-  if (i < n) {
-    const FP damp = before ? FP(lam) * D[i] * D[i] : FP(lam);
-    v = x[i] * (damp * x[i] + rhs[i]);
-    if (!isfinite(D[i] * x[i])) atomicOr(bad, 1);
-  }
-  v = block_sum(v);
-  if (threadIdx.x == 0) part[blockIdx.x] = v;
-}
-
-template <typename FP>
-FP max_parts(const FP* dpart, unsigned n) {
-  std::vector<FP> h(n);
-  GCK(cudaMemcpy(h.data(), dpart, n * sizeof(FP), cudaMemcpyDeviceToHost));
-  FP m = FP(0);
-  for (FP v : h) m = std::max(m, v);
-  return m;
-}
 
 // The model: vertex sets + factor types. Fs... are the factor types in
 // registration order (Graph::add_factor_descriptor).
@@ -891,233 +1156,236 @@ void lm_solve(Model<FP, Fs...>& m, const gb_lm_config& cfg, gb_solve_report* rep
     hsize += static_cast<int64_t>(v.dim) * v.dim * v.n;
   }
   int64_t residual_dims = 0, nfactors = 0;
-  uint64_t maxn = static_cast<uint64_t>(std::max<int64_t>(N, 1));
+  uint64_t chi_parts = 0;
   m.each([&](auto& f) {
     f.build_csr(m.sets);
     nfactors += f.n;
     residual_dims += static_cast<int64_t>(f.n) * std::remove_reference_t<decltype(f)>::kR;
-    maxn = std::max<uint64_t>(maxn, f.n);
+    f.part_off = chi_parts;
+    chi_parts += f.n ? nblk(f.n) : 0;
   });
-  for (auto* v : m.sets) maxn = std::max<uint64_t>(maxn, v->n);
-  DVec<FP> b, diag, clamped, Dv, H, M, vt, acc, rhs, xs, r, z, p, ap, part, part2;
-  DVec<int> flag;
+  uint64_t rz_parts = 0;
+  std::vector<uint64_t> rz_off(m.sets.size());
+  for (size_t st = 0; st < m.sets.size(); ++st) {
+    rz_off[st] = rz_parts;
+    rz_parts += nblk(m.sets[st]->n);
+  }
+  if (m.sets.size() > 4 || sizeof...(Fs) > 4) throw std::invalid_argument("at most 4 vertex sets / factor types");
+  const unsigned nbN = nblk(N);
+  DVec<FP> b, diag, clamped, Dv, H, M, vt, acc, rhs, xs, r, z, p, ap, part_chi, part_dot, part_max, part_rz, beta;
   for (auto* d : {&b, &diag, &clamped, &Dv, &vt, &acc, &rhs, &xs, &r, &z, &p, &ap}) d->alloc(N);
   H.alloc(hsize);
   M.alloc(hsize);
-  part.alloc(nblk(maxn));
-  part2.alloc(nblk(maxn));
-  flag.alloc(2);
-  const unsigned nbN = nblk(N);
-  const bool before = cfg.damping == GB_DAMPING_BEFORE_SCALING;
-
-  bool finite = true;
-  FP gmax = FP(0);
-  auto linearize = [&]() -> FP {  // LinearSystem::linearize (linear_system.hpp:67-82)
-    FP chi = FP(0);
+  part_chi.alloc(chi_parts);
+  part_dot.alloc(nbN);
+  part_max.alloc(nbN);
+  part_rz.alloc(rz_parts);
+  beta.alloc(1);
+  const int max_it = std::max(0, cfg.max_iterations);
+  DVec<gb_iteration_record> drecs;
+  drecs.alloc(std::max(1, max_it));
+  DVec<GState<FP>> dst;
+  dst.alloc(1);
+  GState<FP>* st = dst.p;
+  const int* on_iter = &st->iter_active;
+  const int* on_pcg = &st->pcg_active;
+  const int* on_step = &st->step_ok;
+  const int* on_acc = &st->accepted;
+  const int* on_lin = &st->do_lin;
+  const int before = cfg.damping == GB_DAMPING_BEFORE_SCALING ? 1 : 0;
+  GCfg gc{max_it, cfg.pcg.max_iterations, cfg.pcg.normalize_rhs, cfg.use_rejection_guard, cfg.refresh_on_reject,
+          before, cfg.tolerance, cfg.gradient_tolerance, cfg.lambda_max, cfg.tau, cfg.pcg.tolerance,
+          cfg.pcg.rejection_ratio, cfg.clamp_min, cfg.clamp_max};
+  Segs<FP> chi_segs{}, rz_segs{};
+  {
+    int k = 0;
     m.each([&](auto& f) {
-      chi += ops_lin(S, f, m.loss, part.p);
+      if (f.n) {
+        chi_segs.p[k] = part_chi.p + f.part_off;
+        chi_segs.n[k] = nblk(f.n);
+        ++k;
+      }
     });
-    b.zero();
-    H.zero();
-    m.each([&](auto& f) {
-      ops_acc(S, m.sets, f, b.p, H.p);
-    });
-    diag.zero();
-    for (size_t st = 0; st < m.sets.size(); ++st)
-      k_diag<FP><<<nblk(m.sets[st]->n), kBlock>>>(S, static_cast<int>(st), m.sets[st]->dim, H.p, diag.p);
-    flag.zero();
-    k_scale<FP><<<nbN, kBlock>>>(N, b.p, diag.p, cfg.clamp_min, cfg.clamp_max, clamped.p, Dv.p, part2.p, flag.p);
-    GCK(cudaGetLastError());
-    gmax = max_parts(part2.p, nbN);
-    int bad = 0;
-    GCK(cudaMemcpy(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost));
-    finite = std::isfinite(static_cast<double>(chi)) && !bad;
-    return chi;
-  };
-  auto total_error = [&](int cand) -> FP {
-    FP chi = FP(0);
-    m.each([&](auto& f) {
-      chi += ops_chi(S, f, m.loss, cand, part.p);
-    });
-    return chi;
-  };
-  auto dot = [&](const FP* x, const FP* y) {
-    k_dot<FP><<<nbN, kBlock>>>(N, x, y, part.p);
-    return sum_parts(part.p, nbN);
-  };
-  auto apply_M = [&](const FP* rr, FP* zz, FP* rz) {  // z = M r; returns r.z (r.r unused)
-    FP t = FP(0);
-    for (size_t st = 0; st < m.sets.size(); ++st) {
-      by_dim(m.sets[st]->dim, [&](auto Dc) {
-        constexpr int Dd = decltype(Dc)::value;
-        k_apply<FP, Dd><<<nblk(m.sets[st]->n), kBlock>>>(S, static_cast<int>(st), M.p, rr, zz, part.p, part2.p);
-      });
-      t += sum_parts(part.p, nblk(m.sets[st]->n));
+    chi_segs.count = k;
+    for (size_t s2 = 0; s2 < m.sets.size(); ++s2) {
+      rz_segs.p[s2] = part_rz.p + rz_off[s2];
+      rz_segs.n[s2] = nblk(m.sets[s2]->n);
     }
-    *rz = t;
+    rz_segs.count = static_cast<int>(m.sets.size());
+  }
+  cudaStream_t s;
+  GCK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{s};
+  auto grid = [](uint64_t n) { return std::max(1u, std::min(nblk(n), 148u * 8u)); };
+
+  auto ops = [&](auto& f) -> FactorOps<FP, typename std::remove_reference_t<decltype(f)>::Factor> { return {}; };
+
+  // LinearSystem::linearize (linear_system.hpp:67-82), gated on do_lin: chi
+  // partials, b / H over the CSRs, diag, clamp, D, max|b|, finiteness
+  auto enqueue_linearize = [&]() {
+    m.each([&](auto& f) { ops(f).lin(s, on_lin, S, f, m.loss, part_chi.p); });
+    k_fill<FP><<<grid(N), kBlock, 0, s>>>(on_lin, N, b.p, FP(0));
+    k_fill<FP><<<grid(hsize), kBlock, 0, s>>>(on_lin, hsize, H.p, FP(0));
+    m.each([&](auto& f) { ops(f).acc(s, on_lin, S, m.sets, f, b.p, H.p); });
+    k_fill<FP><<<grid(N), kBlock, 0, s>>>(on_lin, N, diag.p, FP(0));
+    for (size_t q = 0; q < m.sets.size(); ++q)
+      k_diag<FP><<<nblk(m.sets[q]->n), kBlock, 0, s>>>(on_lin, S, static_cast<int>(q), m.sets[q]->dim, H.p, diag.p);
+    k_fill<int><<<1, 32, 0, s>>>(on_lin, 1, &st->bad, 0);
+    k_scale<FP><<<nbN, kBlock, 0, s>>>(on_lin, N, b.p, diag.p, cfg.clamp_min, cfg.clamp_max, clamped.p, Dv.p,
+                                       part_max.p, &st->bad);
+    k_g_lin_end<FP><<<1, kBlock, 0, s>>>(st, chi_segs, part_max.p, nbN);
+    GCK(cudaGetLastError());
   };
-  auto hvp = [&](const FP* pv, FP* out, FP lam) {  // LinearSystem::hvp
-    k_axpy_vt<FP><<<nbN, kBlock>>>(N, Dv.p, pv, vt.p);
-    acc.zero();
-    m.each([&](auto& f) {
-      ops_fwd(S, f, vt.p);
-      ops_back(S, m.sets, f, acc.p);
-    });
-    k_hvp_fin<FP><<<nbN, kBlock>>>(N, Dv.p, pv, acc.p, static_cast<double>(lam), before ? 1 : 0, out);
+  auto enqueue_apply_M = [&](FP* part_out) {  // z = M r (per set), r.z partials
+    for (size_t q = 0; q < m.sets.size(); ++q)
+      by_dim(m.sets[q]->dim, [&](auto Dc) {
+        constexpr int Dd = decltype(Dc)::value;
+        k_apply<FP, Dd><<<nblk(m.sets[q]->n), kBlock, 0, s>>>(on_pcg, S, static_cast<int>(q), M.p, r.p, z.p,
+                                                              part_out + rz_off[q]);
+      });
+  };
+  // One LM iteration (levenberg_marquardt.hpp:149-220) as a fixed kernel
+  // sequence with pcg.max_iterations unrolled PCG steps; every kernel is
+  // gated by the device state.
+  auto enqueue_iteration = [&]() {
+    k_g_iter_begin<FP><<<1, 32, 0, s>>>(st, drecs.p, gc);
+    // solve_step (linear_system.hpp:185-207): block-Jacobi, PCG (pcg.hpp:34-105), pred, dx
+    k_fill<int><<<1, 32, 0, s>>>(on_iter, 1, &st->fallbacks, 0);
+    for (size_t q = 0; q < m.sets.size(); ++q)
+      by_dim(m.sets[q]->dim, [&](auto Dc) {
+        constexpr int Dd = decltype(Dc)::value;
+        k_precond<FP, Dd><<<nblk(m.sets[q]->n), kBlock, 0, s>>>(on_iter, S, static_cast<int>(q), H.p, Dv.p, st,
+                                                                before, cfg.clamp_min, cfg.clamp_max, M.p,
+                                                                &st->fallbacks);
+      });
+    k_rhs<FP><<<nbN, kBlock, 0, s>>>(on_iter, N, Dv.p, b.p, rhs.p);
+    k_dot<FP><<<nbN, kBlock, 0, s>>>(on_iter, N, rhs.p, rhs.p, part_dot.p);
+    k_fill<FP><<<grid(N), kBlock, 0, s>>>(on_iter, N, xs.p, FP(0));
+    k_g_pcg_begin<FP><<<1, kBlock, 0, s>>>(st, part_dot.p, nbN, gc);
+    k_init_r<FP><<<nbN, kBlock, 0, s>>>(on_pcg, N, st, rhs.p, r.p);
+    enqueue_apply_M(part_rz.p);
+    k_copy<FP><<<grid(N), kBlock, 0, s>>>(on_pcg, N, p.p, z.p);
+    k_dot<FP><<<nbN, kBlock, 0, s>>>(on_pcg, N, r.p, r.p, part_dot.p);
+    k_g_rho<FP><<<1, kBlock, 0, s>>>(st, rz_segs, part_dot.p, nbN);
+    for (int it = 0; it < cfg.pcg.max_iterations; ++it) {
+      // A p (LinearSystem::hvp, linear_system.hpp:104-115)
+      k_axpy_vt<FP><<<nbN, kBlock, 0, s>>>(on_pcg, N, Dv.p, p.p, vt.p);
+      k_fill<FP><<<grid(N), kBlock, 0, s>>>(on_pcg, N, acc.p, FP(0));
+      m.each([&](auto& f) {
+        ops(f).fwd(s, on_pcg, S, f, vt.p);
+        ops(f).back(s, on_pcg, S, m.sets, f, acc.p);
+      });
+      k_hvp_fin<FP><<<nbN, kBlock, 0, s>>>(on_pcg, N, Dv.p, p.p, acc.p, st, before, ap.p);
+      k_dot<FP><<<nbN, kBlock, 0, s>>>(on_pcg, N, p.p, ap.p, part_dot.p);
+      k_g_pap<FP><<<1, kBlock, 0, s>>>(st, part_dot.p, nbN);
+      k_update_xr<FP><<<nbN, kBlock, 0, s>>>(on_pcg, N, st, p.p, ap.p, xs.p, r.p);
+      k_dot<FP><<<nbN, kBlock, 0, s>>>(on_pcg, N, r.p, r.p, part_dot.p);
+      k_g_res<FP><<<1, kBlock, 0, s>>>(st, part_dot.p, nbN, gc);
+      enqueue_apply_M(part_rz.p);
+      k_g_beta<FP><<<1, kBlock, 0, s>>>(st, rz_segs, beta.p);
+      k_dir<FP><<<nbN, kBlock, 0, s>>>(on_pcg, N, beta.p, z.p, p.p);
+    }
+    k_unscale<FP><<<nbN, kBlock, 0, s>>>(on_iter, N, st, xs.p);
+    k_pred<FP><<<nbN, kBlock, 0, s>>>(on_iter, N, Dv.p, xs.p, rhs.p, st, before, part_dot.p, &st->badx);
+    k_g_step<FP><<<1, kBlock, 0, s>>>(st, drecs.p, part_dot.p, nbN, gc);
+    // apply_step + total_error at the candidate (graph.hpp:107-128)
+    for (size_t q = 0; q < m.sets.size(); ++q)
+      by_dim(m.sets[q]->dim, [&](auto Dc) {
+        constexpr int Dd = decltype(Dc)::value;
+        k_apply_step<FP, Dd><<<nblk(m.sets[q]->n), kBlock, 0, s>>>(on_step, S, static_cast<int>(q), Dv.p, xs.p);
+      });
+    m.each([&](auto& f) { ops(f).chi(s, on_step, S, f, m.loss, 1, part_chi.p); });
+    k_g_decide<FP><<<1, kBlock, 0, s>>>(st, drecs.p, chi_segs, gc);
+    // accept: x <- x_new, then re-linearize (also on reject with refresh_on_reject)
+    for (auto* v : m.sets) k_copy<FP><<<grid(v->xn.n), kBlock, 0, s>>>(on_acc, v->xn.n, v->x.p, v->xn.p);
+    enqueue_linearize();
+    GCK(cudaGetLastError());
   };
 
   if (rep) std::memset(rep, 0, sizeof(*rep));
-  FP chi2 = linearize();
+  GState<FP> hs{};
+  hs.do_lin = 1;
+  hs.accepted = 1;  // the initial linearization keeps its chi^2
+  GCK(cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+  enqueue_linearize();
+  GCK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  GCK(cudaStreamSynchronize(s));
+  const FP chi2 = hs.chi2;
   if (!std::isfinite(static_cast<double>(chi2)))
     throw std::runtime_error("levenberg_marquardt: non-finite chi^2 at the initial parameters");
-  std::vector<gb_iteration_record> its;
   gb_solve_report R{};
   R.initial_chi2 = R.final_chi2 = static_cast<double>(chi2);
   R.free_dims = N;
   R.active_factors = nfactors;
   R.termination = GB_TERM_MAX_ITERATIONS;
+  std::vector<gb_iteration_record> its;
   if (N == 0) {
     R.termination = GB_TERM_NO_FREE_PARAMETERS;
-  } else {
-    k_damp_max<FP><<<nbN, kBlock>>>(N, Dv.p, clamped.p, part.p);
-    FP lambda = FP(cfg.tau) * max_parts(part.p, nbN);
-    FP nu = FP(2);
-    for (int it = 1; it <= cfg.max_iterations; ++it) {
-      const auto t_it = Clock::now();
-      gb_iteration_record rec{};
-      rec.iteration = it;
-      rec.chi2_before = static_cast<double>(chi2);
-      rec.lambda = static_cast<double>(lambda);
-      if (!finite) {
-        rec.chi2_after = rec.chi2_before;
-        rec.wall_seconds = since(t_it);
-        its.push_back(rec);
-        R.termination = GB_TERM_NON_FINITE_LINEARIZATION;
-        break;
+  } else if (max_it > 0) {
+    k_damp_max<FP><<<nbN, kBlock, 0, s>>>(N, Dv.p, clamped.p, part_max.p);
+    hs.it = 0;
+    hs.terminated = 0;
+    hs.accepted = 0;
+    hs.do_lin = 0;
+    hs.accepted_steps = 0;
+    hs.final_chi2 = static_cast<double>(chi2);
+    GCK(cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+    k_g_init_damping<FP><<<1, kBlock, 0, s>>>(st, part_max.p, nbN, gc);
+    GCK(cudaGetLastError());
+    // capture one iteration; replay it, polling the termination flag one
+    // iteration behind (the device no-ops iterations after termination)
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    GCK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    enqueue_iteration();
+    GCK(cudaStreamEndCapture(s, &graph));
+    GCK(cudaGraphInstantiate(&exec, graph, 0));
+    GCK(cudaGraphDestroy(graph));
+    struct ExecGuard {
+      cudaGraphExec_t e;
+      ~ExecGuard() { cudaGraphExecDestroy(e); }
+    } eg{exec};
+    int* hflag = nullptr;
+    GCK(cudaHostAlloc(&hflag, sizeof(int) * (max_it + 1), cudaHostAllocDefault));
+    struct HostGuard {
+      int* p;
+      ~HostGuard() { cudaFreeHost(p); }
+    } hg{hflag};
+    std::vector<cudaEvent_t> ev(max_it + 1);
+    for (auto& e : ev) GCK(cudaEventCreate(&e));
+    struct EvGuard {
+      std::vector<cudaEvent_t>& v;
+      ~EvGuard() {
+        for (auto e : v) cudaEventDestroy(e);
       }
-      if (gmax < FP(cfg.gradient_tolerance)) {
-        rec.chi2_after = rec.chi2_before;
-        rec.wall_seconds = since(t_it);
-        its.push_back(rec);
-        R.termination = GB_TERM_GRADIENT_SMALL;
-        break;
+    } evg{ev};
+    GCK(cudaEventRecord(ev[0], s));
+    int launched = 0;
+    for (int k = 0; k < max_it; ++k) {
+      if (k >= 2) {  // iteration k-2 finished: did it terminate?
+        GCK(cudaEventSynchronize(ev[k - 1]));
+        if (hflag[k - 2]) break;
       }
-      // solve_step (linear_system.hpp:185-207): preconditioner, PCG (pcg.hpp:34-105), pred, dx
-      flag.zero();
-      for (size_t st = 0; st < m.sets.size(); ++st)
-        by_dim(m.sets[st]->dim, [&](auto Dc) {
-          constexpr int Dd = decltype(Dc)::value;
-          k_precond<FP, Dd><<<nblk(m.sets[st]->n), kBlock>>>(S, static_cast<int>(st), H.p, Dv.p,
-                                                              static_cast<double>(lambda), before ? 1 : 0,
-                                                              cfg.clamp_min, cfg.clamp_max, M.p, flag.p);
-        });
-      GCK(cudaGetLastError());
-      int fb = 0;
-      GCK(cudaMemcpy(&fb, flag.p, sizeof(int), cudaMemcpyDeviceToHost));
-      rec.precond_fallback_blocks = fb;
-      k_rhs<FP><<<nbN, kBlock>>>(N, Dv.p, b.p, rhs.p);
-      const FP rhs_norm = std::sqrt(dot(rhs.p, rhs.p));
-      int pcg_it = 0;
-      bool conv = false;
-      double relres = 0.0;
-      xs.zero();
-      FP unscale = FP(1);
-      if (!(rhs_norm > FP(0))) {
-        conv = std::isfinite(static_cast<double>(rhs_norm));
-      } else {
-        const FP scale = cfg.pcg.normalize_rhs ? FP(1) / rhs_norm : FP(1);
-        const FP ref_norm = cfg.pcg.normalize_rhs ? FP(1) : rhs_norm;
-        GCK(cudaMemcpy(r.p, rhs.p, N * sizeof(FP), cudaMemcpyDeviceToDevice));
-        k_lincomb<FP><<<nbN, kBlock>>>(N, r.p, scale, r.p, FP(0));
-        FP rho;
-        apply_M(r.p, z.p, &rho);
-        GCK(cudaMemcpy(p.p, z.p, N * sizeof(FP), cudaMemcpyDeviceToDevice));
-        FP res = std::sqrt(dot(r.p, r.p));
-        relres = static_cast<double>(res / ref_norm);
-        while (pcg_it < cfg.pcg.max_iterations) {
-          hvp(p.p, ap.p, lambda);
-          const FP pap = dot(p.p, ap.p);
-          if (!(pap > FP(0)) || !std::isfinite(static_cast<double>(pap))) {
-            conv = false;
-            break;
-          }
-          const FP alpha = rho / pap;
-          k_lincomb<FP><<<nbN, kBlock>>>(N, xs.p, FP(1), p.p, alpha);
-          k_lincomb<FP><<<nbN, kBlock>>>(N, r.p, FP(1), ap.p, -alpha);
-          ++pcg_it;
-          res = std::sqrt(dot(r.p, r.p));
-          relres = static_cast<double>(res / ref_norm);
-          if (!std::isfinite(relres)) {
-            conv = false;
-            break;
-          }
-          if (res <= FP(cfg.pcg.tolerance) * ref_norm) {
-            conv = true;
-            break;
-          }
-          FP rho_next;
-          apply_M(r.p, z.p, &rho_next);
-          const FP beta = rho_next / rho;
-          rho = rho_next;
-          k_lincomb<FP><<<nbN, kBlock>>>(N, p.p, beta, z.p, FP(1));
-        }
-        unscale = cfg.pcg.normalize_rhs ? rhs_norm : FP(1);
-      }
-      // x_scaled = xs * unscale: pred and the finiteness of dx = D x_scaled
-      k_lincomb<FP><<<nbN, kBlock>>>(N, xs.p, unscale, xs.p, FP(0));
-      flag.zero();
-      k_pred<FP><<<nbN, kBlock>>>(N, Dv.p, xs.p, rhs.p, static_cast<double>(lambda), before ? 1 : 0, part.p, flag.p);
-      const FP pred = sum_parts(part.p, nbN);
-      int badx = 0;
-      GCK(cudaMemcpy(&badx, flag.p, sizeof(int), cudaMemcpyDeviceToHost));
-      const bool step_finite = !badx;
-      rec.pcg_iterations = pcg_it;
-      rec.pcg_converged = conv ? 1 : 0;
-      rec.pcg_relative_residual = relres;
-      if (cfg.use_rejection_guard && !conv && relres > cfg.pcg.rejection_ratio * cfg.pcg.tolerance) {
-        rec.low_quality_step = 1;
-        lambda *= nu;
-      }
-      FP chi2_new = std::numeric_limits<FP>::quiet_NaN();
-      if (step_finite) {
-        for (size_t st = 0; st < m.sets.size(); ++st)
-          by_dim(m.sets[st]->dim, [&](auto Dc) {
-            constexpr int Dd = decltype(Dc)::value;
-            k_apply_step<FP, Dd><<<nblk(m.sets[st]->n), kBlock>>>(S, static_cast<int>(st), Dv.p, xs.p, FP(1));
-          });
-        chi2_new = total_error(1);
-      }
-      rec.chi2_after = static_cast<double>(chi2_new);
-      const bool accepted = std::isfinite(static_cast<double>(chi2_new)) && chi2_new < chi2;
-      rec.accepted = accepted ? 1 : 0;
-      FP rel = FP(0);
-      if (accepted) {
-        ++R.accepted_steps;
-        const FP gain = pred > FP(0) ? (chi2 - chi2_new) / pred : std::numeric_limits<FP>::infinity();
-        const FP g = FP(2) * gain - FP(1);
-        lambda *= std::max(FP(1) / FP(3), FP(1) - g * g * g);
-        nu = FP(2);
-        rel = (chi2 - chi2_new) / chi2;
-        for (auto* v : m.sets)  // x <- x_new (the accepted parameters)
-          GCK(cudaMemcpy(v->x.p, v->xn.p, v->xn.n * sizeof(FP), cudaMemcpyDeviceToDevice));
-        chi2 = linearize();
-        R.final_chi2 = static_cast<double>(chi2);
-      } else {
-        lambda *= nu;
-        nu *= FP(2);
-        if (cfg.refresh_on_reject) linearize();
-      }
-      rec.wall_seconds = since(t_it);
-      its.push_back(rec);
-      if (accepted && static_cast<double>(rel) < cfg.tolerance) {
-        R.termination = GB_TERM_TOLERANCE_REACHED;
-        break;
-      }
-      if (static_cast<double>(lambda) > cfg.lambda_max) {
-        R.termination = GB_TERM_DAMPING_OVERFLOW;
-        break;
-      }
+      GCK(cudaGraphLaunch(exec, s));
+      GCK(cudaMemcpyAsync(&hflag[k], &st->terminated, sizeof(int), cudaMemcpyDeviceToHost, s));
+      GCK(cudaEventRecord(ev[k + 1], s));
+      ++launched;
     }
+    GCK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    GCK(cudaStreamSynchronize(s));
+    its.resize(hs.it);
+    if (hs.it) GCK(cudaMemcpy(its.data(), drecs.p, sizeof(gb_iteration_record) * hs.it, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < hs.it && i < launched; ++i) {
+      float ms = 0;
+      GCK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      its[i].wall_seconds = 1e-3 * ms;
+    }
+    R.termination = hs.terminated ? hs.termination : GB_TERM_MAX_ITERATIONS;
+    R.accepted_steps = hs.accepted_steps;
+    R.final_chi2 = hs.final_chi2;
   }
   // write back (VertexDescriptor::scatter through Traits::set_parameters)
   for (auto* v : m.sets) {
