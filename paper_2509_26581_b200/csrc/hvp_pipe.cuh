@@ -45,8 +45,12 @@ __host__ __device__ constexpr uint32_t pipe_jstride() {
 
 // Section offsets inside a tile's aux blob (static) and lin blob (per
 // linearization); identical on the host (sizes) and the device (reads).
+// seg / rseg: the recompute HVP's run-aligned edge segments (hvp_rc.cuh):
+// segment q = edges [start, start + count) of one camera run (start | count << 9),
+// run lc = segments [rseg[lc], rseg[lc + 1])
+constexpr int kSegSlots = 128;
 struct AuxSec {
-  uint32_t lcam, lpt, psl, pso, cf, bytes;
+  uint32_t lcam, lpt, psl, pso, cf, seg, rseg, bytes;
 };
 __host__ __device__ inline AuxSec aux_sections(uint32_t ne, uint32_t npt) {
   const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad;
@@ -56,7 +60,9 @@ __host__ __device__ inline AuxSec aux_sections(uint32_t ne, uint32_t npt) {
   a.psl = a.lpt + r16(2ull * ne8);
   a.pso = a.psl + r16(2ull * ne);
   a.cf = a.pso + r16(2ull * (npt + 1));
-  a.bytes = a.cf + r16(3ull * npt);
+  a.seg = a.cf + r16(3ull * npt);
+  a.rseg = a.seg + r16(2ull * kSegSlots);
+  a.bytes = a.rseg + r16(2ull * (kTileCams + 1));
   return a;
 }
 struct LinSec {
@@ -555,6 +561,34 @@ __global__ void k_tile_aux(Dev<FP, SP> d) {
     }
   }
   for (uint32_t k = threadIdx.x; k < 3 * npt; k += blockDim.x) cf[k] = d.col_free[9ull * d.nc + 3ull * pb + k];
+  // run-aligned segments of <= K edges, the smallest K >= 4 with at most
+  // kSegSlots segments (each camera run is cut into ceil(len / K) pieces)
+  __shared__ uint16_t run_lo[kTileCams + 1];
+  const uint32_t ncam = m[kMNcam];
+  for (uint32_t k = threadIdx.x; k < ne; k += blockDim.x) {
+    const uint32_t lc = d.d_lcam[eb + k];
+    if (k == 0 || d.d_lcam[eb + k - 1] != lc) run_lo[lc] = static_cast<uint16_t>(k);
+  }
+  if (threadIdx.x == 0) run_lo[ncam] = static_cast<uint16_t>(ne);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint16_t* seg = reinterpret_cast<uint16_t*>(a + as.seg);
+    uint16_t* rseg = reinterpret_cast<uint16_t*>(a + as.rseg);
+    uint32_t K = 4;
+    for (;; ++K) {
+      uint32_t n = 0;
+      for (uint32_t lc = 0; lc < ncam; ++lc) n += (run_lo[lc + 1] - run_lo[lc] + K - 1) / K;
+      if (n <= kSegSlots) break;
+    }
+    uint32_t q = 0;
+    for (uint32_t lc = 0; lc < ncam; ++lc) {
+      rseg[lc] = static_cast<uint16_t>(q);
+      for (uint32_t e = run_lo[lc]; e < run_lo[lc + 1]; e += K)
+        seg[q++] = static_cast<uint16_t>(e | (min(K, run_lo[lc + 1] - e) << 9));
+    }
+    rseg[ncam] = static_cast<uint16_t>(q);
+    for (; q < kSegSlots; ++q) seg[q] = 0;  // idle threads: count 0
+  }
 }
 
 // Per-linearization lin blobs: point D, camera R f (factored store), Huber w.

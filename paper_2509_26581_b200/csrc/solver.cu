@@ -27,6 +27,7 @@
 #include "gb_bal.h"
 #include "kernels.cuh"
 #include "hvp_pipe.cuh"
+#include "hvp_rc.cuh"
 
 namespace gb {
 
@@ -328,6 +329,14 @@ class Solver final : public SolverBase {
   }
   ~Solver() override {
     cudaSetDevice(g_.device);  // this handle's streams, events and blocks live there
+    if (rc_.prof) {  // GB_RC_DBG & 8: per-role mbarrier wait cycles of k_hvp_rc (summed over CTAs and launches)
+      unsigned long long h[8] = {};
+      if (cudaMemcpy(h, rc_.prof, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess)
+        std::fprintf(stderr,
+                     "[rc prof] per-warp busy fractions: consumer wait ready %.3f | producer wait empty %.3f, "
+                     "ring+setup %.3f, issue %.3f | preparer wait full %.3f\n",
+                     double(h[0]) / h[7], 8.0 * h[2] / h[7], 8.0 * h[4] / h[7], 8.0 * h[5] / h[7], 8.0 * h[3] / h[7]);
+    }
     for (auto& e : ev_) cudaEventDestroy(e);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (flag_host_) cudaFreeHost(flag_host_);
@@ -535,6 +544,21 @@ class Solver final : public SolverBase {
     if (reference_bytes) *reference_bytes = E * (24 * sJ + 8) + N * (sV + sA);
     double b = 0;
     const Dev<FP, SP>& d = dev_;
+    if (rc_ok_) {  // recompute HVP: tile blobs, X / p / z in, ap / p out, camera records and 15-value partials
+      double aux = 0, lin = 0;
+      for (uint32_t t : act_.normal_tiles) {
+        const uint32_t ne = act_.tile_ecnt[t], npt = act_.tile_pbeg[t + 1] - act_.tile_pbeg[t];
+        const uint32_t ncam = act_.tile_cam_off[t + 1] - act_.tile_cam_off[t];
+        aux += aux_sections(ne, npt).bytes;
+        lin += rc_lin_sections<FP>(ne, npt, ncam, d.w != nullptr).bytes;
+      }
+      b += aux + lin + np3 * 2 * sV + np3 * 2 * sV;              // blobs (incl. X); p, z in; ap, p out
+      b += d.ntcams * (kRcRec * sF * 4.0 + 8.0);                 // tile records (write, read), partials (write, read)
+      b += act_.nc * kRcRec * sF * 2 + nc9 * (sF + sF + 2 * sV);  // camera records; x, cpre, p, z
+      b += nc9 * (sV + sF + sV);                                 // camera p, D in; ap out
+      if (kernel_bytes) *kernel_bytes = b;
+      return;
+    }
     if (pipe_ok_) {
       double aux = 0, lin = 0;
       for (uint32_t t : act_.normal_tiles) {
@@ -755,13 +779,16 @@ class Solver final : public SolverBase {
 
   void ls_jacobians(void* out) override {
     need_ls();
-    if (!dev_.J) throw std::logic_error("dynamic mode stores no Jacobians");
+    if (!dev_.J && (!rc_ok_ || g_.diff_mode == GB_DYNAMIC)) throw std::logic_error("dynamic mode stores no Jacobians");
     const uint64_t ns = act_.n_slots;
     std::vector<SP> h(24 * ns);
     {
       DBuf full;
       SP* fj = static_cast<SP*>(full.alloc(24 * ns * sizeof(SP)));
-      k_expand_J<FP, SP><<<grid_for(ns), 256, 0, s_>>>(dev_, fj);
+      if (dev_.J)
+        k_expand_J<FP, SP><<<grid_for(ns), 256, 0, s_>>>(dev_, fj);
+      else  // recompute path: the J a store would hold, from the linearize chain at x
+        k_eval_J<FP, SP><<<act_.ntiles, 128, 0, s_>>>(dev_, fj);
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(h.data(), fj, h.size() * sizeof(SP), cudaMemcpyDeviceToHost, s_));
       CK(cudaStreamSynchronize(s_));
@@ -1210,7 +1237,24 @@ class Solver final : public SolverBase {
   void allocate_work() {
     const uint64_t nc = act_.nc, np = act_.np, ns = act_.n_slots;
     Dev<FP, SP>& d = dev_;
-    const bool dyn = g_.diff_mode == GB_DYNAMIC;
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g_.device));
+    // recompute HVP (hvp_rc.cuh): analytic / dynamic with SP == FP and
+    // the full-system PCG; no Jacobian store at all. GB_HVP_RC=0 keeps the stored J.
+    rc_ok_ = false;
+    if (g_.diff_mode != GB_AUTO && std::is_same<SP, FP>::value && g_.linear_solver != GB_SOLVER_SCHUR &&
+        d.n_normal > 0) {
+      rc_ = rc_layout<FP>(g_.loss_kind == GB_LOSS_HUBER, static_cast<uint32_t>(optin));
+      rc_ok_ = rc_.ring_bytes >= 2 * rc_.max_region;
+      if (const char* e = std::getenv("GB_HVP_RC")) rc_ok_ = rc_ok_ && std::atoi(e) != 0;
+      if (const char* e = std::getenv("GB_RC_DBG")) rc_.dbg = std::atoi(e);
+      rc_.prof = nullptr;
+      if (rc_.dbg & 8) {
+        rc_.prof = static_cast<unsigned long long*>(b_rcprof_.alloc(8 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(rc_.prof, 0, 8 * sizeof(unsigned long long), s_));
+      }
+    }
+    const bool dyn = g_.diff_mode == GB_DYNAMIC || rc_ok_;
     // factored J store: analytic mode with SP == FP; GB_JFACT=0 disables
     d.jfact = (!dyn && g_.diff_mode == GB_ANALYTIC && std::is_same<SP, FP>::value) ? 1 : 0;
     if (const char* e = std::getenv("GB_JFACT")) d.jfact = d.jfact && std::atoi(e) != 0;
@@ -1227,8 +1271,6 @@ class Solver final : public SolverBase {
     d.huber = static_cast<FP>(g_.huber);
     // bulk-copy pipelined HVP (hvp_pipe.cuh): stored J, >= 2 stages in shared memory; GB_HVP_PIPE=0 disables
     {
-      int optin = 0;
-      CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g_.device));
       pipe_ = pipe_layout<FP, SP>(d.jfact ? kJFactRows : 24, d.w != nullptr, d.jfact != 0,
                                   static_cast<uint32_t>(optin));
       pipe_ok_ = d.J != nullptr && pipe_.stages >= 2 && d.n_normal > 0;
@@ -1240,9 +1282,15 @@ class Solver final : public SolverBase {
       d.slot_span = nullptr;
       d.tile_lin = nullptr;
       d.ntcams = act_.tile_cam_off.empty() ? 0 : act_.tile_cam_off.back();
-      if (pipe_ok_) {
-        CK(cudaFuncSetAttribute(k_hvp_pipe<FP, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(pipe_.total_bytes)));
+      d.crec = d.tcrec = d.part15 = nullptr;
+      d.hflag = nullptr;
+      if (pipe_ok_ || rc_ok_) {
+        if (pipe_ok_)
+          CK(cudaFuncSetAttribute(k_hvp_pipe<FP, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(pipe_.total_bytes)));
+        else if constexpr (kRcCapable)
+          for (auto fn : {k_hvp_rc<FP, SP, false>, k_hvp_rc<FP, SP, true>})
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rc_.total_bytes)));
         // tile records with the aux / lin blob offsets (16-byte units)
         std::vector<uint32_t> meta(static_cast<size_t>(kMCount) * d.n_normal, 0);
         uint64_t aux16 = 0, lin16 = 0;
@@ -1259,18 +1307,37 @@ class Solver final : public SolverBase {
           m[kMCb] = act_.tile_cam_off[t];
           m[kMNcam] = ncam;
           m[kMCh0] = act_.tile_chunk_base[t];
-          m[kMAux16] = static_cast<uint32_t>(aux16);
-          m[kMLin16] = static_cast<uint32_t>(lin16);
-          aux16 += aux_sections(ne, npt).bytes / 16;
-          lin16 += lin_sections<FP>(ne, npt, ncam, d.jfact != 0, d.w != nullptr).bytes / 16;
+          if (rc_ok_) {  // one blob per tile: static aux part, then the per-linearization part (one bulk copy)
+            m[kMAux16] = static_cast<uint32_t>(aux16);
+            aux16 += aux_sections(ne, npt).bytes / 16;
+            m[kMLin16] = static_cast<uint32_t>(aux16);
+            aux16 += rc_lin_sections<FP>(ne, npt, ncam, d.w != nullptr).bytes / 16;
+          } else {
+            m[kMAux16] = static_cast<uint32_t>(aux16);
+            m[kMLin16] = static_cast<uint32_t>(lin16);
+            aux16 += aux_sections(ne, npt).bytes / 16;
+            lin16 += lin_sections<FP>(ne, npt, ncam, d.jfact != 0, d.w != nullptr).bytes / 16;
+          }
         }
         if (aux16 > 0xffffffffull || lin16 > 0xffffffffull) throw std::invalid_argument("tile blobs exceed 64 GB");
         d.tile_meta = to_dev(b_tmeta_, meta);
         d.tile_aux = static_cast<unsigned char*>(b_taux_.alloc(std::max<uint64_t>(16, 16 * aux16)));
         d.slot_span = static_cast<uint2*>(b_sspan_.alloc(std::max<uint64_t>(8, 8ull * act_.nparts)));
-        d.tile_lin = static_cast<unsigned char*>(b_tlin_.alloc(std::max<uint64_t>(16, 16 * lin16)));
-        d.tcv = static_cast<A*>(b_tcv_.alloc(std::max<uint64_t>(1, cam_stride<A>() * uint64_t(d.ntcams)) * sizeof(A)));
-        CK(cudaMemsetAsync(d.tcv, 0, std::max<uint64_t>(1, cam_stride<A>() * uint64_t(d.ntcams)) * sizeof(A), s_));
+        d.tile_lin = rc_ok_ ? d.tile_aux : static_cast<unsigned char*>(b_tlin_.alloc(std::max<uint64_t>(16, 16 * lin16)));
+        if (pipe_ok_) {
+          d.tcv = static_cast<A*>(b_tcv_.alloc(std::max<uint64_t>(1, cam_stride<A>() * uint64_t(d.ntcams)) * sizeof(A)));
+          CK(cudaMemsetAsync(d.tcv, 0, std::max<uint64_t>(1, cam_stride<A>() * uint64_t(d.ntcams)) * sizeof(A), s_));
+        } else {
+          const uint64_t nt = std::max<uint64_t>(1, d.ntcams);
+          d.crec = static_cast<FP*>(b_crec_.alloc(std::max<uint64_t>(1, nc) * kRcRec * sizeof(FP)));
+          d.tcrec = static_cast<FP*>(b_tcrec_.alloc(nt * kRcRec * sizeof(FP)));
+          d.part15 = static_cast<FP*>(b_part15_.alloc(nt * kRcRec * sizeof(FP)));
+          CK(cudaMemsetAsync(d.part15, 0, nt * kRcRec * sizeof(FP), s_));  // heavy tiles' entries stay 0
+          CK(cudaMemsetAsync(d.tcrec, 0, nt * kRcRec * sizeof(FP), s_));
+          uint8_t* hf = static_cast<uint8_t*>(b_hflag_.alloc(std::max<uint64_t>(1, act_.nparts)));
+          CK(cudaMemsetAsync(hf, 0, std::max<uint64_t>(1, act_.nparts), s_));
+          d.hflag = hf;
+        }
         pipe_aux_pending_ = true;  // built once the remaining device arrays exist (below)
       }
     }
@@ -1365,6 +1432,10 @@ class Solver final : public SolverBase {
       }
       k_tile_aux<FP, SP><<<d.n_normal, 256, 0, s_>>>(d);
       CK(cudaGetLastError());
+      if (rc_ok_ && d.n_heavy) {
+        k_mark_heavy_slots<FP, SP><<<d.n_heavy, 256, 0, s_>>>(d, const_cast<uint8_t*>(d.hflag));
+        CK(cudaGetLastError());
+      }
       pipe_aux_pending_ = false;
     }
   }
@@ -1520,11 +1591,24 @@ class Solver final : public SolverBase {
     if (pipe_ok_) {
       k_tile_lin<FP, SP><<<dev_.n_normal, 128, 0, s_>>>(dev_, force);
       CK(cudaGetLastError());
+    } else if (rc_ok_) {
+      k_tile_lin_rc<FP, SP><<<dev_.n_normal, 128, 0, s_>>>(dev_, force);
+      CK(cudaGetLastError());
     }
   }
 
   // HVP tile pass (dynamic mode recomputes J per edge).
+  // tcv_ready: the stored-J pipeline's per-tile camera copies are current
+  // (k_pcg_dir_rest ran); on the recompute path it means the direction update
+  // p = z + beta p is pending and is applied here (cameras, heavy-tile points)
+  // and inside k_hvp_rc (normal-tile points).
   void launch_hvp_tiles(const Dev<FP, SP>& d, bool tcv_ready = false) {
+    if constexpr (kRcCapable) {
+      if (rc_ok_) {
+        launch_hvp_rc(d, tcv_ready);
+        return;
+      }
+    }
     if (!d.J) {
       k_hvp_tiles<FP, SP, true><<<act_.ntiles, kTileThreads, 0, s_>>>(d, nullptr);
     } else if (pipe_ok_) {  // normal tiles through the bulk-copy pipeline, heavy tiles one CTA each
@@ -1539,9 +1623,35 @@ class Solver final : public SolverBase {
     CK(cudaGetLastError());
   }
 
+  // recompute HVP (hvp_rc.cuh): camera records (+ direction update), their
+  // per-tile copies, the tile pipeline, heavy tiles with the dynamic tile kernel
+  void launch_hvp_rc(const Dev<FP, SP>& d, bool dir) {
+    k_rc_cams_pre<FP, SP><<<std::max(1u, div_up(act_.nc, 128)), 128, 0, s_>>>(d, dir ? 1 : 0, dir_rbeg_, dir_rend_,
+                                                                              dir_nranges_);
+    k_rc_tcams<FP, SP><<<grid_for(uint64_t(kRcRec / 2) * d.ntcams), 256, 0, s_>>>(d);
+    const uint32_t grid = std::min<uint32_t>(d.n_normal, sms_);
+    if (d.w)
+      k_hvp_rc<FP, SP, true><<<grid, kRcThreadsWS, rc_.total_bytes, s_>>>(d, rc_);
+    else
+      k_hvp_rc<FP, SP, false><<<grid, kRcThreadsWS, rc_.total_bytes, s_>>>(d, rc_);
+    if (d.n_heavy) k_hvp_tiles<FP, SP, true, 1><<<d.n_heavy, kTileThreads, 0, s_>>>(d, d.heavy_tiles);
+    CK(cudaGetLastError());
+  }
+
   void launch_hvp(const Dev<FP, SP>& d, bool tcv_ready = false) {
     launch_hvp_tiles(d, tcv_ready);
-    if (!dist()) {
+    if (rc_ok_) {
+      if constexpr (kRcCapable) {
+        if (!dist()) {
+          k_hvp_cams_rc<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 0);
+        } else {
+          k_hvp_cams_rc<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 1);
+          CK(cudaGetLastError());
+          allreduce(d.red, 9ull * d.nc + 1);
+          k_hvp_cams_rc<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 2);
+        }
+      }
+    } else if (!dist()) {
       k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 0);
     } else {
       k_hvp_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 1);
@@ -1613,7 +1723,7 @@ class Solver final : public SolverBase {
       allreduce(red_s() + kRedInitRz, 2);
       fin(2);
     }
-    const bool dir_fused = pipe_ok_ && !(!dist() && fused_pcg_);
+    const bool dir_fused = (pipe_ok_ || rc_ok_) && !(!dist() && fused_pcg_);
     for (int k = 0; k < pcg_max_it; ++k) {
       launch_hvp(dev_, dir_fused && k > 0);  // after k_pcg_dir_rest the per-tile camera copies are current
       if (!dist() && fused_pcg_) {
@@ -1626,7 +1736,9 @@ class Solver final : public SolverBase {
         allreduce(red_s() + kRedUpdRz, 2);
         fin(3);
       }
-      if (dir_fused)  // normal-tile points get p = z + beta p inside the next k_hvp_pipe
+      if (rc_ok_ && dir_fused)  // applied by the next launch_hvp (k_rc_cams_pre + k_hvp_rc)
+        ;
+      else if (dir_fused)  // normal-tile points get p = z + beta p inside the next k_hvp_pipe
         k_pcg_dir_rest<FP, SP><<<dir_rest_grid_, 256, 0, s_>>>(dev_, dir_rbeg_, dir_rend_, dir_nranges_);
       else
         k_pcg_dir<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
@@ -1745,6 +1857,10 @@ class Solver final : public SolverBase {
       b_pt_slot_off_, b_pt_slots_, b_cam_part_off_, b_cam_part_idx_;
   PipeLayout pipe_{};
   bool pipe_ok_ = false;
+  static constexpr bool kRcCapable = std::is_same<SP, FP>::value;
+  RcLayout rc_{};
+  bool rc_ok_ = false;  // recompute HVP (hvp_rc.cuh): no J store
+  DBuf b_crec_, b_tcrec_, b_part15_, b_hflag_, b_rcprof_;
   uint32_t sms_ = 148;
   unsigned pt_occ_ = 4;
   unsigned chi2_occ_ = 4;

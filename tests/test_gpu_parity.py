@@ -89,6 +89,7 @@ def test_factored_jacobian_store_bit_exact(gpu, ladybug, monkeypatch, precision)
     §2) rebuilds exactly the chain's J: bit-identical to the full 24-value
     store, and the HVP / LM trace through it is bit-identical too."""
     out = {}
+    monkeypatch.setenv("GB_HVP_RC", "0")  # the stored-J path
     for jf in ("1", "0"):
         monkeypatch.setenv("GB_JFACT", jf)
         g = bal.build_graph(ladybug, precision, "analytic")
@@ -119,6 +120,7 @@ def test_pipelined_hvp_bit_exact(gpu, monkeypatch, precision, mode, huber):
 
 def _pipe_vs_tiles(monkeypatch, p, precision, mode, huber):
     out = {}
+    monkeypatch.setenv("GB_HVP_RC", "0")  # the stored-J path
     for pipe in ("1", "0"):
         monkeypatch.setenv("GB_HVP_PIPE", pipe)
         g = bal.build_graph(p, precision, mode, huber)
@@ -131,6 +133,49 @@ def _pipe_vs_tiles(monkeypatch, p, precision, mode, huber):
     assert np.array_equal(out["1"][0], out["0"][0])
     assert out["1"][1] == out["0"][1]
     assert np.array_equal(out["1"][2], out["0"][2])
+
+
+@pytest.mark.parametrize("precision,mode,huber,zipf", [("fp64", "analytic", None, None), ("fp64", "analytic", 2.0, 1.2),
+                                                      ("fp64", "dynamic", None, None), ("fp32", "analytic", 2.0, None)])
+def test_recompute_hvp(gpu, monkeypatch, precision, mode, huber, zipf):
+    """The recompute HVP (hvp_rc.cuh: no Jacobian store, the factored
+    operator applied per camera run) against the stored-J pipeline: the same
+    operator to rounding, the same LM trace (iterations, accept pattern, PCG
+    iterations) and final cost. Several tiles per CTA, heavy tiles (a point
+    seen by > 512 cameras) and skewed camera degrees."""
+    p = bal.synthetic_bal(900, 60000, 330000, seed=11, zipf=zipf) if zipf else bal.synthetic_bal(900, 60000, 330000, seed=11)
+    out = {}
+    for rc in ("1", "0"):
+        monkeypatch.setenv("GB_HVP_RC", rc)
+        g = bal.build_graph(p, precision, mode, huber)
+        n = g.ls_linearize(0)["n"]
+        v = np.random.default_rng(4).standard_normal(n)
+        hs = [g.ls_hvp(v, lam) for lam in (0.0, 1e-3)]
+        g2 = bal.build_graph(p, precision, mode, huber)
+        rep = bal.levenberg_marquardt(g2, bal_cfg(6))
+        out[rc] = (hs, rep, g2.points.copy(), g2.cameras.copy())
+    tol = 1e-12 if precision == "fp64" else 2e-5
+    for a, b in zip(out["1"][0], out["0"][0]):
+        assert rel(a, b) <= tol
+    ra, rb = out["1"][1], out["0"][1]
+    assert ra.termination == rb.termination and len(ra.iterations) == len(rb.iterations)
+    assert [i.accepted for i in ra.iterations] == [i.accepted for i in rb.iterations]
+    assert [i.pcg_iterations for i in ra.iterations] == [i.pcg_iterations for i in rb.iterations]
+    ctol = 1e-9 if precision == "fp64" else 1e-4
+    assert abs(ra.final_chi2 - rb.final_chi2) <= ctol * rb.final_chi2
+    assert rel(out["1"][2], out["0"][2]) <= (1e-7 if precision == "fp64" else 1e-3)
+
+
+def test_recompute_hvp_deterministic(gpu, monkeypatch):
+    """Fixed association order everywhere: two runs are bit-identical."""
+    monkeypatch.setenv("GB_HVP_RC", "1")
+    p = bal.synthetic_bal(300, 20000, 110000, seed=5)
+    res = []
+    for _ in range(2):
+        g = bal.build_graph(p, "fp64", "analytic")
+        n = g.ls_linearize(0)["n"]
+        res.append(g.ls_hvp(np.random.default_rng(2).standard_normal(n), 1e-3))
+    assert np.array_equal(res[0], res[1])
 
 
 @pytest.mark.parametrize("mode", ["analytic", "dynamic"])

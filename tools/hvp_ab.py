@@ -19,14 +19,14 @@ ap.add_argument("settings", nargs="*")
 a = ap.parse_args()
 
 if a.child:
-    from bench import WORKLOADS, lm_config
+    from bench import WORKLOADS, timed_config
     from paper_2509_26581_b200 import _abi, bal
 
     nc, np_, ne, _ = WORKLOADS[a.workload]
     p = bal.synthetic_bal(nc, np_, ne, seed=42)
     g = bal.build_graph(p, a.precision, a.mode)
     L = g.backend
-    c = lm_config(2, bal).to_c()
+    c = timed_config(bal, 2).to_c()
     L.check(L.fn("begin")(g._h, ctypes.byref(c), None))
     L.check(L.fn("step")(g._h, 2))
     rep = _abi.gb_solve_report()
@@ -35,7 +35,11 @@ if a.child:
     m1, m2 = ctypes.c_double(), ctypes.c_double()
     L.check(L.fn("time_hvp")(g._h, 20, ctypes.byref(m1), ctypes.byref(m2)))
     print(json.dumps({"hvp_ms": m1.value, "tiles_ms": m2.value,
-                      "lm_ms": [recs[i].wall_seconds * 1e3 for i in range(2)]}))
+                      "lm_ms": [recs[i].wall_seconds * 1e3 for i in range(2)]}), flush=True)
+    del g  # releases the solver (GB_RC_DBG & 8 prints its wait profile to stderr)
+    import gc
+
+    gc.collect()
 else:
     for st in a.settings or [""]:
         env = dict(os.environ)
@@ -46,3 +50,6 @@ else:
                               a.precision, "--mode", a.mode], env=env, capture_output=True, text=True)
         print(st or "(default)", out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-2000:],
               flush=True)
+        for line in out.stderr.splitlines():
+            if line.startswith("[rc prof]"):
+                print("   ", line, flush=True)

@@ -7,7 +7,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from bench import WORKLOADS, lm_config  # noqa: E402
+from bench import WORKLOADS, timed_config  # noqa: E402
 from paper_2509_26581_b200 import _abi, bal  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -22,7 +22,7 @@ p = bal.synthetic_bal(nc, np_, ne, seed=42)
 g = bal.build_graph(p, a.precision, a.mode)
 if a.solver != "pcg":
     g.set_linear_solver(a.solver)
-c = lm_config(a.iters, bal).to_c()
+c = timed_config(bal, a.iters).to_c()
 L = g.backend
 L.check(L.fn("begin")(g._h, ctypes.byref(c), None))
 L.check(L.fn("step")(g._h, a.iters))
