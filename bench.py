@@ -62,7 +62,7 @@ UNIT = "ms/LM-iteration"
 GEN = os.path.join(ROOT, "paper_2509_26581_b200", "gb_gen_bal")
 # sources of the HVP tile kernel: the committed ncu DRAM traffic is only
 # reported while they are unchanged since the capture
-HVP_SOURCES = ["hvp_pipe.cuh", "kernels.cuh", "common.cuh", "snavely.cuh"]
+HVP_SOURCES = ["hvp_rc.cuh", "hvp_pipe.cuh", "kernels.cuh", "common.cuh", "snavely.cuh"]
 
 
 # ------------------------------------------------------------------ inputs
@@ -413,8 +413,11 @@ def ours(args, shape, desc):
     # live roofline of the dominant kernel pair (HVP) on the solver stream
     ms_hvp, ms_tiles = ctypes.c_double(), ctypes.c_double()
     L.check(L.fn("time_hvp")(g._h, 20, ctypes.byref(ms_hvp), ctypes.byref(ms_tiles)))
-    kbytes, rbytes = ctypes.c_double(), ctypes.c_double()
-    L.check(L.fn("hvp_bytes")(g._h, ctypes.byref(kbytes), ctypes.byref(rbytes)))
+    kbytes, rbytes, aflops, hpath = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+    L.check(L.fn("hvp_info")(g._h, ctypes.byref(hpath), ctypes.byref(kbytes), ctypes.byref(rbytes),
+                             ctypes.byref(aflops)))
+    fma_tf = ctypes.c_double()
+    L.check(L.fn("fma_peak")(local, 0 if args.precision == "fp64" else 1, ctypes.byref(fma_tf)))
 
     ms = ms_total / K
     setup_s = [rep0.setup_seconds]
@@ -461,8 +464,8 @@ def ours(args, shape, desc):
         del g2
         return e2e_s, rep2, parts
 
-    runs = [e2e_once() for _ in range(2)]
-    e2e_s = statistics.mean(r[0] for r in runs)
+    runs = [e2e_once() for _ in range(3)]
+    e2e_s = statistics.median(r[0] for r in runs)
     rep2 = runs[-1][1]
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
@@ -475,11 +478,39 @@ def ours(args, shape, desc):
 
     if rank != 0:
         return
-    hvp_bytes = rbytes.value  # SURVEY.md §8(d) HVP algorithmic bytes: E (24 s_J + 8) + N (s_V + s_A)
+    # SURVEY.md §8(d) algorithmic bytes / flops of the configured HVP path (gb_hvp_info):
+    # stored J  E (24 s_J + 8) + N (s_V + s_A); recompute / dynamic  E (2 s_FP + 8) +
+    # (9 nc + 3 np) s_FP + N (s_V + s_A) bytes and E * 500 flops
+    hvp_bytes, hvp_flops = rbytes.value, aflops.value
     peak, peak_kind = measured_peak()
-    achieved = hvp_bytes / (ms_hvp.value * 1e-3) / 1e9
-    kernel_gbs = kbytes.value / (ms_hvp.value * 1e-3) / 1e9
+    t_hvp = ms_hvp.value * 1e-3
+    achieved = hvp_bytes / t_hvp / 1e9
+    kernel_gbs = kbytes.value / t_hvp / 1e9
+    flop_tf = hvp_flops / t_hvp / 1e12
     traffic, traffic_note = committed_traffic()
+    path_name = {0: "k_hvp_tiles (dynamic J)", 1: "k_hvp_tiles (stored J)",
+                 2: "k_hvp_pipe (stored J, bulk-copy pipeline) + k_tcam_vt",
+                 3: "k_hvp_rc (recompute pipeline, no J store) + k_rc_cams_pre"}[hpath.value]
+    fp_bound = hvp_flops > 0 and flop_tf / fma_tf.value > achieved / peak
+    if fp_bound:
+        roof = {"bound": "fp64" if args.precision == "fp64" else "fp32", "achieved": round(flop_tf, 3),
+                "peak": round(fma_tf.value, 2), "unit": "TFLOP/s", "frac": round(flop_tf / fma_tf.value, 4),
+                "peak_kind": "measured (gb_fma_peak: DFMA/FFMA probe on every SM, this run)",
+                "algorithmic_flops": int(hvp_flops)}
+    else:
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_kind": peak_kind}
+    roof.update({
+        "kernel": path_name + " + k_hvp_cams*: the HVP of one PCG iteration (heavy tiles: k_hvp_tiles)",
+        "traffic": traffic, "traffic_note": traffic_note, "algorithmic_bytes": int(hvp_bytes),
+        "ms_per_launch": round(ms_hvp.value, 4), "ms_tiles_only": round(ms_tiles.value, 4),
+        "hbm": {"achieved": round(achieved, 1), "peak": peak, "frac": round(achieved / peak, 4), "unit": "GB/s",
+                "kernel_bytes": int(kbytes.value), "kernel_gbs": round(kernel_gbs, 1),
+                "kernel_frac": round(kernel_gbs / peak, 4), "peak_kind": peak_kind},
+        "note": "SURVEY §8(d) algorithmic bytes/flops of the configured path (gb_hvp_info); kernel_bytes: what "
+                "this path actually moves (tile blobs, point vectors, camera records, partials; gb_hvp_bytes); "
+                "the stored-J reference layout would need E (24 s_J + 8) + N (s_V + s_A)",
+    })
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": UNIT,
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(ms, 4), "higher_is_better": False,
@@ -497,19 +528,10 @@ def ours(args, shape, desc):
                 "runs": [r[2] for r in runs],
                 "note": "public API: build_graph + levenberg_marquardt (reference config: 50 LM iterations, "
                         "tolerance 1e-6) from pinned host arrays, incl. upload, activation, initial linearize and "
-                        f"write-back; mean of 2 solves, amortized over their {n_it} iterations"},
+                        f"write-back; median of 3 solves, amortized over their {n_it} iterations"},
         "gpu_launches": int(kernels.value) * K,
         "gpu_launches_note": f"{kernels.value} kernel nodes in the captured per-iteration CUDA graph x {K} replays",
-        "roofline": {"kernel": "k_hvp_pipe (+k_tcam_vt, k_hvp_tiles for heavy tiles) + k_hvp_cams: the HVP of one "
-                               "PCG iteration", "bound": "hbm",
-                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic, "traffic_note": traffic_note, "algorithmic_bytes": int(hvp_bytes),
-                     "ms_per_launch": round(ms_hvp.value, 4), "ms_tiles_only": round(ms_tiles.value, 4),
-                     "peak_kind": peak_kind, "kernel_bytes": int(kbytes.value), "kernel_gbs": round(kernel_gbs, 1),
-                     "kernel_frac": round(kernel_gbs / peak, 4),
-                     "note": "achieved/frac: SURVEY §8(d) reference-layout bytes (24 J values per edge) / time; "
-                             "kernel_*: the bytes this path actually moves (factored 16-value J store, per-tile "
-                             "blobs, partial slots; gb_hvp_bytes) / time"},
+        "roofline": roof,
         "window": window_summary(window),
         "solve": {"iterations": rep.iterations_run, "initial_chi2": rep.initial_chi2,
                   "chi2_after_timed": rep.final_chi2, "setup_seconds_per_rank": [round(s, 4) for s in setup_s],

@@ -223,6 +223,18 @@ int gb_time_hvp(gb_graph* g, int32_t reps, double* ms_per_hvp, double* ms_tiles_
  *              reference-layout figure E (24 s_J + 8) + N (s_V + s_A) of
  *              SURVEY.md §8(d) (the roofline's "algorithmic bytes"). */
 int gb_hvp_bytes(gb_graph* g, double* kernel_bytes, double* reference_bytes);
+/* gb_hvp_info  the configured HVP path (0 dynamic tile kernel, 1 stored-J
+ *              tile kernel, 2 stored-J bulk-copy pipeline, 3 recompute
+ *              pipeline (hvp_rc.cuh: no Jacobian store)), the bytes one HVP
+ *              moves on it, and SURVEY.md §8(d)'s algorithmic bytes and flops
+ *              for it: stored J  E (24 s_J + 8) + N (s_V + s_A), 0 flops;
+ *              recompute / dynamic  E (2 s_FP + 8) + (9 nc + 3 np) s_FP +
+ *              N (s_V + s_A) and E * 500 flops.
+ * gb_fma_peak  measured FMA throughput (TFLOP/s, 2 flops per FMA) of this
+ *              device in fp64 (precision 0) or fp32 (1): a dependent-chain-
+ *              free DFMA / FFMA loop over every SM, timed with CUDA events. */
+int gb_hvp_info(gb_graph* g, int32_t* path, double* kernel_bytes, double* algorithmic_bytes, double* algorithmic_flops);
+int gb_fma_peak(int32_t device, int32_t precision, double* tflops);
 /* gb_iteration_kernels  number of kernel launches one LM iteration replays
  *              (kernel nodes of the captured per-iteration CUDA graph, between
  *              gb_begin and gb_end; 0 when the iteration is not captured). */

@@ -111,7 +111,7 @@ EXPORTED = [
     "gb_set_points", "gb_set_observations", "gb_set_differentiation_mode", "gb_optimize", "gb_mse",
     "gb_total_error", "gb_ls_linearize", "gb_ls_hvp", "gb_ls_preconditioner", "gb_ls_solve_step",
     "gb_ls_jacobians", "gb_incidence", "gb_synthetic_bal", "gb_begin", "gb_step", "gb_end", "gb_stream",
-    "gb_time_hvp", "gb_hvp_bytes", "gb_iteration_kernels", "gb_host_alloc", "gb_host_free", "gb_host_copy", "gb_nccl_unique_id", "gb_set_distributed", "gb_shm_allreduce_selftest", "gb_shard_plan", "gb_activation_selfcheck",
+    "gb_time_hvp", "gb_hvp_bytes", "gb_hvp_info", "gb_fma_peak", "gb_iteration_kernels", "gb_host_alloc", "gb_host_free", "gb_host_copy", "gb_nccl_unique_id", "gb_set_distributed", "gb_shm_allreduce_selftest", "gb_shard_plan", "gb_activation_selfcheck",
     "gb_set_linear_solver", "gb_report_json", "gb_report_csv",
     "gbg_last_error", "gbg_circle_solve", "gbg_vi_solve",  # generic path, include/gb_generic.h
 ]
@@ -155,6 +155,8 @@ def declare(lib: ctypes.CDLL, prefix: str = "gb_") -> ctypes.CDLL:
         f("stream", vp, vp)
         f("time_hvp", c_int, vp, c_int32, POINTER(c_double), POINTER(c_double))
         f("hvp_bytes", c_int, vp, POINTER(c_double), POINTER(c_double))
+        f("hvp_info", c_int, vp, POINTER(c_int32), POINTER(c_double), POINTER(c_double), POINTER(c_double))
+        f("fma_peak", c_int, c_int32, c_int32, POINTER(c_double))
         f("iteration_kernels", c_int, vp, POINTER(c_int32))
         f("host_alloc", vp, c_uint64)
         f("host_free", None, vp)

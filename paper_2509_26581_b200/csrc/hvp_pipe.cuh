@@ -50,7 +50,7 @@ __host__ __device__ constexpr uint32_t pipe_jstride() {
 // run lc = segments [rseg[lc], rseg[lc + 1])
 constexpr int kSegSlots = 128;
 struct AuxSec {
-  uint32_t lcam, lpt, psl, pso, cf, seg, rseg, bytes;
+  uint32_t lcam, lpt, psl, pso, cf, seg, rseg, tcam, pos, bytes;
 };
 __host__ __device__ inline AuxSec aux_sections(uint32_t ne, uint32_t npt) {
   const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad;
@@ -62,7 +62,9 @@ __host__ __device__ inline AuxSec aux_sections(uint32_t ne, uint32_t npt) {
   a.cf = a.pso + r16(2ull * (npt + 1));
   a.seg = a.cf + r16(3ull * npt);
   a.rseg = a.seg + r16(2ull * kSegSlots);
-  a.bytes = a.rseg + r16(2ull * (kTileCams + 1));
+  a.tcam = a.rseg + r16(2ull * (kTileCams + 1));  // the tile's cameras (global index), recompute HVP loader
+  a.pos = a.tcam + r16(4ull * kTileCams);          // edge -> its position in the point-slot order (psl inverse)
+  a.bytes = a.pos + r16(2ull * ne8);
   return a;
 }
 struct LinSec {
@@ -535,7 +537,12 @@ __global__ void k_tile_aux(Dev<FP, SP> d) {
     lcam[k] = d.d_lcam[eb + k];
     lpt[k] = d.d_lpt[eb + k];
   }
-  for (uint32_t k = threadIdx.x; k < ne; k += blockDim.x) psl[k] = d.pt_slots[q0 + k];
+  uint16_t* pos = reinterpret_cast<uint16_t*>(a + as.pos);
+  for (uint32_t k = threadIdx.x; k < ne; k += blockDim.x) {
+    const uint16_t e = d.pt_slots[q0 + k];
+    psl[k] = e;
+    pos[e] = static_cast<uint16_t>(k);
+  }
   for (uint32_t k = threadIdx.x; k <= npt; k += blockDim.x) pso[k] = static_cast<uint16_t>(d.pt_slot_off[pb + k] - q0);
   // camera-run slot spans: run r of chunk q (slot chunk_part_base[ch0 + q] + r)
   // covers tile edges [lo, hi), cut at chunk ends like the HVP tile kernels'
@@ -565,6 +572,10 @@ __global__ void k_tile_aux(Dev<FP, SP> d) {
   // kSegSlots segments (each camera run is cut into ceil(len / K) pieces)
   __shared__ uint16_t run_lo[kTileCams + 1];
   const uint32_t ncam = m[kMNcam];
+  {
+    uint32_t* tcam = reinterpret_cast<uint32_t*>(a + as.tcam);
+    for (uint32_t k = threadIdx.x; k < ncam; k += blockDim.x) tcam[k] = d.tile_cams[m[kMCb] + k];
+  }
   for (uint32_t k = threadIdx.x; k < ne; k += blockDim.x) {
     const uint32_t lc = d.d_lcam[eb + k];
     if (k == 0 || d.d_lcam[eb + k - 1] != lc) run_lo[lc] = static_cast<uint16_t>(k);

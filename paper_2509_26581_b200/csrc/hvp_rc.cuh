@@ -286,15 +286,15 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
   uint64_t* full = reinterpret_cast<uint64_t*>(rc_smem + L.bars);
   uint64_t* empty = full + kRcSlots;
   uint64_t* ready = empty + kRcSlots;
-  uint64_t* alloc = ready + kRcSlots;  // producer -> loader: the tile's region and header are set
+  uint64_t* blob = ready + kRcSlots;  // the tile blob's bulk copy (producer) has landed
   unsigned char* ring = rc_smem + L.ring;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < kRcSlots; ++s) {
-      mbar_init(&full[s], 1 + 32);  // producer lane 0 (bulk tx) + every loader lane's cp.async group
+      mbar_init(&full[s], 32);  // every loader lane's cp.async group (p, z, camera records)
       mbar_init(&empty[s], kRcGroupThreads / 32);  // the owning group's warps
       mbar_init(&ready[s], 32);
-      mbar_init(&alloc[s], 1);
+      mbar_init(&blob[s], 1);  // producer lane 0: arrive + bulk tx
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
         const FP* scam = reinterpret_cast<const FP*>(lin + ls.cam);
         const FP* stc = reinterpret_cast<const FP*>(rg + h[kROTc]);
         const FP* sw = reinterpret_cast<const FP*>(lin + ls.w);
+        const uint16_t* spos = reinterpret_cast<const uint16_t*>(aux + as.pos);
         RcCam<FP> C;
         rc_load_cam<FP>(scam, stc, slc[e0], C);
         FP acc[kRcVals];
@@ -356,10 +357,11 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
           const RcEdge<FP> ob = rc_edge<FP, HUBER>(C, Xb, Vb, wb, true);
           rc_accumulate<FP>(oa, Xa, acc);
           rc_accumulate<FP>(ob, Xb, acc);
+          const uint32_t pa = spos[ea], pbb = spos[eb];  // point-slot order: each point's contributions contiguous
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
-            gp[q * kRcGpStr + ea] = oa.g[q];
-            gp[q * kRcGpStr + eb] = ob.g[q];
+            gp[q * kRcGpStr + pa] = oa.g[q];
+            gp[q * kRcGpStr + pbb] = ob.g[q];
           }
         }
         if (k < cnt) {  // odd tail
@@ -369,8 +371,9 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
           const FP wa = HUBER ? sw[ea] : FP(1);
           const RcEdge<FP> oa = rc_edge<FP, HUBER>(C, Xa, Va, wa, true);
           rc_accumulate<FP>(oa, Xa, acc);
+          const uint32_t pa = spos[ea];
 #pragma unroll
-          for (int q = 0; q < 3; ++q) gp[q * kRcGpStr + ea] = oa.g[q];
+          for (int q = 0; q < 3; ++q) gp[q * kRcGpStr + pa] = oa.g[q];
         }
 #pragma unroll
         for (int v = 0; v < kRcVals; ++v) sA[v * kRcAStr + gt] = acc[v];
@@ -396,7 +399,6 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
         d.part15[static_cast<uint64_t>(kRcRec) * (cb + lc) + v] = (a0 + a1) + (a2 + a3);
       }
       // ---- points: thread = point
-      const uint16_t* spsl = reinterpret_cast<const uint16_t*>(aux + as.psl);
       const uint16_t* spso = reinterpret_cast<const uint16_t*>(aux + as.pso);
       const uint8_t* scf = aux + as.cf;
       const FP* sD = reinterpret_cast<const FP*>(lin + ls.D);
@@ -405,11 +407,9 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
       FP dot = FP(0);
       for (uint32_t pi = gt; pi < npt && !(L.dbg & 2); pi += kRcGroupThreads) {
         FP a[3] = {FP(0), FP(0), FP(0)};
-        for (uint32_t q = spso[pi]; q < spso[pi + 1]; ++q) {
-          const uint32_t sl = spsl[q];
+        for (uint32_t q = spso[pi]; q < spso[pi + 1]; ++q)  // contiguous: the edges wrote in slot order
 #pragma unroll
-          for (int k = 0; k < 3; ++k) a[k] += gp[k * kRcGpStr + sl];
-        }
+          for (int k = 0; k < 3; ++k) a[k] += gp[k * kRcGpStr + q];
         const uint64_t col = pcol0 + 3ull * (pb + pi);
         const bool freev = scf[3 * pi];
 #pragma unroll
@@ -528,16 +528,10 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
           hh[kROZ] = o_z;
           hh[kROTc] = o_tc;
           // the tile's static + per-linearization blob: one bulk copy (contiguous, o_lin == o_aux + as.bytes)
-          if (L.dbg & 16) {  // experiments: no bulk copy
-            mbar_arrive(&full[s]);
-          } else {
-            mbar_arrive_expect_tx(&full[s], as.bytes + ls.bytes);
-            bulk_g2s(rg + o_aux, d.tile_aux + 16 * aux16, as.bytes + ls.bytes, &full[s]);
-          }
+          mbar_arrive_expect_tx(&blob[s], as.bytes + ls.bytes);
+          bulk_g2s(rg + o_aux, d.tile_aux + 16 * aux16, as.bytes + ls.bytes, &blob[s]);
         }
         (void)lin16;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&alloc[s]);  // the loader copies p, z and the camera records
         if (pf) {
           const long long tp2 = clock64();
           t_ring += tp1 - tp0;
@@ -559,15 +553,19 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
     // stream faster through the LSU than as extra bulk copies)
     for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i) {
       const int s = static_cast<int>(i % kRcSlots);
-      mbar_sleep_wait(&alloc[s], (i / kRcSlots) & 1u);
+      mbar_sleep_wait(&blob[s], (i / kRcSlots) & 1u);  // header and blob (camera ids) are in place
       unsigned char* rg = ring + slot_off[s];
       const uint32_t* h = reinterpret_cast<const uint32_t*>(rg);
-      const uint32_t npt = h[kRNpt], ncam = h[kRNcam], pb = h[kRPb], cb = h[kRCb];
-      const uint32_t np16 = (h[kROZ] - h[kROP]) / 16, nz16 = dir ? np16 : 0u, nt16 = sizeof(FP) * kRcRec * ncam / 16;
+      const uint32_t ne = h[kRNe], npt = h[kRNpt], ncam = h[kRNcam], pb = h[kRPb];
+      const uint32_t np16 = (h[kROZ] - h[kROP]) / 16, nz16 = dir ? np16 : 0u;
+      constexpr uint32_t kRec16 = sizeof(FP) * kRcRec / 16;  // 16-byte chunks of one camera record
+      const uint32_t nt16 = kRec16 * ncam;
       const char* psrc = reinterpret_cast<const char*>(d.p + pcol0 + 3ull * pb) - h[kRDp];
       const char* zsrc = reinterpret_cast<const char*>(d.z + pcol0 + 3ull * pb) - h[kRDz];
-      const char* tsrc = reinterpret_cast<const char*>(d.tcrec + static_cast<uint64_t>(kRcRec) * cb);
-      (void)npt;
+      const char* csrc = reinterpret_cast<const char*>(d.crec);
+      // the tile's camera ids, from the aux blob once it has landed (the
+      // producer's bulk copy): gathered straight from the per-camera records
+      const uint32_t* tcam = reinterpret_cast<const uint32_t*>(rg + h[kROAux] + aux_sections(ne, npt).tcam);
       if (!(L.dbg & 32)) {
         for (uint32_t c = lane; c < np16; c += 32)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(rg + h[kROP] + 16 * c)),
@@ -577,7 +575,8 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
                        "l"(zsrc + 16 * c) : "memory");
         for (uint32_t c = lane; c < nt16; c += 32)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(rg + h[kROTc] + 16 * c)),
-                       "l"(tsrc + 16 * c) : "memory");
+                       "l"(csrc + sizeof(FP) * kRcRec * static_cast<uint64_t>(tcam[c / kRec16]) + 16 * (c % kRec16))
+                       : "memory");
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&full[s])) : "memory");
     }
@@ -592,6 +591,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
     for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i) {
       const int s = static_cast<int>(i % kRcSlots);
       mbar_wait_t(&full[s], (i / kRcSlots) & 1u, pf, w_full);
+      mbar_sleep_wait(&blob[s], (i / kRcSlots) & 1u);
       unsigned char* rg = ring + slot_off[s];
       const uint32_t* h = reinterpret_cast<const uint32_t*>(rg);
       const uint32_t npt = h[kRNpt];
@@ -682,25 +682,29 @@ __global__ void k_rc_cams_pre(Dev<FP, SP> d, int dir, const uint64_t* rbeg, cons
       }
 }
 
-// per-tile copies of the camera records (tcrec[g] = crec[tile_cams[g]])
-template <typename FP, typename SP>
-__global__ void k_rc_tcams(Dev<FP, SP> d) {
-  if (!d.st->iter_active || d.st->pcg_done) return;
-  const uint64_t n = static_cast<uint64_t>(kRcRec / 2) * d.ntcams;
-  using V2 = typename std::conditional<sizeof(FP) == 8, double2, float2>::type;
-  const V2* src = reinterpret_cast<const V2*>(d.crec);
-  V2* dst = reinterpret_cast<V2*>(d.tcrec);
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t g = i / (kRcRec / 2), k = i % (kRcRec / 2);
-    dst[i] = src[static_cast<uint64_t>(kRcRec / 2) * d.tile_cams[g] + k];
+// Camera side of the recompute HVP + p.Ap (pcg.hpp:332-340): a warp per
+// camera sums the 15-value partials of its tile copies (fixed order, a
+// transposing butterfly: lane l ends with value l / 2), adds the heavy tiles'
+// 9-value partial slots, and contracts S with T_k = Dw(e_k) in closed form:
+//   (sum_k,i T_k(i, j) S(k, i)) = w_j (-s tr S + s1 w.sigma + c2 w^T S w)
+//                                 + s sigma_j + c ((S w)_j + (S^T w)_j),
+// sigma = (S12 - S21, S20 - S02, S01 - S10), the chain coefficients s, c, s1,
+// c2 of snavely.hpp:103-121. Phases as k_hvp_cams (0 fused, 1 per-rank sums
+// -> red, 2 from red).
+template <typename FP>
+__device__ __forceinline__ void rc_butterfly16(FP (&v)[16], int lane) {
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) {  // xor 2o: keep half, send half
+    const bool hi = lane & (2 * o);
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const FP keep = hi ? v[i + o] : v[i], send = hi ? v[i] : v[i + o];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * o);
+    }
   }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);  // lane l: value l >> 1
 }
 
-// Camera side of the recompute HVP + p.Ap (pcg.hpp:332-340): a warp per
-// camera sums the 15-value partials of its tile copies (fixed order), adds
-// the heavy tiles' 9-value partial slots, contracts S with T_k = Dw(e_k).
-// Phases as k_hvp_cams (0 fused, 1 per-rank sums -> red, 2 from red).
 template <typename FP, typename SP>
 __global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams_rc(Dev<FP, SP> d, int phase) {
   if (!d.st->iter_active || d.st->pcg_done) return;
@@ -711,39 +715,40 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams_rc(Dev<FP, SP> d, i
   if (c < d.nc) {
     FP out = FP(0);  // lane k < 9: value k of J_c^T q summed over the camera's edges
     if (phase != 2) {
-      FP acc[kRcVals];
+      FP acc[16];
 #pragma unroll
-      for (int v = 0; v < kRcVals; ++v) acc[v] = FP(0);
+      for (int v = 0; v < 16; ++v) acc[v] = FP(0);
       for (uint32_t q = d.cam_tc_off[c] + lane; q < d.cam_tc_off[c + 1]; q += 32) {
         const FP* src = d.part15 + static_cast<uint64_t>(kRcRec) * d.cam_tc_idx[q];
 #pragma unroll
         for (int v = 0; v < kRcVals; ++v) acc[v] += src[v];
       }
+      rc_butterfly16<FP>(acc, lane);
+      FP S[kRcVals];
 #pragma unroll
-      for (int v = 0; v < kRcVals; ++v) acc[v] = warp_sum(acc[v]);
-      FP cam[9], pre[8];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) cam[k] = d.x[9ull * c + k];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) pre[k] = d.cpre[static_cast<uint64_t>(kCamPre) * c + k];
-      FP T[3][9];
-      rot_basis<FP>(cam, pre, T);
-      FP o9[9];
+      for (int v = 0; v < kRcVals; ++v) S[v] = __shfl_sync(0xffffffffu, acc[0], 2 * v);
+      const FP w0 = d.x[9ull * c], w1 = d.x[9ull * c + 1], w2 = d.x[9ull * c + 2], f = d.x[9ull * c + 6];
+      const FP* pre = d.cpre + static_cast<uint64_t>(kCamPre) * c;
+      const FP s = pre[4], cc = pre[5], s1 = pre[6], c2 = pre[7];
+      const FP w[3] = {w0, w1, w2};
+      const FP sig[3] = {S[5] - S[7], S[6] - S[2], S[1] - S[3]};  // S(k, i) at 3k + i
+      FP Sw[3], STw[3];
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        FP sj = FP(0);
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-#pragma unroll
-          for (int i = 0; i < 3; ++i) sj += T[k][3 * i + j] * acc[3 * k + i];
-        o9[j] = sj;
+        Sw[j] = S[3 * j] * w0 + S[3 * j + 1] * w1 + S[3 * j + 2] * w2;
+        STw[j] = S[j] * w0 + S[3 + j] * w1 + S[6 + j] * w2;
       }
-      o9[3] = acc[9];
-      o9[4] = acc[10];
-      o9[5] = acc[11];
-      o9[6] = acc[12];
-      o9[7] = cam[6] * acc[13];
-      o9[8] = cam[6] * acc[14];
+      const FP wSw = w0 * Sw[0] + w1 * Sw[1] + w2 * Sw[2];
+      const FP sc = -s * (S[0] + S[4] + S[8]) + s1 * (w0 * sig[0] + w1 * sig[1] + w2 * sig[2]) + c2 * wSw;
+      FP o9[9];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) o9[j] = w[j] * sc + s * sig[j] + cc * (Sw[j] + STw[j]);
+      o9[3] = S[9];
+      o9[4] = S[10];
+      o9[5] = S[11];
+      o9[6] = S[12];
+      o9[7] = f * S[13];
+      o9[8] = f * S[14];
       if (d.n_heavy) {  // heavy tiles: 9-value partial slots (k_hvp_tiles), flagged in camera-major order
         FP hv[9];
 #pragma unroll

@@ -112,10 +112,9 @@ struct Dev {
   unsigned char* tile_lin;    // per-linearization per-tile blobs (LinSec)
   const uint32_t* cam_tc_off;  // [nc+1] camera -> its tile-camera entries (tcv rows)
   const uint32_t* cam_tc_idx;
-  // recompute HVP (hvp_rc.cuh): per-camera HVP records, their per-tile copies,
-  // per tile-camera 15-value partials, heavy-tile partial-slot flags
+  // recompute HVP (hvp_rc.cuh): per-camera HVP records, per tile-camera
+  // 15-value partials, heavy-tile partial-slot flags
   FP* crec;              // [nc][16]
-  FP* tcrec;             // [ntcams][16]
   FP* part15;            // [ntcams][16]
   const uint8_t* hflag;  // [nparts] camera-major storage order
   FP* w;            // [na] or null (default loss: w == 1)

@@ -80,6 +80,7 @@ class SolverBase {
   virtual void* stream() = 0;
   virtual void time_hvp(int reps, double* ms_pair, double* ms_tiles) = 0;
   virtual void hvp_bytes(double* kernel_bytes, double* reference_bytes) = 0;
+  virtual void hvp_info(int32_t* path, double* algorithmic_bytes, double* algorithmic_flops) = 0;
   virtual int iteration_kernels() const = 0;  // kernel nodes of one captured LM iteration (0: not captured)
   virtual double residual_sum(int level, bool raw) = 0;
   virtual void ls_linearize(int level, double cmin, double cmax, int damping, double* chi2, int64_t* n, void* b,
@@ -330,12 +331,14 @@ class Solver final : public SolverBase {
   ~Solver() override {
     cudaSetDevice(g_.device);  // this handle's streams, events and blocks live there
     if (rc_.prof) {  // GB_RC_DBG & 8: per-role mbarrier wait cycles of k_hvp_rc (summed over CTAs and launches)
-      unsigned long long h[8] = {};
+      unsigned long long h[16] = {};
       if (cudaMemcpy(h, rc_.prof, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess)
         std::fprintf(stderr,
                      "[rc prof] per-warp busy fractions: consumer wait ready %.3f | producer wait empty %.3f, "
                      "ring+setup %.3f, issue %.3f | preparer wait full %.3f\n",
                      double(h[0]) / h[7], 8.0 * h[2] / h[7], 8.0 * h[4] / h[7], 8.0 * h[5] / h[7], 8.0 * h[3] / h[7]);
+      std::fprintf(stderr, "[rc prof] consumer wait work buffer %.3f | epilogue wait work %.3f\n",
+                   double(h[1]) / h[7], 8.0 / 5.0 * h[6] / h[7]);
     }
     for (auto& e : ev_) cudaEventDestroy(e);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
@@ -553,7 +556,7 @@ class Solver final : public SolverBase {
         lin += rc_lin_sections<FP>(ne, npt, ncam, d.w != nullptr).bytes;
       }
       b += aux + lin + np3 * 2 * sV + np3 * 2 * sV;              // blobs (incl. X); p, z in; ap, p out
-      b += d.ntcams * (kRcRec * sF * 4.0 + 8.0);                 // tile records (write, read), partials (write, read)
+      b += d.ntcams * (kRcRec * sF * 3.0 + 8.0);                 // camera record gathers, partials (write, read)
       b += act_.nc * kRcRec * sF * 2 + nc9 * (sF + sF + 2 * sV);  // camera records; x, cpre, p, z
       b += nc9 * (sV + sF + sV);                                 // camera p, D in; ap out
       if (kernel_bytes) *kernel_bytes = b;
@@ -580,6 +583,18 @@ class Solver final : public SolverBase {
     b += nparts * 9 * sF * 2 + nparts * 4;             // camera partial slots: write, read (+ index)
     b += nc9 * (sV + sF + sV);                         // camera p, D in; ap out
     if (kernel_bytes) *kernel_bytes = b;
+  }
+
+  void hvp_info(int32_t* path, double* algorithmic_bytes, double* algorithmic_flops) override {
+    if (!have_act_) throw std::logic_error("gb_hvp_info before any solve");
+    const double E = static_cast<double>(act_.n_active), N = static_cast<double>(act_.free_dims);
+    const double sJ = sizeof(SP), sV = sizeof(SP), sA = sizeof(A), sF = sizeof(FP);
+    const bool recompute = rc_ok_ || !dev_.J;
+    if (path) *path = rc_ok_ ? 3 : (!dev_.J ? 0 : (pipe_ok_ ? 2 : 1));
+    if (algorithmic_bytes)
+      *algorithmic_bytes = recompute ? E * (2 * sF + 8) + static_cast<double>(ncols_) * sF + N * (sV + sA)
+                                     : E * (24 * sJ + 8) + N * (sV + sA);
+    if (algorithmic_flops) *algorithmic_flops = recompute ? E * 500.0 : 0.0;
   }
 
   int iteration_kernels() const override { return graph_exec_ ? graph_kernels_ : 0; }
@@ -1250,8 +1265,8 @@ class Solver final : public SolverBase {
       if (const char* e = std::getenv("GB_RC_DBG")) rc_.dbg = std::atoi(e);
       rc_.prof = nullptr;
       if (rc_.dbg & 8) {
-        rc_.prof = static_cast<unsigned long long*>(b_rcprof_.alloc(8 * sizeof(unsigned long long)));
-        CK(cudaMemsetAsync(rc_.prof, 0, 8 * sizeof(unsigned long long), s_));
+        rc_.prof = static_cast<unsigned long long*>(b_rcprof_.alloc(16 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(rc_.prof, 0, 16 * sizeof(unsigned long long), s_));
       }
     }
     const bool dyn = g_.diff_mode == GB_DYNAMIC || rc_ok_;
@@ -1282,7 +1297,7 @@ class Solver final : public SolverBase {
       d.slot_span = nullptr;
       d.tile_lin = nullptr;
       d.ntcams = act_.tile_cam_off.empty() ? 0 : act_.tile_cam_off.back();
-      d.crec = d.tcrec = d.part15 = nullptr;
+      d.crec = d.part15 = nullptr;
       d.hflag = nullptr;
       if (pipe_ok_ || rc_ok_) {
         if (pipe_ok_)
@@ -1330,10 +1345,8 @@ class Solver final : public SolverBase {
         } else {
           const uint64_t nt = std::max<uint64_t>(1, d.ntcams);
           d.crec = static_cast<FP*>(b_crec_.alloc(std::max<uint64_t>(1, nc) * kRcRec * sizeof(FP)));
-          d.tcrec = static_cast<FP*>(b_tcrec_.alloc(nt * kRcRec * sizeof(FP)));
           d.part15 = static_cast<FP*>(b_part15_.alloc(nt * kRcRec * sizeof(FP)));
           CK(cudaMemsetAsync(d.part15, 0, nt * kRcRec * sizeof(FP), s_));  // heavy tiles' entries stay 0
-          CK(cudaMemsetAsync(d.tcrec, 0, nt * kRcRec * sizeof(FP), s_));
           uint8_t* hf = static_cast<uint8_t*>(b_hflag_.alloc(std::max<uint64_t>(1, act_.nparts)));
           CK(cudaMemsetAsync(hf, 0, std::max<uint64_t>(1, act_.nparts), s_));
           d.hflag = hf;
@@ -1623,12 +1636,11 @@ class Solver final : public SolverBase {
     CK(cudaGetLastError());
   }
 
-  // recompute HVP (hvp_rc.cuh): camera records (+ direction update), their
-  // per-tile copies, the tile pipeline, heavy tiles with the dynamic tile kernel
+  // recompute HVP (hvp_rc.cuh): camera records (+ direction update), the tile
+  // pipeline (which gathers them per tile), heavy tiles with the dynamic tile kernel
   void launch_hvp_rc(const Dev<FP, SP>& d, bool dir) {
     k_rc_cams_pre<FP, SP><<<std::max(1u, div_up(act_.nc, 128)), 128, 0, s_>>>(d, dir ? 1 : 0, dir_rbeg_, dir_rend_,
                                                                               dir_nranges_);
-    k_rc_tcams<FP, SP><<<grid_for(uint64_t(kRcRec / 2) * d.ntcams), 256, 0, s_>>>(d);
     const uint32_t grid = std::min<uint32_t>(d.n_normal, sms_);
     if (d.w)
       k_hvp_rc<FP, SP, true><<<grid, kRcThreadsWS, rc_.total_bytes, s_>>>(d, rc_);
@@ -1860,7 +1872,7 @@ class Solver final : public SolverBase {
   static constexpr bool kRcCapable = std::is_same<SP, FP>::value;
   RcLayout rc_{};
   bool rc_ok_ = false;  // recompute HVP (hvp_rc.cuh): no J store
-  DBuf b_crec_, b_tcrec_, b_part15_, b_hflag_, b_rcprof_;
+  DBuf b_crec_, b_part15_, b_hflag_, b_rcprof_;
   uint32_t sms_ = 148;
   unsigned pt_occ_ = 4;
   unsigned chi2_occ_ = 4;
@@ -1928,6 +1940,25 @@ struct gb_graph {
     return *solver;
   }
 };
+
+namespace gb {
+// FMA throughput probe: 8 independent accumulator chains per thread, 2 blocks
+// of 256 threads per SM, every SM busy.
+template <typename T>
+__global__ void k_fma_probe(T* out, int iters, T a, T b) {
+  T x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = static_cast<T>(threadIdx.x + k);
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  T s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == static_cast<T>(-1.2345)) out[0] = s;  // keeps the chains alive
+}
+
+}  // namespace gb
 
 extern "C" {
 
@@ -2077,6 +2108,44 @@ int gb_iteration_kernels(gb_graph* g, int32_t* kernels) {
 
 int gb_hvp_bytes(gb_graph* g, double* kernel_bytes, double* reference_bytes) {
   return guarded([&] { g->get().hvp_bytes(kernel_bytes, reference_bytes); });
+}
+
+int gb_hvp_info(gb_graph* g, int32_t* path, double* kernel_bytes, double* algorithmic_bytes,
+                double* algorithmic_flops) {
+  return guarded([&] {
+    g->get().hvp_bytes(kernel_bytes, nullptr);
+    g->get().hvp_info(path, algorithmic_bytes, algorithmic_flops);
+  });
+}
+
+int gb_fma_peak(int32_t device, int32_t precision, double* tflops) {
+  using namespace gb;
+  return guarded([&] {
+    CK(cudaSetDevice(device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    DBuf o;
+    void* out = o.alloc(16);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int iters = 4096, blocks = 2 * sms, threads = 256;
+    float ms = 0;
+    for (int rep = 0; rep < 3; ++rep) {  // first pass warms the clocks
+      CK(cudaEventRecord(e0));
+      if (precision == 0)
+        gb::k_fma_probe<double><<<blocks, threads>>>(static_cast<double*>(out), iters, 0.999999, 1e-7);
+      else
+        gb::k_fma_probe<float><<<blocks, threads>>>(static_cast<float*>(out), iters, 0.999999f, 1e-7f);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads;
+    if (tflops) *tflops = flops / (ms * 1e-3) / 1e12;
+  });
 }
 
 void* gb_host_alloc(uint64_t bytes) { return gb::HostCache::get().alloc(static_cast<size_t>(bytes)); }
