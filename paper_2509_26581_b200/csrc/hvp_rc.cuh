@@ -706,7 +706,7 @@ __device__ __forceinline__ void rc_butterfly16(FP (&v)[16], int lane) {
 }
 
 template <typename FP, typename SP>
-__global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams_rc(Dev<FP, SP> d, int phase) {
+__global__ void __launch_bounds__(32 * kCamWarps, 4) k_hvp_cams_rc(Dev<FP, SP> d, int phase) {
   if (!d.st->iter_active || d.st->pcg_done) return;
   __shared__ FP scratch[32];
   const int lane = threadIdx.x & 31;
@@ -718,10 +718,38 @@ __global__ void __launch_bounds__(32 * kCamWarps) k_hvp_cams_rc(Dev<FP, SP> d, i
       FP acc[16];
 #pragma unroll
       for (int v = 0; v < 16; ++v) acc[v] = FP(0);
-      for (uint32_t q = d.cam_tc_off[c] + lane; q < d.cam_tc_off[c + 1]; q += 32) {
-        const FP* src = d.part15 + static_cast<uint64_t>(kRcRec) * d.cam_tc_idx[q];
+      const uint32_t q1 = d.cam_tc_off[c + 1];
+      for (uint32_t q = d.cam_tc_off[c] + lane; q < q1; q += 64) {  // two rows per lane in flight
+        const bool two = q + 32 < q1;
+        const uint32_t ia = d.cam_tc_idx[q], ib = two ? d.cam_tc_idx[q + 32] : ia;
+        const double2* ra = reinterpret_cast<const double2*>(d.part15 + static_cast<uint64_t>(kRcRec) * ia);
+        const double2* rb = reinterpret_cast<const double2*>(d.part15 + static_cast<uint64_t>(kRcRec) * ib);
+        if constexpr (sizeof(FP) == 8) {
+          double2 va[8], vb[8];
 #pragma unroll
-        for (int v = 0; v < kRcVals; ++v) acc[v] += src[v];
+          for (int k = 0; k < 8; ++k) {
+            va[k] = ra[k];
+            vb[k] = two ? rb[k] : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            acc[2 * k] += va[k].x;
+            acc[2 * k + 1] += va[k].y;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            acc[2 * k] += vb[k].x;
+            acc[2 * k + 1] += vb[k].y;
+          }
+        } else {
+          const FP* sa = d.part15 + static_cast<uint64_t>(kRcRec) * ia;
+          const FP* sb = d.part15 + static_cast<uint64_t>(kRcRec) * ib;
+#pragma unroll
+          for (int v = 0; v < kRcVals; ++v) acc[v] += sa[v];
+          if (two)
+#pragma unroll
+            for (int v = 0; v < kRcVals; ++v) acc[v] += sb[v];
+        }
       }
       rc_butterfly16<FP>(acc, lane);
       FP S[kRcVals];
