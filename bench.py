@@ -341,9 +341,27 @@ def cpu_baseline(args, problem):
         return {"value": round(ms, 2), "unit": UNIT, "cores": cores, "kind": "reference",
                 "sample": f"LM iteration 2 (after 1 warm-up), full workload, workers={cores} "
                           f"(reference solve incl. activation {rep.total_seconds:.1f} s)",
-                "host": host_info()}
+                "host": host_info(), "workers_scaling": reference_worker_scaling(args, cores)}
     except Exception as e:  # the baseline is reported, never the thing measured
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+
+def reference_worker_scaling(args, cores):
+    """The reference's own thread scaling (graph.hpp:50 set_workers) on a
+    bounded sample: the Dubrovnik-356 shape, LM iteration 2 at workers=1 and
+    workers=all (~10 s of host work)."""
+    from oracle import refbind
+    from paper_2509_26581_b200 import bal
+
+    nc, np_, ne, desc = WORKLOADS["dubrovnik"]
+    problem = load_problem(nc, np_, ne)
+    out = {"workload": desc + f" {args.precision} {args.mode}", "sample": "LM iteration 2 (after 1 warm-up)"}
+    for w in (1, cores):
+        r = refbind.build_graph(problem, args.precision, args.mode, workers=w)
+        rep = bal.levenberg_marquardt(r, timed_config(bal, 2))
+        out[f"ms_workers_{w}"] = round(1e3 * rep.iterations[1].wall_seconds, 2)
+    out["speedup"] = round(out["ms_workers_1"] / out[f"ms_workers_{cores}"], 2)
+    return out
 
 
 # ------------------------------------------------------------- device arm
