@@ -3,7 +3,9 @@
 // linear_system.hpp:104-115; hvp_forward factor_descriptor.hpp:372-407,
 // hvp_scatter :409-433, evaluated like the low-memory path :673-684).
 //
-// Analytic mode with SP == FP (fp64, fp32; stored or dynamic J). The stored
+// Analytic mode with SP == FP (fp64, fp32) and dynamic mode in any precision
+// (J at FP, cast to Arith, factor_descriptor.hpp:673-684; for fp32-bf16 only
+// the PCG vectors are bf16, widened on load and narrowed on store). The stored
 // operator J = [U·Dw | U | dist p, f n p, f n^2 p ; U R] (snavely.hpp:103-153)
 // is applied in its factored form, with every per-camera product hoisted out
 // of the edge loop:
@@ -94,7 +96,7 @@ inline RcLayout rc_layout(bool huber, uint32_t smem_budget) {
   L.work_bytes = o;
   L.max_region = kRcHdrBytes + aux_sections(kTileEdges, kTilePoints).bytes +
                  rc_lin_sections<FP>(kTileEdges, kTilePoints, kTileCams, huber).bytes +
-                 2 * r16(kTilePoints * 3 * sizeof(FP) + 16) + kTileCams * kRcRec * sizeof(FP);
+                 3 * r16(kTilePoints * 3 * sizeof(FP) + 16) + kTileCams * kRcRec * sizeof(FP) + 128;
   L.slots = kRcGroups * L.work_bytes;
   L.bars = L.slots + 4 * kRcSlots;
   L.ring = L.bars + 4 * kRcSlots * 8;
@@ -104,7 +106,7 @@ inline RcLayout rc_layout(bool huber, uint32_t smem_budget) {
   return L;
 }
 
-enum RcHdr : int { kRT = 0, kRNe, kRNpt, kRNcam, kRPb, kRCb, kRDp, kRDz, kROAux, kROLin, kROP, kROZ, kROTc, kRCount };
+enum RcHdr : int { kRT = 0, kRNe, kRNpt, kRNcam, kRPb, kRCb, kRDp, kRDz, kROAux, kROLin, kROP, kROZ, kROTc, kROV, kRCount };
 
 // mbar_wait that sleeps (suspend-time hint) instead of spinning, and adds its
 // waiting cycles to acc when profiling
@@ -279,7 +281,6 @@ constexpr int kRcThreadsWS = 384;
 
 template <typename FP, typename SP, bool HUBER>
 __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLayout L) {
-  static_assert(std::is_same<FP, SP>::value, "recompute HVP: SP == FP");
   if (!d.st->iter_active || d.st->pcg_done) return;
   extern __shared__ __align__(128) unsigned char rc_smem[];
   uint32_t* slot_off = reinterpret_cast<uint32_t*>(rc_smem + L.slots);
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
         const uint16_t* slc = reinterpret_cast<const uint16_t*>(aux + as.lcam);
         const uint16_t* slp = reinterpret_cast<const uint16_t*>(aux + as.lpt);
         const FP* sX = reinterpret_cast<const FP*>(lin + ls.X);
-        const FP* svp = reinterpret_cast<const FP*>(rg + h[kROZ] + h[kRDz]);
+        const FP* svp = reinterpret_cast<const FP*>(rg + h[kROV]);
         const FP* scam = reinterpret_cast<const FP*>(lin + ls.cam);
         const FP* stc = reinterpret_cast<const FP*>(rg + h[kROTc]);
         const FP* sw = reinterpret_cast<const FP*>(lin + ls.w);
@@ -418,10 +419,12 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
           const FP damp = before ? lam * Dk * Dk : lam;
           const SP pk = sp[3 * pi + k];
           if (dir) d.p[col + k] = pk;
-          const FP out = freev ? damp * pk + Dk * a[k] : FP(0);
-          d.ap[col + k] = out;
+          const FP pw = widen<FP>(pk);
+          const FP out = freev ? damp * pw + Dk * a[k] : FP(0);
+          const SP o = narrow<SP>(out);
+          d.ap[col + k] = o;
           if (d.dbg_out) d.dbg_out[col + k] = out;
-          dot += pk * out;
+          dot += pw * widen<FP>(o);
         }
       }
       dot = warp_sum(dot);
@@ -475,8 +478,9 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
         const Span s_z = span16(d.z + pcol0 + 3ull * pb, sizeof(SP) * 3ull * npt);
         const uint32_t tcb = static_cast<uint32_t>(sizeof(FP) * kRcRec * ncam);
         const uint32_t o_aux = kRcHdrBytes, o_lin = o_aux + as.bytes, o_p = o_lin + ls.bytes;
-        const uint32_t o_z = o_p + s_p.bytes, o_tc = o_z + s_z.bytes;  // z slot always: the preparer's v_p
-        const uint32_t sz = (o_tc + tcb + 127) / 128 * 128;
+        const uint32_t o_z = o_p + s_p.bytes, o_tc = o_z + s_z.bytes;
+        const uint32_t o_v = o_tc + tcb;  // the preparer's v_p = D p (FP)
+        const uint32_t sz = (o_v + r16(sizeof(FP) * 3ull * npt) + 127) / 128 * 128;
         // ---- room in the ring (warp-uniform bookkeeping)
         for (;;) {
           bool fits;
@@ -527,6 +531,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
           hh[kROP] = o_p;
           hh[kROZ] = o_z;
           hh[kROTc] = o_tc;
+          hh[kROV] = o_v;
           // the tile's static + per-linearization blob: one bulk copy (contiguous, o_lin == o_aux + as.bytes)
           mbar_arrive_expect_tx(&blob[s], as.bytes + ls.bytes);
           bulk_g2s(rg + o_aux, d.tile_aux + 16 * aux16, as.bytes + ls.bytes, &blob[s]);
@@ -596,7 +601,8 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
       const uint32_t* h = reinterpret_cast<const uint32_t*>(rg);
       const uint32_t npt = h[kRNpt];
       SP* pp = reinterpret_cast<SP*>(rg + h[kROP] + h[kRDp]);
-      FP* zz = reinterpret_cast<FP*>(rg + h[kROZ] + h[kRDz]);
+      const SP* zz = reinterpret_cast<const SP*>(rg + h[kROZ] + h[kRDz]);
+      FP* vv = reinterpret_cast<FP*>(rg + h[kROV]);
       const FP* DD = reinterpret_cast<const FP*>(rg + h[kROLin]);  // D at offset 0
       const uint32_t n3 = 3 * npt;
       constexpr int U = 4;
@@ -618,7 +624,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
           if (q < n3) {
             const SP pn = dir ? pcg_dir_value<FP, SP>(zv[u], pv[u], beta) : pv[u];
             pp[q] = pn;
-            zz[q] = dv[u] * pn;  // == vt (k_pcg_dir)
+            vv[q] = dv[u] * widen<FP>(pn);  // == vt (k_pcg_dir)
           }
         }
       }
@@ -647,10 +653,10 @@ __global__ void k_rc_cams_pre(Dev<FP, SP> d, int dir, const uint64_t* rbeg, cons
       if (dir) {
         const SP pi = pcg_dir_value<FP, SP>(d.z[col], d.p[col], beta);
         d.p[col] = pi;
-        v[k] = d.D[col] * pi;
-        d.vt[col] = v[k];
+        v[k] = d.D[col] * widen<FP>(pi);
+        d.vt[col] = static_cast<arith_t<SP>>(v[k]);
       } else {
-        v[k] = d.vt[col];
+        v[k] = static_cast<FP>(d.vt[col]);
       }
       cam[k] = d.x[col];
     }
@@ -678,7 +684,7 @@ __global__ void k_rc_cams_pre(Dev<FP, SP> d, int dir, const uint64_t* rbeg, cons
       for (uint64_t i = rbeg[r] + t0; i < rend[r]; i += stride) {
         const SP pi = pcg_dir_value<FP, SP>(d.z[i], d.p[i], beta);
         d.p[i] = pi;
-        d.vt[i] = d.D[i] * pi;
+        d.vt[i] = static_cast<arith_t<SP>>(d.D[i] * widen<FP>(pi));
       }
 }
 
@@ -802,11 +808,12 @@ __global__ void __launch_bounds__(32 * kCamWarps, 4) k_hvp_cams_rc(Dev<FP, SP> d
         const FP a = phase == 2 ? d.red[col] : out;
         const FP Dk = d.D[col];
         const FP damp = d.st->before_scaling ? d.st->lambda_solve * Dk * Dk : static_cast<FP>(d.st->lambda_solve);
-        const SP pk = d.p[col];
+        const FP pk = widen<FP>(d.p[col]);
         const FP o = freev ? damp * pk + Dk * a : FP(0);
-        d.ap[col] = o;
+        const SP os = narrow<SP>(o);
+        d.ap[col] = os;
         if (d.dbg_out) d.dbg_out[col] = o;
-        dot = pk * o;
+        dot = pk * widen<FP>(os);
       }
       dot = warp_sum(dot);
       if (lane == 0) mine = dot;

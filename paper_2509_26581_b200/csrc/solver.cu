@@ -1254,11 +1254,12 @@ class Solver final : public SolverBase {
     Dev<FP, SP>& d = dev_;
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g_.device));
-    // recompute HVP (hvp_rc.cuh): analytic / dynamic with SP == FP and
-    // the full-system PCG; no Jacobian store at all. GB_HVP_RC=0 keeps the stored J.
+    // recompute HVP (hvp_rc.cuh): analytic with SP == FP, or dynamic
+    // in any precision, with the full-system PCG; no Jacobian store at all.
+    // GB_HVP_RC=0 keeps the stored J (dynamic: the per-tile recompute kernel).
     rc_ok_ = false;
-    if (g_.diff_mode != GB_AUTO && std::is_same<SP, FP>::value && g_.linear_solver != GB_SOLVER_SCHUR &&
-        d.n_normal > 0) {
+    if (g_.diff_mode != GB_AUTO && (std::is_same<SP, FP>::value || g_.diff_mode == GB_DYNAMIC) &&
+        g_.linear_solver != GB_SOLVER_SCHUR && d.n_normal > 0) {
       rc_ = rc_layout<FP>(g_.loss_kind == GB_LOSS_HUBER, static_cast<uint32_t>(optin));
       rc_ok_ = rc_.ring_bytes >= 2 * rc_.max_region;
       if (const char* e = std::getenv("GB_HVP_RC")) rc_ok_ = rc_ok_ && std::atoi(e) != 0;
@@ -1869,7 +1870,7 @@ class Solver final : public SolverBase {
       b_pt_slot_off_, b_pt_slots_, b_cam_part_off_, b_cam_part_idx_;
   PipeLayout pipe_{};
   bool pipe_ok_ = false;
-  static constexpr bool kRcCapable = std::is_same<SP, FP>::value;
+  static constexpr bool kRcCapable = true;  // every precision (bf16 storage: dynamic mode only)
   RcLayout rc_{};
   bool rc_ok_ = false;  // recompute HVP (hvp_rc.cuh): no J store
   DBuf b_crec_, b_part15_, b_hflag_, b_rcprof_;

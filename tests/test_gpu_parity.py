@@ -136,7 +136,8 @@ def _pipe_vs_tiles(monkeypatch, p, precision, mode, huber):
 
 
 @pytest.mark.parametrize("precision,mode,huber,zipf", [("fp64", "analytic", None, None), ("fp64", "analytic", 2.0, 1.2),
-                                                      ("fp64", "dynamic", None, None), ("fp32", "analytic", 2.0, None)])
+                                                      ("fp64", "dynamic", None, None), ("fp32", "analytic", 2.0, None),
+                                                      ("fp32-bf16", "dynamic", None, None)])
 def test_recompute_hvp(gpu, monkeypatch, precision, mode, huber, zipf):
     """The recompute HVP (hvp_rc.cuh: no Jacobian store, the factored
     operator applied per camera run) against the stored-J pipeline: the same
@@ -154,16 +155,19 @@ def test_recompute_hvp(gpu, monkeypatch, precision, mode, huber, zipf):
         g2 = bal.build_graph(p, precision, mode, huber)
         rep = bal.levenberg_marquardt(g2, bal_cfg(6))
         out[rc] = (hs, rep, g2.points.copy(), g2.cameras.copy())
-    tol = 1e-12 if precision == "fp64" else 2e-5
+    # bf16 storage: the HVP output is narrowed to bf16, so float-rounding differences
+    # of the two association orders can move an entry by one bf16 ulp (2^-8)
+    tol = {"fp64": 1e-12, "fp32": 2e-5, "fp32-bf16": 1e-2}[precision]
     for a, b in zip(out["1"][0], out["0"][0]):
         assert rel(a, b) <= tol
     ra, rb = out["1"][1], out["0"][1]
     assert ra.termination == rb.termination and len(ra.iterations) == len(rb.iterations)
     assert [i.accepted for i in ra.iterations] == [i.accepted for i in rb.iterations]
-    assert [i.pcg_iterations for i in ra.iterations] == [i.pcg_iterations for i in rb.iterations]
-    ctol = 1e-9 if precision == "fp64" else 1e-4
+    if precision != "fp32-bf16":
+        assert [i.pcg_iterations for i in ra.iterations] == [i.pcg_iterations for i in rb.iterations]
+    ctol = {"fp64": 1e-9, "fp32": 1e-4, "fp32-bf16": 1e-3}[precision]
     assert abs(ra.final_chi2 - rb.final_chi2) <= ctol * rb.final_chi2
-    assert rel(out["1"][2], out["0"][2]) <= (1e-7 if precision == "fp64" else 1e-3)
+    assert rel(out["1"][2], out["0"][2]) <= {"fp64": 1e-7, "fp32": 1e-3, "fp32-bf16": 1e-2}[precision]
 
 
 def test_recompute_hvp_deterministic(gpu, monkeypatch):
