@@ -380,51 +380,57 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
         for (int v = 0; v < kRcVals; ++v) sA[v * kRcAStr + gt] = acc[v];
       }
       asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kRcGroupThreads) : "memory");
-      // ---- camera runs: one thread per (camera, value); run lc = segments
-      // [rseg[lc], rseg[lc + 1]), summed in segment order
+      // ---- epilogue, one item per thread: camera-run values (camera lc,
+      // value v: segments [rseg[lc], rseg[lc + 1]) in segment order) first,
+      // then points (contiguous point-slot ranges); one pass mixes the tail of
+      // the first kind with the head of the second
       const uint32_t cb = h[kRCb];
       const uint16_t* rseg = reinterpret_cast<const uint16_t*>(aux + as.rseg);
-      for (uint32_t o = gt; o < kRcVals * ncam && !(L.dbg & 2); o += kRcGroupThreads) {
-        const uint32_t lc = o / kRcVals, v = o - kRcVals * lc;
-        const FP* src = sA + v * kRcAStr;
-        FP a0 = FP(0), a1 = FP(0), a2 = FP(0), a3 = FP(0);
-        uint32_t q = rseg[lc];
-        const uint32_t qe = rseg[lc + 1];
-        for (; q + 4 <= qe; q += 4) {
-          a0 += src[q];
-          a1 += src[q + 1];
-          a2 += src[q + 2];
-          a3 += src[q + 3];
-        }
-        for (; q < qe; ++q) a0 += src[q];
-        d.part15[static_cast<uint64_t>(kRcRec) * (cb + lc) + v] = (a0 + a1) + (a2 + a3);
-      }
-      // ---- points: thread = point
       const uint16_t* spso = reinterpret_cast<const uint16_t*>(aux + as.pso);
       const uint8_t* scf = aux + as.cf;
       const FP* sD = reinterpret_cast<const FP*>(lin + ls.D);
       const SP* sp = reinterpret_cast<const SP*>(rg + h[kROP] + h[kRDp]);
       const uint32_t pb = h[kRPb];
+      const uint32_t ncv = kRcVals * ncam;
       FP dot = FP(0);
-      for (uint32_t pi = gt; pi < npt && !(L.dbg & 2); pi += kRcGroupThreads) {
-        FP a[3] = {FP(0), FP(0), FP(0)};
-        for (uint32_t q = spso[pi]; q < spso[pi + 1]; ++q)  // contiguous: the edges wrote in slot order
+      for (uint32_t o = gt; o < ncv + npt && !(L.dbg & 2); o += kRcGroupThreads) {
+        if (o < ncv) {
+          const uint32_t lc = o / kRcVals, v = o - kRcVals * lc;
+          const FP* src = sA + v * kRcAStr;
+          FP a0 = FP(0), a1 = FP(0), a2 = FP(0), a3 = FP(0);
+          uint32_t q = rseg[lc];
+          const uint32_t qe = rseg[lc + 1];
+          for (; q + 4 <= qe; q += 4) {
+            a0 += src[q];
+            a1 += src[q + 1];
+            a2 += src[q + 2];
+            a3 += src[q + 3];
+          }
+          for (; q < qe; ++q) a0 += src[q];
+          d.part15[static_cast<uint64_t>(kRcRec) * (cb + lc) + v] = (a0 + a1) + (a2 + a3);
+        } else {
+          const uint32_t pi = o - ncv;
+          FP a[3] = {FP(0), FP(0), FP(0)};
+          const uint32_t q0 = spso[pi], q1 = spso[pi + 1];
+#pragma unroll 4
+          for (uint32_t q = q0; q < q1; ++q)  // contiguous: the edges wrote in slot order
 #pragma unroll
-          for (int k = 0; k < 3; ++k) a[k] += gp[k * kRcGpStr + q];
-        const uint64_t col = pcol0 + 3ull * (pb + pi);
-        const bool freev = scf[3 * pi];
+            for (int k = 0; k < 3; ++k) a[k] += gp[k * kRcGpStr + q];
+          const uint64_t col = pcol0 + 3ull * (pb + pi);
+          const bool freev = scf[3 * pi];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const FP Dk = sD[3 * pi + k];
-          const FP damp = before ? lam * Dk * Dk : lam;
-          const SP pk = sp[3 * pi + k];
-          if (dir) d.p[col + k] = pk;
-          const FP pw = widen<FP>(pk);
-          const FP out = freev ? damp * pw + Dk * a[k] : FP(0);
-          const SP o = narrow<SP>(out);
-          d.ap[col + k] = o;
-          if (d.dbg_out) d.dbg_out[col + k] = out;
-          dot += pw * widen<FP>(o);
+          for (int k = 0; k < 3; ++k) {
+            const FP Dk = sD[3 * pi + k];
+            const FP damp = before ? lam * Dk * Dk : lam;
+            const SP pk = sp[3 * pi + k];
+            if (dir) d.p[col + k] = pk;
+            const FP pw = widen<FP>(pk);
+            const FP out = freev ? damp * pw + Dk * a[k] : FP(0);
+            const SP os = narrow<SP>(out);
+            d.ap[col + k] = os;
+            if (d.dbg_out) d.dbg_out[col + k] = out;
+            dot += pw * widen<FP>(os);
+          }
         }
       }
       dot = warp_sum(dot);
