@@ -330,6 +330,9 @@ class Solver final : public SolverBase {
   }
   ~Solver() override {
     cudaSetDevice(g_.device);  // this handle's streams, events and blocks live there
+    for (const auto& kv : phase_ms_)
+      std::fprintf(stderr, "[gb phases] %-24s %8.3f ms x %d\n", kv.first.c_str(),
+                   kv.second.first / std::max(1, kv.second.second), kv.second.second);
     if (rc_.prof) {  // GB_RC_DBG & 8: per-role mbarrier wait cycles of k_hvp_rc (summed over CTAs and launches)
       unsigned long long h[16] = {};
       if (cudaMemcpy(h, rc_.prof, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess)
@@ -448,7 +451,7 @@ class Solver final : public SolverBase {
         fin(0);
       }
       pcg_max_it_ = cfg.pcg.max_iterations;
-      if (!dist() || g_.reducer->capturable()) {
+      if ((!dist() || g_.reducer->capturable()) && !phases_on_) {
         build_iteration_graph(cfg.pcg.max_iterations);
       } else if (graph_exec_) {
         cudaGraphExecDestroy(graph_exec_);
@@ -481,6 +484,7 @@ class Solver final : public SolverBase {
   void end(gb_solve_report* rep, gb_iteration_record* recs, int max_recs) override {
     if (!in_solve_) throw std::logic_error("gb_end without gb_begin");
     in_solve_ = false;
+    phase_flush();
     gb_solve_report& r = rep_;
     if (max_it_ > 0) {
       State<FP> hs;
@@ -1578,6 +1582,7 @@ class Solver final : public SolverBase {
     const size_t smem = lin_normal_smem<FP>();
     k_cam_pre<FP, SP><<<std::max(1u, div_up(act_.nc, 128)), 128, 0, s_>>>(dev_, dev_.x, dev_.cpre, 0, force);
     const bool aut = g_.diff_mode == GB_AUTO;
+    phase_mark("lin: k_cam_pre");
     if (dev_.J && aut) {  // Auto: stored J from dual-number passes (factor_descriptor.hpp:610-624)
       if (dev_.n_normal) k_lin_normal<FP, SP, true, true><<<dev_.n_normal, kLinThreads, smem, s_>>>(dev_, force);
       if (dev_.n_heavy)
@@ -1592,6 +1597,7 @@ class Solver final : public SolverBase {
         k_lin_tiles<FP, SP, false, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
     }
     CK(cudaGetLastError());
+    phase_mark("lin: tiles");
     if (!dist()) {
       k_lin_cams<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(dev_, force, 0);
     } else {
@@ -1606,6 +1612,7 @@ class Solver final : public SolverBase {
       k_tile_lin<FP, SP><<<dev_.n_normal, 128, 0, s_>>>(dev_, force);
       CK(cudaGetLastError());
     } else if (rc_ok_) {
+      phase_mark("lin: cameras");
       k_tile_lin_rc<FP, SP><<<dev_.n_normal, 128, 0, s_>>>(dev_, force);
       CK(cudaGetLastError());
     }
@@ -1724,6 +1731,7 @@ class Solver final : public SolverBase {
     }
     launch_precond();
     CK(cudaGetLastError());
+    phase_mark("solve: precond");
     k_rhs_norm<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
     CK(cudaGetLastError());
     if (dist()) {
@@ -1737,8 +1745,10 @@ class Solver final : public SolverBase {
       fin(2);
     }
     const bool dir_fused = (pipe_ok_ || rc_ok_) && !(!dist() && fused_pcg_);
+    phase_mark("solve: rhs + init");
     for (int k = 0; k < pcg_max_it; ++k) {
       launch_hvp(dev_, dir_fused && k > 0);  // after k_pcg_dir_rest the per-tile camera copies are current
+      phase_mark("solve: HVP");
       if (!dist() && fused_pcg_) {
         launch_pcg_step();
         continue;
@@ -1756,6 +1766,7 @@ class Solver final : public SolverBase {
       else
         k_pcg_dir<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
       CK(cudaGetLastError());
+      phase_mark("solve: update");
     }
     k_step<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
     CK(cudaGetLastError());
@@ -1768,9 +1779,11 @@ class Solver final : public SolverBase {
   // One LM iteration (levenberg_marquardt.hpp:149-220) as a fixed kernel
   // sequence; every kernel early-exits on the device flags it depends on.
   void enqueue_iteration(int pcg_max_it) {
+    phase_mark(nullptr);
     k_iter_begin<FP><<<1, 1, 0, s_>>>(st_, dev_.recs);
     CK(cudaGetLastError());
     enqueue_solve(pcg_max_it);
+    phase_mark("solve: step");
     k_cam_pre<FP, SP><<<std::max(1u, div_up(act_.nc, 128)), 128, 0, s_>>>(dev_, dev_.x_new, dev_.cpre_new, 1, 0);
     k_chi2_tiles<FP, SP, false><<<chi2_grid(), kTileThreads, 0, s_>>>(dev_, dev_.x_new, 0);
     CK(cudaGetLastError());
@@ -1778,12 +1791,43 @@ class Solver final : public SolverBase {
       allreduce(red_s() + kRedChi, 1);
       fin(5);
     }
+    phase_mark("candidate chi2");
     k_decide<FP><<<1, 1, 0, s_>>>(st_, dev_.recs);
     CK(cudaGetLastError());
     k_commit<FP, SP><<<col_grid(), 256, 0, s_>>>(dev_);
     CK(cudaGetLastError());
+    phase_mark("decide + commit");
     enqueue_linearize(0);
+    phase_mark("lin: tile blobs");
   }
+
+  // GB_PHASES=1 (experiments): iterations run uncaptured with CUDA events
+  // between phases; the mean device time per phase occurrence is printed when
+  // the handle is destroyed
+  void phase_mark(const char* name) {
+    if (!phases_on_) return;
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, s_));
+    phase_ev_.push_back({e, name});
+  }
+  void phase_flush() {
+    if (phase_ev_.empty()) return;
+    CK(cudaStreamSynchronize(s_));
+    for (size_t i = 1; i < phase_ev_.size(); ++i) {
+      if (!phase_ev_[i].second) continue;
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, phase_ev_[i - 1].first, phase_ev_[i].first));
+      auto& acc = phase_ms_[phase_ev_[i].second];
+      acc.first += ms;
+      acc.second += 1;
+    }
+    for (auto& pe : phase_ev_) cudaEventDestroy(pe.first);
+    phase_ev_.clear();
+  }
+  bool phases_on_ = std::getenv("GB_PHASES") != nullptr;
+  std::vector<std::pair<cudaEvent_t, const char*>> phase_ev_;
+  std::map<std::string, std::pair<double, int>> phase_ms_;
 
   void build_iteration_graph(int pcg_max_it) {
     if (graph_exec_ && graph_pcg_it_ == pcg_max_it && graph_recs_ == dev_.recs) return;
