@@ -191,16 +191,15 @@ __device__ __forceinline__ void rc_load_cam(const FP* scam, const FP* stc, uint3
   C.vk2 = b[14];
 }
 
-// 1/x: IEEE division in fp32; in fp64 the MUFU seed and two Newton steps
-// (<= 1 ulp, no slow-path branch)
+// 1/x: IEEE division in fp32; in fp64 the MUFU seed (rcp.approx.ftz.f64,
+// ~2^-23) refined by one third-order step r (1 + e + e^2), e = 1 - x r (relative
+// error ~2^-69, i.e. rounding level; no slow-path branch)
 __device__ __forceinline__ float rc_rcp(float x) { return 1.0f / x; }
 __device__ __forceinline__ double rc_rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+  const double e = fma(-x, r, 1.0);  // one Newton step with the quadratic term: error ~ e^3
+  return fma(r, fma(e, e, e), r);
 }
 
 // One edge: the forward product and the scatter terms, with U = du/dP
