@@ -1,5 +1,5 @@
 """Small solves for compute-sanitizer (memcheck / racecheck / synccheck):
-every precision, the pipelined and tile HVP paths, Huber, dynamic, Auto and Schur.
+every precision, the recompute / pipelined / tile HVP paths, Huber, dynamic, Auto and Schur.
   compute-sanitizer --tool racecheck python tools/sanitize_run.py"""
 import os
 import sys
@@ -11,7 +11,8 @@ from paper_2509_26581_b200 import bal  # noqa: E402
 p = bal.synthetic_bal(40, 3000, 16000, seed=3)
 for prec, mode, huber, solver in (("fp64", "analytic", None, "pcg"), ("fp32", "analytic", 2.0, "pcg"),
                                   ("fp32-bf16", "analytic", None, "pcg"), ("fp64", "dynamic", None, "pcg"),
-                                  ("fp64", "auto", None, "pcg"), ("fp64", "analytic", None, "schur")):
+                                  ("fp64", "auto", None, "pcg"), ("fp64", "analytic", None, "schur"),
+                                  ("fp32-bf16", "dynamic", None, "pcg")):
     g = bal.build_graph(p, prec, mode, huber)
     g.set_linear_solver(solver)
     cfg = bal.LMConfig(max_iterations=2)
