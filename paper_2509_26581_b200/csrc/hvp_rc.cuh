@@ -96,7 +96,7 @@ inline RcLayout rc_layout(bool huber, uint32_t smem_budget) {
   L.work_bytes = o;
   L.max_region = kRcHdrBytes + aux_sections(kTileEdges, kTilePoints).bytes +
                  rc_lin_sections<FP>(kTileEdges, kTilePoints, kTileCams, huber).bytes +
-                 3 * r16(kTilePoints * 3 * sizeof(FP) + 16) + kTileCams * kRcRec * sizeof(FP) + 128;
+                 4 * r16(kTilePoints * 3 * sizeof(FP) + 16) + kTileCams * kRcRec * sizeof(FP) + 128;
   L.slots = kRcGroups * L.work_bytes;
   L.bars = L.slots + 4 * kRcSlots;
   L.ring = L.bars + 4 * kRcSlots * 8;
@@ -106,7 +106,8 @@ inline RcLayout rc_layout(bool huber, uint32_t smem_budget) {
   return L;
 }
 
-enum RcHdr : int { kRT = 0, kRNe, kRNpt, kRNcam, kRPb, kRCb, kRDp, kRDz, kROAux, kROLin, kROP, kROZ, kROTc, kROV, kRCount };
+enum RcHdr : int { kRT = 0, kRNe, kRNpt, kRNcam, kRPb, kRCb, kRDp, kRDz, kROAux, kROLin, kROP, kROZ, kROTc, kROV, kROX,
+                   kRCount };
 
 // mbar_wait that sleeps (suspend-time hint) instead of spinning, and adds its
 // waiting cycles to acc when profiling
@@ -302,6 +303,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
   const uint64_t pcol0 = 9ull * d.nc;
   const uint32_t ntiles = d.n_normal;
   const bool dir = d.st->dir_pending != 0;
+  const bool xpend = d.st->x_pending != 0;  // x += alpha p of the last PCG update (preparer, on the loaded p)
   const bool pf = (L.dbg & 8) && lane == 0;
 
   if (warp < 2 * kRcGroupThreads / 32) {
@@ -485,7 +487,8 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
         const uint32_t o_aux = kRcHdrBytes, o_lin = o_aux + as.bytes, o_p = o_lin + ls.bytes;
         const uint32_t o_z = o_p + s_p.bytes, o_tc = o_z + s_z.bytes;
         const uint32_t o_v = o_tc + tcb;  // the preparer's v_p = D p (FP)
-        const uint32_t sz = (o_v + r16(sizeof(FP) * 3ull * npt) + 127) / 128 * 128;
+        const uint32_t o_x = o_v + r16(sizeof(FP) * 3ull * npt);  // x (when the deferred update is pending)
+        const uint32_t sz = (o_x + (xpend ? s_p.bytes : 0u) + 127) / 128 * 128;
         // ---- room in the ring (warp-uniform bookkeeping)
         for (;;) {
           bool fits;
@@ -537,6 +540,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
           hh[kROZ] = o_z;
           hh[kROTc] = o_tc;
           hh[kROV] = o_v;
+          hh[kROX] = o_x;
           // the tile's static + per-linearization blob: one bulk copy (contiguous, o_lin == o_aux + as.bytes)
           mbar_arrive_expect_tx(&blob[s], as.bytes + ls.bytes);
           bulk_g2s(rg + o_aux, d.tile_aux + 16 * aux16, as.bytes + ls.bytes, &blob[s]);
@@ -583,6 +587,12 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
         for (uint32_t c = lane; c < nz16; c += 32)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(rg + h[kROZ] + 16 * c)),
                        "l"(zsrc + 16 * c) : "memory");
+        if (xpend) {  // x has the same column span (and alignment delta) as p
+          const char* xsrc = reinterpret_cast<const char*>(d.xs + pcol0 + 3ull * pb) - h[kRDp];
+          for (uint32_t c = lane; c < np16; c += 32)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(rg + h[kROX] + 16 * c)),
+                         "l"(xsrc + 16 * c) : "memory");
+        }
         for (uint32_t c = lane; c < nt16; c += 32)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(rg + h[kROTc] + 16 * c)),
                        "l"(csrc + sizeof(FP) * kRcRec * static_cast<uint64_t>(tcam[c / kRec16]) + 16 * (c % kRec16))
@@ -608,6 +618,9 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
       SP* pp = reinterpret_cast<SP*>(rg + h[kROP] + h[kRDp]);
       const SP* zz = reinterpret_cast<const SP*>(rg + h[kROZ] + h[kRDz]);
       FP* vv = reinterpret_cast<FP*>(rg + h[kROV]);
+      const SP* xx = reinterpret_cast<const SP*>(rg + h[kROX] + h[kRDp]);
+      const FP alpha = d.st->alpha;
+      SP* xg = d.xs + pcol0 + 3ull * h[kRPb];
       const FP* DD = reinterpret_cast<const FP*>(rg + h[kROLin]);  // D at offset 0
       const uint32_t n3 = 3 * npt;
       constexpr int U = 4;
@@ -627,6 +640,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
         for (int u = 0; u < U; ++u) {
           const uint32_t q = q0 + 32 * u;
           if (q < n3) {
+            if (xpend) xg[q] = pcg_x_value<FP, SP>(xx[q], pv[u], alpha);  // on p before the direction update
             const SP pn = dir ? pcg_dir_value<FP, SP>(zv[u], pv[u], beta) : pv[u];
             pp[q] = pn;
             vv[q] = dv[u] * widen<FP>(pn);  // == vt (k_pcg_dir)
@@ -647,6 +661,8 @@ template <typename FP, typename SP>
 __global__ void k_rc_cams_pre(Dev<FP, SP> d, int dir, const uint64_t* rbeg, const uint64_t* rend, int nranges) {
   if (!d.st->iter_active || d.st->pcg_done) return;
   const FP beta = d.st->beta;
+  const bool xpend = d.st->x_pending != 0;  // the last PCG update's x += alpha p (cameras, heavy-tile points)
+  const FP alpha = d.st->alpha;
   if (dir && blockIdx.x == 0 && threadIdx.x == 0) d.st->dir_pending = 1;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t t0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -655,6 +671,7 @@ __global__ void k_rc_cams_pre(Dev<FP, SP> d, int dir, const uint64_t* rbeg, cons
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
       const uint64_t col = 9 * c + k;
+      if (xpend) d.xs[col] = pcg_x_value<FP, SP>(d.xs[col], d.p[col], alpha);
       if (dir) {
         const SP pi = pcg_dir_value<FP, SP>(d.z[col], d.p[col], beta);
         d.p[col] = pi;
@@ -684,9 +701,11 @@ __global__ void k_rc_cams_pre(Dev<FP, SP> d, int dir, const uint64_t* rbeg, cons
 #pragma unroll
     for (int k = 0; k < kRcRec; ++k) d.crec[static_cast<uint64_t>(kRcRec) * c + k] = rec[k];
   }
-  if (dir)
+  if (dir || xpend)
     for (int r = 0; r < nranges; ++r)
       for (uint64_t i = rbeg[r] + t0; i < rend[r]; i += stride) {
+        if (xpend) d.xs[i] = pcg_x_value<FP, SP>(d.xs[i], d.p[i], alpha);
+        if (!dir) continue;
         const SP pi = pcg_dir_value<FP, SP>(d.z[i], d.p[i], beta);
         d.p[i] = pi;
         d.vt[i] = static_cast<arith_t<SP>>(d.D[i] * widen<FP>(pi));
@@ -719,6 +738,7 @@ __device__ __forceinline__ void rc_butterfly16(FP (&v)[16], int lane) {
 template <typename FP, typename SP>
 __global__ void __launch_bounds__(32 * kCamWarps, 4) k_hvp_cams_rc(Dev<FP, SP> d, int phase) {
   if (!d.st->iter_active || d.st->pcg_done) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.st->x_pending = 0;  // applied by k_rc_cams_pre + k_hvp_rc
   __shared__ FP scratch[32];
   const int lane = threadIdx.x & 31;
   const uint32_t c = blockIdx.x * kCamWarps + (threadIdx.x >> 5);

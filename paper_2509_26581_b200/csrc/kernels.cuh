@@ -71,6 +71,7 @@ struct State {
   double pcg_relres;
   int pcg_it, pcg_done, pcg_conv, pcg_zero;
   int dir_pending;  // p = z + beta p still to be applied to normal-tile points (fused into k_hvp_pipe)
+  int x_pending;    // x += alpha p of the last PCG update still to be applied (defer_x: by the next HVP or k_step)
   // step / candidate
   FP pred, chi2_new;
   int step_finite;
@@ -101,6 +102,7 @@ struct Dev {
   FP* cpre_new;     // [nc][kCamPre] at the chi^2 evaluation point
   int jfact;        // 1: factored J store (analytic mode, SP == FP), DESIGN.md §2
   int want_dx;      // k_step also stores dx (the LinearSystem::solve_step surface only)
+  int defer_x;      // recompute path: k_pcg_update leaves x += alpha p to the next HVP (its loader reads p anyway)
   // pipelined HVP (hvp_pipe.cuh): tile records and per-tile camera copies
   const uint32_t* tile_meta;  // [n_normal][12] (hvp_pipe.cuh TileMeta)
   uint32_t ntcams;            // tile_cam_off[ntiles]
@@ -847,6 +849,7 @@ __global__ void k_iter_begin(State<FP>* st, gb_iteration_record* recs) {
   st->pcg_done = 0;
   st->pcg_it = 0;
   st->dir_pending = 0;
+  st->x_pending = 0;
   st->pcg_conv = 0;
   st->pcg_zero = 0;
   st->pcg_relres = 0.0;
@@ -1567,20 +1570,27 @@ __global__ void k_fin(Dev<FP, SP> d, int site) {
 
 // x += alpha p; r -= alpha Ap; z = M r for one N-column vertex block, all
 // loads issued before any store (the vectors are distinct arrays)
+template <typename FP, typename SP>
+__device__ inline SP pcg_x_value(SP x, SP p, FP alpha) {  // x += alpha p (pcg.hpp:340-357)
+  return narrow<SP>(widen<FP>(x) + alpha * widen<FP>(p));
+}
+
 template <typename FP, typename SP, int N>
 __device__ inline void pcg_update_block(const Dev<FP, SP>& d, uint64_t col, const FP* M, FP alpha, FP* rz, FP* rr) {
   SP xs[N], pv[N], rs[N], aps[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    xs[k] = d.xs[col + k];
-    pv[k] = d.p[col + k];
+    if (!d.defer_x) {
+      xs[k] = d.xs[col + k];
+      pv[k] = d.p[col + k];
+    }
     rs[k] = d.r[col + k];
     aps[k] = d.ap[col + k];
   }
   FP rv[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    d.xs[col + k] = narrow<SP>(widen<FP>(xs[k]) + alpha * widen<FP>(pv[k]));
+    if (!d.defer_x) d.xs[col + k] = pcg_x_value<FP, SP>(xs[k], pv[k], alpha);
     const SP rn = narrow<SP>(widen<FP>(rs[k]) - alpha * widen<FP>(aps[k]));
     d.r[col + k] = rn;
     rv[k] = widen<FP>(rn);
@@ -1609,7 +1619,10 @@ __global__ void k_pcg_update(Dev<FP, SP> d) {
   if (!d.st->iter_active || d.st->pcg_done) return;
   __shared__ FP scratch[32];
   const FP alpha = d.st->alpha;
-  if (blockIdx.x == 0 && threadIdx.x == 0) d.st->dir_pending = 0;  // the HVP that consumed it has run
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    d.st->dir_pending = 0;  // the HVP that consumed it has run
+    if (d.defer_x) d.st->x_pending = 1;  // this update's x += alpha p goes to the next HVP (or k_step)
+  }
   FP rz = FP(0), rr = FP(0);
   const uint64_t nv = d.st->schur ? static_cast<uint64_t>(d.nc) : static_cast<uint64_t>(d.nc) + d.np;
   for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv;
@@ -1757,12 +1770,15 @@ __global__ void k_step(Dev<FP, SP> d) {
   const FP lam = d.st->lambda_solve;
   const int before = d.st->before_scaling;
   const bool zero = d.st->pcg_zero;
+  const bool xpend = d.st->x_pending != 0;  // the last PCG update's deferred x += alpha p
+  const FP alpha = d.st->alpha;
   FP pred = FP(0);
   int fin = 1;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const FP Di = d.D[i];
     const bool ptcol = i >= 9ull * d.nc;
+    if (xpend) d.xs[i] = pcg_x_value<FP, SP>(d.xs[i], d.p[i], alpha);
     const FP xsi = (d.st->schur && ptcol) ? d.xp[i - 9ull * d.nc] : (zero ? FP(0) : widen<FP>(d.xs[i]) * unscale);
     const FP rhs = -Di * d.b[i];
     const FP damp = before ? lam * Di * Di : lam;
@@ -1783,6 +1799,7 @@ __global__ void k_step(Dev<FP, SP> d) {
     const FP s = reduce_partials(d.blk_red, gridDim.x, scratch);
     const int f = reduce_flags_and(d.blk_flag, gridDim.x);
     if (threadIdx.x == 0) {
+      d.st->x_pending = 0;
       if (!d.dist) {
         fin_step(d.st, s, f != 0);
       } else {

@@ -714,6 +714,7 @@ class Solver final : public SolverBase {
     hs.lambda_solve = static_cast<FP>(lambda);
     hs.lambda = static_cast<FP>(lambda);
     hs.pcg_done = hs.pcg_it = hs.pcg_conv = hs.pcg_zero = 0;
+    hs.dir_pending = hs.x_pending = 0;
     hs.pcg_relres = 0;
     hs.fallbacks = 0;
     hs.schur = g_.linear_solver == GB_SOLVER_SCHUR ? 1 : 0;
@@ -1268,6 +1269,9 @@ class Solver final : public SolverBase {
       rc_ok_ = rc_.ring_bytes >= 2 * rc_.max_region;
       if (const char* e = std::getenv("GB_HVP_RC")) rc_ok_ = rc_ok_ && std::atoi(e) != 0;
       if (const char* e = std::getenv("GB_RC_DBG")) rc_.dbg = std::atoi(e);
+      // x += alpha p deferred into the next HVP (the fused direction update path only)
+      d.defer_x = rc_ok_ && !fused_pcg_ ? 1 : 0;
+      if (const char* e = std::getenv("GB_DEFER_X")) d.defer_x = d.defer_x && std::atoi(e) != 0;
       rc_.prof = nullptr;
       if (rc_.dbg & 8) {
         rc_.prof = static_cast<unsigned long long*>(b_rcprof_.alloc(16 * sizeof(unsigned long long)));
