@@ -712,137 +712,88 @@ __global__ void k_rc_cams_pre(Dev<FP, SP> d, int dir, const uint64_t* rbeg, cons
       }
 }
 
-// Camera side of the recompute HVP + p.Ap (pcg.hpp:332-340): a warp per
-// camera sums the 15-value partials of its tile copies (fixed order, a
-// transposing butterfly: lane l ends with value l / 2), adds the heavy tiles'
-// 9-value partial slots, and contracts S with T_k = Dw(e_k) in closed form:
+// Camera side of the recompute HVP + p.Ap (pcg.hpp:332-340): 16 lanes per
+// camera, lane v summing value v of the 15-value partials of the camera's tile
+// copies (fixed tile-copy order, four rows in flight), then the 9 output lanes
+// add the heavy tiles' 9-value partial slots and contract S with T_k =
+// Dw(e_k) in closed form:
 //   (sum_k,i T_k(i, j) S(k, i)) = w_j (-s tr S + s1 w.sigma + c2 w^T S w)
 //                                 + s sigma_j + c ((S w)_j + (S^T w)_j),
 // sigma = (S12 - S21, S20 - S02, S01 - S10), the chain coefficients s, c, s1,
 // c2 of snavely.hpp:103-121. Phases as k_hvp_cams (0 fused, 1 per-rank sums
 // -> red, 2 from red).
-template <typename FP>
-__device__ __forceinline__ void rc_butterfly16(FP (&v)[16], int lane) {
-#pragma unroll
-  for (int o = 8; o >= 1; o >>= 1) {  // xor 2o: keep half, send half
-    const bool hi = lane & (2 * o);
-#pragma unroll
-    for (int i = 0; i < o; ++i) {
-      const FP keep = hi ? v[i + o] : v[i], send = hi ? v[i] : v[i + o];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * o);
-    }
-  }
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);  // lane l: value l >> 1
-}
+constexpr int kRcCamsPerBlock = 16;  // 16 lanes per camera (one per partial value), 256 threads
 
 template <typename FP, typename SP>
-__global__ void __launch_bounds__(32 * kCamWarps, 4) k_hvp_cams_rc(Dev<FP, SP> d, int phase) {
+__global__ void __launch_bounds__(16 * kRcCamsPerBlock) k_hvp_cams_rc(Dev<FP, SP> d, int phase) {
   if (!d.st->iter_active || d.st->pcg_done) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) d.st->x_pending = 0;  // applied by k_rc_cams_pre + k_hvp_rc
   __shared__ FP scratch[32];
-  const int lane = threadIdx.x & 31;
-  const uint32_t c = blockIdx.x * kCamWarps + (threadIdx.x >> 5);
-  FP mine = FP(0);
-  if (c < d.nc) {
-    FP out = FP(0);  // lane k < 9: value k of J_c^T q summed over the camera's edges
-    if (phase != 2) {
-      FP acc[16];
-#pragma unroll
-      for (int v = 0; v < 16; ++v) acc[v] = FP(0);
+  const int lane = threadIdx.x & 31, v = lane & 15, gbase = lane & 16;
+  const uint32_t c = blockIdx.x * kRcCamsPerBlock + (threadIdx.x >> 4);
+  const bool cam_ok = c < d.nc;
+  FP out = FP(0);  // lane v < 9: value v of J_c^T q summed over the camera's edges
+  if (phase != 2) {
+    FP acc = FP(0);  // value v (15: padding) of the camera's tile copies, in tile-copy order
+    if (cam_ok) {
       const uint32_t q1 = d.cam_tc_off[c + 1];
-      for (uint32_t q = d.cam_tc_off[c] + lane; q < q1; q += 64) {  // two rows per lane in flight
-        const bool two = q + 32 < q1;
-        const uint32_t ia = d.cam_tc_idx[q], ib = two ? d.cam_tc_idx[q + 32] : ia;
-        const double2* ra = reinterpret_cast<const double2*>(d.part15 + static_cast<uint64_t>(kRcRec) * ia);
-        const double2* rb = reinterpret_cast<const double2*>(d.part15 + static_cast<uint64_t>(kRcRec) * ib);
-        if constexpr (sizeof(FP) == 8) {
-          double2 va[8], vb[8];
+      uint32_t q = d.cam_tc_off[c];
+      for (; q + 4 <= q1; q += 4) {  // four rows in flight
+        FP r[4];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            va[k] = ra[k];
-            vb[k] = two ? rb[k] : make_double2(0.0, 0.0);
-          }
+        for (int u = 0; u < 4; ++u) r[u] = d.part15[static_cast<uint64_t>(kRcRec) * d.cam_tc_idx[q + u] + v];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            acc[2 * k] += va[k].x;
-            acc[2 * k + 1] += va[k].y;
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            acc[2 * k] += vb[k].x;
-            acc[2 * k + 1] += vb[k].y;
-          }
-        } else {
-          const FP* sa = d.part15 + static_cast<uint64_t>(kRcRec) * ia;
-          const FP* sb = d.part15 + static_cast<uint64_t>(kRcRec) * ib;
-#pragma unroll
-          for (int v = 0; v < kRcVals; ++v) acc[v] += sa[v];
-          if (two)
-#pragma unroll
-            for (int v = 0; v < kRcVals; ++v) acc[v] += sb[v];
-        }
+        for (int u = 0; u < 4; ++u) acc += r[u];
       }
-      rc_butterfly16<FP>(acc, lane);
-      FP S[kRcVals];
+      for (; q < q1; ++q) acc += d.part15[static_cast<uint64_t>(kRcRec) * d.cam_tc_idx[q] + v];
+    }
+    FP S[kRcVals];
 #pragma unroll
-      for (int v = 0; v < kRcVals; ++v) S[v] = __shfl_sync(0xffffffffu, acc[0], 2 * v);
+    for (int j = 0; j < kRcVals; ++j) S[j] = __shfl_sync(0xffffffffu, acc, gbase | j);
+    if (cam_ok && v < 9) {
       const FP w0 = d.x[9ull * c], w1 = d.x[9ull * c + 1], w2 = d.x[9ull * c + 2], f = d.x[9ull * c + 6];
       const FP* pre = d.cpre + static_cast<uint64_t>(kCamPre) * c;
       const FP s = pre[4], cc = pre[5], s1 = pre[6], c2 = pre[7];
-      const FP w[3] = {w0, w1, w2};
-      const FP sig[3] = {S[5] - S[7], S[6] - S[2], S[1] - S[3]};  // S(k, i) at 3k + i
-      FP Sw[3], STw[3];
+      if (v < 3) {
+        const FP w[3] = {w0, w1, w2};
+        const FP sig[3] = {S[5] - S[7], S[6] - S[2], S[1] - S[3]};  // S(k, i) at 3k + i
+        FP Sw[3], STw[3];
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        Sw[j] = S[3 * j] * w0 + S[3 * j + 1] * w1 + S[3 * j + 2] * w2;
-        STw[j] = S[j] * w0 + S[3 + j] * w1 + S[6 + j] * w2;
+        for (int j = 0; j < 3; ++j) {
+          Sw[j] = S[3 * j] * w0 + S[3 * j + 1] * w1 + S[3 * j + 2] * w2;
+          STw[j] = S[j] * w0 + S[3 + j] * w1 + S[6 + j] * w2;
+        }
+        const FP wSw = w0 * Sw[0] + w1 * Sw[1] + w2 * Sw[2];
+        const FP sc = -s * (S[0] + S[4] + S[8]) + s1 * (w0 * sig[0] + w1 * sig[1] + w2 * sig[2]) + c2 * wSw;
+        FP o3[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) o3[j] = w[j] * sc + s * sig[j] + cc * (Sw[j] + STw[j]);
+        out = v == 0 ? o3[0] : (v == 1 ? o3[1] : o3[2]);
+      } else if (v < 6) {
+        out = v == 3 ? S[9] : (v == 4 ? S[10] : S[11]);
+      } else {
+        out = v == 6 ? S[12] : f * (v == 7 ? S[13] : S[14]);
       }
-      const FP wSw = w0 * Sw[0] + w1 * Sw[1] + w2 * Sw[2];
-      const FP sc = -s * (S[0] + S[4] + S[8]) + s1 * (w0 * sig[0] + w1 * sig[1] + w2 * sig[2]) + c2 * wSw;
-      FP o9[9];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) o9[j] = w[j] * sc + s * sig[j] + cc * (Sw[j] + STw[j]);
-      o9[3] = S[9];
-      o9[4] = S[10];
-      o9[5] = S[11];
-      o9[6] = S[12];
-      o9[7] = f * S[13];
-      o9[8] = f * S[14];
-      if (d.n_heavy) {  // heavy tiles: 9-value partial slots (k_hvp_tiles), flagged in camera-major order
-        FP hv[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) hv[k] = FP(0);
-        for (uint32_t q = d.cam_part_off[c] + lane; q < d.cam_part_off[c + 1]; q += 32)
-          if (d.hflag[q])
-#pragma unroll
-            for (int k = 0; k < 9; ++k) hv[k] += d.part[9ull * q + k];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) o9[k] += warp_sum(hv[k]);
-      }
-#pragma unroll
-      for (int k = 0; k < 9; ++k)
-        if (lane == k) out = o9[k];
+      if (d.n_heavy)  // heavy tiles: 9-value partial slots (k_hvp_tiles), flagged in camera-major order
+        for (uint32_t q = d.cam_part_off[c]; q < d.cam_part_off[c + 1]; ++q)
+          if (d.hflag[q]) out += d.part[9ull * q + v];
     }
-    if (phase == 1) {
-      if (lane < 9) d.red[9ull * c + lane] = out;
-    } else {
-      FP dot = FP(0);
-      const bool freev = d.col_free[9ull * c];
-      if (lane < 9) {
-        const uint64_t col = 9ull * c + lane;
-        const FP a = phase == 2 ? d.red[col] : out;
-        const FP Dk = d.D[col];
-        const FP damp = d.st->before_scaling ? d.st->lambda_solve * Dk * Dk : static_cast<FP>(d.st->lambda_solve);
-        const FP pk = widen<FP>(d.p[col]);
-        const FP o = freev ? damp * pk + Dk * a : FP(0);
-        const SP os = narrow<SP>(o);
-        d.ap[col] = os;
-        if (d.dbg_out) d.dbg_out[col] = o;
-        dot = pk * widen<FP>(os);
-      }
-      dot = warp_sum(dot);
-      if (lane == 0) mine = dot;
-    }
+  }
+  FP mine = FP(0);
+  if (phase == 1) {
+    if (cam_ok && v < 9) d.red[9ull * c + v] = out;
+  } else if (cam_ok && v < 9) {
+    const bool freev = d.col_free[9ull * c];
+    const uint64_t col = 9ull * c + v;
+    const FP a = phase == 2 ? d.red[col] : out;
+    const FP Dk = d.D[col];
+    const FP damp = d.st->before_scaling ? d.st->lambda_solve * Dk * Dk : static_cast<FP>(d.st->lambda_solve);
+    const FP pk = widen<FP>(d.p[col]);
+    const FP o = freev ? damp * pk + Dk * a : FP(0);
+    const SP os = narrow<SP>(o);
+    d.ap[col] = os;
+    if (d.dbg_out) d.dbg_out[col] = o;
+    mine = pk * widen<FP>(os);
   }
   if (phase != 2) {  // this block's slice of the tiles' point dot partials
     const uint64_t ntp = 8ull * d.ntiles;

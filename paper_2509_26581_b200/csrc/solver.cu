@@ -1667,12 +1667,12 @@ class Solver final : public SolverBase {
     if (rc_ok_) {
       if constexpr (kRcCapable) {
         if (!dist()) {
-          k_hvp_cams_rc<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 0);
+          k_hvp_cams_rc<FP, SP><<<std::max(1u, div_up(act_.nc, kRcCamsPerBlock)), 16 * kRcCamsPerBlock, 0, s_>>>(d, 0);
         } else {
-          k_hvp_cams_rc<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 1);
+          k_hvp_cams_rc<FP, SP><<<std::max(1u, div_up(act_.nc, kRcCamsPerBlock)), 16 * kRcCamsPerBlock, 0, s_>>>(d, 1);
           CK(cudaGetLastError());
           allreduce(d.red, 9ull * d.nc + 1);
-          k_hvp_cams_rc<FP, SP><<<cam_grid(), 32 * kCamWarps, 0, s_>>>(d, 2);
+          k_hvp_cams_rc<FP, SP><<<std::max(1u, div_up(act_.nc, kRcCamsPerBlock)), 16 * kRcCamsPerBlock, 0, s_>>>(d, 2);
         }
       }
     } else if (!dist()) {
