@@ -124,9 +124,6 @@ inline PipeLayout pipe_layout(int rows, bool huber, bool fact, uint32_t smem_bud
   return L;
 }
 
-// tile record, one per normal tile (list order)
-// kMSlot0 / kMNruns: the tile's camera-run slots [slot0, slot0 + nruns) (filled on the device by k_tile_aux)
-enum TileMeta : int { kMT = 0, kMEb, kMNe, kMPb, kMNpt, kMCb, kMNcam, kMCh0, kMAux16, kMLin16, kMSlot0, kMNruns, kMCount };
 
 // N contiguous T from 16-byte aligned shared memory in 16-byte loads
 template <typename T, int N>

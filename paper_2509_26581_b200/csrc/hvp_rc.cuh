@@ -41,24 +41,6 @@
 namespace gb {
 
 constexpr int kRcVals = 15;  // camera-run partial: S(k, i) = X_k h_i (9), h (3), dist p.q, n p.q, n^2 p.q
-constexpr int kRcRec = 16;   // per-camera record stride (static [R t f k1 k2 0], dynamic [M v_t v_int 0])
-
-// lin blob of the recompute path (per linearization): point D, tile camera
-// static records, Huber weights, point parameters X
-struct RcLinSec {
-  uint32_t D, cam, w, X, bytes;
-};
-template <typename FP>
-__host__ __device__ inline RcLinSec rc_lin_sections(uint32_t ne, uint32_t npt, uint32_t ncam, bool huber) {
-  const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad;
-  RcLinSec l;
-  l.D = 0;
-  l.cam = l.D + r16(sizeof(FP) * 3ull * npt);
-  l.w = l.cam + r16(sizeof(FP) * static_cast<uint64_t>(kRcRec) * ncam);
-  l.X = l.w + (huber ? r16(sizeof(FP) * 1ull * ne8) : 0u);
-  l.bytes = l.X + r16(sizeof(FP) * 3ull * npt);
-  return l;
-}
 
 // Shared memory: a byte ring of tile regions (each tile's inputs at their
 // exact size, so ~10 typical tiles are in flight: the stream is latency-bound

@@ -1328,6 +1328,32 @@ __device__ __forceinline__ void lin_cam_shfl(bool in, const FP* jc_in, FP wr0, F
 
 // 128-thread CTAs (four passes over a 512-edge tile), four per SM: while one
 // CTA waits at a barrier or on its prologue gathers, three others compute.
+// tile record, one per normal tile (list order)
+// kMSlot0 / kMNruns: the tile's camera-run slots [slot0, slot0 + nruns) (filled on the device by k_tile_aux)
+enum TileMeta : int { kMT = 0, kMEb, kMNe, kMPb, kMNpt, kMCb, kMNcam, kMCh0, kMAux16, kMLin16, kMSlot0, kMNruns, kMCount };
+
+// Recompute-HVP per-tile lin blob (hvp_rc.cuh): written per linearization by
+// k_lin_normal (recompute path) or k_tile_lin_rc.
+constexpr int kRcRec = 16;   // per-camera record stride (static [R t f k1 k2 0], dynamic [M v_t v_int 0])
+__host__ __device__ constexpr uint32_t rc_r16(uint64_t b) { return static_cast<uint32_t>((b + 15) / 16 * 16); }
+// lin blob of the recompute path (per linearization): point D, tile camera
+// static records, Huber weights, point parameters X
+struct RcLinSec {
+  uint32_t D, cam, w, X, bytes;
+};
+template <typename FP>
+__host__ __device__ inline RcLinSec rc_lin_sections(uint32_t ne, uint32_t npt, uint32_t ncam, bool huber) {
+  const uint32_t ne8 = (ne + kEdgePad - 1) / kEdgePad * kEdgePad;
+  RcLinSec l;
+  l.D = 0;
+  l.cam = l.D + rc_r16(sizeof(FP) * 3ull * npt);
+  l.w = l.cam + rc_r16(sizeof(FP) * static_cast<uint64_t>(kRcRec) * ncam);
+  l.X = l.w + (huber ? rc_r16(sizeof(FP) * 1ull * ne8) : 0u);
+  l.bytes = l.X + rc_r16(sizeof(FP) * 3ull * npt);
+  return l;
+}
+
+
 constexpr int kLinThreads = 128;
 template <typename FP>
 __host__ __device__ constexpr size_t lin_normal_smem() {
@@ -1354,7 +1380,22 @@ __global__ void __launch_bounds__(kLinThreads, 4) k_lin_normal(Dev<FP, SP> d, in
   if (!AUTO)
     for (uint32_t i = tid; i < ncam * kCamPre; i += blockDim.x)
       sPre[i] = d.cpre[static_cast<uint64_t>(kCamPre) * d.tile_cams[cb + i / kCamPre] + i % kCamPre];
+  // recompute path: this pass also writes the tile's per-linearization blob
+  // (point D, camera records [R t f k1 k2], Huber w, point X; hvp_rc.cuh)
+  const bool blob = !AUTO && d.part15 != nullptr;
+  unsigned char* lb = blob ? d.tile_lin + 16ull * d.tile_meta[static_cast<uint64_t>(kMCount) * blockIdx.x + kMLin16]
+                           : nullptr;
+  const RcLinSec lsec = rc_lin_sections<FP>(ne_t, npt, ncam, d.w != nullptr);
   __syncthreads();
+  if (blob) {
+    FP* bx = reinterpret_cast<FP*>(lb + lsec.X);
+    for (uint32_t i = tid; i < npt * 3; i += blockDim.x) bx[i] = sX[i];
+    FP* bc = reinterpret_cast<FP*>(lb + lsec.cam);
+    for (uint32_t k = tid; k < kRcRec * ncam; k += blockDim.x) {
+      const uint32_t lc = k / kRcRec, v = k % kRcRec;
+      bc[k] = v < 9 ? sPre[kCamPre * lc + 8 + v] : (v < 15 ? sC[9 * lc + v - 6] : FP(0));
+    }
+  }
   FP chi = FP(0);
   for (uint32_t c0 = 0; c0 < ne_t; c0 += kLinThreads) {
   const uint32_t j = c0 + tid;
@@ -1380,7 +1421,10 @@ __global__ void __launch_bounds__(kLinThreads, 4) k_lin_normal(Dev<FP, SP> d, in
 #pragma unroll
     for (int k = 0; k < 6; ++k) jp[k] = widen<FP>(narrow<SP>(jp[k]));
   }
-  if (d.w && valid) d.w[e] = w;
+  if (d.w && valid) {
+    d.w[e] = w;
+    if (blob) reinterpret_cast<FP*>(lb + lsec.w)[j] = w;
+  }
   const FP wr0 = valid ? w * res[0] : FP(0), wr1 = valid ? w * res[1] : FP(0);
   if (valid) {
     FP* pv = pst + j * 9;
@@ -1439,7 +1483,9 @@ __global__ void __launch_bounds__(kLinThreads, 4) k_lin_normal(Dev<FP, SP> d, in
       const FP diag = freev ? acc[3 + p3(k, k)] : FP(0);
       const FP cl = clampv(diag, FP(d.st->clamp_min), FP(d.st->clamp_max));
       d.clamped[col + k] = freev ? cl : FP(0);
-      d.D[col + k] = freev ? FP(1) / sqrt(cl) : FP(0);
+      const FP Dv = freev ? FP(1) / sqrt(cl) : FP(0);
+      d.D[col + k] = Dv;
+      if (blob) reinterpret_cast<FP*>(lb + lsec.D)[3 * i + k] = Dv;
       if (freev) {
         fin &= (is_finite(bk) && is_finite(diag)) ? 1 : 0;
         gmax = fmax(gmax, fabs(bk));

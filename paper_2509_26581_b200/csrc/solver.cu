@@ -1615,7 +1615,7 @@ class Solver final : public SolverBase {
     if (pipe_ok_) {
       k_tile_lin<FP, SP><<<dev_.n_normal, 128, 0, s_>>>(dev_, force);
       CK(cudaGetLastError());
-    } else if (rc_ok_) {
+    } else if (rc_ok_ && (g_.diff_mode == GB_AUTO || !dev_.part15)) {  // else k_lin_normal wrote the blobs
       phase_mark("lin: cameras");
       k_tile_lin_rc<FP, SP><<<dev_.n_normal, 128, 0, s_>>>(dev_, force);
       CK(cudaGetLastError());
