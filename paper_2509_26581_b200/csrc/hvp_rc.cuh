@@ -374,23 +374,24 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
       const FP* sD = reinterpret_cast<const FP*>(lin + ls.D);
       const SP* sp = reinterpret_cast<const SP*>(rg + h[kROP] + h[kRDp]);
       const uint32_t pb = h[kRPb];
-      const uint32_t ncv = kRcVals * ncam;
+      constexpr uint32_t kVG = 5;  // values per camera item: 3 items per camera, so a tile's camera
+                                   // items and points usually fit one pass of the group's 128 threads
+      const uint32_t ncv = (kRcVals / kVG) * ncam;
       FP dot = FP(0);
       for (uint32_t o = gt; o < ncv + npt && !(L.dbg & 2); o += kRcGroupThreads) {
         if (o < ncv) {
-          const uint32_t lc = o / kRcVals, v = o - kRcVals * lc;
-          const FP* src = sA + v * kRcAStr;
-          FP a0 = FP(0), a1 = FP(0), a2 = FP(0), a3 = FP(0);
-          uint32_t q = rseg[lc];
+          const uint32_t lc = o / (kRcVals / kVG), v0 = kVG * (o - (kRcVals / kVG) * lc);
+          const FP* src = sA + v0 * kRcAStr;
+          FP a[kVG];
+#pragma unroll
+          for (int u = 0; u < static_cast<int>(kVG); ++u) a[u] = FP(0);
           const uint32_t qe = rseg[lc + 1];
-          for (; q + 4 <= qe; q += 4) {
-            a0 += src[q];
-            a1 += src[q + 1];
-            a2 += src[q + 2];
-            a3 += src[q + 3];
-          }
-          for (; q < qe; ++q) a0 += src[q];
-          d.part15[static_cast<uint64_t>(kRcRec) * (cb + lc) + v] = (a0 + a1) + (a2 + a3);
+          for (uint32_t q = rseg[lc]; q < qe; ++q)
+#pragma unroll
+            for (int u = 0; u < static_cast<int>(kVG); ++u) a[u] += src[u * kRcAStr + q];
+#pragma unroll
+          for (int u = 0; u < static_cast<int>(kVG); ++u)
+            d.part15[static_cast<uint64_t>(kRcRec) * (cb + lc) + v0 + u] = a[u];
         } else {
           const uint32_t pi = o - ncv;
           FP a[3] = {FP(0), FP(0), FP(0)};
