@@ -79,7 +79,7 @@ inline RcLayout rc_layout(bool huber, uint32_t smem_budget) {
   L.max_region = kRcHdrBytes + aux_sections(kTileEdges, kTilePoints).bytes +
                  rc_lin_sections<FP>(kTileEdges, kTilePoints, kTileCams, huber).bytes +
                  4 * r16(kTilePoints * 3 * sizeof(FP) + 16) + kTileCams * kRcRec * sizeof(FP) + 128;
-  L.slots = kRcGroups * L.work_bytes;
+  L.slots = 2 * kRcGroups * L.work_bytes;  // two work buffers per group (alternating tiles)
   L.bars = L.slots + 4 * kRcSlots;
   L.ring = L.bars + 4 * kRcSlots * 8;
   L.ring = (L.ring + 127) / 128 * 128;
@@ -293,14 +293,17 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
     // ---------------------------------------------------------- consumer groups
     const uint32_t g = static_cast<uint32_t>(warp) / (kRcGroupThreads / 32);
     const uint32_t gt = static_cast<uint32_t>(tid) - g * kRcGroupThreads;  // 0..127
-    unsigned char* wk = rc_smem + g * L.work_bytes;
-    FP* sA = reinterpret_cast<FP*>(wk + L.A);
-    FP* gp = reinterpret_cast<FP*>(wk + L.gp);
     const FP lam = static_cast<FP>(d.st->lambda_solve);
     const int before = d.st->before_scaling;
     unsigned long long w_ready = 0;
     const long long t_start = clock64();
-    for (uint32_t it = g;; it += kRcGroups) {
+    for (uint32_t it = g, k2 = 0;; it += kRcGroups, ++k2) {
+      // the group's two work buffers alternate: the edge phase of tile k2 + 1
+      // writes one while no thread can still read it (every thread passed the
+      // barrier of tile k2 only after finishing the epilogue of tile k2 - 1)
+      unsigned char* wk = rc_smem + (2 * g + (k2 & 1u)) * L.work_bytes;
+      FP* sA = reinterpret_cast<FP*>(wk + L.A);
+      FP* gp = reinterpret_cast<FP*>(wk + L.gp);
       if (blockIdx.x + it * gridDim.x >= ntiles) break;
       const int s = static_cast<int>(it % kRcSlots);
       mbar_wait_t(&ready[s], (it / kRcSlots) & 1u, pf, w_ready);
@@ -423,9 +426,8 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
         d.tile_red[8ull * t + w] = dot;
         d.tile_red[8ull * t + 4 + w] = FP(0);
       }
-      // the group's work buffer is reused by its next tile; the tile region is free
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kRcGroupThreads) : "memory");
-      if (lane == 0) mbar_arrive(&empty[s]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // this warp no longer reads the tile region
     }
     if (pf) {
       atomicAdd(&L.prof[0], w_ready);
