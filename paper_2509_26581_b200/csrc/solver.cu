@@ -1266,7 +1266,7 @@ class Solver final : public SolverBase {
     if (g_.diff_mode != GB_AUTO && (std::is_same<SP, FP>::value || g_.diff_mode == GB_DYNAMIC) &&
         g_.linear_solver != GB_SOLVER_SCHUR && d.n_normal > 0) {
       rc_ = rc_layout<FP>(g_.loss_kind == GB_LOSS_HUBER, static_cast<uint32_t>(optin));
-      rc_ok_ = rc_.ring_bytes >= 2 * rc_.max_region;
+      rc_ok_ = rc_.ring_bytes >= rc_.max_region;  // any single tile fits (the ring drains before a huge one)
       if (const char* e = std::getenv("GB_HVP_RC")) rc_ok_ = rc_ok_ && std::atoi(e) != 0;
       if (const char* e = std::getenv("GB_RC_DBG")) rc_.dbg = std::atoi(e);
       // x += alpha p deferred into the next HVP (the fused direction update path only)

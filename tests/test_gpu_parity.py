@@ -8,6 +8,8 @@ BASELINE.json's north star states: index structures bit-exact; final chi^2
 within 1e-6 relative (fp64) / 1e-4 (fp32, fp32-bf16) with the same LM
 iteration count.
 """
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -150,6 +152,9 @@ def test_recompute_hvp(gpu, monkeypatch, precision, mode, huber, zipf):
         monkeypatch.setenv("GB_HVP_RC", rc)
         g = bal.build_graph(p, precision, mode, huber)
         n = g.ls_linearize(0)["n"]
+        path = ctypes.c_int32()
+        g.backend.check(g.backend.fn("hvp_info")(g._h, ctypes.byref(path), None, None, None))
+        assert path.value == (3 if rc == "1" else (0 if mode == "dynamic" else 2)), path.value  # the path under test
         v = np.random.default_rng(4).standard_normal(n)
         hs = [g.ls_hvp(v, lam) for lam in (0.0, 1e-3)]
         g2 = bal.build_graph(p, precision, mode, huber)
