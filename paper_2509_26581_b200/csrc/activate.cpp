@@ -58,13 +58,14 @@ void build_incidence(uint64_t nvert, const std::vector<uint32_t>& vert_of_a, con
 }  // namespace
 
 void greedy_tiles(const std::vector<uint32_t>& deg_int, std::vector<uint32_t>& tile_pbeg,
-                  std::vector<uint32_t>& tile_ebeg, std::vector<uint32_t>& tile_of_pt) {
+                  std::vector<uint32_t>& tile_ebeg, std::vector<uint32_t>& tile_of_pt, uint32_t edge_cap) {
   tile_of_pt.resize(deg_int.size());
-  greedy_tiles(deg_int.data(), deg_int.size(), tile_pbeg, tile_ebeg, tile_of_pt.data());
+  greedy_tiles(deg_int.data(), deg_int.size(), tile_pbeg, tile_ebeg, tile_of_pt.data(), edge_cap);
 }
 
 void greedy_tiles(const uint32_t* deg_int, uint64_t np, std::vector<uint32_t>& tile_pbeg,
-                  std::vector<uint32_t>& tile_ebeg, uint32_t* tile_of_pt) {
+                  std::vector<uint32_t>& tile_ebeg, uint32_t* tile_of_pt, uint32_t edge_cap) {
+  const uint64_t cap = std::min<uint64_t>(edge_cap, kTileEdges);
   tile_pbeg.assign(1, 0);
   tile_ebeg.assign(1, 0);
   tile_pbeg.reserve(np / 64 + 2);
@@ -73,7 +74,7 @@ void greedy_tiles(const uint32_t* deg_int, uint64_t np, std::vector<uint32_t>& t
   for (uint64_t i = 0; i < np; ++i) {
     const uint64_t d = deg_int[i];
     const bool heavy = d > static_cast<uint64_t>(kTileEdges);
-    if (tp > 0 && (heavy || te + d > static_cast<uint64_t>(kTileEdges) || tp >= static_cast<uint64_t>(kTilePoints))) {
+    if (tp > 0 && (heavy || te + d > cap || tp >= static_cast<uint64_t>(kTilePoints))) {
       tile_pbeg.push_back(static_cast<uint32_t>(i));
       tile_ebeg.push_back(static_cast<uint32_t>(ecount));
       te = tp = 0;
@@ -214,7 +215,7 @@ void activate(const ActivationInput& in, Activation& out) {
   std::vector<uint32_t> deg_int(in.np);
   for (uint64_t i = 0; i < in.np; ++i) deg_int[i] = deg[out.pt_order[i]];
   std::vector<uint32_t> tile_of_pt;
-  greedy_tiles(deg_int, out.tile_pbeg, out.tile_ebeg, tile_of_pt);
+  greedy_tiles(deg_int, out.tile_pbeg, out.tile_ebeg, tile_of_pt, in.tile_edge_cap);
   out.ntiles = static_cast<uint32_t>(out.tile_pbeg.size() - 1);
 
   // device edge order: active edges sorted by camera (stable in a), then

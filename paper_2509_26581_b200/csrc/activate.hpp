@@ -37,6 +37,7 @@ struct ActivationInput {
   const uint8_t* cam_fixed = nullptr;  // may be null
   const uint8_t* pt_fixed = nullptr;   // may be null
   int active_level = 0;
+  uint32_t tile_edge_cap = kTileEdges;  // greedy tile edge budget (<= kTileEdges; the recompute HVP uses less)
 };
 
 struct Activation {
@@ -88,10 +89,10 @@ void shard_bounds(const uint32_t* tile_ebeg, const uint32_t* tile_pbeg, uint32_t
 
 // building blocks shared with the device activation (activate_dev.cuh)
 void greedy_tiles(const std::vector<uint32_t>& deg_int, std::vector<uint32_t>& tile_pbeg,
-                  std::vector<uint32_t>& tile_ebeg, std::vector<uint32_t>& tile_of_pt);
+                  std::vector<uint32_t>& tile_ebeg, std::vector<uint32_t>& tile_of_pt, uint32_t edge_cap = kTileEdges);
 // the same over a raw degree array; tile_of_pt may be null
 void greedy_tiles(const uint32_t* deg_int, uint64_t np, std::vector<uint32_t>& tile_pbeg,
-                  std::vector<uint32_t>& tile_ebeg, uint32_t* tile_of_pt);
+                  std::vector<uint32_t>& tile_ebeg, uint32_t* tile_of_pt, uint32_t edge_cap = kTileEdges);
 void classify_tiles(Activation& out);
 // FactorDescriptor::build_incidence for one slot (factor_descriptor.hpp:710-753)
 void build_incidence_host(uint64_t nvert, const std::vector<uint32_t>& vert_of_a, const uint8_t* fixed, Incidence& inc);

@@ -834,7 +834,17 @@ class Solver final : public SolverBase {
     in.cam_fixed = g_.cam_fixed.empty() ? nullptr : g_.cam_fixed.data();
     in.pt_fixed = g_.pt_fixed.empty() ? nullptr : g_.pt_fixed.data();
     in.active_level = level;
+    in.tile_edge_cap = tile_edge_cap();
     return in;
+  }
+
+  // Greedy tile edge budget (experiments: GB_TILE_CAP). Measured on the
+  // recompute path at Final: 512 edges 0.739 ms per HVP, 480: 0.814, 448:
+  // 0.858 — the per-tile costs outweigh the shorter segments.
+  uint32_t tile_edge_cap() const {
+    uint32_t cap = static_cast<uint32_t>(kTileEdges);
+    if (const char* e = std::getenv("GB_TILE_CAP")) cap = static_cast<uint32_t>(std::atoi(e));
+    return std::max<uint32_t>(32, std::min<uint32_t>(cap, kTileEdges));
   }
 
   void ensure_structure(int level) {
@@ -1097,7 +1107,7 @@ class Solver final : public SolverBase {
     // points: the tile plan, and with it every rank's shard, is global
     ptm.mark("act: compact + point order");
     std::vector<uint32_t> gpbeg, greal;
-    greedy_tiles(hdeg, np, gpbeg, greal, nullptr);
+    greedy_tiles(hdeg, np, gpbeg, greal, nullptr, tile_edge_cap());
     ptm.mark("act: host greedy tiles");
     const uint32_t GT = static_cast<uint32_t>(gpbeg.size() - 1);
     std::vector<uint32_t> gebeg(GT + 1, 0);
