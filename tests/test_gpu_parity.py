@@ -175,6 +175,23 @@ def test_recompute_hvp(gpu, monkeypatch, precision, mode, huber, zipf):
     assert rel(out["1"][2], out["0"][2]) <= {"fp64": 1e-7, "fp32": 1e-3, "fp32-bf16": 1e-2}[precision]
 
 
+@pytest.mark.parametrize("precision,huber", [("fp64", None), ("fp32", 2.0)])
+def test_deferred_x_update_bit_exact(gpu, monkeypatch, precision, huber):
+    """PCG's x += alpha p deferred into the next HVP (defer_x) evaluates the
+    same expression on the same operands as the in-place update: the LM trace
+    and the refined parameters are bit-identical with it on and off."""
+    p = bal.synthetic_bal(900, 60000, 330000, seed=11)
+    out = {}
+    for dx in ("1", "0"):
+        monkeypatch.setenv("GB_DEFER_X", dx)
+        g = bal.build_graph(p, precision, "analytic", huber)
+        rep = bal.levenberg_marquardt(g, bal_cfg(5))
+        out[dx] = ([(i.chi2_after, i.lambda_, i.pcg_iterations) for i in rep.iterations], g.points.copy(),
+                   g.cameras.copy())
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1]) and np.array_equal(out["1"][2], out["0"][2])
+
+
 def test_recompute_hvp_deterministic(gpu, monkeypatch):
     """Fixed association order everywhere: two runs are bit-identical."""
     monkeypatch.setenv("GB_HVP_RC", "1")
