@@ -119,6 +119,7 @@ struct Dev {
   FP* crec;              // [nc][16]
   FP* part15;            // [ntcams][16]
   const uint8_t* hflag;  // [nparts] camera-major storage order
+  FP* lpart;             // [ntcams][54] linearize camera-run sums of normal tiles (k_lin_seg), or null
   FP* w;            // [na] or null (default loss: w == 1)
   const uint32_t* tile_ebeg;  // padded slot begin of each tile
   const uint32_t* tile_ecnt;  // real edges of each tile
@@ -657,9 +658,38 @@ __global__ void __launch_bounds__(kTileThreads) k_lin_tiles(Dev<FP, SP> d, const
 // the finalize.
 // Sum of camera c's 54-value linearize partials in slot-list order (lane v:
 // value v in a0, value 32 + v in a1); eight slots' loads in flight at a time.
+// With lpart (recompute path): the camera's tile-camera entries (cam_tc order),
+// then the flagged partial slots of heavy tiles.
 template <typename FP, typename SP>
 __device__ inline void lin_cam_sum(const Dev<FP, SP>& d, uint32_t c, int lane, FP& a0, FP& a1) {
   constexpr int B = 8;
+  if (d.lpart) {
+    const uint32_t beg = d.cam_tc_off[c], end = d.cam_tc_off[c + 1];
+    for (uint32_t q0 = beg; q0 < end; q0 += B) {
+      const uint32_t mine = q0 + (lane & (B - 1)) < end ? d.cam_tc_idx[q0 + (lane & (B - 1))] : 0u;
+      FP v0[B], v1[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const FP* src = d.lpart + static_cast<uint64_t>(__shfl_sync(0xffffffffu, mine, u)) * kLinVals;
+        const bool ok = q0 + u < end;
+        v0[u] = ok ? src[lane] : FP(0);
+        v1[u] = ok && lane < kLinVals - 32 ? src[32 + lane] : FP(0);
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        if (q0 + u < end) {
+          a0 += v0[u];
+          a1 += v1[u];
+        }
+    }
+    if (d.n_heavy)
+      for (uint32_t q = d.cam_part_off[c]; q < d.cam_part_off[c + 1]; ++q)
+        if (d.hflag[q]) {
+          a0 += d.part[static_cast<uint64_t>(q) * kLinVals + lane];
+          if (lane < kLinVals - 32) a1 += d.part[static_cast<uint64_t>(q) * kLinVals + 32 + lane];
+        }
+    return;
+  }
   const uint32_t beg = d.cam_part_off[c], end = d.cam_part_off[c + 1];
   for (uint32_t q0 = beg; q0 < end; q0 += B) {
     const uint32_t mine = q0 + (lane & (B - 1)) < end ? q0 + (lane & (B - 1)) : 0u;  // storage slot = position

@@ -1318,6 +1318,7 @@ class Solver final : public SolverBase {
       d.ntcams = act_.tile_cam_off.empty() ? 0 : act_.tile_cam_off.back();
       d.crec = d.part15 = nullptr;
       d.hflag = nullptr;
+      d.lpart = nullptr;
       if (pipe_ok_ || rc_ok_) {
         if (pipe_ok_)
           CK(cudaFuncSetAttribute(k_hvp_pipe<FP, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1369,6 +1370,15 @@ class Solver final : public SolverBase {
           uint8_t* hf = static_cast<uint8_t*>(b_hflag_.alloc(std::max<uint64_t>(1, act_.nparts)));
           CK(cudaMemsetAsync(hf, 0, std::max<uint64_t>(1, act_.nparts), s_));
           d.hflag = hf;
+          // linearize camera-run sums per tile camera (k_lin_seg); heavy tiles' entries stay 0
+          bool seg = g_.diff_mode != GB_AUTO;
+          if (const char* e = std::getenv("GB_LIN_SEG")) seg = seg && std::atoi(e) != 0;
+          if (seg) {
+            d.lpart = static_cast<FP*>(b_lpart_.alloc(nt * kLinVals * sizeof(FP)));
+            CK(cudaMemsetAsync(d.lpart, 0, nt * kLinVals * sizeof(FP), s_));
+            CK(cudaFuncSetAttribute(k_lin_seg<FP, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(lin_seg_smem<FP>())));
+          }
         }
         pipe_aux_pending_ = true;  // built once the remaining device arrays exist (below)
       }
@@ -1606,7 +1616,10 @@ class Solver final : public SolverBase {
       if (dev_.n_heavy)
         k_lin_tiles<FP, SP, true, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
     } else {
-      if (dev_.n_normal) k_lin_normal<FP, SP, false, false><<<dev_.n_normal, kLinThreads, smem, s_>>>(dev_, force);
+      if (dev_.n_normal && dev_.lpart)
+        k_lin_seg<FP, SP><<<dev_.n_normal, kLinSegThreads, lin_seg_smem<FP>(), s_>>>(dev_, force);
+      else if (dev_.n_normal)
+        k_lin_normal<FP, SP, false, false><<<dev_.n_normal, kLinThreads, smem, s_>>>(dev_, force);
       if (dev_.n_heavy)
         k_lin_tiles<FP, SP, false, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
     }
@@ -1931,7 +1944,7 @@ class Solver final : public SolverBase {
   static constexpr bool kRcCapable = true;  // every precision (bf16 storage: dynamic mode only)
   RcLayout rc_{};
   bool rc_ok_ = false;  // recompute HVP (hvp_rc.cuh): no J store
-  DBuf b_crec_, b_part15_, b_hflag_, b_rcprof_;
+  DBuf b_crec_, b_part15_, b_hflag_, b_rcprof_, b_lpart_;
   uint32_t sms_ = 148;
   unsigned pt_occ_ = 4;
   unsigned chi2_occ_ = 4;
