@@ -842,7 +842,8 @@ constexpr int kLinSegHalf = kLinVals / 2;  // values per shared-memory pass (and
 static_assert(kLinSegHalf * kSegSlots <= kTileEdges * 9, "segment sums fit the point buffer");
 template <typename FP>
 __host__ __device__ constexpr size_t lin_seg_smem() {
-  return sizeof(FP) * (kTilePoints * 3 + kTileCams * 9 + kTileCams * kCamPre + kTileEdges * 9 + 32);
+  return sizeof(FP) * (kTilePoints * 3 + kTileCams * 9 + kTileCams * kCamPre + kTileEdges * 9 + 32 + 2 * kTileEdges) +
+         sizeof(uint16_t) * (2 * kTileEdges + kTilePoints + 8);
 }
 
 // camera value V of one edge folded into its accumulator, with jc and r
@@ -868,6 +869,9 @@ __device__ __forceinline__ void cp_async_elem(T* dst, const T* src) {
   static_assert(sizeof(T) == 4 || sizeof(T) == 8, "cp.async.ca element size");
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_addr(dst)), "l"(src), "n"(sizeof(T)) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <typename FP, typename SP>
@@ -880,6 +884,10 @@ __global__ void __launch_bounds__(kLinSegThreads, 3) k_lin_seg(Dev<FP, SP> d, in
   FP* pst = sPre + kTileCams * kCamPre;
   FP* sA = pst;  // after the point epilogue
   FP* scratch = pst + kTileEdges * 9;
+  FP* sObs = scratch + 32;  // [2][kTileEdges] the tile's observations
+  uint16_t* sLpt = reinterpret_cast<uint16_t*>(sObs + 2 * kTileEdges);  // aux lpt, psl, pso
+  uint16_t* sPsl = sLpt + kTileEdges;
+  uint16_t* sPso = sPsl + kTileEdges;
   const int tid = threadIdx.x;
   const uint32_t i = blockIdx.x, t = d.normal_tiles[i];
   const uint32_t* m = d.tile_meta + static_cast<uint64_t>(kMCount) * i;
@@ -902,6 +910,17 @@ __global__ void __launch_bounds__(kLinSegThreads, 3) k_lin_seg(Dev<FP, SP> d, in
     for (int k = 0; k < kCamPre; ++k) cp_async_elem(&sPre[kCamPre * tid + k], d.cpre + kCamPre * c + k);
   }
   for (uint32_t k = tid; k < npt * 3; k += blockDim.x) cp_async_elem(&sX[k], d.x + pcol0 + 3ull * pb + k);
+  {  // observations and the aux index sections (16-byte aligned, 16-byte copies)
+    const uint32_t ne8 = (ne_t + kEdgePad - 1) / kEdgePad * kEdgePad;
+    constexpr uint32_t E16 = 16 / sizeof(FP);
+    for (uint32_t k = tid; k < 2 * ne8 / E16; k += blockDim.x) {
+      const uint32_t row = k / (ne8 / E16), c = k % (ne8 / E16);
+      cp_async16(sObs + row * kTileEdges + c * E16, d.d_obs + static_cast<uint64_t>(row) * d.na + eb + c * E16);
+    }
+    for (uint32_t k = tid; k < ne8 / 8; k += blockDim.x) cp_async16(sLpt + 8 * k, aux + as.lpt + 16 * k);
+    for (uint32_t k = tid; k < (ne_t + 7) / 8; k += blockDim.x) cp_async16(sPsl + 8 * k, aux + as.psl + 16 * k);
+    for (uint32_t k = tid; k < (npt + 8) / 8; k += blockDim.x) cp_async16(sPso + 8 * k, aux + as.pso + 16 * k);
+  }
   unsigned char* lb = d.tile_lin + 16ull * m[kMLin16];
   const RcLinSec lsec = rc_lin_sections<FP>(ne_t, npt, ncam, d.w != nullptr);
   cp_async_wait_all();
@@ -919,12 +938,11 @@ __global__ void __launch_bounds__(kLinSegThreads, 3) k_lin_seg(Dev<FP, SP> d, in
 #pragma unroll
   for (int v = 0; v < kLinVals; ++v) acc[v] = FP(0);
   FP chi = FP(0);
-  const uint16_t* lpt = reinterpret_cast<const uint16_t*>(aux + as.lpt);
   FP* bw = reinterpret_cast<FP*>(lb + lsec.w);
   for (uint32_t k = 0; k < cnt; ++k) {
     const uint32_t j = s0 + k, e = eb + j;
-    const uint32_t lp = lpt[j];
-    const FP o0 = d.d_obs[e], o1 = d.d_obs[static_cast<uint64_t>(d.na) + e];
+    const uint32_t lp = sLpt[j];
+    const FP o0 = sObs[j], o1 = sObs[kTileEdges + j];
     FP res[2], jc[18], jp[6];
     snavely_linearize<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res, jc, jp, nullptr, &sPre[kCamPre * lc]);
     const FP s = res[0] * res[0] + res[1] * res[1];
@@ -964,8 +982,8 @@ __global__ void __launch_bounds__(kLinSegThreads, 3) k_lin_seg(Dev<FP, SP> d, in
     FP pa[9];
 #pragma unroll
     for (int u = 0; u < 9; ++u) pa[u] = FP(0);
-    for (uint32_t q = d.pt_slot_off[pb + k]; q < d.pt_slot_off[pb + k + 1]; ++q) {
-      const uint32_t sl = d.pt_slots[q];
+    for (uint32_t q = sPso[k]; q < sPso[k + 1]; ++q) {
+      const uint32_t sl = sPsl[q];
 #pragma unroll
       for (int u = 0; u < 9; ++u) pa[u] += pst[sl * 9 + u];
     }
