@@ -28,6 +28,7 @@
 #include "kernels.cuh"
 #include "hvp_pipe.cuh"
 #include "hvp_rc.cuh"
+#include "lin_seg.cuh"
 
 namespace gb {
 
