@@ -60,7 +60,8 @@ struct RcLayout {
   uint32_t A, gp, work_bytes;
   uint32_t ring, ring_bytes, slots, bars, total_bytes;
   uint32_t max_region;  // largest tile region (a tile never needs more)
-  int dbg;  // experiments only (GB_RC_DBG): 1 skip the edge math, 2 skip the epilogue, 8 per-role wait cycles
+  int dbg;  // experiments only (GB_RC_DBG): 1 skip the edge math, 2 skip the epilogue, 8 per-role wait cycles,
+           // 16 utility warps wait with the suspend hint instead of the nanosleep back-off
   unsigned long long* prof;  // [8] (dbg & 8): cycles waiting / total per role, summed over CTAs
 };
 
@@ -105,6 +106,35 @@ __device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, unsigned parity) 
       " @!P bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
       "r"(parity), "r"(1000000)
       : "memory");
+}
+// utility-warp wait: non-blocking probes with an exponential nanosleep
+// back-off (32 -> 512 ns), so a waiting producer / loader / preparer does not
+// keep issuing probe instructions on an SMSP it shares with consumer warps
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred P;\n mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_backoff_wait(uint64_t* bar, unsigned parity, bool backoff) {
+  if (!backoff) {
+    mbar_sleep_wait(bar, parity);
+    return;
+  }
+  unsigned ns = 32;  // measured: caps of 256 / 2048 ns were slower than 512
+  while (!mbar_test(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 512u ? 2 * ns : 512u;
+  }
+}
+__device__ __forceinline__ void mbar_wait_u(uint64_t* bar, unsigned parity, bool backoff, bool on,
+                                            unsigned long long& acc) {
+  const long long t0 = on ? clock64() : 0;
+  mbar_backoff_wait(bar, parity, backoff);
+  if (on) acc += static_cast<unsigned long long>(clock64() - t0);
 }
 __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, unsigned parity, bool on, unsigned long long& acc) {
   if (!on) {
@@ -287,6 +317,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
   const bool dir = d.st->dir_pending != 0;
   const bool xpend = d.st->x_pending != 0;  // x += alpha p of the last PCG update (preparer, on the loaded p)
   const bool pf = (L.dbg & 8) && lane == 0;
+  const bool bo = !(L.dbg & 16);  // utility warps poll with a nanosleep back-off (GB_RC_DBG & 16: suspend-hint waits)
 
   if (warp < 2 * kRcGroupThreads / 32) {
     rc_setmaxnreg_inc216();
@@ -496,7 +527,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
           }
           if (fits) break;
           const uint32_t os = oldest % kRcSlots;
-          mbar_wait_t(&empty[os], (oldest / kRcSlots) & 1u, pf, w_prod);
+          mbar_wait_u(&empty[os], (oldest / kRcSlots) & 1u, bo, pf, w_prod);
           ++oldest;
           --inflight;
           tail_off = inflight ? slot_off[oldest % kRcSlots] : head;
@@ -552,7 +583,7 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
     // stream faster through the LSU than as extra bulk copies)
     for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i) {
       const int s = static_cast<int>(i % kRcSlots);
-      mbar_sleep_wait(&blob[s], (i / kRcSlots) & 1u);  // header and blob (camera ids) are in place
+      mbar_backoff_wait(&blob[s], (i / kRcSlots) & 1u, bo);  // header and blob (camera ids) are in place
       unsigned char* rg = ring + slot_off[s];
       const uint32_t* h = reinterpret_cast<const uint32_t*>(rg);
       const uint32_t ne = h[kRNe], npt = h[kRNpt], ncam = h[kRNcam], pb = h[kRPb];
@@ -595,8 +626,8 @@ __global__ void __launch_bounds__(kRcThreadsWS, 1) k_hvp_rc(Dev<FP, SP> d, RcLay
     unsigned long long w_full = 0;
     for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i) {
       const int s = static_cast<int>(i % kRcSlots);
-      mbar_wait_t(&full[s], (i / kRcSlots) & 1u, pf, w_full);
-      mbar_sleep_wait(&blob[s], (i / kRcSlots) & 1u);
+      mbar_wait_u(&full[s], (i / kRcSlots) & 1u, bo, pf, w_full);
+      mbar_backoff_wait(&blob[s], (i / kRcSlots) & 1u, bo);
       unsigned char* rg = ring + slot_off[s];
       const uint32_t* h = reinterpret_cast<const uint32_t*>(rg);
       const uint32_t npt = h[kRNpt];
