@@ -1578,7 +1578,7 @@ class Solver final : public SolverBase {
     CK(cudaGetLastError());
   }
   void launch_pcg_update() {
-    k_pcg_update<FP, SP><<<vert_grid(), 256, 0, s_>>>(dev_);
+    k_pcg_update<FP, SP><<<std::min(vert_grid(), sms_ * 4u), 256, 0, s_>>>(dev_);  // resident: 4 per SM (launch bounds)
     CK(cudaGetLastError());
   }
   void launch_precond() {
