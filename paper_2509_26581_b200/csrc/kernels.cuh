@@ -1743,7 +1743,7 @@ __device__ inline void pcg_update_pair(const Dev<FP, SP>& d, uint64_t q, FP alph
 
 // x += alpha p; r -= alpha Ap; z = M r; rr, rz (pcg.hpp:340-357)
 template <typename FP, typename SP>
-__global__ void __launch_bounds__(256, 4) k_pcg_update(Dev<FP, SP> d) {
+__global__ void __launch_bounds__(256, sizeof(SP) == 8 ? 4 : 1) k_pcg_update(Dev<FP, SP> d) {
   if (!d.st->iter_active || d.st->pcg_done) return;
   __shared__ FP scratch[32];
   const FP alpha = d.st->alpha;

@@ -1578,7 +1578,9 @@ class Solver final : public SolverBase {
     CK(cudaGetLastError());
   }
   void launch_pcg_update() {
-    k_pcg_update<FP, SP><<<std::min(vert_grid(), sms_ * 4u), 256, 0, s_>>>(dev_);  // resident: 4 per SM (launch bounds)
+    // 8-byte storage: a resident grid of 4 CTAs per SM (64-register bound); else the vertex grid
+    const unsigned g = sizeof(SP) == 8 ? std::min(vert_grid(), sms_ * 4u) : vert_grid();
+    k_pcg_update<FP, SP><<<g, 256, 0, s_>>>(dev_);
     CK(cudaGetLastError());
   }
   void launch_precond() {

@@ -85,6 +85,7 @@ def main():
     ap.add_argument("--full-lin")
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--hvp-label", default="hvp_pipe")
+    ap.add_argument("--lin-label", default="lin_seg")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
@@ -101,7 +102,7 @@ def main():
                        "tag": a.tag, "kernel_source_sha": hvp_source_sha(), "note": "dram__bytes_read.sum + dram__bytes_write.sum of one HVP tile-kernel launch"},
                       f, indent=1)
     if a.full_lin:
-        full(a.full_lin, a.tag, "lin_normal")
+        full(a.full_lin, a.tag, a.lin_label)
 
 
 if __name__ == "__main__":
