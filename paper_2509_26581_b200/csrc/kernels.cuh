@@ -1913,18 +1913,27 @@ __global__ void k_step(Dev<FP, SP> d) {
   int fin = 1;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d.ncols;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    // every load before the first store (the compiler cannot reorder them
+    // across the xs store, which would serialize two round trips per column)
     const FP Di = d.D[i];
     const bool ptcol = i >= 9ull * d.nc;
-    if (xpend) d.xs[i] = pcg_x_value<FP, SP>(d.xs[i], d.p[i], alpha);
-    const FP xsi = (d.st->schur && ptcol) ? d.xp[i - 9ull * d.nc] : (zero ? FP(0) : widen<FP>(d.xs[i]) * unscale);
-    const FP rhs = -Di * d.b[i];
+    const bool schur_pt = d.st->schur && ptcol;
+    const SP xs0 = d.xs[i];
+    const SP pv = xpend ? d.p[i] : xs0;
+    const FP xpv = schur_pt ? d.xp[i - 9ull * d.nc] : FP(0);
+    const FP bi = d.b[i];
+    const FP xi = d.x[i];
+    const bool fr = d.col_free[i];
+    const SP xsn = xpend ? pcg_x_value<FP, SP>(xs0, pv, alpha) : xs0;
+    if (xpend) d.xs[i] = xsn;
+    const FP xsi = schur_pt ? xpv : (zero ? FP(0) : widen<FP>(xsn) * unscale);
+    const FP rhs = -Di * bi;
     const FP damp = before ? lam * Di * Di : lam;
     if (counted(d, i)) pred += xsi * (damp * xsi + rhs);
     const FP dxi = Di * xsi;
     if (d.want_dx) d.dx[i] = dxi;
     if (!is_finite(dxi)) fin = 0;
-    const FP xi = d.x[i];
-    d.x_new[i] = d.col_free[i] ? xi + dxi : xi;
+    d.x_new[i] = fr ? xi + dxi : xi;
   }
   pred = block_sum(pred, scratch);
   fin = __syncthreads_and(fin);
