@@ -54,7 +54,9 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <typename FP, typename SP>
+// HUB: Huber loss (d.w allocated); the squared-loss instantiation has no
+// weight, sqrt or division in its edge loop (w = 1 folds away exactly).
+template <typename FP, typename SP, bool HUB>
 __global__ void __launch_bounds__(kLinSegThreads, 3) k_lin_seg(Dev<FP, SP> d, int force) {
   if (!force && !d.st->do_linearize) return;
   extern __shared__ __align__(16) unsigned char lin_smem[];
@@ -126,9 +128,9 @@ __global__ void __launch_bounds__(kLinSegThreads, 3) k_lin_seg(Dev<FP, SP> d, in
     FP res[2], jc[18], jp[6];
     snavely_linearize<FP>(&sC[9 * lc], &sX[3 * lp], o0, o1, res, jc, jp, nullptr, &sPre[kCamPre * lc]);
     const FP s = res[0] * res[0] + res[1] * res[1];
-    const FP w = loss_weight<FP>(d.loss_kind, d.huber, s);
-    chi += loss_value<FP>(d.loss_kind, d.huber, s);
-    if (d.w) {
+    const FP w = HUB ? loss_weight<FP>(d.loss_kind, d.huber, s) : FP(1);
+    chi += HUB ? loss_value<FP>(d.loss_kind, d.huber, s) : s;
+    if (HUB) {
       d.w[e] = w;
       bw[j] = w;
     }
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(kLinSegThreads, 3) k_lin_seg(Dev<FP, SP> d, in
     pv[7] = w * (jp[1] * jp[2] + jp[4] * jp[5]);
     pv[8] = w * (jp[2] * jp[2] + jp[5] * jp[5]);
     FP r0 = res[0], r1 = res[1];
-    if (d.w) {  // robust loss: w J^T J = (sqrt(w) J)^T (sqrt(w) J), w J^T r = (sqrt(w) J)^T (sqrt(w) r)
+    if (HUB) {  // robust loss: w J^T J = (sqrt(w) J)^T (sqrt(w) J), w J^T r = (sqrt(w) J)^T (sqrt(w) r)
       const FP sw = sqrt(w);
 #pragma unroll
       for (int u = 0; u < 18; ++u) jc[u] *= sw;

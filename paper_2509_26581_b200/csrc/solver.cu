@@ -1377,7 +1377,9 @@ class Solver final : public SolverBase {
           if (seg) {
             d.lpart = static_cast<FP*>(b_lpart_.alloc(nt * kLinVals * sizeof(FP)));
             CK(cudaMemsetAsync(d.lpart, 0, nt * kLinVals * sizeof(FP), s_));
-            CK(cudaFuncSetAttribute(k_lin_seg<FP, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CK(cudaFuncSetAttribute(k_lin_seg<FP, SP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(lin_seg_smem<FP>())));
+            CK(cudaFuncSetAttribute(k_lin_seg<FP, SP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(lin_seg_smem<FP>())));
           }
         }
@@ -1620,7 +1622,10 @@ class Solver final : public SolverBase {
         k_lin_tiles<FP, SP, true, false><<<dev_.n_heavy, kTileThreads, 0, s_>>>(dev_, dev_.heavy_tiles, force);
     } else {
       if (dev_.n_normal && dev_.lpart)
-        k_lin_seg<FP, SP><<<dev_.n_normal, kLinSegThreads, lin_seg_smem<FP>(), s_>>>(dev_, force);
+        if (dev_.w)
+          k_lin_seg<FP, SP, true><<<dev_.n_normal, kLinSegThreads, lin_seg_smem<FP>(), s_>>>(dev_, force);
+        else
+          k_lin_seg<FP, SP, false><<<dev_.n_normal, kLinSegThreads, lin_seg_smem<FP>(), s_>>>(dev_, force);
       else if (dev_.n_normal)
         k_lin_normal<FP, SP, false, false><<<dev_.n_normal, kLinThreads, smem, s_>>>(dev_, force);
       if (dev_.n_heavy)
